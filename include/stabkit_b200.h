@@ -1,0 +1,200 @@
+/* stabkit_b200.h -- C ABI of the B200-native stabilizer-tableau engine.
+ *
+ * This is the drop-in boundary: the `stabkit::` C++ host classes
+ * (include/stabkit/*.hpp) and any foreign binding (ctypes, cgo, JNI ...) call
+ * ONLY these entry points; behind them are hand-written sm_100a CUDA kernels
+ * (paper_2507_03092_b200/csrc/).  There is no CPU fallback: every call that
+ * computes fails with SK_ECUDA when no CUDA device is usable.
+ *
+ * Each entry point names the reference interface it replaces.  "ref:" paths
+ * are relative to /root/reference ; SPEC = SPEC.md, the behavioural contract
+ * for everything the reference ships only as specification.
+ *
+ * Conventions (ref: proj/include/stabkit/bitvec.hpp:26-35, pauli.hpp:28-31,53-54)
+ *   - 64-bit words; qubit q lives in word q>>6, bit q&63; padding bits zero.
+ *   - I=(0,0) X=(1,0) Z=(0,1) Y=(1,1); sign byte 1 means -1.
+ *   - Host tableau/row arrays are ROW-MAJOR: row i occupies words
+ *     [i*W, (i+1)*W) of the x array and of the z array, W = ceil(n/64).
+ *     Tableau row order is SPEC:110: rows 0..n-1 stabilizers, n..2n-1
+ *     destabilizers (the scratch row never leaves the chip).
+ *   - Every function returns an sk_status; sk_last_error() gives the text.
+ *     The C++ wrappers map the codes to the reference's exception types
+ *     (ref: proj/include/stabkit/error.hpp:25-51).
+ *   - Handles own device memory.  Host arrays are borrowed for the call.
+ *   - One host thread drives a context; calls are ordered on the context's
+ *     stream; calls that return data synchronise that stream.
+ */
+#ifndef STABKIT_B200_H
+#define STABKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sk_status {
+    SK_OK = 0,
+    SK_EDIM = 1,         /* stabkit::DimensionError   (error.hpp:38-41) */
+    SK_EUNSUPPORTED = 2, /* stabkit::UnsupportedError (error.hpp:43-46) */
+    SK_EINVARIANT = 3,   /* stabkit::InvariantError   (error.hpp:48-51) */
+    SK_ECUDA = 4,        /* CUDA runtime / no device: stabkit::Error */
+    SK_ENCCL = 5,
+    SK_EPARSE = 6,       /* stabkit::ParseError       (error.hpp:31-36) */
+    SK_EARG = 7          /* null pointer / bad enum: stabkit::Error */
+} sk_status;
+
+/* Gate kinds.  M, T, TDG are circuit-level only. */
+typedef enum sk_gate_kind {
+    SK_H = 0, SK_S = 1, SK_SDG = 2, SK_X = 3, SK_Y = 4, SK_Z = 5,
+    SK_CX = 6, SK_CZ = 7, SK_SWAP = 8, SK_M = 9, SK_T = 10, SK_TDG = 11
+} sk_gate_kind;
+
+typedef struct sk_gate {
+    uint8_t kind;        /* sk_gate_kind */
+    uint8_t pad[3];
+    uint32_t q0;         /* target, or control of CX */
+    uint32_t q1;         /* second qubit of CX/CZ/SWAP, else 0 */
+} sk_gate;
+
+typedef struct sk_ctx sk_ctx;
+typedef struct sk_tableau sk_tableau;
+typedef struct sk_program sk_program;
+typedef struct sk_rows sk_rows;
+
+/* Counters for the roofline report. */
+typedef struct sk_counters {
+    uint64_t n_rand, n_det;        /* measurements by branch                    */
+    uint64_t k_rand, k_det;        /* rowsums performed in each branch          */
+    uint64_t gate_hist[12];        /* gates applied, by sk_gate_kind            */
+    uint64_t layers;               /* fused layer launches                      */
+    uint64_t waves;                /* measurement scheduler waves               */
+    uint64_t transposes;           /* column-major <-> row-major conversions    */
+    uint64_t kernel_launches;      /* kernels launched by this library          */
+} sk_counters;
+
+/* ---- context ---------------------------------------------------------- */
+/* device: CUDA ordinal.  stream: a cudaStream_t to run on, or NULL to create
+ * one.  Fails with SK_ECUDA if the device cannot be used. */
+int32_t sk_ctx_create(int device, void* stream, sk_ctx** out);
+void sk_ctx_destroy(sk_ctx* ctx);
+const char* sk_last_error(const sk_ctx* ctx);
+void* sk_ctx_stream(const sk_ctx* ctx);           /* the cudaStream_t in use */
+int32_t sk_ctx_sync(sk_ctx* ctx);
+int32_t sk_get_counters(sk_ctx* ctx, sk_counters* out);   /* syncs */
+int32_t sk_reset_counters(sk_ctx* ctx);
+const char* sk_version(void);
+
+/* ---- tableau  (replaces SPEC:104-224 `tableau`) ------------------------ */
+/* SPEC:125-133 new_identity.  n == 0 -> SK_EDIM. */
+int32_t sk_tableau_create(sk_ctx* ctx, uint64_t n, sk_tableau** out);
+void sk_tableau_destroy(sk_tableau* t);
+int32_t sk_tableau_reset(sk_tableau* t);                 /* back to identity */
+uint64_t sk_tableau_qubits(const sk_tableau* t);
+/* Row-major 2n x W words for x and z, 2n sign bytes. */
+int32_t sk_tableau_upload(sk_tableau* t, const uint64_t* x, const uint64_t* z, const uint8_t* sign);
+int32_t sk_tableau_download(sk_tableau* t, uint64_t* x, uint64_t* z, uint8_t* sign);
+
+/* One fused layer of Clifford gates on pairwise-disjoint qubits: every
+ * tableau word is read/written once per layer.  Replaces a loop of
+ * apply_h/apply_s/apply_cx/apply_gate (row rules
+ * ref: proj/src/pauli.cpp:146-187).  Qubit collision -> SK_EARG; M/T -> SK_EUNSUPPORTED. */
+int32_t sk_apply_layer(sk_tableau* t, const sk_gate* gates, size_t ngates);
+/* Any ordered Clifford sequence; layered internally (order per qubit kept). */
+int32_t sk_apply_gates(sk_tableau* t, const sk_gate* gates, size_t ngates);
+
+/* SPEC:175-185 measure_z with the counter RNG of rng.hpp:30-39:
+ * random outcome = CounterRng{seed}.bit(ordinal). */
+int32_t sk_measure_z(sk_tableau* t, uint32_t q, uint64_t seed, uint64_t ordinal,
+                     uint8_t* outcome, uint8_t* deterministic);
+/* m consecutive measurements; bit-identical to m sequential sk_measure_z
+ * calls with ordinals ordinal0 .. ordinal0+m-1. */
+int32_t sk_measure_batch(sk_tableau* t, const uint32_t* qubits, size_t m, uint64_t seed,
+                         uint64_t ordinal0, uint8_t* outcomes, uint8_t* deterministic);
+/* SPEC:165-173 rowsum(h, i) on tableau rows (h, i in [0, 2n)). Odd mod-4 sum -> SK_EINVARIANT. */
+int32_t sk_tableau_rowsum(sk_tableau* t, uint64_t h, uint64_t i);
+
+/* ---- engine  (replaces SPEC:294-362 `engine`: sim / sim2d) ------------- */
+/* Compile a circuit once: validates it, fuses Clifford runs into layers,
+ * groups measurement runs into blocks, uploads everything to the device.
+ * mode 0 = sim (chunk marks ignored), 1 = sim2d (chunks that pass
+ * validate_chunks become layers; others fall back and set bit 0 of
+ * *warnings).  T/TDG -> SK_EUNSUPPORTED. */
+int32_t sk_program_create(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates,
+                          const uint32_t* chunk_marks, size_t nmarks, int mode,
+                          sk_program** out, uint32_t* warnings);
+void sk_program_destroy(sk_program* p);
+uint64_t sk_program_measurements(const sk_program* p);
+/* Runs the whole program on t from its current state (asynchronous; the
+ * measurement record stays on the device until read). */
+int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed);
+/* outcome / deterministic byte per M gate in circuit order (MeasurementRecord). */
+int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic);
+/* Convenience: identity tableau -> run -> record.  *out_t receives the final tableau. */
+int32_t sk_sim(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates,
+               const uint32_t* chunk_marks, size_t nmarks, int mode, uint64_t seed,
+               sk_tableau** out_t, uint8_t* outcomes, uint8_t* deterministic, uint32_t* warnings);
+
+/* ---- circuit_io / qec_gen host helpers ---------- */
+/* Arrays returned through ** are malloc'ed by the library; release with sk_free. */
+void sk_free(void* p);
+/* SPEC:375-383.  final_data_measure != 0 appends `m` on the d*d data qubits
+ * (BASELINE.json configs 1-3 "Z-basis measurement"). */
+int32_t sk_circuit_surface_code(uint32_t d, uint32_t rounds, int final_data_measure,
+                                uint64_t* n, sk_gate** gates, size_t* ngates,
+                                uint32_t** chunk_marks, size_t* nmarks);
+/* SPEC:385-393 */
+int32_t sk_circuit_random_layered(uint64_t n, uint64_t seed, sk_gate** gates, size_t* ngates,
+                                  uint32_t** chunk_marks, size_t* nmarks);
+/* SPEC:242-250 parse_native (.stab text).  On error *err_line is the 1-based line. */
+int32_t sk_circuit_parse_native(const char* text, size_t len, uint64_t* n, sk_gate** gates,
+                                size_t* ngates, uint32_t** chunk_marks, size_t* nmarks,
+                                size_t* err_line, char* err_msg, size_t err_cap);
+/* SPEC:262-270.  violations: pairs (chunk index, gate index); kind bit 0 = collision, bit 1 = measurement. */
+int32_t sk_circuit_validate_chunks(uint64_t n, const sk_gate* gates, size_t ngates,
+                                   const uint32_t* chunk_marks, size_t nmarks,
+                                   uint32_t** viol_chunk, uint32_t** viol_gate, uint8_t** viol_kind,
+                                   size_t* nviol);
+
+/* ---- Pauli row sets on the device (grouping + Clifford+T pass) ---------- */
+/* A resizable block of signed n-qubit Pauli rows (T_tab / layer / term list). */
+int32_t sk_rows_create(sk_ctx* ctx, uint64_t n, uint64_t capacity, sk_rows** out);
+void sk_rows_destroy(sk_rows* r);
+uint64_t sk_rows_count(const sk_rows* r);
+int32_t sk_rows_upload(sk_rows* r, const uint64_t* x, const uint64_t* z, const uint8_t* sign, uint64_t m);
+int32_t sk_rows_download(sk_rows* r, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* ref: proj/src/pauli.cpp:146-187 applied to every row (Algorithm 2 inner loop). */
+int32_t sk_rows_conj_layer(sk_rows* r, const sk_gate* gates, size_t ngates);
+/* ref: proj/src/pauli.cpp:215-237 commutation_vector: bit i set iff p anticommutes with row i. */
+int32_t sk_commutation_vector(sk_rows* r, const uint64_t* px, const uint64_t* pz, uint64_t* out_bits);
+/* ref: proj/src/pauli.cpp:239-254 rowsum_plus_i on every row that anticommutes with (p, psign). */
+int32_t sk_rowsum_plus_i_where_anticommuting(sk_rows* r, const uint64_t* px, const uint64_t* pz,
+                                             uint8_t psign, uint64_t* n_updated);
+/* ref: proj/src/pauli.cpp:142-144 same_axis: first duplicate pair in scan order. found=0 if none. */
+int32_t sk_find_first_duplicate(sk_rows* r, int* found, uint64_t* i, uint64_t* j);
+/* ref: proj/src/pauli.cpp:100-106 weight, summed over rows. */
+int32_t sk_weight_sum(sk_rows* r, uint64_t* out);
+
+/* SPEC:444-452 group_greedy on terms ALREADY in sorted order (rows of r);
+ * mode 0 = GC, 1 = QWC; group_of[i] = first-fit group of row i. */
+int32_t sk_group_first_fit(sk_rows* r, int mode, uint32_t* group_of, uint64_t* ngroups);
+/* SPEC:454-462 verify_grouping: number of violating intra-group pairs. */
+int32_t sk_verify_grouping(sk_rows* r, int mode, const uint32_t* group_of, uint64_t* nviolations);
+
+/* SPEC:545-553 transpile (Algorithms 2-4).  Results are read back with the
+ * accessors below.  Mid-circuit M -> SK_EUNSUPPORTED. */
+typedef struct sk_pbc sk_pbc;
+int32_t sk_transpile(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out);
+void sk_pbc_destroy(sk_pbc* p);
+/* stats: initial_t, final_rotations_rowcount, final_rotations_pauliweight, layers, passes */
+int32_t sk_pbc_stats(sk_pbc* p, uint64_t out5[5]);
+uint64_t sk_pbc_layer_rows(sk_pbc* p, uint64_t layer);
+int32_t sk_pbc_layer_download(sk_pbc* p, uint64_t layer, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* final M_tab, 2n rows row-major (measurement_rows are rows 0..n-1) */
+int32_t sk_pbc_mtab_download(sk_pbc* p, uint64_t* x, uint64_t* z, uint8_t* sign);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STABKIT_B200_H */

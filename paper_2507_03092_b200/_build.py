@@ -1,0 +1,91 @@
+"""Build recipe for libstabkit_b200.so (sm_100a only, in-tree).
+
+`python -m paper_2507_03092_b200._build` or `__graft_entry__.build()`.
+nvcc cross-compiles without a GPU; the .so travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libstabkit_b200.so")
+HOSTLIB = os.path.join(PKG, "libstabkit_host.so")
+
+NVCC_FLAGS = [
+    "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared",
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA extension cannot be built (no CPU fallback exists)")
+
+
+def _sources() -> list[str]:
+    out = []
+    for name in sorted(os.listdir(CSRC)):
+        if name.endswith((".cu", ".cpp")) and not name.startswith("host_"):
+            out.append(os.path.join(CSRC, name))
+    return out
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    srcs = _sources()
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
+    deps += [os.path.join(ROOT, "include", "stabkit_b200.h")]
+    if force or _stale(LIB, deps):
+        cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs]
+        if verbose:
+            cmd.insert(1, "-Xptxas"); cmd.insert(2, "-v")
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libstabkit_b200.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    return LIB
+
+
+def build_host(force: bool = False) -> str | None:
+    """C++ `stabkit::` host library + its self-test binary (g++, links libstabkit_b200.so)."""
+    hsrc = os.path.join(CSRC, "host_stabkit.cpp")
+    if not os.path.exists(hsrc):
+        return None
+    deps = [hsrc] + [os.path.join(ROOT, "include", "stabkit", f) for f in os.listdir(os.path.join(ROOT, "include", "stabkit"))]
+    if force or _stale(HOSTLIB, deps + [LIB]):
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-o", HOSTLIB, hsrc,
+               "-L", PKG, "-lstabkit_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("g++ failed building libstabkit_host.so")
+    tsrc = os.path.join(ROOT, "tests", "cpp", "test_host_api.cpp")
+    tbin = os.path.join(ROOT, "tests", "cpp", "test_host_api")
+    if os.path.exists(tsrc) and (force or _stale(tbin, [tsrc, HOSTLIB])):
+        cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-o", tbin, tsrc,
+               "-L", PKG, "-lstabkit_host", "-lstabkit_b200", f"-Wl,-rpath,{PKG}"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("g++ failed building tests/cpp/test_host_api")
+    return HOSTLIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_host(force="--force" in sys.argv))

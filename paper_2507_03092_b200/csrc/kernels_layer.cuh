@@ -1,0 +1,137 @@
+// kernels_layer.cuh -- K1: one fused layer of Clifford gates on disjoint qubits,
+// applied to the qubit-major (C) form.  Every touched column word is loaded once
+// and stored once per layer; the sign column is updated once per layer.
+//
+// Row rules (per row, pre-update bits; ref: proj/src/pauli.cpp:146-187, SPEC:135-163,
+// derived gates SPEC:190 collapsed to their closed forms -- same tableau result):
+//   H    r ^= x&z        ; swap(x,z)
+//   S    r ^= x&z        ; z ^= x
+//   SDG  r ^= x&~z       ; z ^= x
+//   X    r ^= z          Y   r ^= x^z          Z   r ^= x
+//   CX   r ^= xc&zt&~(xt^zc) ; xt ^= xc ; zc ^= zt
+//   CZ   r ^= xa&xb&(za^zb)  ; za ^= xb ; zb ^= xa
+//   SWAP exchange columns
+// Here one "bit" is a 64-bit word = 64 rows, processed as 128-bit vectors.
+//
+// Roofline: HBM/L2 streaming.  Algorithmic bytes per gate (fused form):
+// H 4 columns, S/SDG 3, X/Z 1, Y 2, CX/CZ 6, SWAP 8, times RW*8 bytes, plus 2*RW*8 per layer.
+#pragma once
+#include "common.cuh"
+
+namespace skd {
+
+__device__ __forceinline__ ulonglong2 ld2(const ulonglong2* p) { return __ldcg(p); }
+__device__ __forceinline__ void st2(ulonglong2* p, ulonglong2 v) { __stcg(p, v); }
+__device__ __forceinline__ bool nz2(ulonglong2 v) { return (v.x | v.y) != 0; }
+__device__ __forceinline__ ulonglong2 operator^(ulonglong2 a, ulonglong2 b) { return make_ulonglong2(a.x ^ b.x, a.y ^ b.y); }
+__device__ __forceinline__ ulonglong2 operator&(ulonglong2 a, ulonglong2 b) { return make_ulonglong2(a.x & b.x, a.y & b.y); }
+__device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulonglong2(~a.x, ~a.y); }
+
+// gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb); thread v owns
+// 128-bit row-vector v of every column it visits.
+__global__ void __launch_bounds__(256)
+k_layer(u64* __restrict__ cols, u64* __restrict__ sgn, const sk_gate* __restrict__ gates,
+        int ngates, int RW, int gpb) {
+    const int g0 = blockIdx.x * gpb;
+    const int g1 = min(ngates, g0 + gpb);
+    const int RW2 = RW >> 1;
+    for (int v = threadIdx.x; v < RW2; v += blockDim.x) {
+        ulonglong2 s = make_ulonglong2(0, 0);
+        for (int g = g0; g < g1; ++g) {
+            const sk_gate G = gates[g];
+            ulonglong2* xa = reinterpret_cast<ulonglong2*>(cols + (size_t)(2 * G.q0) * RW) + v;
+            ulonglong2* za = xa + RW2;
+            switch (G.kind) {
+                case SK_H: {
+                    ulonglong2 x = ld2(xa), z = ld2(za);
+                    s = s ^ (x & z);
+                    if (nz2(x ^ z)) { st2(xa, z); st2(za, x); }
+                } break;
+                case SK_S: {
+                    ulonglong2 x = ld2(xa);
+                    if (nz2(x)) { ulonglong2 z = ld2(za); s = s ^ (x & z); st2(za, z ^ x); }
+                } break;
+                case SK_SDG: {
+                    ulonglong2 x = ld2(xa);
+                    if (nz2(x)) { ulonglong2 z = ld2(za); s = s ^ (x & ~z); st2(za, z ^ x); }
+                } break;
+                case SK_X: s = s ^ ld2(za); break;
+                case SK_Z: s = s ^ ld2(xa); break;
+                case SK_Y: s = s ^ ld2(xa) ^ ld2(za); break;
+                case SK_CX: {
+                    ulonglong2* xt = reinterpret_cast<ulonglong2*>(cols + (size_t)(2 * G.q1) * RW) + v;
+                    ulonglong2* zt = xt + RW2;
+                    ulonglong2 xc = ld2(xa), ztv = ld2(zt);
+                    bool hx = nz2(xc), hz = nz2(ztv);
+                    if (hx | hz) {                       // all-zero source words: nothing moves
+                        ulonglong2 xtv = ld2(xt), zc = ld2(za);
+                        s = s ^ (xc & ztv & ~(xtv ^ zc));
+                        if (hx) st2(xt, xtv ^ xc);
+                        if (hz) st2(za, zc ^ ztv);
+                    }
+                } break;
+                case SK_CZ: {
+                    ulonglong2* xb = reinterpret_cast<ulonglong2*>(cols + (size_t)(2 * G.q1) * RW) + v;
+                    ulonglong2* zb = xb + RW2;
+                    ulonglong2 x0 = ld2(xa), x1 = ld2(xb);
+                    bool h0 = nz2(x0), h1 = nz2(x1);
+                    if (h0 | h1) {
+                        ulonglong2 z0 = ld2(za), z1 = ld2(zb);
+                        s = s ^ (x0 & x1 & (z0 ^ z1));
+                        if (h1) st2(za, z0 ^ x1);
+                        if (h0) st2(zb, z1 ^ x0);
+                    }
+                } break;
+                case SK_SWAP: {
+                    ulonglong2* xb = reinterpret_cast<ulonglong2*>(cols + (size_t)(2 * G.q1) * RW) + v;
+                    ulonglong2* zb = xb + RW2;
+                    ulonglong2 x0 = ld2(xa), x1 = ld2(xb), z0 = ld2(za), z1 = ld2(zb);
+                    if (nz2(x0 ^ x1)) { st2(xa, x1); st2(xb, x0); }
+                    if (nz2(z0 ^ z1)) { st2(za, z1); st2(zb, z0); }
+                } break;
+                default: break;
+            }
+        }
+        if (s.x) atomicXor(&sgn[2 * v], s.x);
+        if (s.y) atomicXor(&sgn[2 * v + 1], s.y);
+    }
+}
+
+// Row-major twin used for short gate runs while the R form is live: one thread
+// per row-bit applies the whole (ordered) gate list to its row.  Keeps R valid
+// without a full re-transposition.  Signs are NOT touched here (k_layer owns them).
+__global__ void __launch_bounds__(256)
+k_gates_rowmajor(u64* __restrict__ rows, const sk_gate* __restrict__ gates, int ngates, int Wp, int nrowbits) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nrowbits) return;
+    u64* x = rows + (size_t)(2 * r) * Wp;
+    u64* z = x + Wp;
+    for (int g = 0; g < ngates; ++g) {
+        const sk_gate G = gates[g];
+        const u32 wa = G.q0 >> 6; const u64 ma = 1ull << (G.q0 & 63);
+        switch (G.kind) {
+            case SK_H: { u64 xv = x[wa], zv = z[wa]; u64 d = (xv ^ zv) & ma; if (d) { x[wa] = xv ^ d; z[wa] = zv ^ d; } } break;
+            case SK_S: case SK_SDG: { u64 xv = x[wa] & ma; if (xv) z[wa] ^= xv; } break;
+            case SK_CX: {
+                const u32 wb = G.q1 >> 6; const u64 mb = 1ull << (G.q1 & 63);
+                if (x[wa] & ma) x[wb] ^= mb;
+                if (z[wb] & mb) z[wa] ^= ma;
+            } break;
+            case SK_CZ: {
+                const u32 wb = G.q1 >> 6; const u64 mb = 1ull << (G.q1 & 63);
+                bool xa_ = x[wa] & ma, xb_ = x[wb] & mb;
+                if (xb_) z[wa] ^= ma;
+                if (xa_) z[wb] ^= mb;
+            } break;
+            case SK_SWAP: {
+                const u32 wb = G.q1 >> 6; const u64 mb = 1ull << (G.q1 & 63);
+                bool xa_ = x[wa] & ma, xb_ = x[wb] & mb, za_ = z[wa] & ma, zb_ = z[wb] & mb;
+                if (xa_ != xb_) { x[wa] ^= ma; x[wb] ^= mb; }
+                if (za_ != zb_) { z[wa] ^= ma; z[wb] ^= mb; }
+            } break;
+            default: break;   // X, Y, Z: signs only
+        }
+    }
+}
+
+}  // namespace skd

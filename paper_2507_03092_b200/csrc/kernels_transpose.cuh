@@ -1,0 +1,104 @@
+// kernels_transpose.cuh -- bit-matrix transposition between the qubit-major (C)
+// and row-major (R) forms.   dst[r][c] = src[c][r].
+//
+// One CTA moves a 256 x 256-bit tile through shared memory so that both the
+// global loads and the global stores are 32-byte contiguous per matrix row;
+// each warp transposes 32x32-bit blocks with 32 __ballot_sync votes (lane l
+// contributes bit b of its word; the vote IS output row b).
+// Roofline: HBM/L2 streaming, reads + writes the matrix once (2 * bits/8 bytes).
+#pragma once
+#include "common.cuh"
+
+namespace skd {
+
+// All sizes in 32-bit words.  Loads outside [src_rows) x [src_words) read 0;
+// stores outside [dst_rows) x [dst_words) are dropped.
+__global__ void __launch_bounds__(256)
+k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                 u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words) {
+    __shared__ u32 tin[256][9];    // [src row in tile][word], +1 pad: conflict-free column reads
+    __shared__ u32 tout[256][9];   // [dst row in tile][word]
+    const int c0 = blockIdx.x * 256;          // first src row of the tile  (= dst bit offset)
+    const int w0 = blockIdx.y * 8;            // first src word of the tile (= dst row offset / 32)
+    const int t = threadIdx.x;
+    // load: 8 consecutive threads read 32 contiguous bytes of one src row
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        int rr = k * 32 + (t >> 3), ww = t & 7;
+        int gr = c0 + rr, gw = w0 + ww;
+        u32 v = 0;
+        if (gr < src_rows && gw < src_words) v = __ldcg(src + (size_t)gr * src_stride + gw);
+        tin[rr][ww] = v;
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    // 8 x 8 blocks of 32x32 bits; warp handles block-row `warp` (src rows 32*warp ..)
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) {
+        u32 v = tin[warp * 32 + lane][bj];    // src row (c0 + 32*warp + lane), bits 32*(w0+bj) ..
+        u32 mine = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            u32 vote = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+            if (lane == b) mine = vote;
+        }
+        // lane b holds dst row (32*(w0+bj) + b), word (c0/32 + warp)
+        tout[bj * 32 + lane][warp] = mine;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        int rr = k * 32 + (t >> 3), ww = t & 7;
+        int gr = w0 * 32 + rr, gw = (c0 >> 5) + ww;
+        if (gr < dst_rows && gw < dst_words) __stcg(dst + (size_t)gr * dst_stride + gw, tout[rr][ww]);
+    }
+}
+
+// sign bit-vector <-> one byte per row (host ABI); rowbit = map of tableau row index
+__global__ void k_signs_to_bytes(const u64* __restrict__ sgn, uint8_t* __restrict__ out, int nrows, int split, int NS) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int rb = (i < split) ? i : NS + (i - split);
+    out[i] = uint8_t((__ldcg(sgn + (rb >> 6)) >> (rb & 63)) & 1ull);
+}
+__global__ void k_bytes_to_signs(const uint8_t* __restrict__ in, u64* __restrict__ sgn, int nrows, int split, int NS) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int rb = (i < split) ? i : NS + (i - split);
+    if (in[i]) atomicOr(&sgn[rb >> 6], 1ull << (rb & 63));
+}
+
+// host row-major (nrows x W, separate x / z arrays) <-> device R form (stride 2*Wp, row-bit mapped)
+__global__ void k_pack_rows(const u64* __restrict__ hx, const u64* __restrict__ hz, u64* __restrict__ rows,
+                            int nrows, int W, int Wp, int split, int NS) {
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)nrows * W) return;
+    int i = int(idx / W), w = int(idx % W);
+    int rb = (i < split) ? i : NS + (i - split);
+    rows[(size_t)(2 * rb) * Wp + w] = hx[idx];
+    rows[(size_t)(2 * rb + 1) * Wp + w] = hz[idx];
+}
+__global__ void k_unpack_rows(const u64* __restrict__ rows, u64* __restrict__ hx, u64* __restrict__ hz,
+                              int nrows, int W, int Wp, int split, int NS) {
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)nrows * W) return;
+    int i = int(idx / W), w = int(idx % W);
+    int rb = (i < split) ? i : NS + (i - split);
+    hx[idx] = __ldcg(rows + (size_t)(2 * rb) * Wp + w);
+    hz[idx] = __ldcg(rows + (size_t)(2 * rb + 1) * Wp + w);
+}
+
+// identity tableau in both forms: stabilizer q = Z_q, destabilizer q = X_q
+__global__ void k_identity(u64* __restrict__ cols, u64* __restrict__ rows, int n, int RW, int Wp, int NS) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const u64 qb = 1ull << (q & 63);
+    // C: z column of qubit q has bit (row q); x column has bit (row NS+q)
+    cols[(size_t)(2 * q + 1) * RW + (q >> 6)] = qb;
+    cols[(size_t)(2 * q) * RW + ((NS + q) >> 6)] = 1ull << ((NS + q) & 63);
+    // R: row q has z bit q ; row NS+q has x bit q
+    rows[(size_t)(2 * q + 1) * Wp + (q >> 6)] = qb;
+    rows[(size_t)(2 * (NS + q)) * Wp + (q >> 6)] = qb;
+}
+
+}  // namespace skd

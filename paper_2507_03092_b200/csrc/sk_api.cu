@@ -1,0 +1,580 @@
+// sk_api.cu -- C ABI (include/stabkit_b200.h): context, tableau, engine.
+// Host orchestration only; all arithmetic is in the kernels_*.cuh files.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "kernels_layer.cuh"
+#include "kernels_measure.cuh"
+#include "kernels_transpose.cuh"
+#include "sk_internal.hpp"
+
+using namespace skd;
+
+// ------------------------------------------------------------------ context --
+extern "C" const char* sk_version(void) { return "stabkit-b200 0.1 (sm_100a)"; }
+
+extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
+    if (!out) return SK_EARG;
+    *out = nullptr;
+    static thread_local std::string s_err;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count <= 0 || device < 0 || device >= count) {
+        fprintf(stderr, "stabkit_b200: no usable CUDA device %d (%s); there is no CPU fallback\n", device,
+                e != cudaSuccess ? cudaGetErrorString(e) : "device ordinal out of range");
+        return SK_ECUDA;
+    }
+    sk_ctx* c = new (std::nothrow) sk_ctx();
+    if (!c) return SK_ECUDA;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; return SK_ECUDA; }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
+    c->num_sms = prop.multiProcessorCount;
+    c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
+    if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
+    else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return SK_ECUDA; }
+        c->own_stream = true;
+    }
+    if (cudaMalloc(&c->d_err, 256) != cudaSuccess) { delete c; return SK_ECUDA; }
+    cudaMemsetAsync(c->d_err, 0, 256, c->stream);
+    if (cudaMalloc(&c->d_ws, sizeof(MeasWs)) != cudaSuccess) { cudaFree(c->d_err); delete c; return SK_ECUDA; }
+    cudaMemsetAsync(c->d_ws, 0, sizeof(MeasWs), c->stream);
+    *out = c;
+    return SK_OK;
+}
+
+extern "C" void sk_ctx_destroy(sk_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_gates); cudaFree(c->d_tmp); cudaFree(c->d_err); cudaFree(c->d_ws);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+extern "C" const char* sk_last_error(const sk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+extern "C" void* sk_ctx_stream(const sk_ctx* c) { return c ? (void*)c->stream : nullptr; }
+extern "C" int32_t sk_ctx_sync(sk_ctx* c) {
+    if (!c) return SK_EARG;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+int32_t sk_ctx_reserve_gates(sk_ctx* c, size_t bytes) {
+    if (bytes <= c->d_gates_cap) return SK_OK;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_gates); c->d_gates = nullptr; c->d_gates_cap = 0;
+    size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+    SK_CUDA(c, cudaMalloc(&c->d_gates, cap));
+    c->d_gates_cap = cap;
+    return SK_OK;
+}
+int32_t sk_ctx_reserve_tmp(sk_ctx* c, size_t bytes) {
+    if (bytes <= c->d_tmp_cap) return SK_OK;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_tmp); c->d_tmp = nullptr; c->d_tmp_cap = 0;
+    size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+    SK_CUDA(c, cudaMalloc(&c->d_tmp, cap));
+    c->d_tmp_cap = cap;
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ tableau --
+struct sk_tableau {
+    sk_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    int W = 0, Wp = 0, RW = 0, NS = 0;
+    DMat m;
+    bool r_valid = false;           // C form is always valid; R form on demand
+    size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
+    u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
+    int meas_grid = 0; size_t meas_smem = 0;
+};
+
+static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int srows, int swords,
+                                u32* dst, size_t dstride, int drows, int dwords) {
+    dim3 grid((srows + 255) / 256, (swords + 7) / 8);
+    k_transpose_bits<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    return SK_OK;
+}
+// C -> R
+static int32_t rows_from_cols(sk_tableau* t) {
+    sk_ctx* c = t->ctx;
+    const u32* src = reinterpret_cast<const u32*>(t->m.cols);
+    u32* dst = reinterpret_cast<u32*>(t->m.rows);
+    for (int h = 0; h < 2; ++h) {
+        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * t->RW, (size_t)4 * t->RW, int(t->n), 2 * t->RW,
+                                      dst + (size_t)h * 2 * t->Wp, (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp);
+        if (rc) return rc;
+    }
+    c->cnt.transposes++;
+    t->r_valid = true;
+    return SK_OK;
+}
+// R -> C
+static int32_t cols_from_rows(sk_tableau* t) {
+    sk_ctx* c = t->ctx;
+    const u32* src = reinterpret_cast<const u32*>(t->m.rows);
+    u32* dst = reinterpret_cast<u32*>(t->m.cols);
+    for (int h = 0; h < 2; ++h) {
+        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * t->Wp, (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp,
+                                      dst + (size_t)h * 2 * t->RW, (size_t)4 * t->RW, int(t->n), 2 * t->RW);
+        if (rc) return rc;
+    }
+    c->cnt.transposes++;
+    return SK_OK;
+}
+
+static int32_t tableau_identity(sk_tableau* t) {
+    sk_ctx* c = t->ctx;
+    SK_CUDA(c, cudaMemsetAsync(t->m.cols, 0, t->cols_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->m.rows, 0, t->rows_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->m.sgn, 0, t->sgn_bytes, c->stream));
+    k_identity<<<(unsigned)((t->n + 255) / 256), 256, 0, c->stream>>>(t->m.cols, t->m.rows, int(t->n), t->RW, t->Wp, t->NS);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    t->r_valid = true;
+    return SK_OK;
+}
+
+extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
+    if (!c || !out) return SK_EARG;
+    *out = nullptr;
+    if (n == 0) SK_FAIL(c, SK_EDIM, "new_identity: n must be >= 1 (SPEC:129)");
+    if (n > (1u << 20)) SK_FAIL(c, SK_EDIM, "n=%llu exceeds the supported 2^20 qubits", (unsigned long long)n);
+    SK_CUDA(c, cudaSetDevice(c->device));
+    sk_tableau* t = new sk_tableau();
+    t->ctx = c; t->n = n;
+    t->W = int((n + 63) / 64); t->Wp = (t->W + 1) & ~1; t->RW = 2 * t->W; t->NS = 64 * t->W;
+    t->m.n = n; t->m.W = t->W; t->m.Wp = t->Wp; t->m.RW = t->RW;
+    t->cols_bytes = (size_t)n * 2 * t->RW * 8;
+    t->rows_bytes = (size_t)64 * t->RW * 2 * t->Wp * 8;
+    t->sgn_bytes = (size_t)t->RW * 8;
+    t->meas_smem = (size_t)(t->RW + 4 * t->Wp + kMeasWarps * 2 * t->Wp) * 8;
+    if (t->meas_smem > (size_t)c->max_smem_optin) {
+        size_t need = t->meas_smem; delete t;
+        SK_FAIL(c, SK_EDIM, "n=%llu needs %zu B of shared memory per CTA (limit %d)", (unsigned long long)n, need, c->max_smem_optin);
+    }
+    cudaError_t e1 = cudaMalloc(&t->m.cols, t->cols_bytes);
+    cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
+    cudaError_t e3 = cudaMalloc(&t->m.sgn, t->sgn_bytes);
+    if (e1 || e2 || e3) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
+    SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, c->max_smem_optin));
+    int per_sm = 0;
+    SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_measure_block, kMeasThreads, t->meas_smem));
+    if (per_sm < 1) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "measurement kernel does not fit on an SM"); }
+    t->meas_grid = c->num_sms;
+    int32_t rc = tableau_identity(t);
+    if (rc) { sk_tableau_destroy(t); return rc; }
+    *out = t;
+    return SK_OK;
+}
+
+extern "C" void sk_tableau_destroy(sk_tableau* t) {
+    if (!t) return;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn);
+    cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
+    delete t;
+}
+extern "C" int32_t sk_tableau_reset(sk_tableau* t) { return t ? tableau_identity(t) : SK_EARG; }
+extern "C" uint64_t sk_tableau_qubits(const sk_tableau* t) { return t ? t->n : 0; }
+
+extern "C" int32_t sk_tableau_upload(sk_tableau* t, const uint64_t* x, const uint64_t* z, const uint8_t* sign) {
+    if (!t || !x || !z || !sign) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    const size_t nrows = 2 * t->n, words = nrows * t->W;
+    int32_t rc = sk_ctx_reserve_tmp(c, words * 16 + nrows + 64);
+    if (rc) return rc;
+    u64* dx = (u64*)c->d_tmp; u64* dz = dx + words; uint8_t* ds = (uint8_t*)(dz + words);
+    SK_CUDA(c, cudaMemcpyAsync(dx, x, words * 8, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(dz, z, words * 8, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(ds, sign, nrows, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->m.rows, 0, t->rows_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->m.sgn, 0, t->sgn_bytes, c->stream));
+    k_pack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(dx, dz, t->m.rows, int(nrows), t->W, t->Wp, int(t->n), t->NS);
+    k_bytes_to_signs<<<(unsigned)((nrows + 255) / 256), 256, 0, c->stream>>>(ds, t->m.sgn, int(nrows), int(t->n), t->NS);
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    t->r_valid = true;
+    rc = cols_from_rows(t);
+    if (rc) return rc;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+static int32_t check_ws(sk_ctx* c) {
+    MeasWs* ws = (MeasWs*)c->d_ws;
+    MeasWs h;
+    SK_CUDA(c, cudaMemcpyAsync(&h, ws, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    u32 e2 = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&e2, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    if ((h.err & 0xC0000000u)) SK_FAIL(c, SK_ECUDA, "measurement kernel timed out (err=0x%x)", h.err);
+    if ((h.err & 1u) || (e2 & 1u)) {
+        cudaMemsetAsync(&ws->err, 0, 4, c->stream); cudaMemsetAsync(c->d_err, 0, 4, c->stream);
+        SK_FAIL(c, SK_EINVARIANT, "rowsum produced an odd mod-4 phase (SPEC:169)");
+    }
+    return SK_OK;
+}
+
+extern "C" int32_t sk_tableau_download(sk_tableau* t, uint64_t* x, uint64_t* z, uint8_t* sign) {
+    if (!t || !x || !z || !sign) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    const size_t nrows = 2 * t->n, words = nrows * t->W;
+    int32_t rc = sk_ctx_reserve_tmp(c, words * 16 + nrows + 64);
+    if (rc) return rc;
+    u64* dx = (u64*)c->d_tmp; u64* dz = dx + words; uint8_t* ds = (uint8_t*)(dz + words);
+    k_unpack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(t->m.rows, dx, dz, int(nrows), t->W, t->Wp, int(t->n), t->NS);
+    k_signs_to_bytes<<<(unsigned)((nrows + 255) / 256), 256, 0, c->stream>>>(t->m.sgn, ds, int(nrows), int(t->n), t->NS);
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaMemcpyAsync(x, dx, words * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(z, dz, words * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(sign, ds, nrows, cudaMemcpyDeviceToHost, c->stream));
+    return check_ws(c);
+}
+
+// ------------------------------------------------------------- gate layers --
+static int32_t validate_gate(sk_ctx* c, const sk_gate& g, uint64_t n, size_t idx) {
+    if (g.kind > SK_TDG) SK_FAIL(c, SK_EARG, "gate %zu: unknown kind %u", idx, g.kind);
+    if (g.q0 >= n) SK_FAIL(c, SK_EDIM, "gate %zu: qubit %u out of range for %llu qubits", idx, g.q0, (unsigned long long)n);
+    if (sk_is_two_qubit(g.kind)) {
+        if (g.q1 >= n) SK_FAIL(c, SK_EDIM, "gate %zu: qubit %u out of range for %llu qubits", idx, g.q1, (unsigned long long)n);
+        if (g.q0 == g.q1) SK_FAIL(c, SK_EARG, "gate %zu: two-qubit gate on identical qubits %u (SPEC:159)", idx, g.q0);
+    }
+    return SK_OK;
+}
+
+static void launch_layer(sk_tableau* t, const sk_gate* d_gates, int ngates) {
+    sk_ctx* c = t->ctx;
+    const int RW2 = t->RW / 2;
+    int threads = std::min(256, std::max(32, (RW2 + 31) & ~31));
+    int target_ctas = c->num_sms * std::max(1, 1536 / threads);
+    int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
+    int grid = (ngates + gpb - 1) / gpb;
+    k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb);
+    c->cnt.kernel_launches++; c->cnt.layers++;
+    t->r_valid = false;
+}
+
+extern "C" int32_t sk_apply_layer(sk_tableau* t, const sk_gate* gates, size_t ngates) {
+    if (!t || (!gates && ngates)) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (ngates == 0) return SK_OK;
+    if (c->q_epoch.size() < t->n) c->q_epoch.assign(t->n, 0);
+    if (++c->epoch == 0) { std::fill(c->q_epoch.begin(), c->q_epoch.end(), 0); c->epoch = 1; }
+    for (size_t i = 0; i < ngates; ++i) {
+        int32_t rc = validate_gate(c, gates[i], t->n, i);
+        if (rc) return rc;
+        if (gates[i].kind >= SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: M/T/TDG cannot be part of a Clifford layer (SPEC:191)", i);
+        uint32_t qs[2] = {gates[i].q0, gates[i].q1};
+        for (int k = 0; k < (sk_is_two_qubit(gates[i].kind) ? 2 : 1); ++k) {
+            if (c->q_epoch[qs[k]] == c->epoch) SK_FAIL(c, SK_EARG, "gate %zu: qubit %u used twice in one layer (SPEC:263)", i, qs[k]);
+            c->q_epoch[qs[k]] = c->epoch;
+        }
+        c->cnt.gate_hist[gates[i].kind]++;
+    }
+    int32_t rc = sk_ctx_reserve_gates(c, ngates * sizeof(sk_gate));
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemcpyAsync(c->d_gates, gates, ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+    launch_layer(t, (const sk_gate*)c->d_gates, int(ngates));
+    SK_CUDA(c, cudaGetLastError());
+    // the staging buffer is reused by the next call
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+void sk_layer_run(const sk_gate* g, size_t ng, uint64_t n, std::vector<uint32_t>& level,
+                  std::vector<sk_gate>& out, std::vector<uint32_t>& layer_sizes) {
+    if (level.size() < n) level.assign(n, 0);
+    std::vector<uint32_t> lay(ng);
+    uint32_t depth = 0;
+    for (size_t i = 0; i < ng; ++i) {
+        uint32_t l = level[g[i].q0];
+        if (sk_is_two_qubit(g[i].kind)) l = std::max(l, level[g[i].q1]);
+        lay[i] = l;
+        level[g[i].q0] = l + 1;
+        if (sk_is_two_qubit(g[i].kind)) level[g[i].q1] = l + 1;
+        depth = std::max(depth, l + 1);
+    }
+    for (size_t i = 0; i < ng; ++i) { level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) level[g[i].q1] = 0; }
+    std::vector<uint32_t> start(depth + 1, 0);
+    for (size_t i = 0; i < ng; ++i) start[lay[i] + 1]++;
+    for (uint32_t d = 0; d < depth; ++d) { layer_sizes.push_back(start[d + 1]); start[d + 1] += start[d]; }
+    size_t base = out.size();
+    out.resize(base + ng);
+    for (size_t i = 0; i < ng; ++i) out[base + start[lay[i]]++] = g[i];
+}
+
+extern "C" int32_t sk_apply_gates(sk_tableau* t, const sk_gate* gates, size_t ngates) {
+    if (!t || (!gates && ngates)) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (ngates == 0) return SK_OK;
+    for (size_t i = 0; i < ngates; ++i) {
+        int32_t rc = validate_gate(c, gates[i], t->n, i);
+        if (rc) return rc;
+        if (gates[i].kind >= SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: M/T/TDG in a Clifford sequence (SPEC:191)", i);
+        c->cnt.gate_hist[gates[i].kind]++;
+    }
+    std::vector<sk_gate> ordered; std::vector<uint32_t> sizes, scratch;
+    sk_layer_run(gates, ngates, t->n, scratch, ordered, sizes);
+    int32_t rc = sk_ctx_reserve_gates(c, ngates * sizeof(sk_gate));
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemcpyAsync(c->d_gates, ordered.data(), ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+    size_t off = 0;
+    for (uint32_t s : sizes) { launch_layer(t, (const sk_gate*)c->d_gates + off, int(s)); off += s; }
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+// ------------------------------------------------------------ measurement --
+static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uint64_t seed, uint64_t ordinal0,
+                              uint8_t* d_out, uint8_t* d_det) {
+    sk_ctx* c = t->ctx;
+    if (count <= 0) return SK_OK;
+    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    // reset barrier counter and the three wave slots (counters persist)
+    MeasWs* ws = (MeasWs*)c->d_ws;
+    SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->first[0], 0xFF, 24, c->stream));
+    MeasArgs a;
+    a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
+    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws;
+    void* args[] = {&a};
+    SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
+    c->cnt.kernel_launches++;
+    return SK_OK;
+}
+
+static int32_t reserve_record(sk_tableau* t, size_t m) {
+    sk_ctx* c = t->ctx;
+    if (m <= t->rec_cap) return SK_OK;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
+    t->d_q = nullptr; t->d_out = nullptr; t->d_det = nullptr; t->rec_cap = 0;
+    size_t cap = std::max<size_t>(m * 2, 1024);
+    SK_CUDA(c, cudaMalloc(&t->d_q, cap * 4));
+    SK_CUDA(c, cudaMalloc(&t->d_out, cap));
+    SK_CUDA(c, cudaMalloc(&t->d_det, cap));
+    t->rec_cap = cap;
+    return SK_OK;
+}
+
+extern "C" int32_t sk_measure_batch(sk_tableau* t, const uint32_t* qubits, size_t m, uint64_t seed,
+                                    uint64_t ordinal0, uint8_t* outcomes, uint8_t* deterministic) {
+    if (!t || (!qubits && m) || !outcomes || !deterministic) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (m == 0) return SK_OK;
+    for (size_t i = 0; i < m; ++i)
+        if (qubits[i] >= t->n) SK_FAIL(c, SK_EDIM, "measure: qubit %u out of range for %llu qubits", qubits[i], (unsigned long long)t->n);
+    int32_t rc = reserve_record(t, m);
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemcpyAsync(t->d_q, qubits, m * 4, cudaMemcpyHostToDevice, c->stream));
+    rc = launch_measure(t, t->d_q, int(m), seed, ordinal0, t->d_out, t->d_det);
+    if (rc) return rc;
+    c->cnt.gate_hist[SK_M] += m;
+    SK_CUDA(c, cudaMemcpyAsync(outcomes, t->d_out, m, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(deterministic, t->d_det, m, cudaMemcpyDeviceToHost, c->stream));
+    return check_ws(c);
+}
+
+extern "C" int32_t sk_measure_z(sk_tableau* t, uint32_t q, uint64_t seed, uint64_t ordinal,
+                                uint8_t* outcome, uint8_t* deterministic) {
+    return sk_measure_batch(t, &q, 1, seed, ordinal, outcome, deterministic);
+}
+
+extern "C" int32_t sk_tableau_rowsum(sk_tableau* t, uint64_t h, uint64_t i) {
+    if (!t) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (h >= 2 * t->n || i >= 2 * t->n || h == i) SK_FAIL(c, SK_EDIM, "rowsum(%llu,%llu): rows must differ and be < 2n (SPEC:167)", (unsigned long long)h, (unsigned long long)i);
+    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    int hb = h < t->n ? int(h) : t->NS + int(h - t->n);
+    int ib = i < t->n ? int(i) : t->NS + int(i - t->n);
+    k_rowsum_single<<<1, 256, 0, c->stream>>>(t->m, hb, ib, c->d_err);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    return check_ws(c);
+}
+
+// ---------------------------------------------------------------- counters --
+extern "C" int32_t sk_reset_counters(sk_ctx* c) {
+    if (!c) return SK_EARG;
+    c->cnt = sk_counters{};
+    MeasWs* ws = (MeasWs*)c->d_ws;
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 5 * 8, c->stream));
+    return SK_OK;
+}
+extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
+    if (!c || !out) return SK_EARG;
+    MeasWs h;
+    SK_CUDA(c, cudaMemcpyAsync(&h, c->d_ws, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    *out = c->cnt;
+    out->n_rand = h.n_rand; out->n_det = h.n_det; out->k_rand = h.k_rand; out->k_det = h.k_det; out->waves = h.waves;
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ engine --
+struct ProgOp { uint8_t type; uint32_t off, count; };   // 0 = layer, 1 = measurement block
+struct sk_program {
+    sk_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    std::vector<ProgOp> ops;
+    sk_gate* d_gates = nullptr; size_t ngates = 0;
+    u32* d_mq = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t nmeas = 0;
+    uint64_t hist[12] = {0};
+    sk_tableau* last_t = nullptr;
+};
+
+extern "C" void sk_program_destroy(sk_program* p) {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    cudaFree(p->d_gates); cudaFree(p->d_mq); cudaFree(p->d_out); cudaFree(p->d_det);
+    delete p;
+}
+extern "C" uint64_t sk_program_measurements(const sk_program* p) { return p ? p->nmeas : 0; }
+
+extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates,
+                                     const uint32_t* marks, size_t nmarks, int mode,
+                                     sk_program** out, uint32_t* warnings) {
+    if (!c || !out || (!gates && ngates) || (!marks && nmarks)) return SK_EARG;
+    *out = nullptr;
+    if (warnings) *warnings = 0;
+    if (n == 0) SK_FAIL(c, SK_EDIM, "circuit has zero qubits");
+    for (size_t i = 0; i < ngates; ++i) {
+        int32_t rc = validate_gate(c, gates[i], n, i);
+        if (rc) return rc;
+        if (gates[i].kind == SK_T || gates[i].kind == SK_TDG)
+            SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
+    }
+    for (size_t k = 0; k < nmarks; ++k)
+        if (marks[k] >= ngates || (k && marks[k] <= marks[k - 1])) SK_FAIL(c, SK_EARG, "chunk_marks must be strictly increasing and < gate count (SPEC:238)");
+
+    sk_program* p = new sk_program();
+    p->ctx = c; p->n = n;
+    std::vector<sk_gate> ordered; ordered.reserve(ngates);
+    std::vector<uint32_t> mq; std::vector<uint32_t> scratch, sizes;
+    uint32_t warn = 0;
+
+    auto emit_sequential = [&](size_t lo, size_t hi) {      // sim semantics on gates [lo, hi)
+        size_t i = lo;
+        while (i < hi) {
+            if (gates[i].kind == SK_M) {
+                size_t j = i;
+                while (j < hi && gates[j].kind == SK_M) { mq.push_back(gates[j].q0); ++j; }
+                if (!p->ops.empty() && p->ops.back().type == 1) p->ops.back().count += uint32_t(j - i);
+                else p->ops.push_back({1, uint32_t(mq.size() - (j - i)), uint32_t(j - i)});
+                i = j; continue;
+            }
+            size_t j = i;
+            while (j < hi && gates[j].kind != SK_M) ++j;
+            sizes.clear();
+            size_t base = ordered.size();
+            sk_layer_run(gates + i, j - i, n, scratch, ordered, sizes);
+            for (uint32_t s : sizes) { p->ops.push_back({0, uint32_t(base), s}); base += s; }
+            i = j;
+        }
+    };
+    if (mode == 0 || nmarks == 0) {
+        emit_sequential(0, ngates);
+    } else {
+        if (c->q_epoch.size() < n) c->q_epoch.assign(n, 0);
+        size_t lo = 0;
+        for (size_t k = 0; k <= nmarks; ++k) {
+            size_t hi = (k < nmarks) ? marks[k] : ngates;
+            if (hi == lo) continue;
+            if (++c->epoch == 0) { std::fill(c->q_epoch.begin(), c->q_epoch.end(), 0); c->epoch = 1; }
+            bool ok = true;
+            for (size_t i = lo; i < hi && ok; ++i) {
+                if (gates[i].kind == SK_M) { ok = false; break; }
+                uint32_t qs[2] = {gates[i].q0, gates[i].q1};
+                for (int e = 0; e < (sk_is_two_qubit(gates[i].kind) ? 2 : 1); ++e) {
+                    if (c->q_epoch[qs[e]] == c->epoch) ok = false;
+                    c->q_epoch[qs[e]] = c->epoch;
+                }
+            }
+            if (ok) {                                     // validated chunk == one fused layer
+                p->ops.push_back({0, uint32_t(ordered.size()), uint32_t(hi - lo)});
+                ordered.insert(ordered.end(), gates + lo, gates + hi);
+            } else {                                      // SPEC:324 fall back to sequential
+                bool only_m = true;
+                for (size_t i = lo; i < hi; ++i) only_m = only_m && gates[i].kind == SK_M;
+                if (!only_m) warn |= 1u;
+                emit_sequential(lo, hi);
+            }
+            lo = hi;
+        }
+    }
+    for (size_t i = 0; i < ngates; ++i) p->hist[gates[i].kind]++;
+    p->ngates = ordered.size(); p->nmeas = mq.size();
+    cudaError_t e = cudaSuccess;
+    if (p->ngates) { e = cudaMalloc(&p->d_gates, p->ngates * sizeof(sk_gate)); }
+    if (!e && p->nmeas) { e = cudaMalloc(&p->d_mq, p->nmeas * 4); if (!e) e = cudaMalloc(&p->d_out, p->nmeas); if (!e) e = cudaMalloc(&p->d_det, p->nmeas); }
+    if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
+    if (p->ngates) e = cudaMemcpyAsync(p->d_gates, ordered.data(), p->ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
+    if (!e && p->nmeas) e = cudaMemcpyAsync(p->d_mq, mq.data(), p->nmeas * 4, cudaMemcpyHostToDevice, c->stream);
+    if (!e) e = cudaStreamSynchronize(c->stream);     // host vectors die at return
+    if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "program upload failed: %s", cudaGetErrorString(e)); }
+    if (warnings) *warnings = warn;
+    *out = p;
+    return SK_OK;
+}
+
+extern "C" int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed) {
+    if (!p || !t) return SK_EARG;
+    sk_ctx* c = p->ctx;
+    if (t->ctx != c) SK_FAIL(c, SK_EARG, "program and tableau belong to different contexts");
+    if (t->n != p->n) SK_FAIL(c, SK_EDIM, "program is for %llu qubits, tableau has %llu", (unsigned long long)p->n, (unsigned long long)t->n);
+    for (const ProgOp& op : p->ops) {
+        if (op.type == 0) {
+            launch_layer(t, p->d_gates + op.off, int(op.count));
+        } else {
+            int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
+            if (rc) return rc;
+        }
+    }
+    SK_CUDA(c, cudaGetLastError());
+    for (int k = 0; k < 12; ++k) c->cnt.gate_hist[k] += p->hist[k];
+    p->last_t = t;
+    return SK_OK;
+}
+
+extern "C" int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic) {
+    if (!p) return SK_EARG;
+    sk_ctx* c = p->ctx;
+    if (p->nmeas) {
+        if (!outcomes || !deterministic) return SK_EARG;
+        SK_CUDA(c, cudaMemcpyAsync(outcomes, p->d_out, p->nmeas, cudaMemcpyDeviceToHost, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(deterministic, p->d_det, p->nmeas, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (p->last_t) return check_ws(c);
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+extern "C" int32_t sk_sim(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates,
+                          const uint32_t* marks, size_t nmarks, int mode, uint64_t seed,
+                          sk_tableau** out_t, uint8_t* outcomes, uint8_t* deterministic, uint32_t* warnings) {
+    if (!c || !out_t) return SK_EARG;
+    *out_t = nullptr;
+    sk_program* p = nullptr; sk_tableau* t = nullptr;
+    int32_t rc = sk_program_create(c, n, gates, ngates, marks, nmarks, mode, &p, warnings);
+    if (rc) return rc;
+    rc = sk_tableau_create(c, n, &t);
+    if (!rc) rc = sk_program_run(p, t, seed);
+    if (!rc) rc = sk_program_read_record(p, outcomes, deterministic);
+    sk_program_destroy(p);
+    if (rc) { sk_tableau_destroy(t); return rc; }
+    *out_t = t;
+    return SK_OK;
+}

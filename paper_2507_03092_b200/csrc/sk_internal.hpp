@@ -1,0 +1,51 @@
+// sk_internal.hpp -- host-side internals shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "stabkit_b200.h"
+
+struct sk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 0;
+    int max_smem_optin = 0;
+    std::string err;
+    // growable device scratch
+    void* d_gates = nullptr; size_t d_gates_cap = 0;
+    void* d_tmp = nullptr; size_t d_tmp_cap = 0;
+    skd::u32* d_err = nullptr;              // generic error word for small kernels
+    void* d_ws = nullptr;                   // skd::MeasWs: barrier, wave slots, device-side counters
+    // host-side counters (device-side ones live in MeasWs)
+    sk_counters cnt{};
+    std::vector<uint32_t> q_epoch; uint32_t epoch = 0;   // qubit-collision scratch
+};
+
+#define SK_FAIL(ctx, code, ...)                                   \
+    do {                                                          \
+        char _b[512]; snprintf(_b, sizeof _b, __VA_ARGS__);       \
+        (ctx)->err = _b; return (code);                           \
+    } while (0)
+
+#define SK_CUDA(ctx, call)                                                                 \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess) SK_FAIL(ctx, SK_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+
+int32_t sk_ctx_reserve_gates(sk_ctx* ctx, size_t bytes);
+int32_t sk_ctx_reserve_tmp(sk_ctx* ctx, size_t bytes);
+
+// layering of an ordered Clifford run into layers of disjoint qubits (order per
+// qubit preserved => same tableau as gate-by-gate application).  Appends the
+// re-ordered gates to `out` and the layer sizes to `layer_sizes`.
+void sk_layer_run(const sk_gate* g, size_t ng, uint64_t n, std::vector<uint32_t>& scratch,
+                  std::vector<sk_gate>& out, std::vector<uint32_t>& layer_sizes);
+
+static inline bool sk_is_two_qubit(uint8_t k) { return k == SK_CX || k == SK_CZ || k == SK_SWAP; }
