@@ -88,7 +88,7 @@ __device__ __forceinline__ bool grid_barrier(u32* bar, u32& epoch, u32* err) {
         u32 ok = 1;
         unsigned long long spins = 0;
         while (int(ld_acquire(bar) - epoch) < 0) {
-            if (++spins > (1ull << 26)) { ok = 0; atomicExch(err, 0x80000000u); break; }
+            if (++spins > (1ull << 24)) { ok = 0; atomicExch(err, 0x80000000u); break; }
         }
         __threadfence();
         s_ok = ok;
@@ -113,7 +113,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
 // returns false on timeout
 __device__ __forceinline__ bool mbar_wait(u64* bar, u32 parity) {
     u32 done = 0;
-    for (u32 it = 0; it < (1u << 24); ++it) {
+    for (u32 it = 0; it < (1u << 20); ++it) {
         asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                      : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
         if (done) return true;

@@ -1,0 +1,221 @@
+// kernels_rows.cuh -- K5..K9: kernels over row-major (R form) sets of signed Pauli rows:
+// commutation vectors / conflict bitmaps (popcount parity, ref: proj/src/pauli.cpp:117-140,
+// 215-237), rowsum+i push-through (pauli.cpp:239-254), duplicate detection (same_axis,
+// pauli.cpp:142-144), Pauli weight (pauli.cpp:100-106) and the first-fit resolver used by
+// group_greedy and t_separate (Algorithm 3).
+// R form: rows[(2*r + h) * Wp + w], h = 0 x / 1 z; signs are a bit-vector sgn[r>>6] bit r&63.
+#pragma once
+#include "common.cuh"
+
+namespace skd {
+
+// ---- predicates -------------------------------------------------------------
+// mode 0 (GC): conflict = anticommute = parity of popc((ax&bz)^(bx&az))      (pauli.cpp:117-127)
+// mode 1 (QWC): conflict = any word of (ax&bz)^(bx&az) non-zero               (pauli.cpp:129-140)
+__device__ __forceinline__ bool conflict_words(const u64* ax, const u64* az, const u64* bx, const u64* bz, int W, int mode) {
+    u64 acc = 0; int par = 0;
+    for (int w = 0; w < W; ++w) {
+        u64 v = (ax[w] & bz[w]) ^ (bx[w] & az[w]);
+        acc |= v; par ^= __popcll(v);
+    }
+    return mode ? (acc != 0) : (par & 1);
+}
+
+// K5 vector form: bit i of out = p anticommutes with row i.  One warp per row.
+__global__ void __launch_bounds__(256)
+k_commutation_vector(const u64* __restrict__ rows, int Wp, int W, int nrows,
+                     const u64* __restrict__ p /* x[Wp] z[Wp] */, u64* __restrict__ out_bits) {
+    const int lane = threadIdx.x & 31;
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (row >= nrows) return;
+    const u64* rx = rows + (size_t)(2 * row) * Wp; const u64* rz = rx + Wp;
+    int par = 0;
+    for (int w = lane; w < W; w += 32) par ^= __popcll((p[w] & rz[w]) ^ (rx[w] & p[Wp + w]));
+    par = warp_sum(par) & 1;
+    if (lane == 0 && par) atomicOr(&out_bits[row >> 6], 1ull << (row & 63));
+}
+
+// K7: rowsum_plus_i on every live row that anticommutes with the pushed rotations, applied IN ORDER.
+// pushes: npush entries of (x[Wp] z[Wp]) ; psign[q] ; plevel[q] = source layer of push q (sorted
+// descending).  Row r (layer lvl[r], or lvl == INT_MAX for M_tab rows) takes only pushes with
+// plevel < lvl[r]; rows with lvl < 0 are dead.  One warp per row; row words stay in registers.
+template <int WPL>   // words per lane: W <= 32*WPL
+__global__ void __launch_bounds__(256)
+k_push_through(u64* __restrict__ rows, u64* __restrict__ sgn, int Wp, int W, int row0, int nrows,
+               const int* __restrict__ lvl, const u64* __restrict__ pushes, const uint8_t* __restrict__ psign,
+               const int* __restrict__ plevel, int npush, u32* __restrict__ err, unsigned long long* __restrict__ n_updated) {
+    const int lane = threadIdx.x & 31;
+    const int r = row0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= row0 + nrows) return;
+    const int my = lvl ? lvl[r - row0] : 0x7fffffff;
+    if (my < 0) return;
+    u64* rx = rows + (size_t)(2 * r) * Wp; u64* rz = rx + Wp;
+    u64 x[WPL], z[WPL];
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) { int w = lane + 32 * k; x[k] = (w < W) ? rx[w] : 0; z[k] = (w < W) ? rz[w] : 0; }
+    int sign = int((sgn[r >> 6] >> (r & 63)) & 1ull);
+    const int sign0 = sign;
+    bool dirty = false; unsigned long long upd = 0;
+    for (int q = 0; q < npush; ++q) {
+        if (plevel && plevel[q] >= my) continue;
+        const u64* px = pushes + (size_t)q * 2 * Wp; const u64* pz = px + Wp;
+        int par = 0, g = 0;
+        u64 qx[WPL], qz[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            int w = lane + 32 * k;
+            qx[k] = (w < W) ? px[w] : 0; qz[k] = (w < W) ? pz[w] : 0;
+            par ^= __popcll((qx[k] & z[k]) ^ (x[k] & qz[k]));
+        }
+        par = warp_sum(par) & 1;
+        if (!par) continue;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) { g += g_word(qx[k], qz[k], x[k], z[k]); x[k] ^= qx[k]; z[k] ^= qz[k]; }
+        g = warp_sum(g);
+        const int sum = (2 * sign + 2 * int(psign[q]) + g + 1) & 3;     // pauli.cpp:240
+        if (sum & 1) { if (lane == 0) atomicOr(err, 1u); }
+        sign = sum >> 1;
+        dirty = true; ++upd;
+    }
+    if (dirty) {
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) { int w = lane + 32 * k; if (w < W) { rx[w] = x[k]; rz[w] = z[k]; } }
+        if (lane == 0) {
+            if (sign != sign0) atomicXor(&sgn[r >> 6], 1ull << (r & 63));
+            if (n_updated) atomicAdd(n_updated, upd);
+        }
+    }
+}
+
+// K9: sum of popcount(x|z) over rows [0, nrows)
+__global__ void __launch_bounds__(256)
+k_weight_sum(const u64* __restrict__ rows, int Wp, int W, int nrows, const int* __restrict__ lvl, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    const size_t total = (size_t)nrows * W;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int r = int(i / W), w = int(i % W);
+        if (lvl && lvl[r] < 0) continue;
+        acc += __popcll(rows[(size_t)(2 * r) * Wp + w] | rows[(size_t)(2 * r + 1) * Wp + w]);
+    }
+    int lo = warp_sum(int(acc & 0x7fffffff)), hi = warp_sum(int(acc >> 31));
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)lo + ((unsigned long long)hi << 31));
+}
+
+// K8a: 64-bit content hash of (x,z) per row; one warp per row.
+__global__ void __launch_bounds__(256)
+k_row_hash(const u64* __restrict__ rows, int Wp, int W, int nrows, u64* __restrict__ hash) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= nrows) return;
+    const u64* rx = rows + (size_t)(2 * r) * Wp; const u64* rz = rx + Wp;
+    u64 h = 0;
+    for (int w = lane; w < W; w += 32) h ^= splitmix64(rx[w] + 0x9e3779b97f4a7c15ULL * (2 * w + 1)) ^ splitmix64(~rz[w] + 0xc2b2ae3d27d4eb4fULL * (2 * w + 2));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) hash[r] = h;
+}
+// K8b: for row j: rank = number of earlier live rows in the same layer with identical (x,z);
+// pred = the latest such row.  Odd rank => (pred, j) is a duplicate pair in scan order.
+// Thread per row j; all lanes sweep the same i, so hash[i]/lvl[i] loads are broadcasts.
+__global__ void __launch_bounds__(256)
+k_dup_rank(const u64* __restrict__ rows, int Wp, int W, int nrows, const u64* __restrict__ hash,
+           const int* __restrict__ lvl, int* __restrict__ pair_first /* [nrows], -1 if none */) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jmax = min(nrows, (int)((blockIdx.x + 1) * blockDim.x));
+    const bool live = j < nrows && (!lvl || lvl[j] >= 0);
+    const u64 hj = live ? hash[j] : 0; const int lj = (live && lvl) ? lvl[j] : 0;
+    int rank = 0, pred = -1;
+    for (int i = 0; i < jmax; ++i) {
+        if (!live || i >= j) continue;
+        if (hash[i] != hj) continue;
+        if (lvl && lvl[i] != lj) continue;
+        const u64* a = rows + (size_t)(2 * i) * Wp; const u64* b = rows + (size_t)(2 * j) * Wp;
+        bool eq = true;
+        for (int w = 0; w < W && eq; ++w) eq = (a[w] == b[w]) && (a[Wp + w] == b[Wp + w]);
+        if (eq) { ++rank; pred = i; }
+    }
+    if (j < nrows) pair_first[j] = (live && (rank & 1)) ? pred : -1;
+}
+
+// K5 matrix form for first-fit: block terms [t0, t0+B) against every earlier term m < t0.
+// bitmap[(t - t0) * GW32 + (g >> 5)] bit (g & 31) = term t conflicts with a member of group g.
+// Thread per earlier term m (coalesced load of its words + group id), block terms broadcast from smem.
+__global__ void __launch_bounds__(256)
+k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, const u32* __restrict__ group_of,
+                  int mode, u32* __restrict__ bitmap, int GW32) {
+    extern __shared__ u64 s_blk[];          // [Bt][2*W]
+    const int Bt = blockDim.y;              // block terms staged per CTA row (gridDim.y tiles B)
+    const int tb = t0 + blockIdx.y * Bt;
+    for (int i = threadIdx.x; i < Bt * 2 * W; i += blockDim.x) {
+        int k = i / (2 * W), w = i % (2 * W);
+        int t = tb + k;
+        s_blk[i] = (t < t0 + B) ? rows[(size_t)(2 * t + (w >= W)) * Wp + (w % W)] : 0;
+    }
+    __syncthreads();
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= t0) return;
+    const u64* mx = rows + (size_t)(2 * m) * Wp; const u64* mz = mx + Wp;
+    const u32 g = group_of[m];
+    for (int k = 0; k < Bt && tb + k < t0 + B; ++k) {
+        const u64* bx = s_blk + (size_t)k * 2 * W; const u64* bz = bx + W;
+        if (conflict_words(bx, bz, mx, mz, W, mode)) {
+            u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + (g >> 5);
+            const u32 bit = 1u << (g & 31);
+            if (!(__ldcg(word) & bit)) atomicOr(word, bit);
+        }
+    }
+}
+
+// First-fit resolver for one block (single CTA, sequential over the block's terms):
+// term t takes the first group whose bit is clear; later block-mates that conflict with t get that bit set.
+__global__ void __launch_bounds__(1024)
+k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode,
+                  u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io) {
+    __shared__ u32 s_first;
+    __shared__ u32 s_ng;
+    if (threadIdx.x == 0) s_ng = *ngroups_io;
+    __syncthreads();
+    for (int k = 0; k < B; ++k) {
+        const int t = t0 + k;
+        if (threadIdx.x == 0) s_first = 0xffffffffu;
+        __syncthreads();
+        const u32 ng = s_ng;
+        const u32* bm = bitmap + (size_t)k * GW32;
+        // groups >= ng are free by construction; scan words covering [0, ng]
+        const int words = int(ng >> 5) + 1;
+        for (int w = threadIdx.x; w < words; w += blockDim.x) {
+            u32 freeb = ~bm[w];
+            if (freeb) { atomicMin(&s_first, u32(w * 32 + __ffs(freeb) - 1)); break; }
+        }
+        __syncthreads();
+        const u32 g = min(s_first, ng);             // first free existing group, else a new one
+        if (threadIdx.x == 0) { group_of[t] = g; if (g == ng) s_ng = ng + 1; }
+        // propagate to later block-mates
+        const u64* tx = rows + (size_t)(2 * t) * Wp; const u64* tz = tx + Wp;
+        for (int k2 = k + 1 + threadIdx.x; k2 < B; k2 += blockDim.x) {
+            const u64* ox = rows + (size_t)(2 * (t0 + k2)) * Wp; const u64* oz = ox + Wp;
+            if (conflict_words(ox, oz, tx, tz, W, mode)) bitmap[(size_t)k2 * GW32 + (g >> 5)] |= 1u << (g & 31);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *ngroups_io = s_ng;
+}
+
+// verify_grouping: number of intra-group pairs violating the predicate.
+// Thread per row j sweeps all i < j (broadcast loads of group ids).
+__global__ void __launch_bounds__(256)
+k_verify_grouping(const u64* __restrict__ rows, int Wp, int W, int nrows, const u32* __restrict__ group_of,
+                  int mode, unsigned long long* __restrict__ nviol) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jmax = min(nrows, (int)((blockIdx.x + 1) * blockDim.x));
+    const u32 gj = j < nrows ? group_of[j] : 0xffffffffu;
+    unsigned long long bad = 0;
+    for (int i = 0; i < jmax; ++i) {
+        if (j >= nrows || i >= j || group_of[i] != gj) continue;
+        const u64* a = rows + (size_t)(2 * i) * Wp; const u64* b = rows + (size_t)(2 * j) * Wp;
+        bad += conflict_words(a, a + Wp, b, b + Wp, W, mode);
+    }
+    if (bad) atomicAdd(nviol, bad);
+}
+
+}  // namespace skd

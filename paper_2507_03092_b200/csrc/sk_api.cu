@@ -156,7 +156,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     t->rows_bytes = (size_t)64 * t->RW * 2 * t->Wp * 8;
     t->sgn_bytes = (size_t)t->RW * 8;
     t->meas_smem = (size_t)(t->RW + 4 * t->Wp + kMeasWarps * 2 * t->Wp) * 8;
-    if (t->meas_smem > (size_t)c->max_smem_optin) {
+    if (t->meas_smem + 1024 > (size_t)c->max_smem_optin) {
         size_t need = t->meas_smem; delete t;
         SK_FAIL(c, SK_EDIM, "n=%llu needs %zu B of shared memory per CTA (limit %d)", (unsigned long long)n, need, c->max_smem_optin);
     }
@@ -164,7 +164,10 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
     cudaError_t e3 = cudaMalloc(&t->m.sgn, t->sgn_bytes);
     if (e1 || e2 || e3) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
-    SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, c->max_smem_optin));
+    if ((int)t->meas_smem > c->meas_smem_attr) {
+        SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
+        c->meas_smem_attr = (int)t->meas_smem;
+    }
     int per_sm = 0;
     SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_measure_block, kMeasThreads, t->meas_smem));
     if (per_sm < 1) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "measurement kernel does not fit on an SM"); }

@@ -1,0 +1,104 @@
+"""CPU-only checks of the product's host logic and of the C-ABI surface (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol(sk):
+    hdr = open(os.path.join(ROOT, "include", "stabkit_b200.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    declared = sorted(set(re.findall(r"\b(sk_[a-z0-9_]+)\s*\(", hdr)))
+    assert len(declared) >= 45
+    L = C.CDLL(sk.LIB_PATH)
+    missing = [s for s in declared if not hasattr(L, s)]
+    assert not missing, missing
+    assert sorted(sk.EXPORTS) == declared
+
+
+def test_no_cpu_fallback_without_device(sk):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(sk.CudaError):
+        sk.Context(0)
+
+
+def test_product_does_not_touch_the_oracle():
+    bad = []
+    for base, _, files in os.walk(os.path.join(ROOT, "paper_2507_03092_b200")):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
+                txt = open(os.path.join(base, f), errors="ignore").read()
+                if re.search(r"oracle_py|liboracle|stab_oracle|from oracle|import oracle|oracle/", txt):
+                    bad.append(f)
+    for f in os.listdir(os.path.join(ROOT, "include", "stabkit")) if os.path.isdir(os.path.join(ROOT, "include", "stabkit")) else []:
+        txt = open(os.path.join(ROOT, "include", "stabkit", f)).read()
+        if re.search(r"liboracle|stab_oracle|oracle/", txt):
+            bad.append(f)
+    assert not bad, bad
+
+
+def test_surface_code_generator(sk):                # SPEC:375-383, 397; SURVEY 8 config sizes
+    c = sk.surface_code_circuit(3, 1)
+    assert (c.n, c.num_measurements) == (17, 8)
+    assert sk.surface_code_circuit(3, 2).num_measurements == 16
+    with pytest.raises(sk.StabkitError):
+        sk.surface_code_circuit(2, 1)
+    with pytest.raises(sk.StabkitError):
+        sk.surface_code_circuit(3, 0)
+    for d, nH, nCX, nM in ((25, 15600, 60000, 15600 + 625), (71, 357840, 1411480, 357840 + 5041)):
+        c = sk.surface_code_circuit(d, d, True)
+        k = c.gates["kind"]
+        assert c.n == 2 * d * d - 1
+        assert ((k == sk.H).sum(), (k == sk.CX).sum(), (k == sk.M).sum()) == (nH, nCX, nM)
+    c = sk.surface_code_circuit(5, 2)
+    v = sk.validate_chunks(c)
+    assert v and all(kind == "measurement" for _, _, kind in v)       # no collisions in any emitted chunk
+    # every ancilla has 2 or 4 neighbours; X and Z checks each (d^2-1)/2
+    deg = {}
+    for g in sk.surface_code_circuit(5, 1).gates:
+        if g["kind"] == sk.CX:
+            a = int(max(g["q0"], g["q1"])); deg[a] = deg.get(a, 0) + 1
+    assert len(deg) == 24 and set(deg.values()) == {2, 4}
+
+
+def test_random_layered_generator(sk):
+    c = sk.random_layered_circuit(8, 1)
+    k = c.gates["kind"]
+    assert len(c.gates) == 3 * (4 + 4 + 1) and (k == sk.M).sum() == 3 and (k == sk.CX).sum() == 12
+    a, b = sk.random_layered_circuit(4, 9), sk.random_layered_circuit(4, 9)
+    assert (a.gates == b.gates).all()
+    with pytest.raises(sk.StabkitError):
+        sk.random_layered_circuit(7, 1)
+    c = sk.random_layered_circuit(64, 3)
+    assert all(kind == "measurement" for _, _, kind in sk.validate_chunks(c))
+    m = [int(g["q0"]) for g in c.gates[:32 + 32 + 7] if g["kind"] == sk.M]
+    assert len(m) == 7 and len(set(m)) == 7 and all(q >= 32 for q in m)
+
+
+def test_parse_native(sk):
+    c = sk.parse_native("qubits 2\nh 0\ncx 0 1\nm 0\nm 1")
+    assert c.n == 2 and [int(k) for k in c.gates["kind"]] == [sk.H, sk.CX, sk.M, sk.M]
+    with pytest.raises(sk.ParseError) as e:
+        sk.parse_native("qubits 1\ncx 0 0")
+    assert e.value.line == 2
+    c = sk.parse_native("qubits 2\nh 0\nchunk\nh 1")
+    assert len(c.gates) == 2 and list(c.chunk_marks) == [1]
+    for bad, line in (("h 0\n", 1), ("qubits 2\nfoo 1\n", 2), ("qubits 2\n# c\n\nh 5\n", 4), ("qubits 2\nh\n", 2), ("qubits 2\ncx 0\n", 2)):
+        with pytest.raises(sk.ParseError) as e:
+            sk.parse_native(bad)
+        assert e.value.line == line
+    c = sk.random_layered_circuit(16, 4)
+    c2 = sk.parse_native(c.emit_native())
+    assert c2.n == c.n and (c2.gates == c.gates).all() and (c2.chunk_marks == c.chunk_marks).all()
+
+
+def test_validate_chunks(sk):
+    assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\nh 1")) == []
+    assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\ncx 0 1")) == [(0, 1, "collision")]
+    assert sk.validate_chunks(sk.parse_native("qubits 1\nm 0")) == [(0, 0, "measurement")]
