@@ -72,6 +72,7 @@ typedef struct sk_counters {
     uint64_t waves;                /* measurement scheduler waves               */
     uint64_t transposes;           /* column-major <-> row-major conversions    */
     uint64_t kernel_launches;      /* kernels launched by this library          */
+    uint64_t meas_phase_ns[8];     /* measurement kernel, CTA 0 wall ns per phase: inspect, barrier, classify+det, barrier, random, barrier, window */
 } sk_counters;
 
 /* ---- context ---------------------------------------------------------- */

@@ -43,7 +43,7 @@ _ERR = {SK_EDIM: DimensionError, SK_EUNSUPPORTED: UnsupportedError, SK_EINVARIAN
 class Counters(C.Structure):
     _fields_ = [("n_rand", C.c_uint64), ("n_det", C.c_uint64), ("k_rand", C.c_uint64), ("k_det", C.c_uint64),
                 ("gate_hist", C.c_uint64 * 12), ("layers", C.c_uint64), ("waves", C.c_uint64),
-                ("transposes", C.c_uint64), ("kernel_launches", C.c_uint64)]
+                ("transposes", C.c_uint64), ("kernel_launches", C.c_uint64), ("meas_phase_ns", C.c_uint64 * 8)]
 
 
 _lib = None
@@ -270,6 +270,7 @@ class Context:
         self.check(lib().sk_get_counters(self._h, C.byref(c)))
         d = {k: int(getattr(c, k)) for k in ("n_rand", "n_det", "k_rand", "k_det", "layers", "waves", "transposes", "kernel_launches")}
         d["gate_hist"] = [int(v) for v in c.gate_hist]
+        d["meas_phase_ns"] = [int(v) for v in c.meas_phase_ns]
         return d
 
     def reset_counters(self):

@@ -1,30 +1,35 @@
 // kernels_measure.cuh -- K2/K3/K4: a block of consecutive Z measurements executed by
-// ONE persistent cooperative kernel (no host round trips; the branch taken is
-// data dependent).  Exact CHP semantics (Algorithm 1):
-// results are bit-identical to measuring one qubit at a time, in order.
+// ONE persistent cooperative kernel (no host round trips; branches are data dependent).
+// Exact CHP semantics (Algorithm 1): the tableau, signs and
+// record are bit-identical to measuring one qubit at a time, in order.
 //
-// Scheduler (per wave):
-//   A  every warp takes one pending measurement j (window = #warps in the grid):
-//      pivot search = scan of the stabilizer half of column x_q in the C form
-//      (contiguous, warp ballot + min) -- K2.  If there is no pivot the
-//      measurement is deterministic and the warp evaluates it at once from the
-//      read-only R form: ordered product of the stabilizer partners of the
-//      destabilizers with x_q = 1, phase by popcounts (mod 4) -- K4.  A random
-//      one only publishes (j, pivot) with a 64-bit atomicMin.
-//   -- grid barrier --
-//      f = first random measurement of the window.  Everything before f is final
-//      (deterministic measurements do not modify the tableau).
-//   B  if f exists, the whole grid performs that one random measurement -- K3:
-//      stage column mask + pivot row P + old destabilizer row D in shared memory
-//      (1-D TMA bulk copies, mbarrier), barrier, then concurrently
-//        B1 R form: rowsum(i, p) for every i in the mask (warp per row, P from smem)
-//        B2 C form: column_j ^= mask for every j in supp(P)   (word parallel)
-//        B3 C form: bit fixes for the overwritten rows p and p+n ; sign bits ; record
-//        B4 R form: row p+n := P ; row p := Z_q
-//      barrier; the next window starts at f+1.
-// Both forms stay valid, so later measurements (and gate layers) need no
-// re-transposition.  Row i = p+n is skipped in B1 (it is overwritten; SURVEY.md
-// section 7 "rowsum on the pivot's own destabilizer").
+// Out-of-order wave scheduler.  The FOOTPRINT of a pending measurement j in the current
+// state is the set of row slots F_j = {i mod n : x_iq = 1} (slot i = stabilizer i and its
+// destabilizer partner; the pivot and its partner are in it by construction).  Two
+// measurements with disjoint footprints act on disjoint rows, cannot change each other's
+// column x_q, pivot, branch or phases, and therefore commute bit-exactly -- also with
+// everything the earlier one may turn into once ITS predecessors have run (DESIGN.md,
+// "independence of measurements"; tools/proto_waves.py checks the rule against the oracle).
+// Per wave, over a window of pending measurements (kSlotsPerWarp per warp of the grid):
+//
+//   P1  pivot search = scan of the stabilizer half of column x_q in the C form (contiguous;
+//       ffs + warp min) -- K2.  Every window member CLAIMS its slots with a 64-bit atomicMax
+//       of (wave, ~j); the first random index r0 is min-reduced.           -- grid barrier --
+//   P2  j < r0: deterministic and final (nothing before it writes).  j >= r0: runnable iff
+//       no slot of F_j is claimed by a smaller index.  Runnable deterministic measurements
+//       are evaluated at once from the read-only R form: ordered product of the stabilizer
+//       partners, phase by popcounts mod 4 -- K4.                           -- grid barrier --
+//   P3  runnable random measurements, one CTA each -- K3: column mask, pivot row P and old
+//       destabilizer row D staged in shared memory by 1-D TMA bulk copies, then
+//         B1 R form: rowsum(i, p) for every i in the mask (warp per row, P from smem)
+//         B2 C form: column_j ^= mask for j in supp(P)            (word parallel, atomicXor)
+//         B3 C form: bit fixes for the overwritten rows p and p+n ; sign bits ; record
+//         B4 R form: row p+n := P ; row p := Z_q                            -- grid barrier --
+//   A window without random measurements needs only the first barrier.  The first pending
+//   measurement is always runnable, so every wave makes progress; RNG ordinal and record
+//   slot are those of the measurement's position, never of its execution order.
+// Both forms stay valid throughout.  Row i = p+n is skipped in B1 (it is overwritten;
+// SURVEY.md section 7 "rowsum on the pivot's own destabilizer").
 //
 // Roofline: HBM/L2.  Algorithmic bytes: random  RW*8 + 16W + k*32W + 32W ;
 // deterministic  RW*8/2 + k*16W  -- reported from the k counters kept here.
@@ -36,9 +41,20 @@ namespace skd {
 struct MeasWs {
     u32 bar;            // grid barrier counter (zeroed before each launch)
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 tma timeout
-    u64 first[3];       // per-wave (j << 32 | pivot), min-reduced; 3 slots rotate
+    u32 r0[4];          // per-wave index of the first random measurement, min-reduced; 3 slots rotate
     u64 n_rand, n_det, k_rand, k_det, waves;
+    u64 prof[8];        // block-0 wall time (ns) per phase: P1, barrier, P2, barrier, P3, barrier, sequential, window search
+    u32 ncommit;        // measurements executed so far in this launch
+    u32 pad;
+    u64 seqprof[8];     // sequential mode, CTA 0: inspect, det, random, fence ns ; [4] det count, [5] random count, [6] SM cycles, [7] ns
 };
+
+constexpr int kMeasThreads = 512;
+constexpr int kMeasWarps = kMeasThreads / 32;
+constexpr int kSlotsPerWarp = 4;
+constexpr int kColChunk = 6;         // column words per lane loaded back-to-back (192 words per chunk)
+constexpr int kSeqMin = 64, kSeqMax = 1024;   // sequential run length (doubles while waves stay narrow)
+constexpr int kHeavyDet = 48;        // partner rows above which a deterministic product is tree-reduced by a CTA
 
 struct MeasArgs {
     DMat m;             // tableau (C and R valid)
@@ -50,23 +66,239 @@ struct MeasArgs {
     uint8_t* outcomes;  // [count]
     uint8_t* dets;      // [count]
     MeasWs* ws;
+    u64* claim;         // [64*W] slot claims, zeroed before each launch
+    u32* wpiv;          // [2][window] pivot of a window slot (0xffffffff = deterministic), by wave parity
+    uint8_t* wrun;      // [2][window] 1 = runnable random measurement, by wave parity
+    uint8_t* done;      // [count], zeroed before each launch
+    int seq_threshold;  // a wave committing fewer measurements than this switches to sequential mode (0 = never)
 };
 
-constexpr int kMeasThreads = 512;
-constexpr int kMeasWarps = kMeasThreads / 32;
+__device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+#define SK_PROF(k) do { if (blockIdx.x == 0 && tid == 0) { u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
+
+__device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
+
+// K4: ordered product of the stabilizer partners selected by the destabilizer half of xcol.
+// One warp accumulates the partners number part, part+nparts, ... of the selection (stabilizer rows
+// commute, so any grouping/order of the factors gives the same Hermitian product); 8 partner rows
+// are loaded per step so their latencies overlap.  acc_x/acc_z [Wp] are private to the warp
+// (lane-strided words).  Returns the phase exponent mod 4 of the partial product (warp-uniform).
+__device__ __forceinline__ int det_partial(const DMat& m, const u64* xcol, u64* acc_x, u64* acc_z,
+                                           int lane, int part, int nparts, int* k_out) {
+    const int W = m.W, Wp = m.Wp;
+    for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
+    int e = 0, k = 0, seen = 0;
+    int s[8]; int ns = 0;
+    auto flush = [&]() {
+        if (lane == 0) for (int t = 0; t < ns; ++t) e += 2 * sign_bit(m.sgn, s[t]);
+        for (int w = lane; w < W; w += 32) {
+            u64 sx[8], sz[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) if (t < ns) {
+                const u64* rx = m.rows + (size_t)(2 * s[t]) * Wp;
+                sx[t] = ldcg(rx + w); sz[t] = ldcg(rx + Wp + w);
+            }
+            u64 ax = acc_x[w], az = acc_z[w];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) if (t < ns) {
+                e += g_word(sx[t], sz[t], ax, az);      // rowsum(scratch, s): left factor = row s
+                ax ^= sx[t]; az ^= sz[t];
+            }
+            acc_x[w] = ax; acc_z[w] = az;
+        }
+        k += ns; ns = 0;
+    };
+    for (int c = 0; c < W; c += 32) {
+        u64 v = (c + lane < W) ? ldcg(xcol + W + c + lane) : 0ull;
+        u32 nz = __ballot_sync(0xffffffffu, v != 0);
+        while (nz) {
+            const int l = __ffs(nz) - 1; nz &= nz - 1;
+            u64 word = __shfl_sync(0xffffffffu, v, l);
+            while (word) {
+                const int b = __ffsll((long long)word) - 1; word &= word - 1;
+                if ((seen++ % nparts) == part) { s[ns++] = (c + l) * 64 + b; if (ns == 8) flush(); }
+            }
+        }
+    }
+    if (ns) flush();
+    *k_out = k;
+    return warp_sum(e) & 3;
+}
+
+// ---- CTA-wide building blocks (all kMeasThreads threads call them together) -------------
+struct MeasSmem {
+    u64* mask;      // [RW]   column x_q (rows to update; pivot bits cleared)
+    u64* P;         // [2*Wp] pivot row
+    u64* D;         // [2*Wp] old destabilizer row of the pivot
+    u64* acc;       // [kMeasWarps][2*Wp] per-warp product accumulators
+    u64* mbar;
+    int* pe; int* pk;
+};
+
+// K3: one random measurement (index jr, qubit q, pivot stabilizer row-bit p) by one CTA.
+__device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm, int jr, u32 q, int p, u32& tma_parity) {
+    const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    MeasWs* ws = a.ws;
+    const int pd = a.NS + p;
+    const u64* qcol = a.m.cols + (size_t)(2 * q) * RW;
+    if (tid == 0) {
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_expect_tx(sm.mbar, u32(RW * 8 + 4 * Wp * 8));
+        tma_load_1d(sm.mask, qcol, u32(RW * 8), sm.mbar);
+        tma_load_1d(sm.P, a.m.rows + (size_t)(2 * p) * Wp, u32(2 * Wp * 8), sm.mbar);
+        tma_load_1d(sm.D, a.m.rows + (size_t)(2 * pd) * Wp, u32(2 * Wp * 8), sm.mbar);
+    }
+    if (!mbar_wait(sm.mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
+    tma_parity ^= 1;
+    const int sp = sign_bit(a.m.sgn, p), sd = sign_bit(a.m.sgn, pd);
+    __syncthreads();
+    if (tid == 0) { sm.mask[p >> 6] &= ~(1ull << (p & 63)); sm.mask[pd >> 6] &= ~(1ull << (pd & 63)); }
+    __syncthreads();
+    // B1: rowsum(i, p) for every i in the mask; warp w takes mask words w, w+16, ...
+    for (int mw = warp; mw < RW; mw += kMeasWarps) {
+        u64 bits = sm.mask[mw];
+        while (bits) {
+            int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            const int i = mw * 64 + b;
+            u64* tx = a.m.rows + (size_t)(2 * i) * Wp;
+            u64* tz = tx + Wp;
+            int e = 0;
+            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {     // loads first, then phase + stores
+                u64 xv[kColChunk], zv[kColChunk];
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) {
+                    const int w = w0 + 32 * t + lane;
+                    xv[t] = (w < W) ? ldcg(tx + w) : 0ull; zv[t] = (w < W) ? ldcg(tz + w) : 0ull;
+                }
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) {
+                    const int w = w0 + 32 * t + lane;
+                    if (w >= W) continue;
+                    const u64 px = sm.P[w], pz = sm.P[Wp + w];
+                    e += g_word(px, pz, xv[t], zv[t]);             // left factor = pivot row
+                    if (px) __stcg(tx + w, xv[t] ^ px);
+                    if (pz) __stcg(tz + w, zv[t] ^ pz);
+                }
+            }
+            e = warp_sum(e) & 3;
+            if (lane == 0) {
+                if (e & 1) atomicOr(&ws->err, 1u);
+                if (sp ^ (e >> 1)) atomicXor(a.m.sgn + (i >> 6), 1ull << (i & 63));
+            }
+        }
+    }
+    // B2: C form, column_j ^= mask for j in supp(P); warp unit = (half h, qubit word pw)
+    for (int u = warp; u < 2 * W; u += kMeasWarps) {
+        const int h = u / W, pw = u % W;
+        u64 bits = sm.P[h * Wp + pw];
+        while (bits) {
+            int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            u64* col = a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW;
+            for (int w = lane; w < RW; w += 32) {
+                u64 mv = sm.mask[w];
+                if (mv) atomicXor(col + w, mv);
+            }
+        }
+    }
+    // B3: C form, single-bit fixes for rows p (-> Z_q) and p+n (-> P); thread per (list, word)
+    {
+        const u64 pbit = 1ull << (p & 63), dbit = 1ull << (pd & 63);
+        for (int u = tid; u < 4 * W; u += kMeasThreads) {
+            const int list = u / W, pw = u % W;
+            const int h = list & 1;
+            u64 bits; int word; u64 bit;
+            if (list < 2) {          // row p: old P -> Z_q
+                bits = sm.P[h * Wp + pw];
+                if (h == 1 && pw == int(q >> 6)) bits ^= 1ull << (q & 63);
+                word = p >> 6; bit = pbit;
+            } else {                 // row p+n: old D -> P
+                bits = sm.D[h * Wp + pw] ^ sm.P[h * Wp + pw];
+                word = pd >> 6; bit = dbit;
+            }
+            while (bits) {
+                int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                atomicXor(a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW + word, bit);
+            }
+        }
+    }
+    // B4: R form, row p+n := P ; row p := Z_q
+    {
+        u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
+        u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
+        for (int w = tid; w < 2 * Wp; w += kMeasThreads) {
+            __stcg(rd + w, sm.P[w]);
+            u64 v = 0;
+            if (w == Wp + int(q >> 6)) v = 1ull << (q & 63);
+            __stcg(rp + w, v);
+        }
+    }
+    // signs, record, counters
+    if (warp == 0) {
+        int k = 0;
+        for (int w = lane; w < RW; w += 32) k += __popcll(sm.mask[w]);
+        k = warp_sum(k);
+        if (lane == 0) {
+            const int out = counter_bit(a.seed, a.ordinal0 + (uint64_t)jr);
+            if (sp != out) atomicXor(a.m.sgn + (p >> 6), 1ull << (p & 63));
+            if (sd != sp) atomicXor(a.m.sgn + (pd >> 6), 1ull << (pd & 63));
+            a.outcomes[jr] = uint8_t(out);
+            a.dets[jr] = 0; a.done[jr] = 1;
+            atomicAdd(&ws->n_rand, 1ull); atomicAdd(&ws->k_rand, (u64)k); atomicAdd(&ws->ncommit, 1u);
+        }
+    }
+    __syncthreads();      // smem is restaged by the next measurement
+}
+
+// K4 by a whole CTA: 16 warp partial products, combined by warp 0 (tree reduction; valid
+// because stabilizer rows commute and Pauli multiplication is associative).
+__device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, int j, const u64* xcol) {
+    const int Wp = a.m.Wp, W = a.m.W;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    MeasWs* ws = a.ws;
+    u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
+    int k;
+    const int e = det_partial(a.m, xcol, acc_x, acc_x + Wp, lane, warp, kMeasWarps, &k);
+    if (lane == 0) { sm.pe[warp] = e; sm.pk[warp] = k; }
+    __syncthreads();
+    if (warp == 0) {
+        int et = 0, kt = 0;
+        for (int t = 0; t < kMeasWarps; ++t) { et += sm.pe[t]; kt += sm.pk[t]; }
+        int g = 0;
+        for (int w = lane; w < W; w += 32) {
+            u64 ax = sm.acc[w], az = sm.acc[Wp + w];
+            for (int t = 1; t < kMeasWarps; ++t) {
+                u64 bx = sm.acc[(size_t)t * 2 * Wp + w], bz = sm.acc[(size_t)t * 2 * Wp + Wp + w];
+                g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+            }
+        }
+        et = (et + warp_sum(g)) & 3;
+        if (lane == 0) {
+            if (et & 1) atomicOr(&ws->err, 1u);
+            a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
+            atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)kt); atomicAdd(&ws->ncommit, 1u);
+        }
+    }
+    __syncthreads();
+}
 
 // dynamic smem: mask[RW] | P[2*Wp] | D[2*Wp] | acc[kMeasWarps][2*Wp]   (u64 each)
 __global__ void __launch_bounds__(kMeasThreads, 1)
 k_measure_block(MeasArgs a) {
     extern __shared__ __align__(16) u64 smem[];
     __shared__ __align__(8) u64 s_mbar;
-    const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W, NS = a.NS;
-    u64* s_mask = smem;
-    u64* s_P = s_mask + RW;
-    u64* s_D = s_P + 2 * Wp;
-    u64* s_acc = s_D + 2 * Wp;
+    __shared__ int s_red[2];
+    __shared__ int s_nrun, s_run[kMeasWarps * kSlotsPerWarp];
+    __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
+    __shared__ u32 s_piv;
+    const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
+    MeasSmem sm;
+    sm.mask = smem; sm.P = sm.mask + RW; sm.D = sm.P + 2 * Wp; sm.acc = sm.D + 2 * Wp;
+    sm.mbar = &s_mbar; sm.pe = s_pe; sm.pk = s_pk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int GW = gridDim.x * kMeasWarps;
+    const int G = gridDim.x;
+    const int GW = G * kMeasWarps;
+    const int WS = GW * kSlotsPerWarp;              // window size
     const int gw = blockIdx.x * kMeasWarps + warp;
     MeasWs* ws = a.ws;
     u32 epoch = 0;
@@ -74,181 +306,176 @@ k_measure_block(MeasArgs a) {
     if (tid == 0) mbar_init(&s_mbar, 1);
     __syncthreads();
 
-    u64* acc_x = s_acc + (size_t)warp * 2 * Wp;
+    u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
     u64* acc_z = acc_x + Wp;
 
     int pos = 0;
-    u32 wave = 0;
+    u32 wave = 1;
+    u32 commits_seen = 0;
+    int seqlen = 0;
+    u64 t_prof = gtime();
     while (pos < a.count) {
-        // ------------------------------------------------ phase A -------------
-        if (blockIdx.x == 0 && tid == 0) { ws->first[(wave + 1) % 3] = ~0ull; }
-        const int j = pos + gw;
-        int my_det = 0, my_k = 0;
-        if (j < a.count) {
-            const u32 q = a.qubits[j];
-            const u64* xcol = a.m.cols + (size_t)(2 * q) * RW;
-            // K2: pivot = smallest stabilizer row with x_q = 1
-            u32 best = 0xffffffffu;
-            for (int w = lane; w < W; w += 32) {
-                u64 v = ldcg(xcol + w);
-                if (v) best = min(best, u32(w * 64 + __ffsll((long long)v) - 1));
+        const int wend = min(a.count, pos + WS);
+        const int par = int(wave & 1);
+        u32* wpiv = a.wpiv + (size_t)par * WS;
+        uint8_t* wrun = a.wrun + (size_t)par * WS;
+        // ------------------------------------------------------------ P1 -----
+        if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0xffffffffu;
+        for (int slot = gw; pos + slot < wend; slot += GW) {
+            const int j = pos + slot;
+            if (__ldcg(a.done + j)) { if (lane == 0) wpiv[slot] = 0xfffffffeu; continue; }       // executed in an earlier wave
+            const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
+            const u64 key = ((u64)wave << 32) | (u64)(0xffffffffu - (u32)j);
+            u32 piv = 0xffffffffu;
+            for (int w0 = 0; w0 < RW; w0 += 32 * kColChunk) {        // loads first (one L2 round trip per chunk)
+                u64 cv[kColChunk];
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < RW) ? ldcg(xcol + w) : 0ull; }
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) {
+                    const int w = w0 + 32 * t + lane;
+                    u64 v = cv[t];
+                    if (v && w < W) piv = min(piv, u32(w * 64 + __ffsll((long long)v) - 1));
+                    const int base = (w < W ? w : w - W) * 64;
+                    while (v) { int b = __ffsll((long long)v) - 1; v &= v - 1; atomicMax(a.claim + base + b, key); }
+                }
             }
-            best = warp_min(best);
-            if (best != 0xffffffffu) {
-                if (lane == 0) atomicMin(&ws->first[wave % 3], ((u64)(u32)j << 32) | best);
-            } else {
-                // K4: deterministic.  scratch := product of stabilizer rows s with destab x_{s,q} = 1
-                my_det = 1;
-                for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
-                int e = 0;
-                for (int c = 0; c < W; c += 32) {
-                    u64 v = (c + lane < W) ? ldcg(xcol + W + c + lane) : 0ull;
-                    u32 nz = __ballot_sync(0xffffffffu, v != 0);
-                    while (nz) {
-                        int l = __ffs(nz) - 1; nz &= nz - 1;
-                        u64 word = __shfl_sync(0xffffffffu, v, l);
-                        while (word) {
-                            int b = __ffsll((long long)word) - 1; word &= word - 1;
-                            const int s = (c + l) * 64 + b;            // stabilizer row-bit
-                            const u64* rx = a.m.rows + (size_t)(2 * s) * Wp;
-                            const u64* rz = rx + Wp;
-                            if (lane == 0) e += 2 * int((ldcg(a.m.sgn + (s >> 6)) >> (s & 63)) & 1ull);
-                            for (int w = lane; w < W; w += 32) {
-                                u64 sx = ldcg(rx + w), sz = ldcg(rz + w);
-                                u64 ax = acc_x[w], az = acc_z[w];
-                                e += g_word(sx, sz, ax, az);            // rowsum(scratch, s): left factor = row s
-                                acc_x[w] = ax ^ sx; acc_z[w] = az ^ sz;
-                            }
-                            ++my_k;
-                        }
+            piv = warp_min(piv);
+            if (lane == 0) {
+                wpiv[slot] = piv;
+                if (piv != 0xffffffffu) atomicMin(&ws->r0[wave % 3], (u32)j);
+            }
+        }
+        SK_PROF(0);
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+        SK_PROF(1);
+        const u32 r0 = __ldcg(&ws->r0[wave % 3]);
+        if (tid == 0) s_nheavy = 0;
+        __syncthreads();
+        // ------------------------------------------------------------ P2 (+K4) --
+        for (int slot = gw; pos + slot < wend; slot += GW) {
+            const int j = pos + slot;
+            const u32 piv = __ldcg(wpiv + slot);      // written by this warp in P1
+            if (piv == 0xfffffffeu) { if (lane == 0) wrun[slot] = 0; continue; }
+            const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
+            bool blocked = false;
+            int npart = 0;                               // partner rows (destabilizer half population)
+            for (int w0 = 0; w0 < RW; w0 += 32 * kColChunk) {
+                u64 cv[kColChunk];
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < RW) ? ldcg(xcol + w) : 0ull; }
+#pragma unroll
+                for (int t = 0; t < kColChunk; ++t) {
+                    const int w = w0 + 32 * t + lane;
+                    u64 v = cv[t];
+                    if (w >= W) npart += __popcll(v);
+                    if ((u32)j < r0) continue;
+                    const int base = (w < W ? w : w - W) * 64;
+                    while (v) {
+                        int b = __ffsll((long long)v) - 1; v &= v - 1;
+                        const u64 c = ldcg(a.claim + base + b);
+                        if ((u32)(c >> 32) == wave && (0xffffffffu - (u32)c) < (u32)j) blocked = true;
                     }
                 }
-                e = warp_sum(e) & 3;
-                if (lane == 0) {
-                    if (e & 1) atomicOr(&ws->err, 1u);
-                    a.outcomes[j] = uint8_t(e >> 1);
-                    a.dets[j] = 1;
-                }
+            }
+            blocked = __any_sync(0xffffffffu, blocked);
+            if (lane == 0) wrun[slot] = uint8_t(!blocked && piv != 0xffffffffu);
+            if (blocked || piv != 0xffffffffu) continue;
+            npart = warp_sum(npart);
+            if (npart > kHeavyDet) {                  // tree-reduced by the whole CTA below
+                if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = slot; }
+                continue;
+            }
+            int k;
+            const int e = det_partial(a.m, xcol, acc_x, acc_z, lane, 0, 1, &k);
+            if (lane == 0) {
+                if (e & 1) atomicOr(&ws->err, 1u);
+                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1; a.done[j] = 1;
+                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)k); atomicAdd(&ws->ncommit, 1u);
             }
         }
-        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        const u64 fkey = ldcg(&ws->first[wave % 3]);
-        const int wend = min(a.count, pos + GW);
-        const int f = (fkey == ~0ull) ? wend : int(fkey >> 32);
-        if (my_det && j < f && lane == 0) {
-            atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)my_k);
+        __syncthreads();
+        for (int h = 0; h < s_nheavy; ++h) {
+            const int j = pos + s_heavy[h];
+            cta_det(a, sm, j, a.m.cols + (size_t)(2 * a.qubits[j]) * RW);
         }
         if (blockIdx.x == 0 && tid == 0) atomicAdd(&ws->waves, 1ull);
-        ++wave;
-        if (f >= wend) { pos = wend; continue; }
+        SK_PROF(2);
+        if (r0 == 0xffffffffu) { pos = wend; ++wave; commits_seen = 0xffffffffu; continue; }   // window was all deterministic: done
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;          // reads of the wave-start state done
+        SK_PROF(3);
 
-        // ------------------------------------------------ phase B: random at f --
-        const u32 q = a.qubits[f];
-        const int p = int(fkey & 0xffffffffu);          // pivot stabilizer row-bit
-        const int pd = NS + p;                           // its destabilizer
-        const u64* xcol = a.m.cols + (size_t)(2 * q) * RW;
-        // stage mask, P, D with 1-D TMA
-        if (tid == 0) {
-            asm volatile("fence.proxy.async;" ::: "memory");
-            const u32 bytes = u32(RW * 8 + 4 * Wp * 8);
-            mbar_expect_tx(&s_mbar, bytes);
-            tma_load_1d(s_mask, xcol, u32(RW * 8), &s_mbar);
-            tma_load_1d(s_P, a.m.rows + (size_t)(2 * p) * Wp, u32(2 * Wp * 8), &s_mbar);
-            tma_load_1d(s_D, a.m.rows + (size_t)(2 * pd) * Wp, u32(2 * Wp * 8), &s_mbar);
-        }
-        if (!mbar_wait(&s_mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
-        tma_parity ^= 1;
-        const int sp = int((ldcg(a.m.sgn + (p >> 6)) >> (p & 63)) & 1ull);
-        const int sd = int((ldcg(a.m.sgn + (pd >> 6)) >> (pd & 63)) & 1ull);
+        // ------------------------------------------------------------ P3: K3 ----
+        // this CTA owns window slots blockIdx.x, +G, +2G, ...: gather the runnable ones in parallel
+        if (tid == 0) s_nrun = 0;
         __syncthreads();
-        if (tid == 0) { s_mask[p >> 6] &= ~(1ull << (p & 63)); s_mask[pd >> 6] &= ~(1ull << (pd & 63)); }
-        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;     // everyone has staged
-
-        // B1: rowsum(i, p) on R for every i in the mask; unit = one byte of the mask
-        for (int u = gw; u < RW * 8; u += GW) {
-            u32 byte = u32((s_mask[u >> 3] >> ((u & 7) * 8)) & 0xffull);
-            while (byte) {
-                int b = __ffs(byte) - 1; byte &= byte - 1;
-                const int i = u * 8 + b;
-                u64* tx = a.m.rows + (size_t)(2 * i) * Wp;
-                u64* tz = tx + Wp;
-                int e = 0;
-                for (int w = lane; w < W; w += 32) {
-                    u64 x = ldcg(tx + w), z = ldcg(tz + w);
-                    u64 px = s_P[w], pz = s_P[Wp + w];
-                    e += g_word(px, pz, x, z);                     // left factor = pivot row
-                    if (px) __stcg(tx + w, x ^ px);
-                    if (pz) __stcg(tz + w, z ^ pz);
-                }
-                e = warp_sum(e) & 3;
-                if (lane == 0) {
-                    if (e & 1) atomicOr(&ws->err, 1u);
-                    if (sp ^ (e >> 1)) atomicXor(a.m.sgn + (i >> 6), 1ull << (i & 63));
-                }
-            }
+        for (int i = tid; pos + blockIdx.x + i * G < wend; i += kMeasThreads) {
+            const int slot = blockIdx.x + i * G;
+            if (__ldcg(wrun + slot)) { int h = atomicAdd(&s_nrun, 1); s_run[h] = slot; }
         }
-        // B2: C form, column_j ^= mask for j in supp(P); unit = (half h, qubit word pw)
-        for (int u = gw; u < 2 * W; u += GW) {
-            const int h = u / W, pw = u % W;
-            u64 bits = s_P[h * Wp + pw];
-            while (bits) {
-                int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                u64* col = a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW;
-                for (int w = lane; w < RW; w += 32) {
-                    u64 mv = s_mask[w];
-                    if (mv) atomicXor(col + w, mv);
-                }
-            }
+        __syncthreads();
+        for (int h = 0; h < s_nrun; ++h) {
+            const int slot = s_run[h];
+            cta_random(a, sm, pos + slot, a.qubits[pos + slot], int(__ldcg(wpiv + slot)), tma_parity);
         }
-        // B3: C form, single-bit fixes for rows p (-> Z_q) and p+n (-> P); thread per (list, word)
-        {
-            const int gt = blockIdx.x * kMeasThreads + tid, GT = gridDim.x * kMeasThreads;
-            const u64 pbit = 1ull << (p & 63), dbit = 1ull << (pd & 63);
-            for (int u = gt; u < 4 * W; u += GT) {
-                const int list = u / W, pw = u % W;
-                const int h = list & 1;
-                u64 bits; int word; u64 bit;
-                if (list < 2) {          // row p: old P -> Z_q
-                    bits = s_P[h * Wp + pw];
-                    if (h == 1 && pw == int(q >> 6)) bits ^= 1ull << (q & 63);
-                    word = p >> 6; bit = pbit;
-                } else {                 // row p+n: old D -> P
-                    bits = s_D[h * Wp + pw] ^ s_P[h * Wp + pw];
-                    word = pd >> 6; bit = dbit;
-                }
-                while (bits) {
-                    int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                    atomicXor(a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW + word, bit);
-                }
-            }
-        }
-        // B4: R form, row p+n := P ; row p := Z_q   (block 1 if it exists)
-        if (blockIdx.x == (gridDim.x > 1 ? 1 : 0)) {
-            u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
-            u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
-            for (int w = tid; w < 2 * Wp; w += kMeasThreads) {
-                __stcg(rd + w, s_P[w]);
-                u64 v = 0;
-                if (w == Wp + int(q >> 6)) v = 1ull << (q & 63);
-                __stcg(rp + w, v);
-            }
-        }
-        // signs, record, counters (block 0)
-        if (blockIdx.x == 0 && warp == 0) {
-            int k = 0;
-            for (int w = lane; w < RW; w += 32) k += __popcll(s_mask[w]);
-            k = warp_sum(k);
-            if (lane == 0) {
-                const int out = counter_bit(a.seed, a.ordinal0 + (uint64_t)f);
-                if (sp != out) atomicXor(a.m.sgn + (p >> 6), 1ull << (p & 63));
-                if (sd != sp) atomicXor(a.m.sgn + (pd >> 6), 1ull << (pd & 63));
-                a.outcomes[f] = uint8_t(out);
-                a.dets[f] = 0;
-                atomicAdd(&ws->n_rand, 1ull); atomicAdd(&ws->k_rand, (u64)k);
-            }
-        }
+        SK_PROF(4);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        pos = f + 1;
+        SK_PROF(5);
+        // ---- sequential mode: when a wave commits only a handful of measurements the block is
+        // dependency-limited; CTA 0 then runs the next `seqlen` measurements strictly in order
+        // with CTA-level synchronisation only (no grid barriers), the other CTAs wait.
+        {
+            const u32 nc = __ldcg(&ws->ncommit);
+            const u32 committed = (commits_seen == 0xffffffffu) ? 0xffffu : nc - commits_seen;
+            seqlen = (committed < (u32)a.seq_threshold) ? min(kSeqMax, max(kSeqMin, seqlen * 2)) : 0;
+        }
+        if (seqlen > 0) {
+            if (blockIdx.x == 0) {
+                int j = pos, ran = 0;
+                u64 t0s = gtime(); const long long c0 = clock64();
+                for (; j < a.count && ran < seqlen; ++j) {
+                    if (__ldcg(a.done + j)) continue;                   // uniform: every thread reads the same byte
+                    const u32 q = a.qubits[j];
+                    const u64* xcol = a.m.cols + (size_t)(2 * q) * RW;
+                    if (tid == 0) s_piv = 0xffffffffu;
+                    __syncthreads();
+                    u32 piv = 0xffffffffu;
+                    for (int w = tid; w < W; w += kMeasThreads) {
+                        u64 v = ldcg(xcol + w);
+                        if (v) piv = min(piv, u32(w * 64 + __ffsll((long long)v) - 1));
+                    }
+                    piv = warp_min(piv);
+                    if (lane == 0 && piv != 0xffffffffu) atomicMin(&s_piv, piv);
+                    __syncthreads();
+                    piv = s_piv;
+                    u64 t1 = gtime();
+                    if (tid == 0) ws->seqprof[0] += t1 - t0s;
+                    if (piv == 0xffffffffu) cta_det(a, sm, j, xcol);
+                    else cta_random(a, sm, j, q, int(piv), tma_parity);
+                    u64 t2 = gtime();
+                    if (tid == 0) { ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
+                    __threadfence();                                    // this measurement's updates before the next column read
+                    __syncthreads();
+                    t0s = gtime();
+                    if (tid == 0) ws->seqprof[3] += t0s - t2;
+                    ++ran;
+                }
+                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - t0s + 0; }
+            }
+            SK_PROF(6);
+            if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+        }
+        commits_seen = __ldcg(&ws->ncommit);
+        // next window starts at the first measurement not yet executed (same value in every CTA)
+        int first = 0x7fffffff;
+        for (int jj = pos + tid; jj < wend; jj += kMeasThreads) if (!__ldcg(a.done + jj)) first = min(first, jj);   // no early exit: loads overlap
+        if (tid == 0) s_red[0] = 0x7fffffff;
+        __syncthreads();
+        if (first != 0x7fffffff) atomicMin(&s_red[0], first);
+        __syncthreads();
+        pos = min(s_red[0], wend);
+        ++wave;
+        SK_PROF(7);
     }
 }
 

@@ -3,13 +3,17 @@
 //
 // One CTA moves a 256 x 256-bit tile through shared memory so that both the
 // global loads and the global stores are 32-byte contiguous per matrix row;
-// each warp transposes 32x32-bit blocks with 32 __ballot_sync votes (lane l
-// contributes bit b of its word; the vote IS output row b).
+// each warp transposes 32x32-bit blocks in registers with a 5-stage shuffle butterfly.
 // Roofline: HBM/L2 streaming, reads + writes the matrix once (2 * bits/8 bytes).
 #pragma once
 #include "common.cuh"
 
 namespace skd {
+
+__device__ __forceinline__ void bfly(u32& v, int j, u32 m, int lane) {
+    const u32 p = __shfl_xor_sync(0xffffffffu, v, j);
+    v = (lane & j) ? (((p >> j) & m) | (v & ~m)) : ((v & m) | ((p & m) << j));
+}
 
 // All sizes in 32-bit words.  Loads outside [src_rows) x [src_words) read 0;
 // stores outside [dst_rows) x [dst_words) are dropped.
@@ -36,12 +40,10 @@ k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, i
 #pragma unroll
     for (int bj = 0; bj < 8; ++bj) {
         u32 v = tin[warp * 32 + lane][bj];    // src row (c0 + 32*warp + lane), bits 32*(w0+bj) ..
-        u32 mine = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            u32 vote = __ballot_sync(0xffffffffu, (v >> b) & 1u);
-            if (lane == b) mine = vote;
-        }
+        // 32x32 bit transpose across the warp: 5 butterfly stages (swap off-diagonal j x j blocks)
+        bfly(v, 16, 0x0000ffffu, lane); bfly(v, 8, 0x00ff00ffu, lane); bfly(v, 4, 0x0f0f0f0fu, lane);
+        bfly(v, 2, 0x33333333u, lane); bfly(v, 1, 0x55555555u, lane);
+        const u32 mine = v;
         // lane b holds dst row (32*(w0+bj) + b), word (c0/32 + warp)
         tout[bj * 32 + lane][warp] = mine;
     }

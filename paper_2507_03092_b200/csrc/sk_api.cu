@@ -33,6 +33,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
     c->num_sms = prop.multiProcessorCount;
+    if (const char* e = getenv("SK_SEQ_THRESHOLD")) c->seq_threshold = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
     else {
@@ -92,6 +93,8 @@ struct sk_tableau {
     size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
     u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
     int meas_grid = 0; size_t meas_smem = 0;
+    u64* d_claim = nullptr; u32* d_wpiv = nullptr; uint8_t* d_wrun = nullptr; uint8_t* d_done = nullptr;
+    size_t claim_bytes = 0, done_cap = 0;
 };
 
 static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int srows, int swords,
@@ -163,7 +166,12 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e1 = cudaMalloc(&t->m.cols, t->cols_bytes);
     cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
     cudaError_t e3 = cudaMalloc(&t->m.sgn, t->sgn_bytes);
-    if (e1 || e2 || e3) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
+    t->claim_bytes = (size_t)64 * t->W * 8;
+    const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
+    cudaError_t e4 = cudaMalloc(&t->d_claim, t->claim_bytes);
+    cudaError_t e5 = cudaMalloc(&t->d_wpiv, 2 * window * 4);
+    cudaError_t e6 = cudaMalloc(&t->d_wrun, 2 * window);
+    if (e1 || e2 || e3 || e4 || e5 || e6) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
     if ((int)t->meas_smem > c->meas_smem_attr) {
         SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
         c->meas_smem_attr = (int)t->meas_smem;
@@ -182,7 +190,7 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     if (!t) return;
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
-    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn);
+    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_claim); cudaFree(t->d_wpiv); cudaFree(t->d_wrun); cudaFree(t->d_done);
     cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
     delete t;
 }
@@ -348,10 +356,20 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     // reset barrier counter and the three wave slots (counters persist)
     MeasWs* ws = (MeasWs*)c->d_ws;
     SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->first[0], 0xFF, 24, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->r0[0], 0xFF, 16, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->ncommit, 0, 4, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->d_claim, 0, t->claim_bytes, c->stream));
+    if ((size_t)count > t->done_cap) {
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        cudaFree(t->d_done); t->d_done = nullptr; t->done_cap = 0;
+        SK_CUDA(c, cudaMalloc(&t->d_done, (size_t)count * 2));
+        t->done_cap = (size_t)count * 2;
+    }
+    SK_CUDA(c, cudaMemsetAsync(t->d_done, 0, (size_t)count, c->stream));
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
-    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws;
+    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.claim = t->d_claim; a.wpiv = t->d_wpiv; a.wrun = t->d_wrun; a.done = t->d_done;
+    a.seq_threshold = c->seq_threshold;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -413,7 +431,8 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     if (!c) return SK_EARG;
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 5 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 13 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->seqprof[0], 0, 8 * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -423,6 +442,8 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
     *out = c->cnt;
     out->n_rand = h.n_rand; out->n_det = h.n_det; out->k_rand = h.k_rand; out->k_det = h.k_det; out->waves = h.waves;
+    for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
+    if (getenv("SK_SEQPROF")) fprintf(stderr, "seqprof: inspect %.0f us det %.0f us (n=%llu) random %.0f us (n=%llu) fence %.0f us ; cycles %llu\n", h.seqprof[0] / 1e3, h.seqprof[1] / 1e3, (unsigned long long)h.seqprof[4], h.seqprof[2] / 1e3, (unsigned long long)h.seqprof[5], h.seqprof[3] / 1e3, (unsigned long long)h.seqprof[6]);
     return SK_OK;
 }
 

@@ -16,6 +16,7 @@ struct sk_ctx {
     bool own_stream = false;
     int num_sms = 0;
     int max_smem_optin = 0;
+    int seq_threshold = 0;                  // measurement scheduler: sequential-mode trigger (SK_SEQ_THRESHOLD)
     int meas_smem_attr = 0;                 // largest dynamic-smem attribute set on k_measure_block
     std::string err;
     // growable device scratch
