@@ -130,6 +130,9 @@ uint64_t sk_program_measurements(const sk_program* p);
 /* Runs the whole program on t from its current state (asynchronous; the
  * measurement record stays on the device until read). */
 int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed);
+/* Same, with CUDA events around every launch: class_ms = device ms spent in {fused layers,
+ * transposes, measurement blocks}.  Synchronises; for roofline reporting, not for timing runs. */
+int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[3]);
 /* outcome / deterministic byte per M gate in circuit order (MeasurementRecord). */
 int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic);
 /* Convenience: identity tableau -> run -> record.  *out_t receives the final tableau. */

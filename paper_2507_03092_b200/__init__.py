@@ -84,6 +84,7 @@ def lib() -> C.CDLL:
             "sk_program_destroy": (None, [vp]),
             "sk_program_measurements": (u64, [vp]),
             "sk_program_run": (i32, [vp, vp, u64]),
+            "sk_program_run_profiled": (i32, [vp, vp, u64, P(C.c_float)]),
             "sk_program_read_record": (i32, [vp, vp, vp]),
             "sk_sim": (i32, [vp, u64, vp, sz, vp, sz, C.c_int, u64, P(vp), vp, vp, P(u32)]),
             "sk_free": (None, [vp]),
@@ -122,7 +123,7 @@ EXPORTS = [
     "sk_get_counters", "sk_reset_counters", "sk_tableau_create", "sk_tableau_destroy", "sk_tableau_reset",
     "sk_tableau_qubits", "sk_tableau_upload", "sk_tableau_download", "sk_apply_layer", "sk_apply_gates",
     "sk_measure_z", "sk_measure_batch", "sk_tableau_rowsum", "sk_program_create", "sk_program_destroy",
-    "sk_program_measurements", "sk_program_run", "sk_program_read_record", "sk_sim", "sk_free",
+    "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_sim", "sk_free",
     "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native",
     "sk_circuit_validate_chunks", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
     "sk_rows_download", "sk_rows_conj_layer", "sk_commutation_vector",
@@ -357,6 +358,11 @@ class Program:
 
     def run(self, t: Tableau, seed: int):
         self.ctx.check(lib().sk_program_run(self._h, t._h, seed))
+
+    def run_profiled(self, t: Tableau, seed: int) -> dict:
+        ms = (C.c_float * 3)()
+        self.ctx.check(lib().sk_program_run_profiled(self._h, t._h, seed, ms))
+        return {"layer_ms": float(ms[0]), "transpose_ms": float(ms[1]), "measure_ms": float(ms[2])}
 
     def read_record(self):
         nm = self.num_measurements

@@ -54,7 +54,8 @@ constexpr int kMeasWarps = kMeasThreads / 32;
 constexpr int kSlotsPerWarp = 4;
 constexpr int kColChunk = 6;         // column words per lane loaded back-to-back (192 words per chunk)
 constexpr int kSeqMin = 64, kSeqMax = 1024;   // sequential run length (doubles while waves stay narrow)
-constexpr int kHeavyDet = 48;        // partner rows above which a deterministic product is tree-reduced by a CTA
+constexpr int kMaxTargets = 2048, kMaxMaskWords = 512, kMaxSupport = 4096;   // sparse work-list capacities (dense fallback above)
+constexpr int kWarpList = 48;        // partner rows a single warp multiplies itself; longer products are tree-reduced by a CTA
 
 struct MeasArgs {
     DMat m;             // tableau (C and R valid)
@@ -70,6 +71,7 @@ struct MeasArgs {
     u32* wpiv;          // [2][window] pivot of a window slot (0xffffffff = deterministic), by wave parity
     uint8_t* wrun;      // [2][window] 1 = runnable random measurement, by wave parity
     uint8_t* done;      // [count], zeroed before each launch
+    int use_tma;        // stage mask/P/D with cp.async.bulk (1) or ld.global.cg (0)
     int seq_threshold;  // a wave committing fewer measurements than this switches to sequential mode (0 = never)
 };
 
@@ -78,19 +80,21 @@ __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globa
 
 __device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
 
-// K4: ordered product of the stabilizer partners selected by the destabilizer half of xcol.
-// One warp accumulates the partners number part, part+nparts, ... of the selection (stabilizer rows
-// commute, so any grouping/order of the factors gives the same Hermitian product); 8 partner rows
-// are loaded per step so their latencies overlap.  acc_x/acc_z [Wp] are private to the warp
-// (lane-strided words).  Returns the phase exponent mod 4 of the partial product (warp-uniform).
-__device__ __forceinline__ int det_partial(const DMat& m, const u64* xcol, u64* acc_x, u64* acc_z,
-                                           int lane, int part, int nparts, int* k_out) {
+// K4: product of the stabilizer rows listed in `list` (entries part, part+nparts, ...), phase
+// exponent mod 4 returned warp-uniform.  Stabilizer rows commute and Pauli multiplication is
+// associative, so any grouping/order of the factors gives the same Hermitian product; 8 rows are
+// loaded per step so their latencies overlap.  acc_x/acc_z [Wp] are private to the warp
+// (lane-strided words).
+__device__ __forceinline__ int det_list_partial(const DMat& m, const u32* list, int cnt, int part, int nparts,
+                                                u64* acc_x, u64* acc_z, int lane, int* k_out) {
     const int W = m.W, Wp = m.Wp;
     for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
-    int e = 0, k = 0, seen = 0;
-    int s[8]; int ns = 0;
-    auto flush = [&]() {
-        if (lane == 0) for (int t = 0; t < ns; ++t) e += 2 * sign_bit(m.sgn, s[t]);
+    int e = 0, k = 0;
+    for (int i0 = part; i0 < cnt; i0 += 8 * nparts) {
+        int s[8]; int ns = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) { const int i = i0 + t * nparts; if (i < cnt) { s[t] = int(list[i]); ns = t + 1; } else s[t] = 0; }
+        if (lane < ns) e += 2 * sign_bit(m.sgn, int(list[i0 + lane * nparts]));
         for (int w = lane; w < W; w += 32) {
             u64 sx[8], sz[8];
 #pragma unroll
@@ -106,21 +110,8 @@ __device__ __forceinline__ int det_partial(const DMat& m, const u64* xcol, u64* 
             }
             acc_x[w] = ax; acc_z[w] = az;
         }
-        k += ns; ns = 0;
-    };
-    for (int c = 0; c < W; c += 32) {
-        u64 v = (c + lane < W) ? ldcg(xcol + W + c + lane) : 0ull;
-        u32 nz = __ballot_sync(0xffffffffu, v != 0);
-        while (nz) {
-            const int l = __ffs(nz) - 1; nz &= nz - 1;
-            u64 word = __shfl_sync(0xffffffffu, v, l);
-            while (word) {
-                const int b = __ffsll((long long)word) - 1; word &= word - 1;
-                if ((seen++ % nparts) == part) { s[ns++] = (c + l) * 64 + b; if (ns == 8) flush(); }
-            }
-        }
+        k += ns;
     }
-    if (ns) flush();
     *k_out = k;
     return warp_sum(e) & 3;
 }
@@ -133,6 +124,10 @@ struct MeasSmem {
     u64* acc;       // [kMeasWarps][2*Wp] per-warp product accumulators
     u64* mbar;
     int* pe; int* pk;
+    int* cnt;                 // [3] list lengths
+    u32* targets;             // [kMaxTargets] rows to rowsum
+    unsigned short* mwords;   // [kMaxMaskWords] non-zero mask words
+    u32* support;             // [kMaxSupport] (2*qubit + half) entries of supp(P)
 };
 
 // K3: one random measurement (index jr, qubit q, pivot stabilizer row-bit p) by one CTA.
@@ -142,62 +137,103 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     MeasWs* ws = a.ws;
     const int pd = a.NS + p;
     const u64* qcol = a.m.cols + (size_t)(2 * q) * RW;
-    if (tid == 0) {
-        asm volatile("fence.proxy.async;" ::: "memory");
-        mbar_expect_tx(sm.mbar, u32(RW * 8 + 4 * Wp * 8));
-        tma_load_1d(sm.mask, qcol, u32(RW * 8), sm.mbar);
-        tma_load_1d(sm.P, a.m.rows + (size_t)(2 * p) * Wp, u32(2 * Wp * 8), sm.mbar);
-        tma_load_1d(sm.D, a.m.rows + (size_t)(2 * pd) * Wp, u32(2 * Wp * 8), sm.mbar);
-    }
-    if (!mbar_wait(sm.mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
-    tma_parity ^= 1;
     const int sp = sign_bit(a.m.sgn, p), sd = sign_bit(a.m.sgn, pd);
-    __syncthreads();
-    if (tid == 0) { sm.mask[p >> 6] &= ~(1ull << (p & 63)); sm.mask[pd >> 6] &= ~(1ull << (pd & 63)); }
-    __syncthreads();
-    // B1: rowsum(i, p) for every i in the mask; warp w takes mask words w, w+16, ...
-    for (int mw = warp; mw < RW; mw += kMeasWarps) {
-        u64 bits = sm.mask[mw];
-        while (bits) {
-            int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            const int i = mw * 64 + b;
-            u64* tx = a.m.rows + (size_t)(2 * i) * Wp;
-            u64* tz = tx + Wp;
-            int e = 0;
-            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {     // loads first, then phase + stores
-                u64 xv[kColChunk], zv[kColChunk];
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) {
-                    const int w = w0 + 32 * t + lane;
-                    xv[t] = (w < W) ? ldcg(tx + w) : 0ull; zv[t] = (w < W) ? ldcg(tz + w) : 0ull;
-                }
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) {
-                    const int w = w0 + 32 * t + lane;
-                    if (w >= W) continue;
-                    const u64 px = sm.P[w], pz = sm.P[Wp + w];
-                    e += g_word(px, pz, xv[t], zv[t]);             // left factor = pivot row
-                    if (px) __stcg(tx + w, xv[t] ^ px);
-                    if (pz) __stcg(tz + w, zv[t] ^ pz);
-                }
-            }
-            e = warp_sum(e) & 3;
-            if (lane == 0) {
-                if (e & 1) atomicOr(&ws->err, 1u);
-                if (sp ^ (e >> 1)) atomicXor(a.m.sgn + (i >> 6), 1ull << (i & 63));
-            }
+    if (a.use_tma) {          // 1-D TMA bulk copies on one mbarrier (UBLKCP)
+        if (tid == 0) {
+            asm volatile("fence.proxy.async;" ::: "memory");
+            mbar_expect_tx(sm.mbar, u32(RW * 8 + 4 * Wp * 8));
+            tma_load_1d(sm.mask, qcol, u32(RW * 8), sm.mbar);
+            tma_load_1d(sm.P, a.m.rows + (size_t)(2 * p) * Wp, u32(2 * Wp * 8), sm.mbar);
+            tma_load_1d(sm.D, a.m.rows + (size_t)(2 * pd) * Wp, u32(2 * Wp * 8), sm.mbar);
+        }
+        if (!mbar_wait(sm.mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
+        tma_parity ^= 1;
+    } else {                  // same bytes with ld.global.cg: lower latency for this 5 KB, latency-critical copy
+        const u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
+        const u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
+        for (int w = tid; w < RW + 4 * Wp; w += kMeasThreads) {
+            const u64 v = (w < RW) ? ldcg(qcol + w) : (w < RW + 2 * Wp ? ldcg(rp + (w - RW)) : ldcg(rd + (w - RW - 2 * Wp)));
+            sm.mask[w] = v;   // mask | P | D are contiguous in shared memory
         }
     }
-    // B2: C form, column_j ^= mask for j in supp(P); warp unit = (half h, qubit word pw)
-    for (int u = warp; u < 2 * W; u += kMeasWarps) {
-        const int h = u / W, pw = u % W;
+    __syncthreads();
+    if (tid == 0) {
+        sm.mask[p >> 6] &= ~(1ull << (p & 63)); sm.mask[pd >> 6] &= ~(1ull << (pd & 63));
+        sm.cnt[0] = 0; sm.cnt[1] = 0; sm.cnt[2] = 0;
+    }
+    __syncthreads();
+    // compact work lists (sparse case): target rows, non-zero mask words, support of P
+    for (int w = tid; w < RW; w += kMeasThreads) {
+        u64 bits = sm.mask[w];
+        if (!bits) continue;
+        const int mi = atomicAdd(&sm.cnt[1], 1);
+        if (mi < kMaxMaskWords) sm.mwords[mi] = (unsigned short)w;
+        while (bits) {
+            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            const int ti = atomicAdd(&sm.cnt[0], 1);
+            if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
+        }
+    }
+    for (int u = tid; u < 2 * W; u += kMeasThreads) {
+        const int h = u >= W, pw = h ? u - W : u;
         u64 bits = sm.P[h * Wp + pw];
         while (bits) {
-            int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            u64* col = a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW;
-            for (int w = lane; w < RW; w += 32) {
-                u64 mv = sm.mask[w];
-                if (mv) atomicXor(col + w, mv);
+            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            const int pi = atomicAdd(&sm.cnt[2], 1);
+            if (pi < kMaxSupport) sm.support[pi] = (u32(pw * 64 + b) << 1) | u32(h);
+        }
+    }
+    __syncthreads();
+    const int nt = sm.cnt[0], nmw = sm.cnt[1], nsup = sm.cnt[2];
+    const bool sparse = nt <= kMaxTargets && nmw <= kMaxMaskWords && nsup <= kMaxSupport;
+    // B1: rowsum(i, p) for every target row i (warp per row, P from smem)
+    auto rowsum_into = [&](int i) {
+        u64* tx = a.m.rows + (size_t)(2 * i) * Wp;
+        u64* tz = tx + Wp;
+        int e = 0;
+        for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {     // loads first, then phase + stores
+            u64 xv[kColChunk], zv[kColChunk];
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                xv[t] = (w < W) ? ldcg(tx + w) : 0ull; zv[t] = (w < W) ? ldcg(tz + w) : 0ull;
+            }
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                if (w >= W) continue;
+                const u64 px = sm.P[w], pz = sm.P[Wp + w];
+                e += g_word(px, pz, xv[t], zv[t]);             // left factor = pivot row
+                if (px) __stcg(tx + w, xv[t] ^ px);
+                if (pz) __stcg(tz + w, zv[t] ^ pz);
+            }
+        }
+        e = warp_sum(e) & 3;
+        if (lane == 0) {
+            if (e & 1) atomicOr(&ws->err, 1u);
+            if (sp ^ (e >> 1)) atomicXor(a.m.sgn + (i >> 6), 1ull << (i & 63));
+        }
+    };
+    if (sparse) {
+        for (int t = warp; t < nt; t += kMeasWarps) rowsum_into(int(sm.targets[t]));
+        // B2: C form, column_j ^= mask for j in supp(P): warp per support entry, lanes over the non-zero mask words
+        for (int e = warp; e < nsup; e += kMeasWarps) {
+            const u32 ent = sm.support[e];
+            u64* col = a.m.cols + (size_t)ent * RW;           // ent == 2*qubit + half
+            for (int i = lane; i < nmw; i += 32) { const int w = sm.mwords[i]; atomicXor(col + w, sm.mask[w]); }
+        }
+    } else {
+        for (int mw = warp; mw < RW; mw += kMeasWarps) {
+            u64 bits = sm.mask[mw];
+            while (bits) { int b = __ffsll((long long)bits) - 1; bits &= bits - 1; rowsum_into(mw * 64 + b); }
+        }
+        for (int u = warp; u < 2 * W; u += kMeasWarps) {
+            const int h = u >= W, pw = h ? u - W : u;
+            u64 bits = sm.P[h * Wp + pw];
+            while (bits) {
+                int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                u64* col = a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW;
+                for (int w = lane; w < RW; w += 32) { u64 mv = sm.mask[w]; if (mv) atomicXor(col + w, mv); }
             }
         }
     }
@@ -205,7 +241,7 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     {
         const u64 pbit = 1ull << (p & 63), dbit = 1ull << (pd & 63);
         for (int u = tid; u < 4 * W; u += kMeasThreads) {
-            const int list = u / W, pw = u % W;
+            const int list = (u >= 2 * W) ? (u >= 3 * W ? 3 : 2) : (u >= W ? 1 : 0), pw = u - list * W;
             const int h = list & 1;
             u64 bits; int word; u64 bit;
             if (list < 2) {          // row p: old P -> Z_q
@@ -235,9 +271,7 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     }
     // signs, record, counters
     if (warp == 0) {
-        int k = 0;
-        for (int w = lane; w < RW; w += 32) k += __popcll(sm.mask[w]);
-        k = warp_sum(k);
+        const int k = nt;
         if (lane == 0) {
             const int out = counter_bit(a.seed, a.ordinal0 + (uint64_t)jr);
             if (sp != out) atomicXor(a.m.sgn + (p >> 6), 1ull << (p & 63));
@@ -250,34 +284,91 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     __syncthreads();      // smem is restaged by the next measurement
 }
 
-// K4 by a whole CTA: 16 warp partial products, combined by warp 0 (tree reduction; valid
-// because stabilizer rows commute and Pauli multiplication is associative).
+// K4 by a whole CTA: partner list compacted into shared memory, up to 16 warp partial products,
+// combined by warp 0 (tree reduction; valid because stabilizer rows commute and Pauli
+// multiplication is associative).
 __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, int j, const u64* xcol) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     MeasWs* ws = a.ws;
-    u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
-    int k;
-    const int e = det_partial(a.m, xcol, acc_x, acc_x + Wp, lane, warp, kMeasWarps, &k);
-    if (lane == 0) { sm.pe[warp] = e; sm.pk[warp] = k; }
+    if (tid == 0) sm.cnt[0] = 0;
     __syncthreads();
-    if (warp == 0) {
-        int et = 0, kt = 0;
-        for (int t = 0; t < kMeasWarps; ++t) { et += sm.pe[t]; kt += sm.pk[t]; }
-        int g = 0;
-        for (int w = lane; w < W; w += 32) {
-            u64 ax = sm.acc[w], az = sm.acc[Wp + w];
-            for (int t = 1; t < kMeasWarps; ++t) {
-                u64 bx = sm.acc[(size_t)t * 2 * Wp + w], bz = sm.acc[(size_t)t * 2 * Wp + Wp + w];
-                g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+    for (int w = tid; w < W; w += kMeasThreads) {
+        u64 bits = ldcg(xcol + W + w);
+        while (bits) {
+            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            const int ti = atomicAdd(&sm.cnt[0], 1);
+            if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
+        }
+    }
+    __syncthreads();
+    const int total = sm.cnt[0];
+    int done_cnt = 0, et = 0, kt = 0;
+    // lists longer than the smem capacity are consumed in column-order slices (rare: > 2048 partners)
+    for (int base = 0; base < total || base == 0; base += kMaxTargets) {
+        int cnt = min(total - base, kMaxTargets);
+        if (base > 0) {                       // rebuild the slice [base, base+cnt) deterministically by rank
+            __syncthreads();
+            if (tid == 0) sm.cnt[1] = 0;
+            __syncthreads();
+            // rank of a bit = number of set bits before it in column order (warp 0 computes word prefix)
+            for (int w = 0; w < W; ++w) {
+                const u64 bits = ldcg(xcol + W + w);
+                const int pc = __popcll(bits);
+                if (done_cnt + pc > base && done_cnt < base + cnt && tid < 64 && ((bits >> tid) & 1ull)) {
+                    const int r = done_cnt + __popcll(bits & ((1ull << tid) - 1ull));
+                    if (r >= base && r < base + cnt) sm.targets[r - base] = u32(w * 64 + tid);
+                }
+                done_cnt += pc;
             }
+            done_cnt = 0;
+            __syncthreads();
+        } else if (total > kMaxTargets) {     // first slice must also be rank-ordered to make slices disjoint
+            __syncthreads();
+            for (int w = 0; w < W; ++w) {
+                const u64 bits = ldcg(xcol + W + w);
+                const int pc = __popcll(bits);
+                if (done_cnt < cnt && tid < 64 && ((bits >> tid) & 1ull)) {
+                    const int r = done_cnt + __popcll(bits & ((1ull << tid) - 1ull));
+                    if (r < cnt) sm.targets[r] = u32(w * 64 + tid);
+                }
+                done_cnt += pc;
+            }
+            done_cnt = 0;
+            __syncthreads();
         }
-        et = (et + warp_sum(g)) & 3;
-        if (lane == 0) {
-            if (et & 1) atomicOr(&ws->err, 1u);
-            a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
-            atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)kt); atomicAdd(&ws->ncommit, 1u);
+        const int nparts = min(kMeasWarps, max(1, (cnt + 3) / 4));     // at least ~4 rows per working warp
+        u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
+        int k = 0, e = 0;
+        if (warp < nparts) e = det_list_partial(a.m, sm.targets, cnt, warp, nparts, acc_x, acc_x + Wp, lane, &k);
+        if (lane == 0) { sm.pe[warp] = e; sm.pk[warp] = k; }
+        __syncthreads();
+        if (warp == 0) {
+            int g = 0;
+            for (int t = 0; t < nparts; ++t) { et += sm.pe[t]; kt += sm.pk[t]; }
+            // fold partials 1..nparts-1 (and the running product of earlier slices, kept in slot 0 of acc... see below)
+            for (int w = lane; w < W; w += 32) {
+                u64 ax = sm.acc[w], az = sm.acc[Wp + w];
+                for (int t = 1; t < nparts; ++t) {
+                    u64 bx = sm.acc[(size_t)t * 2 * Wp + w], bz = sm.acc[(size_t)t * 2 * Wp + Wp + w];
+                    g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                }
+                if (base > 0) {               // multiply with the product of the previous slices (saved in P/D area)
+                    u64 bx = sm.P[w], bz = sm.P[Wp + w];
+                    g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                }
+                sm.P[w] = ax; sm.P[Wp + w] = az;
+            }
+            et += warp_sum(g);
         }
+        __syncthreads();
+        if (total <= kMaxTargets) break;
+    }
+    if (warp == 0 && lane == 0) {
+        et &= 3;
+        if (et & 1) atomicOr(&ws->err, 1u);
+        a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
+        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)kt); atomicAdd(&ws->ncommit, 1u);
     }
     __syncthreads();
 }
@@ -291,10 +382,16 @@ k_measure_block(MeasArgs a) {
     __shared__ int s_nrun, s_run[kMeasWarps * kSlotsPerWarp];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
     __shared__ u32 s_piv;
+    __shared__ int s_wcnt[kMeasWarps];
+    __shared__ u32 s_wlist[kMeasWarps][kWarpList];
+    __shared__ int s_cnt3[3];
+    __shared__ u32 s_targets[kMaxTargets], s_support[kMaxSupport];
+    __shared__ unsigned short s_mwords[kMaxMaskWords];
     const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
     MeasSmem sm;
     sm.mask = smem; sm.P = sm.mask + RW; sm.D = sm.P + 2 * Wp; sm.acc = sm.D + 2 * Wp;
     sm.mbar = &s_mbar; sm.pe = s_pe; sm.pk = s_pk;
+    sm.cnt = s_cnt3; sm.targets = s_targets; sm.mwords = s_mwords; sm.support = s_support;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int GW = G * kMeasWarps;
@@ -359,7 +456,9 @@ k_measure_block(MeasArgs a) {
             if (piv == 0xfffffffeu) { if (lane == 0) wrun[slot] = 0; continue; }
             const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
             bool blocked = false;
-            int npart = 0;                               // partner rows (destabilizer half population)
+            const bool isdet = piv == 0xffffffffu;
+            if (lane == 0) s_wcnt[warp] = 0;
+            __syncwarp();
             for (int w0 = 0; w0 < RW; w0 += 32 * kColChunk) {
                 u64 cv[kColChunk];
 #pragma unroll
@@ -368,26 +467,29 @@ k_measure_block(MeasArgs a) {
                 for (int t = 0; t < kColChunk; ++t) {
                     const int w = w0 + 32 * t + lane;
                     u64 v = cv[t];
-                    if (w >= W) npart += __popcll(v);
-                    if ((u32)j < r0) continue;
                     const int base = (w < W ? w : w - W) * 64;
+                    const bool chk = (u32)j >= r0;
                     while (v) {
                         int b = __ffsll((long long)v) - 1; v &= v - 1;
-                        const u64 c = ldcg(a.claim + base + b);
-                        if ((u32)(c >> 32) == wave && (0xffffffffu - (u32)c) < (u32)j) blocked = true;
+                        if (isdet) { const int ti = atomicAdd(&s_wcnt[warp], 1); if (ti < kWarpList) s_wlist[warp][ti] = u32(base + b); }
+                        if (chk) {
+                            const u64 c = ldcg(a.claim + base + b);
+                            if ((u32)(c >> 32) == wave && (0xffffffffu - (u32)c) < (u32)j) blocked = true;
+                        }
                     }
                 }
             }
             blocked = __any_sync(0xffffffffu, blocked);
-            if (lane == 0) wrun[slot] = uint8_t(!blocked && piv != 0xffffffffu);
-            if (blocked || piv != 0xffffffffu) continue;
-            npart = warp_sum(npart);
-            if (npart > kHeavyDet) {                  // tree-reduced by the whole CTA below
+            if (lane == 0) wrun[slot] = uint8_t(!blocked && !isdet);
+            if (blocked || !isdet) continue;
+            __syncwarp();
+            const int npart = s_wcnt[warp];
+            if (npart > kWarpList) {                  // tree-reduced by the whole CTA below
                 if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = slot; }
                 continue;
             }
             int k;
-            const int e = det_partial(a.m, xcol, acc_x, acc_z, lane, 0, 1, &k);
+            const int e = det_list_partial(a.m, s_wlist[warp], npart, 0, 1, acc_x, acc_z, lane, &k);
             if (lane == 0) {
                 if (e & 1) atomicOr(&ws->err, 1u);
                 a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1; a.done[j] = 1;
@@ -432,7 +534,7 @@ k_measure_block(MeasArgs a) {
         if (seqlen > 0) {
             if (blockIdx.x == 0) {
                 int j = pos, ran = 0;
-                u64 t0s = gtime(); const long long c0 = clock64();
+                u64 t0s = gtime(); const long long c0 = clock64(); const u64 tseq0 = t0s;
                 for (; j < a.count && ran < seqlen; ++j) {
                     if (__ldcg(a.done + j)) continue;                   // uniform: every thread reads the same byte
                     const u32 q = a.qubits[j];
@@ -448,19 +550,17 @@ k_measure_block(MeasArgs a) {
                     if (lane == 0 && piv != 0xffffffffu) atomicMin(&s_piv, piv);
                     __syncthreads();
                     piv = s_piv;
-                    u64 t1 = gtime();
-                    if (tid == 0) ws->seqprof[0] += t1 - t0s;
+                    u64 t1 = 0, t2 = 0;
+                    if (tid == 0) { t1 = gtime(); ws->seqprof[0] += t1 - t0s; }
                     if (piv == 0xffffffffu) cta_det(a, sm, j, xcol);
                     else cta_random(a, sm, j, q, int(piv), tma_parity);
-                    u64 t2 = gtime();
-                    if (tid == 0) { ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
+                    if (tid == 0) { t2 = gtime(); ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
                     __threadfence();                                    // this measurement's updates before the next column read
                     __syncthreads();
-                    t0s = gtime();
-                    if (tid == 0) ws->seqprof[3] += t0s - t2;
+                    if (tid == 0) { t0s = gtime(); ws->seqprof[3] += t0s - t2; }
                     ++ran;
                 }
-                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - t0s + 0; }
+                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - tseq0; }
             }
             SK_PROF(6);
             if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;

@@ -34,6 +34,8 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
     c->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("SK_SEQ_THRESHOLD")) c->seq_threshold = atoi(e);
+    if (const char* e = getenv("SK_TMA")) c->use_tma = atoi(e);
+    if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
     else {
@@ -179,7 +181,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     int per_sm = 0;
     SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_measure_block, kMeasThreads, t->meas_smem));
     if (per_sm < 1) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "measurement kernel does not fit on an SM"); }
-    t->meas_grid = c->num_sms;
+    t->meas_grid = c->meas_grid_override > 0 ? std::min(c->meas_grid_override, c->num_sms) : c->num_sms;
     int32_t rc = tableau_identity(t);
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out = t;
@@ -369,7 +371,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.claim = t->d_claim; a.wpiv = t->d_wpiv; a.wrun = t->d_wrun; a.done = t->d_done;
-    a.seq_threshold = c->seq_threshold;
+    a.seq_threshold = c->seq_threshold; a.use_tma = c->use_tma;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -554,23 +556,45 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     return SK_OK;
 }
 
-extern "C" int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed) {
+static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, float* class_ms) {
     if (!p || !t) return SK_EARG;
     sk_ctx* c = p->ctx;
     if (t->ctx != c) SK_FAIL(c, SK_EARG, "program and tableau belong to different contexts");
     if (t->n != p->n) SK_FAIL(c, SK_EDIM, "program is for %llu qubits, tableau has %llu", (unsigned long long)p->n, (unsigned long long)t->n);
+    // profiled mode: CUDA events around every op on the launching stream; ms per kernel class
+    // (0 fused layers, 1 transposes, 2 measurement blocks)
+    std::vector<cudaEvent_t> ev; std::vector<int> cls;
+    auto mark = [&](int k) {
+        if (!class_ms) return;
+        cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->stream); ev.push_back(e); cls.push_back(k);
+    };
+    mark(-1);
     for (const ProgOp& op : p->ops) {
         if (op.type == 0) {
             launch_layer(t, p->d_gates + op.off, int(op.count));
+            mark(0);
         } else {
+            if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; mark(1); }
             int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
             if (rc) return rc;
+            mark(2);
         }
     }
     SK_CUDA(c, cudaGetLastError());
     for (int k = 0; k < 12; ++k) c->cnt.gate_hist[k] += p->hist[k];
     p->last_t = t;
+    if (class_ms) {
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        class_ms[0] = class_ms[1] = class_ms[2] = 0.f;
+        for (size_t i = 1; i < ev.size(); ++i) { float ms = 0; cudaEventElapsedTime(&ms, ev[i - 1], ev[i]); class_ms[cls[i]] += ms; }
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
     return SK_OK;
+}
+extern "C" int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed) { return program_run_impl(p, t, seed, nullptr); }
+extern "C" int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[3]) {
+    if (!class_ms) return SK_EARG;
+    return program_run_impl(p, t, seed, class_ms);
 }
 
 extern "C" int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic) {
