@@ -1,7 +1,7 @@
 /* stabkit_b200.h -- C ABI of the B200-native stabilizer-tableau engine.
  *
  * This is the drop-in boundary: the `stabkit::` C++ host classes
- * (include/stabkit/*.hpp) and any foreign binding (ctypes, cgo, JNI ...) call
+ * (the headers under include/stabkit/) and any foreign binding (ctypes, cgo, JNI ...) call
  * ONLY these entry points; behind them are hand-written sm_100a CUDA kernels
  * (paper_2507_03092_b200/csrc/).  There is no CPU fallback: every call that
  * computes fails with SK_ECUDA when no CUDA device is usable.

@@ -380,3 +380,115 @@ class Program:
             self.close()
         except Exception:
             pass
+
+
+class Rows:
+    """Device block of signed n-qubit Pauli rows (sk_rows_*): term lists, T_tab, layers."""
+
+    def __init__(self, ctx: Context, n: int, x=None, z=None, sign=None, capacity: int | None = None):
+        self.ctx, self.n, self.W = ctx, int(n), words_for(int(n))
+        m = 0 if x is None else int(np.asarray(x).reshape(-1, self.W).shape[0])
+        self._h = C.c_void_p()
+        ctx.check(lib().sk_rows_create(ctx._h, n, max(capacity or m, 1), C.byref(self._h)))
+        if x is not None:
+            self.upload(x, z, sign if sign is not None else np.zeros(m, np.uint8))
+
+    def close(self):
+        if self._h and self.ctx._h:
+            lib().sk_rows_destroy(self._h)
+        self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def count(self) -> int:
+        return int(lib().sk_rows_count(self._h))
+
+    def upload(self, x, z, sign):
+        x = np.ascontiguousarray(x, np.uint64).reshape(-1, self.W); z = np.ascontiguousarray(z, np.uint64).reshape(-1, self.W)
+        s = np.ascontiguousarray(sign, np.uint8)
+        self.ctx.check(lib().sk_rows_upload(self._h, _ptr(x), _ptr(z), _ptr(s), x.shape[0]))
+
+    def download(self):
+        m = self.count
+        x = np.zeros((m, self.W), np.uint64); z = np.zeros_like(x); s = np.zeros(m, np.uint8)
+        if m:
+            self.ctx.check(lib().sk_rows_download(self._h, _ptr(x), _ptr(z), _ptr(s)))
+        return x, z, s
+
+    def conj_layer(self, gates):
+        g = gates_array(gates)
+        self.ctx.check(lib().sk_rows_conj_layer(self._h, _ptr(g), len(g)))
+
+    def commutation_vector(self, px, pz) -> np.ndarray:
+        out = np.zeros(max(1, words_for(self.count)), np.uint64)
+        px = np.ascontiguousarray(px, np.uint64); pz = np.ascontiguousarray(pz, np.uint64)
+        self.ctx.check(lib().sk_commutation_vector(self._h, _ptr(px), _ptr(pz), _ptr(out)))
+        return out
+
+    def rowsum_plus_i_where_anticommuting(self, px, pz, psign) -> int:
+        n = C.c_uint64()
+        px = np.ascontiguousarray(px, np.uint64); pz = np.ascontiguousarray(pz, np.uint64)
+        self.ctx.check(lib().sk_rowsum_plus_i_where_anticommuting(self._h, _ptr(px), _ptr(pz), int(psign), C.byref(n)))
+        return int(n.value)
+
+    def find_first_duplicate(self):
+        f, i, j = C.c_int(), C.c_uint64(), C.c_uint64()
+        self.ctx.check(lib().sk_find_first_duplicate(self._h, C.byref(f), C.byref(i), C.byref(j)))
+        return (int(i.value), int(j.value)) if f.value else None
+
+    def weight_sum(self) -> int:
+        o = C.c_uint64()
+        self.ctx.check(lib().sk_weight_sum(self._h, C.byref(o)))
+        return int(o.value)
+
+    def group_first_fit(self, mode: int):
+        g = np.zeros(max(1, self.count), np.uint32); ng = C.c_uint64()
+        self.ctx.check(lib().sk_group_first_fit(self._h, mode, _ptr(g), C.byref(ng)))
+        return g[:self.count], int(ng.value)
+
+    def verify_grouping(self, mode: int, group_of) -> int:
+        g = np.ascontiguousarray(group_of, np.uint32); nv = C.c_uint64()
+        self.ctx.check(lib().sk_verify_grouping(self._h, mode, _ptr(g), C.byref(nv)))
+        return int(nv.value)
+
+
+class Pbc:
+    """Result of sk_transpile (PbcProgram)."""
+
+    def __init__(self, ctx: Context, circ: Circuit):
+        self.ctx, self.n, self.W = ctx, circ.n, words_for(circ.n)
+        self._h = C.c_void_p()
+        ctx.check(lib().sk_transpile(ctx._h, circ.n, _ptr(circ.gates), len(circ.gates), C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().sk_pbc_destroy(self._h)
+        self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        s = (C.c_uint64 * 5)()
+        self.ctx.check(lib().sk_pbc_stats(self._h, s))
+        return dict(zip(["initial_t", "final_rotations_rowcount", "final_rotations_pauliweight", "layers", "passes"], map(int, s)))
+
+    def layer(self, k: int):
+        m = int(lib().sk_pbc_layer_rows(self._h, k))
+        x = np.zeros((m, self.W), np.uint64); z = np.zeros_like(x); s = np.zeros(m, np.uint8)
+        if m:
+            self.ctx.check(lib().sk_pbc_layer_download(self._h, k, _ptr(x), _ptr(z), _ptr(s)))
+        return x, z, s
+
+    def mtab(self):
+        x = np.zeros((2 * self.n, self.W), np.uint64); z = np.zeros_like(x); s = np.zeros(2 * self.n, np.uint8)
+        self.ctx.check(lib().sk_pbc_mtab_download(self._h, _ptr(x), _ptr(z), _ptr(s)))
+        return x, z, s

@@ -20,6 +20,9 @@
 
 namespace skd {
 
+// internal op kinds of the Clifford+T pass (never cross the C ABI): append a T / T-dagger row
+constexpr uint8_t SK_APPEND_T = 12, SK_APPEND_TDG = 13;
+
 __device__ __forceinline__ ulonglong2 ld2(const ulonglong2* p) { return __ldcg(p); }
 __device__ __forceinline__ void st2(ulonglong2* p, ulonglong2 v) { __stcg(p, v); }
 __device__ __forceinline__ bool nz2(ulonglong2 v) { return (v.x | v.y) != 0; }
@@ -88,6 +91,15 @@ k_layer(u64* __restrict__ cols, u64* __restrict__ sgn, const sk_gate* __restrict
                     ulonglong2 x0 = ld2(xa), x1 = ld2(xb), z0 = ld2(za), z1 = ld2(zb);
                     if (nz2(x0 ^ x1)) { st2(xa, x1); st2(xb, x0); }
                     if (nz2(z0 ^ z1)) { st2(za, z1); st2(zb, z0); }
+                } break;
+                case SK_APPEND_T: case SK_APPEND_TDG: {      // Algorithm 2: new row q1 := (+|-) Z_q0 (row was all-zero)
+                    if (int(G.q1 >> 7) == v) {
+                        ulonglong2 z = ld2(za);
+                        const unsigned long long bit = 1ull << (G.q1 & 63);
+                        if (G.q1 & 64) { z.y |= bit; if (G.kind == SK_APPEND_TDG) s.y ^= bit; }
+                        else { z.x |= bit; if (G.kind == SK_APPEND_TDG) s.x ^= bit; }
+                        st2(za, z);
+                    }
                 } break;
                 default: break;
             }

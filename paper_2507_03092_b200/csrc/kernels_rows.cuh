@@ -141,14 +141,13 @@ k_dup_rank(const u64* __restrict__ rows, int Wp, int W, int nrows, const u64* __
 // bitmap[(t - t0) * GW32 + (g >> 5)] bit (g & 31) = term t conflicts with a member of group g.
 // Thread per earlier term m (coalesced load of its words + group id), block terms broadcast from smem.
 __global__ void __launch_bounds__(256)
-k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, const u32* __restrict__ group_of,
+k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int Bt, const u32* __restrict__ group_of,
                   int mode, u32* __restrict__ bitmap, int GW32) {
-    extern __shared__ u64 s_blk[];          // [Bt][2*W]
-    const int Bt = blockDim.y;              // block terms staged per CTA row (gridDim.y tiles B)
-    const int tb = t0 + blockIdx.y * Bt;
+    extern __shared__ u64 s_blk[];          // [Bt][2*W]: x words then z words of each staged block term
+    const int tb = t0 + blockIdx.y * Bt;    // first block term of this tile
     for (int i = threadIdx.x; i < Bt * 2 * W; i += blockDim.x) {
-        int k = i / (2 * W), w = i % (2 * W);
-        int t = tb + k;
+        const int k = i / (2 * W), w = i % (2 * W);
+        const int t = tb + k;
         s_blk[i] = (t < t0 + B) ? rows[(size_t)(2 * t + (w >= W)) * Wp + (w % W)] : 0;
     }
     __syncthreads();
@@ -216,6 +215,19 @@ k_verify_grouping(const u64* __restrict__ rows, int Wp, int W, int nrows, const 
         bad += conflict_words(a, a + Wp, b, b + Wp, W, mode);
     }
     if (bad) atomicAdd(nviol, bad);
+}
+
+// copy rows idx[k] (x and z halves) into a dense push list  out[k][2*Wp]
+__global__ void k_gather_rows(const u64* __restrict__ rows, int Wp, const int* __restrict__ idx, int count, u64* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)count * 2 * Wp) return;
+    const int k = int(i / (2 * Wp)), w = int(i % (2 * Wp));
+    out[i] = rows[(size_t)(2 * idx[k]) * Wp + w];
+}
+// min over j of (pair_first[j] << 32 | j) for pair_first[j] >= 0
+__global__ void k_min_pair(const int* __restrict__ pair_first, int nrows, unsigned long long* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nrows && pair_first[j] >= 0) atomicMin(out, ((unsigned long long)(u32)pair_first[j] << 32) | (u32)j);
 }
 
 }  // namespace skd

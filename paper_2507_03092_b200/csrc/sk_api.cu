@@ -626,3 +626,5 @@ extern "C" int32_t sk_sim(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ng
     *out_t = t;
     return SK_OK;
 }
+
+#include "sk_rows_impl.cuh"

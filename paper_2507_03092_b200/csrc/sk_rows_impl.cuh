@@ -1,0 +1,589 @@
+// sk_rows_impl.cuh -- C ABI part 2 (included by sk_api.cu): device Pauli row sets, grouping
+// and the Clifford+T -> PBC pass (Algorithms 2-4).
+// Host orchestration only; kernels are in kernels_rows.cuh / kernels_layer.cuh / kernels_transpose.cuh.
+#pragma once
+#include <climits>
+#include <numeric>
+
+#include "kernels_rows.cuh"
+
+// ---- generic C/R store helpers (any row-bit count; no stabilizer/destabilizer split) -----------
+static int32_t dm_transpose_c2r(sk_ctx* c, const DMat& m) {
+    const u32* src = reinterpret_cast<const u32*>(m.cols);
+    u32* dst = reinterpret_cast<u32*>(m.rows);
+    for (int h = 0; h < 2; ++h) {
+        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * m.RW, (size_t)4 * m.RW, int(m.n), 2 * m.RW,
+                                      dst + (size_t)h * 2 * m.Wp, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp);
+        if (rc) return rc;
+    }
+    c->cnt.transposes++;
+    return SK_OK;
+}
+static int32_t dm_transpose_r2c(sk_ctx* c, const DMat& m) {
+    const u32* src = reinterpret_cast<const u32*>(m.rows);
+    u32* dst = reinterpret_cast<u32*>(m.cols);
+    for (int h = 0; h < 2; ++h) {
+        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * m.Wp, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp,
+                                      dst + (size_t)h * 2 * m.RW, (size_t)4 * m.RW, int(m.n), 2 * m.RW);
+        if (rc) return rc;
+    }
+    c->cnt.transposes++;
+    return SK_OK;
+}
+static void dm_launch_layer(sk_ctx* c, const DMat& m, const sk_gate* d_gates, int ngates) {
+    const int RW2 = m.RW / 2;
+    int threads = std::min(256, std::max(32, (RW2 + 31) & ~31));
+    int target_ctas = c->num_sms * std::max(1, 1536 / threads);
+    int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
+    int grid = (ngates + gpb - 1) / gpb;
+    k_layer<<<grid, threads, 0, c->stream>>>(m.cols, m.sgn, d_gates, ngates, m.RW, gpb);
+    c->cnt.kernel_launches++; c->cnt.layers++;
+}
+template <class... A> static void launch_push(sk_ctx* c, int W, int nrows, A... args) {
+    const int wpl = (W + 31) / 32;
+    dim3 grid((unsigned)((nrows * 32 + 255) / 256));
+    if (wpl <= 1) k_push_through<1><<<grid, 256, 0, c->stream>>>(args...);
+    else if (wpl <= 2) k_push_through<2><<<grid, 256, 0, c->stream>>>(args...);
+    else if (wpl <= 4) k_push_through<4><<<grid, 256, 0, c->stream>>>(args...);
+    else if (wpl <= 8) k_push_through<8><<<grid, 256, 0, c->stream>>>(args...);
+    else k_push_through<16><<<grid, 256, 0, c->stream>>>(args...);
+    c->cnt.kernel_launches++;
+}
+
+// first-fit over rows [0, count) of an R-form array (K5 bitmap + resolver, block by block).
+// d_group: device u32[count] (output).  Returns the number of groups.
+static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int count, int mode, u32* d_group, uint64_t* ngroups) {
+    *ngroups = 0;
+    if (count == 0) return SK_OK;
+    const int B = std::min(count, 1024);
+    const int GW32 = count / 32 + 2;
+    u32* d_bitmap = nullptr; u32* d_ng = nullptr;
+    SK_CUDA(c, cudaMalloc(&d_bitmap, (size_t)B * GW32 * 4));
+    SK_CUDA(c, cudaMalloc(&d_ng, 4));
+    SK_CUDA(c, cudaMemsetAsync(d_ng, 0, 4, c->stream));
+    const int Bt = std::max(1, std::min(B, (40 * 1024) / (2 * W * 8)));     // block terms staged per CTA (<= 40 KB smem)
+    const size_t smem = (size_t)Bt * 2 * W * 8;
+    if (smem > 48 * 1024) { cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_EDIM, "rows too wide for the conflict kernel (W=%d)", W); }
+    for (int t0 = 0; t0 < count; t0 += B) {
+        const int b = std::min(B, count - t0);
+        SK_CUDA(c, cudaMemsetAsync(d_bitmap, 0, (size_t)b * GW32 * 4, c->stream));
+        if (t0 > 0) {
+            dim3 grid((t0 + 255) / 256, (b + Bt - 1) / Bt);
+            k_conflict_bitmap<<<grid, 256, smem, c->stream>>>(d_rows, Wp, W, t0, b, Bt, d_group, mode, d_bitmap, GW32);
+            c->cnt.kernel_launches++;
+        }
+        k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng);
+        c->cnt.kernel_launches++;
+    }
+    SK_CUDA(c, cudaGetLastError());
+    u32 ng = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&ng, d_ng, 4, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(d_bitmap); cudaFree(d_ng);
+    *ngroups = ng;
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------------------- sk_rows ------
+struct sk_rows {
+    sk_ctx* ctx = nullptr;
+    uint64_t n = 0, cap = 0, count = 0;
+    DMat m;                      // rows (R) always allocated; cols (C) on first conj_layer
+    bool r_valid = true, c_valid = false;
+    size_t rows_bytes = 0, cols_bytes = 0, sgn_bytes = 0;
+};
+
+extern "C" int32_t sk_rows_create(sk_ctx* c, uint64_t n, uint64_t capacity, sk_rows** out) {
+    if (!c || !out) return SK_EARG;
+    *out = nullptr;
+    if (n == 0) SK_FAIL(c, SK_EDIM, "rows: n must be >= 1");
+    if (capacity == 0) capacity = 1;
+    if (capacity > (1ull << 26)) SK_FAIL(c, SK_EDIM, "rows: capacity %llu too large", (unsigned long long)capacity);
+    sk_rows* r = new sk_rows();
+    r->ctx = c; r->n = n; r->cap = capacity;
+    r->m.n = n; r->m.W = uint32_t((n + 63) / 64); r->m.Wp = (r->m.W + 1) & ~1u;
+    r->m.RW = uint32_t(((capacity + 63) / 64 + 1) & ~1ull);
+    r->rows_bytes = (size_t)64 * r->m.RW * 2 * r->m.Wp * 8;
+    r->cols_bytes = (size_t)n * 2 * r->m.RW * 8;
+    r->sgn_bytes = (size_t)r->m.RW * 8;
+    if (cudaMalloc(&r->m.rows, r->rows_bytes) || cudaMalloc(&r->m.sgn, r->sgn_bytes)) { sk_rows_destroy(r); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for %llu rows", (unsigned long long)capacity); }
+    SK_CUDA(c, cudaMemsetAsync(r->m.rows, 0, r->rows_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(r->m.sgn, 0, r->sgn_bytes, c->stream));
+    *out = r;
+    return SK_OK;
+}
+extern "C" void sk_rows_destroy(sk_rows* r) {
+    if (!r) return;
+    cudaSetDevice(r->ctx->device);
+    cudaStreamSynchronize(r->ctx->stream);
+    cudaFree(r->m.rows); cudaFree(r->m.cols); cudaFree(r->m.sgn);
+    delete r;
+}
+extern "C" uint64_t sk_rows_count(const sk_rows* r) { return r ? r->count : 0; }
+
+static int32_t rows_need_r(sk_rows* r) {
+    if (r->r_valid) return SK_OK;
+    int32_t rc = dm_transpose_c2r(r->ctx, r->m);
+    if (!rc) r->r_valid = true;
+    return rc;
+}
+static int32_t rows_need_c(sk_rows* r) {
+    sk_ctx* c = r->ctx;
+    if (!r->m.cols) SK_CUDA(c, cudaMalloc(&r->m.cols, r->cols_bytes));
+    if (r->c_valid) return SK_OK;
+    int32_t rc = dm_transpose_r2c(c, r->m);
+    if (!rc) r->c_valid = true;
+    return rc;
+}
+
+extern "C" int32_t sk_rows_upload(sk_rows* r, const uint64_t* x, const uint64_t* z, const uint8_t* sign, uint64_t m) {
+    if (!r || (m && (!x || !z || !sign))) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    if (m > r->cap) SK_FAIL(c, SK_EDIM, "rows: %llu rows exceed the capacity %llu", (unsigned long long)m, (unsigned long long)r->cap);
+    const int W = r->m.W; const size_t words = (size_t)m * W;
+    SK_CUDA(c, cudaMemsetAsync(r->m.rows, 0, r->rows_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(r->m.sgn, 0, r->sgn_bytes, c->stream));
+    if (m) {
+        int32_t rc = sk_ctx_reserve_tmp(c, words * 16 + m + 64);
+        if (rc) return rc;
+        u64* dx = (u64*)c->d_tmp; u64* dz = dx + words; uint8_t* ds = (uint8_t*)(dz + words);
+        SK_CUDA(c, cudaMemcpyAsync(dx, x, words * 8, cudaMemcpyHostToDevice, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(dz, z, words * 8, cudaMemcpyHostToDevice, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(ds, sign, m, cudaMemcpyHostToDevice, c->stream));
+        k_pack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(dx, dz, r->m.rows, int(m), W, r->m.Wp, int(m), 0);
+        k_bytes_to_signs<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(ds, r->m.sgn, int(m), int(m), 0);
+        c->cnt.kernel_launches += 2;
+        SK_CUDA(c, cudaGetLastError());
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    r->count = m; r->r_valid = true; r->c_valid = false;
+    return SK_OK;
+}
+extern "C" int32_t sk_rows_download(sk_rows* r, uint64_t* x, uint64_t* z, uint8_t* sign) {
+    if (!r) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    const uint64_t m = r->count;
+    if (m == 0) return SK_OK;
+    if (!x || !z || !sign) return SK_EARG;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    const int W = r->m.W; const size_t words = (size_t)m * W;
+    rc = sk_ctx_reserve_tmp(c, words * 16 + m + 64);
+    if (rc) return rc;
+    u64* dx = (u64*)c->d_tmp; u64* dz = dx + words; uint8_t* ds = (uint8_t*)(dz + words);
+    k_unpack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(r->m.rows, dx, dz, int(m), W, r->m.Wp, int(m), 0);
+    k_signs_to_bytes<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(r->m.sgn, ds, int(m), int(m), 0);
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaMemcpyAsync(x, dx, words * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(z, dz, words * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(sign, ds, m, cudaMemcpyDeviceToHost, c->stream));
+    return check_ws(c);
+}
+
+extern "C" int32_t sk_rows_conj_layer(sk_rows* r, const sk_gate* gates, size_t ngates) {
+    if (!r || (!gates && ngates)) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    if (ngates == 0 || r->count == 0) return SK_OK;
+    for (size_t i = 0; i < ngates; ++i) {
+        int32_t rc = validate_gate(c, gates[i], r->n, i);
+        if (rc) return rc;
+        if (gates[i].kind >= SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: only Clifford gates conjugate a row set (SPEC:518)", i);
+    }
+    int32_t rc = rows_need_c(r);
+    if (rc) return rc;
+    std::vector<sk_gate> ordered; std::vector<uint32_t> sizes, scratch;
+    sk_layer_run(gates, ngates, r->n, scratch, ordered, sizes);
+    rc = sk_ctx_reserve_gates(c, ngates * sizeof(sk_gate));
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemcpyAsync(c->d_gates, ordered.data(), ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+    size_t off = 0;
+    for (uint32_t s : sizes) { dm_launch_layer(c, r->m, (const sk_gate*)c->d_gates + off, int(s)); off += s; }
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    r->r_valid = false;
+    return SK_OK;
+}
+
+// uploads p as [x Wp | z Wp] into the tmp buffer at byte offset `at`
+static int32_t upload_pauli(sk_ctx* c, const DMat& m, const uint64_t* px, const uint64_t* pz, u64* d_p) {
+    std::vector<u64> h(2 * m.Wp, 0);
+    for (uint32_t w = 0; w < m.W; ++w) { h[w] = px[w]; h[m.Wp + w] = pz[w]; }
+    SK_CUDA(c, cudaMemcpyAsync(d_p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));      // h dies at return
+    return SK_OK;
+}
+
+extern "C" int32_t sk_commutation_vector(sk_rows* r, const uint64_t* px, const uint64_t* pz, uint64_t* out_bits) {
+    if (!r || !px || !pz || !out_bits) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    const int m = int(r->count);
+    if (m == 0) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    const size_t ow = (size_t)(m + 63) / 64;
+    rc = sk_ctx_reserve_tmp(c, (2 * r->m.Wp + ow + 8) * 8);
+    if (rc) return rc;
+    u64* d_p = (u64*)c->d_tmp; u64* d_out = d_p + 2 * r->m.Wp;
+    rc = upload_pauli(c, r->m, px, pz, d_p);
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemsetAsync(d_out, 0, ow * 8, c->stream));
+    k_commutation_vector<<<(unsigned)((m * 32 + 255) / 256), 256, 0, c->stream>>>(r->m.rows, r->m.Wp, r->m.W, m, d_p, d_out);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaMemcpyAsync(out_bits, d_out, ow * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+extern "C" int32_t sk_rowsum_plus_i_where_anticommuting(sk_rows* r, const uint64_t* px, const uint64_t* pz,
+                                                        uint8_t psign, uint64_t* n_updated) {
+    if (!r || !px || !pz) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    if (n_updated) *n_updated = 0;
+    const int m = int(r->count);
+    if (m == 0) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    rc = sk_ctx_reserve_tmp(c, (2 * r->m.Wp + 8) * 8);
+    if (rc) return rc;
+    u64* d_p = (u64*)c->d_tmp; unsigned long long* d_n = (unsigned long long*)(d_p + 2 * r->m.Wp); uint8_t* d_s = (uint8_t*)(d_n + 1);
+    rc = upload_pauli(c, r->m, px, pz, d_p);
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemsetAsync(d_n, 0, 8, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_s, &psign, 1, cudaMemcpyHostToDevice, c->stream));
+    launch_push(c, r->m.W, m, r->m.rows, r->m.sgn, int(r->m.Wp), int(r->m.W), 0, m, (const int*)nullptr, (const u64*)d_p,
+                (const uint8_t*)d_s, (const int*)nullptr, 1, c->d_err, d_n);
+    SK_CUDA(c, cudaGetLastError());
+    unsigned long long hn = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&hn, d_n, 8, cudaMemcpyDeviceToHost, c->stream));
+    r->c_valid = false;
+    rc = check_ws(c);
+    if (n_updated) *n_updated = hn;
+    return rc;
+}
+
+static int32_t dup_pairs(sk_ctx* c, const u64* d_rows, int Wp, int W, int m, const int* d_lvl, int* d_pair /* [m] */, u64* d_hash /* [m] */) {
+    k_row_hash<<<(unsigned)((m * 32 + 255) / 256), 256, 0, c->stream>>>(d_rows, Wp, W, m, d_hash);
+    k_dup_rank<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(d_rows, Wp, W, m, d_hash, d_lvl, d_pair);
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    return SK_OK;
+}
+
+extern "C" int32_t sk_find_first_duplicate(sk_rows* r, int* found, uint64_t* i, uint64_t* j) {
+    if (!r || !found || !i || !j) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    *found = 0;
+    const int m = int(r->count);
+    if (m < 2) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    rc = sk_ctx_reserve_tmp(c, (size_t)m * 12 + 64);
+    if (rc) return rc;
+    u64* d_hash = (u64*)c->d_tmp; int* d_pair = (int*)(d_hash + m); unsigned long long* d_min = (unsigned long long*)(d_hash + m + (m + 1) / 2 + 1);
+    rc = dup_pairs(c, r->m.rows, r->m.Wp, r->m.W, m, nullptr, d_pair, d_hash);
+    if (rc) return rc;
+    SK_CUDA(c, cudaMemsetAsync(d_min, 0xFF, 8, c->stream));
+    k_min_pair<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(d_pair, m, d_min);
+    c->cnt.kernel_launches++;
+    unsigned long long key = ~0ull;
+    SK_CUDA(c, cudaMemcpyAsync(&key, d_min, 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (key != ~0ull) { *found = 1; *i = key >> 32; *j = key & 0xffffffffu; }
+    return SK_OK;
+}
+
+extern "C" int32_t sk_weight_sum(sk_rows* r, uint64_t* out) {
+    if (!r || !out) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    *out = 0;
+    const int m = int(r->count);
+    if (m == 0) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    rc = sk_ctx_reserve_tmp(c, 64);
+    if (rc) return rc;
+    unsigned long long* d_o = (unsigned long long*)c->d_tmp;
+    SK_CUDA(c, cudaMemsetAsync(d_o, 0, 8, c->stream));
+    k_weight_sum<<<std::min(1024, (m * int(r->m.W) + 255) / 256), 256, 0, c->stream>>>(r->m.rows, r->m.Wp, r->m.W, m, nullptr, d_o);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    unsigned long long h = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&h, d_o, 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    *out = h;
+    return SK_OK;
+}
+
+extern "C" int32_t sk_group_first_fit(sk_rows* r, int mode, uint32_t* group_of, uint64_t* ngroups) {
+    if (!r || !group_of || !ngroups || (mode != 0 && mode != 1)) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    *ngroups = 0;
+    const int m = int(r->count);
+    if (m == 0) SK_FAIL(c, SK_EARG, "group_greedy: empty input (SPEC:448)");
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    u32* d_group = nullptr;
+    SK_CUDA(c, cudaMalloc(&d_group, (size_t)m * 4));
+    rc = device_first_fit(c, r->m.rows, r->m.Wp, r->m.W, m, mode, d_group, ngroups);
+    if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(group_of, d_group, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream);
+        if (!e) e = cudaStreamSynchronize(c->stream);
+        if (e) { cudaFree(d_group); SK_FAIL(c, SK_ECUDA, "group download: %s", cudaGetErrorString(e)); }
+    }
+    cudaFree(d_group);
+    return rc;
+}
+
+extern "C" int32_t sk_verify_grouping(sk_rows* r, int mode, const uint32_t* group_of, uint64_t* nviolations) {
+    if (!r || !group_of || !nviolations || (mode != 0 && mode != 1)) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    *nviolations = 0;
+    const int m = int(r->count);
+    if (m == 0) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    rc = sk_ctx_reserve_tmp(c, (size_t)m * 4 + 64);
+    if (rc) return rc;
+    unsigned long long* d_n = (unsigned long long*)c->d_tmp; u32* d_g = (u32*)(d_n + 1);
+    SK_CUDA(c, cudaMemsetAsync(d_n, 0, 8, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_g, group_of, (size_t)m * 4, cudaMemcpyHostToDevice, c->stream));
+    k_verify_grouping<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(r->m.rows, r->m.Wp, r->m.W, m, d_g, mode, d_n);
+    c->cnt.kernel_launches++;
+    SK_CUDA(c, cudaGetLastError());
+    unsigned long long h = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&h, d_n, 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    *nviolations = h;
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------------------- transpile ----
+struct sk_pbc {
+    sk_ctx* ctx = nullptr;
+    uint64_t n = 0; int W = 0;
+    uint64_t stats[5] = {0, 0, 0, 0, 0};
+    std::vector<std::vector<uint32_t>> layers;        // T-row ids per layer, forward time order
+    std::vector<u64> tx, tz; std::vector<uint8_t> ts; // all T rows (row-major, W words), host cache
+    std::vector<u64> mx, mz; std::vector<uint8_t> ms; // final M_tab, 2n rows
+};
+extern "C" void sk_pbc_destroy(sk_pbc* p) { delete p; }
+extern "C" int32_t sk_pbc_stats(sk_pbc* p, uint64_t out5[5]) { if (!p || !out5) return SK_EARG; for (int k = 0; k < 5; ++k) out5[k] = p->stats[k]; return SK_OK; }
+extern "C" uint64_t sk_pbc_layer_rows(sk_pbc* p, uint64_t layer) { return (p && layer < p->layers.size()) ? p->layers[layer].size() : 0; }
+extern "C" int32_t sk_pbc_layer_download(sk_pbc* p, uint64_t layer, uint64_t* x, uint64_t* z, uint8_t* sign) {
+    if (!p || layer >= p->layers.size() || !x || !z || !sign) return SK_EARG;
+    const auto& L = p->layers[layer];
+    for (size_t k = 0; k < L.size(); ++k) {
+        std::copy(&p->tx[(size_t)L[k] * p->W], &p->tx[(size_t)L[k] * p->W] + p->W, x + k * p->W);
+        std::copy(&p->tz[(size_t)L[k] * p->W], &p->tz[(size_t)L[k] * p->W] + p->W, z + k * p->W);
+        sign[k] = p->ts[L[k]];
+    }
+    return SK_OK;
+}
+extern "C" int32_t sk_pbc_mtab_download(sk_pbc* p, uint64_t* x, uint64_t* z, uint8_t* sign) {
+    if (!p || !x || !z || !sign) return SK_EARG;
+    std::copy(p->mx.begin(), p->mx.end(), x); std::copy(p->mz.begin(), p->mz.end(), z); std::copy(p->ms.begin(), p->ms.end(), sign);
+    return SK_OK;
+}
+
+extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out) {
+    if (!c || !out || (!gates && ngates)) return SK_EARG;
+    *out = nullptr;
+    if (n == 0) SK_FAIL(c, SK_EDIM, "transpile: circuit has zero qubits");
+    size_t end = ngates;
+    while (end > 0 && gates[end - 1].kind == SK_M) --end;                    // terminal measurements are stripped
+    size_t nT = 0;
+    for (size_t i = 0; i < end; ++i) {
+        int32_t rc = validate_gate(c, gates[i], n, i);
+        if (rc) return rc;
+        if (gates[i].kind == SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: mid-circuit measurement is not supported by the transpiler (SPEC:519)", i);
+        nT += (gates[i].kind == SK_T || gates[i].kind == SK_TDG);
+    }
+    // ---- Algorithm 2 on one C-form matrix: M_tab rows (stab [0,n), destab [NS,NS+n)) and the T rows
+    //      at row-bits 2*NS + k, k = index of the T gate in forward time.  Unappended rows are all-zero,
+    //      i.e. identity, and every Clifford rule maps identity to identity with sign 0, so "apply G to
+    //      the rows appended so far" is simply "apply G to all rows".
+    DMat m; m.n = n; m.W = uint32_t((n + 63) / 64); m.Wp = (m.W + 1) & ~1u;
+    const int W = m.W, NS = 64 * W, T0 = 2 * NS;
+    m.RW = uint32_t((2 * W + (nT + 63) / 64 + 1) & ~1ull);
+    const size_t cols_bytes = (size_t)n * 2 * m.RW * 8, rows_bytes = (size_t)64 * m.RW * 2 * m.Wp * 8, sgn_bytes = (size_t)m.RW * 8;
+    struct Guard { DMat* m; std::vector<void*> extra; ~Guard() { cudaFree(m->cols); cudaFree(m->rows); cudaFree(m->sgn); for (void* p : extra) cudaFree(p); } } guard{&m, {}};
+    SK_CUDA(c, cudaMalloc(&m.cols, cols_bytes));
+    SK_CUDA(c, cudaMalloc(&m.rows, rows_bytes));
+    SK_CUDA(c, cudaMalloc(&m.sgn, sgn_bytes));
+    SK_CUDA(c, cudaMemsetAsync(m.cols, 0, cols_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(m.rows, 0, rows_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(m.sgn, 0, sgn_bytes, c->stream));
+    k_identity<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(m.cols, m.rows, int(n), m.RW, m.Wp, NS);
+    c->cnt.kernel_launches++;
+    {
+        std::vector<sk_gate> rev; rev.reserve(end);
+        size_t tk = nT;
+        for (size_t k = end; k-- > 0;) {
+            sk_gate g = gates[k];
+            if (g.kind == SK_T || g.kind == SK_TDG) { --tk; g.kind = (g.kind == SK_T) ? SK_APPEND_T : SK_APPEND_TDG; g.q1 = uint32_t(T0 + tk); }
+            rev.push_back(g);
+        }
+        std::vector<sk_gate> ordered; std::vector<uint32_t> sizes, scratch;
+        sk_layer_run(rev.data(), rev.size(), n, scratch, ordered, sizes);   // append ops are single-qubit ops on q0
+        if (!ordered.empty()) {
+            int32_t rc = sk_ctx_reserve_gates(c, ordered.size() * sizeof(sk_gate));
+            if (rc) return rc;
+            SK_CUDA(c, cudaMemcpyAsync(c->d_gates, ordered.data(), ordered.size() * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+            size_t off = 0;
+            for (uint32_t s : sizes) { dm_launch_layer(c, m, (const sk_gate*)c->d_gates + off, int(s)); off += s; }
+            SK_CUDA(c, cudaGetLastError());
+            SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        }
+    }
+    int32_t rc = dm_transpose_c2r(c, m);
+    if (rc) return rc;
+    u64* rowsT = m.rows + (size_t)2 * T0 * m.Wp;                             // R-form view of the T rows
+    sk_pbc* p = new sk_pbc();
+    p->ctx = c; p->n = n; p->W = W; p->stats[0] = nT;
+    std::vector<int> lvl(nT, 0);
+    uint64_t passes = 0;
+    if (nT > 0) {
+        // ---- Algorithm 3: first fit (GC) in forward time order == T-row id order
+        u32* d_group = nullptr; int* d_lvl = nullptr; int* d_pair = nullptr; u64* d_hash = nullptr;
+        SK_CUDA(c, cudaMalloc(&d_group, nT * 4)); guard.extra.push_back(d_group);
+        SK_CUDA(c, cudaMalloc(&d_lvl, nT * 4)); guard.extra.push_back(d_lvl);
+        SK_CUDA(c, cudaMalloc(&d_pair, nT * 4)); guard.extra.push_back(d_pair);
+        SK_CUDA(c, cudaMalloc(&d_hash, nT * 8)); guard.extra.push_back(d_hash);
+        uint64_t nl = 0;
+        rc = device_first_fit(c, rowsT, m.Wp, W, int(nT), 0, d_group, &nl);
+        if (rc) { delete p; return rc; }
+        SK_CUDA(c, cudaMemcpyAsync(lvl.data(), d_group, nT * 4, cudaMemcpyDeviceToHost, c->stream));
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        // ---- Algorithm 4, one pass = pairs from the pass-start state + ordered push-through
+        std::vector<int> pair(nT); std::vector<u64> sg(m.RW);
+        for (;;) {
+            ++passes;
+            SK_CUDA(c, cudaMemcpyAsync(d_lvl, lvl.data(), nT * 4, cudaMemcpyHostToDevice, c->stream));
+            rc = dup_pairs(c, rowsT, m.Wp, W, int(nT), d_lvl, d_pair, d_hash);
+            if (rc) { delete p; return rc; }
+            SK_CUDA(c, cudaMemcpyAsync(pair.data(), d_pair, nT * 4, cudaMemcpyDeviceToHost, c->stream));
+            SK_CUDA(c, cudaMemcpyAsync(sg.data(), m.sgn, sgn_bytes, cudaMemcpyDeviceToHost, c->stream));
+            SK_CUDA(c, cudaStreamSynchronize(c->stream));
+            auto sign_of = [&](int k) { const int rb = T0 + k; return int((sg[rb >> 6] >> (rb & 63)) & 1ull); };
+            struct Push { int level, first, sign; };
+            std::vector<Push> pushes; bool any = false;
+            for (size_t j = 0; j < nT; ++j) {
+                if (pair[j] < 0) continue;
+                any = true;
+                const int i = pair[j];
+                if (sign_of(i) == sign_of(int(j))) pushes.push_back({lvl[i], i, sign_of(i)});   // equal signs: quarter rotation
+                // opposite signs cancel; either way both rows leave the layer
+            }
+            if (!any) break;
+            std::sort(pushes.begin(), pushes.end(), [](const Push& a, const Push& b) { return a.level != b.level ? a.level > b.level : a.first < b.first; });
+            const int np = int(pushes.size());
+            if (np > 0) {
+                std::vector<int> idx(np), plevel(np); std::vector<uint8_t> psign(np);
+                for (int k = 0; k < np; ++k) { idx[k] = pushes[k].first; plevel[k] = pushes[k].level; psign[k] = uint8_t(pushes[k].sign); }
+                const size_t need = (size_t)np * 2 * m.Wp * 8 + (size_t)np * 9 + 256;
+                rc = sk_ctx_reserve_tmp(c, need);
+                if (rc) { delete p; return rc; }
+                u64* d_push = (u64*)c->d_tmp; int* d_idx = (int*)(d_push + (size_t)np * 2 * m.Wp); int* d_plevel = d_idx + np; uint8_t* d_psign = (uint8_t*)(d_plevel + np);
+                SK_CUDA(c, cudaMemcpyAsync(d_idx, idx.data(), np * 4, cudaMemcpyHostToDevice, c->stream));
+                SK_CUDA(c, cudaMemcpyAsync(d_plevel, plevel.data(), np * 4, cudaMemcpyHostToDevice, c->stream));
+                SK_CUDA(c, cudaMemcpyAsync(d_psign, psign.data(), np, cudaMemcpyHostToDevice, c->stream));
+                k_gather_rows<<<(unsigned)(((size_t)np * 2 * m.Wp + 255) / 256), 256, 0, c->stream>>>(rowsT, m.Wp, d_idx, np, d_push);
+                c->cnt.kernel_launches++;
+                for (size_t j = 0; j < nT; ++j) if (pair[j] >= 0) { lvl[j] = -1; lvl[pair[j]] = -1; }
+                SK_CUDA(c, cudaMemcpyAsync(d_lvl, lvl.data(), nT * 4, cudaMemcpyHostToDevice, c->stream));
+                // T rows of later layers, then both halves of M_tab (every push reaches the measurement end)
+                launch_push(c, W, int(nT), m.rows, m.sgn, int(m.Wp), W, T0, int(nT), (const int*)d_lvl, (const u64*)d_push,
+                            (const uint8_t*)d_psign, (const int*)d_plevel, np, c->d_err, (unsigned long long*)nullptr);
+                launch_push(c, W, int(n), m.rows, m.sgn, int(m.Wp), W, 0, int(n), (const int*)nullptr, (const u64*)d_push,
+                            (const uint8_t*)d_psign, (const int*)nullptr, np, c->d_err, (unsigned long long*)nullptr);
+                launch_push(c, W, int(n), m.rows, m.sgn, int(m.Wp), W, NS, int(n), (const int*)nullptr, (const u64*)d_push,
+                            (const uint8_t*)d_psign, (const int*)nullptr, np, c->d_err, (unsigned long long*)nullptr);
+                SK_CUDA(c, cudaGetLastError());
+                SK_CUDA(c, cudaStreamSynchronize(c->stream));       // host vectors die at scope end
+            } else {
+                for (size_t j = 0; j < nT; ++j) if (pair[j] >= 0) { lvl[j] = -1; lvl[pair[j]] = -1; }
+            }
+        }
+    }
+    rc = check_ws(c);
+    if (rc) { delete p; return rc; }
+    // ---- read back: T rows (host cache), M_tab
+    {
+        const size_t words = nT * (size_t)W;
+        p->tx.assign(words, 0); p->tz.assign(words, 0); p->ts.assign(nT, 0);
+        p->mx.assign(2 * n * W, 0); p->mz.assign(2 * n * W, 0); p->ms.assign(2 * n, 0);
+        const size_t total_rows = 2 * n + nT, tw = total_rows * W;
+        rc = sk_ctx_reserve_tmp(c, tw * 16 + total_rows + 64);
+        if (rc) { delete p; return rc; }
+        u64* dx = (u64*)c->d_tmp; u64* dz = dx + tw; uint8_t* ds = (uint8_t*)(dz + tw);
+        // M_tab with the tableau split mapping, then the T rows with a flat mapping shifted by T0
+        k_unpack_rows<<<(unsigned)((2 * n * W + 255) / 256), 256, 0, c->stream>>>(m.rows, dx, dz, int(2 * n), W, m.Wp, int(n), NS);
+        k_signs_to_bytes<<<(unsigned)((2 * n + 255) / 256), 256, 0, c->stream>>>(m.sgn, ds, int(2 * n), int(n), NS);
+        if (nT) {
+            k_unpack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(rowsT, dx + 2 * n * W, dz + 2 * n * W, int(nT), W, m.Wp, int(nT), 0);
+            k_signs_to_bytes<<<(unsigned)((nT + 255) / 256), 256, 0, c->stream>>>(m.sgn, ds + 2 * n, int(nT), 0, T0);
+        }
+        c->cnt.kernel_launches += 4;
+        SK_CUDA(c, cudaGetLastError());
+        SK_CUDA(c, cudaMemcpyAsync(p->mx.data(), dx, 2 * n * W * 8, cudaMemcpyDeviceToHost, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(p->mz.data(), dz, 2 * n * W * 8, cudaMemcpyDeviceToHost, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(p->ms.data(), ds, 2 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (nT) {
+            SK_CUDA(c, cudaMemcpyAsync(p->tx.data(), dx + 2 * n * W, words * 8, cudaMemcpyDeviceToHost, c->stream));
+            SK_CUDA(c, cudaMemcpyAsync(p->tz.data(), dz + 2 * n * W, words * 8, cudaMemcpyDeviceToHost, c->stream));
+            SK_CUDA(c, cudaMemcpyAsync(p->ts.data(), ds + 2 * n, nT, cudaMemcpyDeviceToHost, c->stream));
+        }
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    // ---- layers in forward order; empty layers dropped; safety re-separation
+    int maxl = -1;
+    for (size_t k = 0; k < nT; ++k) maxl = std::max(maxl, lvl[k]);
+    std::vector<std::vector<uint32_t>> layers(maxl + 1);
+    for (size_t k = 0; k < nT; ++k) if (lvl[k] >= 0) layers[lvl[k]].push_back(uint32_t(k));
+    for (auto& L : layers) {
+        if (L.empty()) continue;
+        // intra-layer commutation check on the device: group ids = 0 for members, unique for the rest
+        std::vector<uint32_t> gid(nT);
+        for (size_t k = 0; k < nT; ++k) gid[k] = 0x40000000u + uint32_t(k);
+        for (uint32_t k : L) gid[k] = 0;
+        rc = sk_ctx_reserve_tmp(c, nT * 4 + 64);
+        if (rc) { delete p; return rc; }
+        unsigned long long* d_n = (unsigned long long*)c->d_tmp; u32* d_g = (u32*)(d_n + 1);
+        SK_CUDA(c, cudaMemsetAsync(d_n, 0, 8, c->stream));
+        SK_CUDA(c, cudaMemcpyAsync(d_g, gid.data(), nT * 4, cudaMemcpyHostToDevice, c->stream));
+        k_verify_grouping<<<(unsigned)((nT + 255) / 256), 256, 0, c->stream>>>(rowsT, m.Wp, W, int(nT), d_g, 0, d_n);
+        c->cnt.kernel_launches++;
+        unsigned long long bad = 0;
+        SK_CUDA(c, cudaMemcpyAsync(&bad, d_n, 8, cudaMemcpyDeviceToHost, c->stream));
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (bad == 0) { p->layers.push_back(L); continue; }
+        // re-separate this layer's rows (in order) with the same first-fit kernels
+        sk_rows* sub = nullptr;
+        rc = sk_rows_create(c, n, L.size(), &sub);
+        if (rc) { delete p; return rc; }
+        std::vector<u64> sx(L.size() * W), sz(L.size() * W); std::vector<uint8_t> ss(L.size());
+        for (size_t k = 0; k < L.size(); ++k) {
+            std::copy(&p->tx[(size_t)L[k] * W], &p->tx[(size_t)L[k] * W] + W, &sx[k * W]);
+            std::copy(&p->tz[(size_t)L[k] * W], &p->tz[(size_t)L[k] * W] + W, &sz[k * W]);
+            ss[k] = p->ts[L[k]];
+        }
+        std::vector<uint32_t> sub_of(L.size()); uint64_t nsub = 0;
+        rc = sk_rows_upload(sub, reinterpret_cast<const uint64_t*>(sx.data()), reinterpret_cast<const uint64_t*>(sz.data()), ss.data(), L.size());
+        if (!rc) rc = sk_group_first_fit(sub, 0, sub_of.data(), &nsub);
+        sk_rows_destroy(sub);
+        if (rc) { delete p; return rc; }
+        std::vector<std::vector<uint32_t>> parts(nsub);
+        for (size_t k = 0; k < L.size(); ++k) parts[sub_of[k]].push_back(L[k]);
+        for (auto& q : parts) p->layers.push_back(q);
+    }
+    uint64_t rows_left = 0, weight = 0;
+    for (auto& L : p->layers) for (uint32_t k : L) {
+        ++rows_left;
+        for (int w = 0; w < W; ++w) weight += __builtin_popcountll(p->tx[(size_t)k * W + w] | p->tz[(size_t)k * W + w]);
+    }
+    p->stats[1] = rows_left; p->stats[2] = weight; p->stats[3] = p->layers.size(); p->stats[4] = nT ? passes : 1;
+    *out = p;
+    return SK_OK;
+}

@@ -1,0 +1,130 @@
+"""-m gpu: grouping and Clifford+T kernels (through the C ABI) against the CPU oracle, bit-exact."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+H, S, SDG, X, Y, Z, CX, CZ, SWAP, M, T, TDG = range(12)
+
+
+def rand_rows(rng, n, m, density=0.5):
+    W = (n + 63) // 64
+    x = np.zeros((m, W), np.uint64); z = np.zeros((m, W), np.uint64)
+    bx = rng.random((m, n)) < density; bz = rng.random((m, n)) < density
+    for w in range(W):
+        for b in range(min(64, n - 64 * w)):
+            x[:, w] |= (bx[:, 64 * w + b].astype(np.uint64) << np.uint64(b))
+            z[:, w] |= (bz[:, 64 * w + b].astype(np.uint64) << np.uint64(b))
+    return x, z, rng.integers(0, 2, m).astype(np.uint8)
+
+
+@pytest.mark.parametrize("n,m", [(1, 3), (2, 5), (17, 40), (64, 100), (130, 257), (1000, 600)])
+def test_row_primitives(sk, ctx, orc, n, m):
+    rng = np.random.default_rng(n * 7 + m)
+    x, z, s = rand_rows(rng, n, m, 0.3)
+    d = sk.Rows(ctx, n, x, z, s); o = orc.Rows(n, x, z, s)
+    assert d.weight_sum() == o.weight_sum()                                   # pauli.cpp:100-106
+    for _ in range(3):                                                        # pauli.cpp:215-237
+        px, pz, _ = rand_rows(rng, n, 1, 0.4)
+        assert (d.commutation_vector(px[0], pz[0]) == o.commutation_vector(px[0], pz[0])).all()
+    # plant duplicates, then compare the first pair in scan order
+    assert d.find_first_duplicate() == o.first_duplicate()
+    if m >= 5:
+        x[m - 1] = x[1]; z[m - 1] = z[1]; x[m - 2] = x[0]; z[m - 2] = z[0]; x[3] = x[1]; z[3] = z[1]
+        d.upload(x, z, s); o = orc.Rows(n, x, z, s)
+        assert d.find_first_duplicate() == o.first_duplicate()
+        if n >= 64: assert o.first_duplicate() == (0, m - 2)
+    # conj_* on every row (pauli.cpp:146-187)
+    gates = []
+    for _ in range(60):
+        k = int(rng.choice([H, S, SDG, X, Y, Z, CX, CZ, SWAP])); a = int(rng.integers(0, n)); b = 0
+        if k in (CX, CZ, SWAP):
+            if n == 1: k = H
+            else: b = int(rng.integers(0, n - 1)); b += b >= a
+        gates.append((k, a, b))
+    d.conj_layer(gates); o.apply(gates)
+    dx, dz, ds = d.download(); ox, oz, os_ = o.get()
+    assert (dx == ox).all() and (dz == oz).all() and (ds == os_).all()
+    # rowsum_plus_i on all anticommuting rows (pauli.cpp:239-254)
+    px, pz, ps = rand_rows(rng, n, 1, 0.4)
+    anti = o.commutation_vector(px[0], pz[0])
+    cnt = 0
+    for i in range(m):
+        if (int(anti[i >> 6]) >> (i & 63)) & 1:
+            assert o.rowsum_plus_i(i, px[0], pz[0], ps[0]) == 0; cnt += 1
+    assert d.rowsum_plus_i_where_anticommuting(px[0], pz[0], int(ps[0])) == cnt
+    dx, dz, ds = d.download(); ox, oz, os_ = o.get()
+    assert (dx == ox).all() and (dz == oz).all() and (ds == os_).all()
+
+
+def test_grouping_examples(sk, ctx, orc):
+    n, x, z, s = 2, [], [], []
+    for t in ("ZZ", "XX", "ZI"):
+        _, px, pz, _ = orc.pauli_from_text(t); x.append(px); z.append(pz)
+    d = sk.Rows(ctx, 2, np.stack(x), np.stack(z))
+    g, ng = d.group_first_fit(0); assert list(g) == [0, 0, 1] and ng == 2
+    g, ng = d.group_first_fit(1); assert list(g) == [0, 1, 0] and ng == 2
+    assert d.verify_grouping(0, [0, 0, 1]) == 0 and d.verify_grouping(0, [0, 1, 1]) == 1   # {XX, ZI} anticommute
+    one = sk.Rows(ctx, 2, np.stack(x[:1]), np.stack(z[:1])); g, ng = one.group_first_fit(0); assert list(g) == [0] and ng == 1
+
+
+@pytest.mark.parametrize("n,m,density", [(16, 500, 0.5), (10, 3000, 0.3), (128, 2500, 0.5), (128, 5000, 0.05), (300, 1500, 0.02)])
+def test_grouping_matches_oracle(sk, ctx, orc, n, m, density):
+    rng = np.random.default_rng(m + n)
+    x, z, s = rand_rows(rng, n, m, density)
+    d = sk.Rows(ctx, n, x, z); o = orc.Rows(n, x, z, np.zeros(m, np.uint8))
+    counts = {}
+    for mode in (0, 1):
+        g, ng = d.group_first_fit(mode)
+        og, ong, _ = o.group_first_fit(mode)
+        assert ng == ong and (g == og).all()
+        assert d.verify_grouping(mode, g) == 0 == o.verify_grouping(mode, og)
+        counts[mode] = ng
+    assert counts[0] <= counts[1]
+    bad = np.zeros(m, np.uint32)                                              # everything in one group
+    assert d.verify_grouping(0, bad) == o.verify_grouping(0, bad) > 0
+
+
+def rand_ct(rng, n, G, pt=0.1):
+    gates = []
+    for _ in range(G):
+        u = rng.random(); a = int(rng.integers(0, n)); b = 0
+        if n > 1: b = int(rng.integers(0, n - 1)); b += b >= a
+        if u < pt / 2: gates.append((T, a, 0))
+        elif u < pt: gates.append((TDG, a, 0))
+        elif u < pt + 0.3: gates.append((H, a, 0))
+        elif u < pt + 0.6 or n == 1: gates.append((S, a, 0))
+        else: gates.append((CX, a, b))
+    return gates
+
+
+def assert_same_pbc(d, o):
+    ds, os_ = d.stats(), o.stats()
+    assert ds == os_, (ds, os_)
+    for k in range(ds["layers"]):
+        dx, dz, dsg = d.layer(k); ox, oz, osg = o.layer(k)
+        assert dx.shape == ox.shape and (dx == ox).all() and (dz == oz).all() and (dsg == osg).all(), f"layer {k}"
+    mx, mz, ms = d.mtab(); ox, oz, osg = o.mtab().get()
+    assert (mx == ox).all() and (mz == oz).all() and (ms == osg).all()
+
+
+def test_transpile_examples(sk, ctx, orc):
+    for n, gates in ((1, [(T, 0, 0), (H, 0, 0)]), (1, [(H, 0, 0), (T, 0, 0)]), (2, [(H, 0, 0), (CX, 0, 1), (M, 0, 0), (M, 1, 0)]),
+                     (1, [(T, 0, 0)] * 2), (1, [(T, 0, 0)] * 8), (1, [(T, 0, 0), (TDG, 0, 0)]), (1, [(H, 0, 0), (T, 0, 0), (H, 0, 0), (M, 0, 0)]),
+                     (3, [(H, 1, 0), (CX, 1, 2)])):
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+    with pytest.raises(sk.UnsupportedError):
+        sk.Pbc(ctx, sk.Circuit(2, [(M, 0, 0), (H, 0, 0)]))
+
+
+def test_transpile_random_small(sk, ctx, orc):                                # SPEC:576-580 (acceptance #8 sizes)
+    rng = np.random.default_rng(8)
+    for trial in range(120):
+        n = int(rng.integers(1, 7)); gates = rand_ct(rng, n, int(rng.integers(5, 60)), pt=float(rng.uniform(0.1, 0.5)))
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+
+
+@pytest.mark.parametrize("n,G,pt", [(20, 2000, 0.2), (100, 4000, 0.1), (1000, 6000, 0.1), (70, 6000, 0.4)])
+def test_transpile_random_large(sk, ctx, orc, n, G, pt):                      # BASELINE config 5 shape
+    rng = np.random.default_rng(n + G)
+    gates = rand_ct(rng, n, G, pt)
+    assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
