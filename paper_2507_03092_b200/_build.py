@@ -14,7 +14,6 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libstabkit_b200.so")
-HOSTLIB = os.path.join(PKG, "libstabkit_host.so")
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -62,28 +61,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_host(force: bool = False) -> str | None:
-    """C++ `stabkit::` host library + its self-test binary (g++, links libstabkit_b200.so)."""
-    hsrc = os.path.join(CSRC, "host_stabkit.cpp")
-    if not os.path.exists(hsrc):
-        return None
-    deps = [hsrc] + [os.path.join(ROOT, "include", "stabkit", f) for f in os.listdir(os.path.join(ROOT, "include", "stabkit"))]
-    if force or _stale(HOSTLIB, deps + [LIB]):
-        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-o", HOSTLIB, hsrc,
-               "-L", PKG, "-lstabkit_b200", "-Wl,-rpath,$ORIGIN"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("g++ failed building libstabkit_host.so")
+    """Self-test binary of the header-only C++ `stabkit::` host API (g++ -std=c++20, links libstabkit_b200.so)."""
     tsrc = os.path.join(ROOT, "tests", "cpp", "test_host_api.cpp")
     tbin = os.path.join(ROOT, "tests", "cpp", "test_host_api")
-    if os.path.exists(tsrc) and (force or _stale(tbin, [tsrc, HOSTLIB])):
-        cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-o", tbin, tsrc,
-               "-L", PKG, "-lstabkit_host", "-lstabkit_b200", f"-Wl,-rpath,{PKG}"]
+    if not os.path.exists(tsrc):
+        return None
+    inc = os.path.join(ROOT, "include", "stabkit")
+    deps = [tsrc, LIB, os.path.join(ROOT, "include", "stabkit_b200.h")] + [os.path.join(inc, f) for f in os.listdir(inc)]
+    if force or _stale(tbin, deps):
+        cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"), "-o", tbin, tsrc,
+               "-L", PKG, "-lstabkit_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_2507_03092_b200"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("g++ failed building tests/cpp/test_host_api")
-    return HOSTLIB
+    return tbin
 
 
 if __name__ == "__main__":
