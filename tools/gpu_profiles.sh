@@ -1,0 +1,27 @@
+#!/bin/bash
+# Evidence for profiles/: bench line, ncu launch list of the bench command, one full capture of the top kernels.
+mkdir -p gpurun_out
+R=${ROUND:-r01}
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_${R}.json 2> gpurun_out/bench_${R}.err
+tail -c 600 gpurun_out/bench_${R}.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_bench_${R}.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_bench_${R}.log 2>&1
+python - <<PY
+import csv, collections
+lines = [l for l in open('gpurun_out/launches_bench_${R}.csv') if l.startswith('"')]
+agg = collections.OrderedDict()
+for row in csv.DictReader(lines):
+    k = row['Kernel Name'].split('(')[0]; v = float(row['Metric Value'].replace(',', '')); u = row['Metric Unit']
+    v = v / 1e3 if u == 'ns' else v * 1e3 if u == 'ms' else v * 1e6 if u == 's' else v
+    agg.setdefault(k, []).append(v)
+tot = sum(sum(v) for v in agg.values())
+with open('gpurun_out/launches_bench_${R}_summary.txt', 'w') as f:
+    f.write("ncu --metrics gpu__time_duration.sum --clock-control none : python bench.py --steps 1 --warmup 1 (cold-cache, serialised; compare SHARES)\n")
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        f.write(f"{k:40s} launches={len(v):5d} total_us={sum(v):12.1f} share={100*sum(v)/tot:6.2f}% mean_us={sum(v)/len(v):10.1f} max_us={max(v):10.1f}\n")
+print(open('gpurun_out/launches_bench_${R}_summary.txt').read())
+PY
+# full captures: one k_layer launch (CX layer), one transpose, the round-2 (all-deterministic) measurement block
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_layer -s 10 -c 2 -f -o gpurun_out/k_layer_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_transpose -s 2 -c 1 -f -o gpurun_out/k_transpose_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_measure_block -s 1 -c 1 -f -o gpurun_out/k_measure_det_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+ls -la gpurun_out/*.ncu-rep
