@@ -53,7 +53,8 @@ constexpr int kMeasThreads = 512;
 constexpr int kMeasWarps = kMeasThreads / 32;
 constexpr int kSlotsPerWarp = 4;
 constexpr int kColChunk = 6;         // column words per lane loaded back-to-back (192 words per chunk)
-constexpr int kSeqMin = 64, kSeqMax = 1024;   // sequential run length (doubles while waves stay narrow)
+constexpr int kNarrowWaves = 32;      // consecutive narrow waves before switching to sequential mode
+constexpr int kSeqMin = 256, kSeqMax = 4096;   // sequential run length (doubles while waves stay narrow)
 constexpr int kMaxTargets = 2048, kMaxMaskWords = 512, kMaxSupport = 4096;   // sparse work-list capacities (dense fallback above)
 constexpr int kWarpList = 48;        // partner rows a single warp multiplies itself; longer products are tree-reduced by a CTA
 
@@ -284,91 +285,90 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     __syncthreads();      // smem is restaged by the next measurement
 }
 
-// K4 by a whole CTA: partner list compacted into shared memory, up to 16 warp partial products,
-// combined by warp 0 (tree reduction; valid because stabilizer rows commute and Pauli
-// multiplication is associative).
+// K4 by a whole CTA: the partner list is compacted into shared memory, then thread w owns word w
+// of the product and multiplies the listed rows in (x, z, phase) word by word, 8 row loads in
+// flight; the per-word phase contributions are block-reduced (popcounts mod 4).  Word-parallel
+// evaluation is the same ordered product: g is a sum over qubit positions.
 __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, int j, const u64* xcol) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     MeasWs* ws = a.ws;
     if (tid == 0) sm.cnt[0] = 0;
     __syncthreads();
-    for (int w = tid; w < W; w += kMeasThreads) {
-        u64 bits = ldcg(xcol + W + w);
-        while (bits) {
-            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            const int ti = atomicAdd(&sm.cnt[0], 1);
-            if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
+    int e = 0, ktot = 0;
+    u64 ax = 0, az = 0;                                   // this thread's word of the running product
+    // thread (w, g): word w = tid % Wq, row group g = tid / Wq  (Wq = W rounded up to 32)
+    const int Wq = (W + 31) & ~31;
+    const int ngroups = max(1, kMeasThreads / Wq);
+    const int myw = tid % Wq, myg = tid / Wq;
+    for (int base = 0; ; base += kMaxTargets) {           // column-order slices of at most kMaxTargets partners
+        // compact the partners with rank in [base, base + kMaxTargets) (rank = position in column order)
+        if (tid == 0) sm.cnt[1] = 0;
+        __syncthreads();
+        int seen = 0;
+        for (int w0 = 0; w0 < W; w0 += kMeasThreads) {    // block-wide exclusive prefix over words, chunk by chunk
+            const int w = w0 + tid;
+            const u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
+            const int pc = __popcll(bits);
+            int incl = pc;                                 // warp inclusive scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+            if (lane == 31) sm.pk[warp] = incl;
+            __syncthreads();
+            int woff = 0;
+            for (int t = 0; t < warp; ++t) woff += sm.pk[t];
+            int chunk_total = 0;
+            for (int t = 0; t < kMeasWarps; ++t) chunk_total += sm.pk[t];
+            int rank = seen + woff + incl - pc;
+            u64 bb = bits;
+            while (bb) {
+                const int b = __ffsll((long long)bb) - 1; bb &= bb - 1;
+                if (rank >= base && rank < base + kMaxTargets) sm.targets[rank - base] = u32(w * 64 + b);
+                ++rank;
+            }
+            seen += chunk_total;
+            __syncthreads();
         }
+        const int total = seen;
+        const int cnt = min(max(total - base, 0), kMaxTargets);
+        if (myw < W && myg < ngroups) {
+            for (int i0 = myg; i0 < cnt; i0 += 8 * ngroups) {
+                u64 sx[8], sz[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int i = i0 + t * ngroups;
+                    if (i < cnt) { const u64* rx = a.m.rows + (size_t)(2 * sm.targets[i]) * Wp; sx[t] = ldcg(rx + myw); sz[t] = ldcg(rx + Wp + myw); }
+                    else { sx[t] = 0; sz[t] = 0; }
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t) { e += g_word(sx[t], sz[t], ax, az); ax ^= sx[t]; az ^= sz[t]; }
+            }
+        }
+        for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
+        ktot += cnt;
+        if (base + kMaxTargets >= total) break;
+        __syncthreads();
     }
+    // combine the row groups (each holds a partial product of its word) and reduce the phase
+    if (ngroups > 1) {
+        if (myw < W && myg > 0 && myg < ngroups) { sm.acc[(size_t)(myg - 1) * 2 * Wp + myw] = ax; sm.acc[(size_t)(myg - 1) * 2 * Wp + Wp + myw] = az; }
+        __syncthreads();
+        if (myw < W && myg == 0)
+            for (int g = 1; g < ngroups; ++g) {
+                const u64 bx = sm.acc[(size_t)(g - 1) * 2 * Wp + myw], bz = sm.acc[(size_t)(g - 1) * 2 * Wp + Wp + myw];
+                e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+            }
+    }
+    e = warp_sum(e);
+    if (lane == 0) sm.pe[warp] = e;
     __syncthreads();
-    const int total = sm.cnt[0];
-    int done_cnt = 0, et = 0, kt = 0;
-    // lists longer than the smem capacity are consumed in column-order slices (rare: > 2048 partners)
-    for (int base = 0; base < total || base == 0; base += kMaxTargets) {
-        int cnt = min(total - base, kMaxTargets);
-        if (base > 0) {                       // rebuild the slice [base, base+cnt) deterministically by rank
-            __syncthreads();
-            if (tid == 0) sm.cnt[1] = 0;
-            __syncthreads();
-            // rank of a bit = number of set bits before it in column order (warp 0 computes word prefix)
-            for (int w = 0; w < W; ++w) {
-                const u64 bits = ldcg(xcol + W + w);
-                const int pc = __popcll(bits);
-                if (done_cnt + pc > base && done_cnt < base + cnt && tid < 64 && ((bits >> tid) & 1ull)) {
-                    const int r = done_cnt + __popcll(bits & ((1ull << tid) - 1ull));
-                    if (r >= base && r < base + cnt) sm.targets[r - base] = u32(w * 64 + tid);
-                }
-                done_cnt += pc;
-            }
-            done_cnt = 0;
-            __syncthreads();
-        } else if (total > kMaxTargets) {     // first slice must also be rank-ordered to make slices disjoint
-            __syncthreads();
-            for (int w = 0; w < W; ++w) {
-                const u64 bits = ldcg(xcol + W + w);
-                const int pc = __popcll(bits);
-                if (done_cnt < cnt && tid < 64 && ((bits >> tid) & 1ull)) {
-                    const int r = done_cnt + __popcll(bits & ((1ull << tid) - 1ull));
-                    if (r < cnt) sm.targets[r] = u32(w * 64 + tid);
-                }
-                done_cnt += pc;
-            }
-            done_cnt = 0;
-            __syncthreads();
-        }
-        const int nparts = min(kMeasWarps, max(1, (cnt + 3) / 4));     // at least ~4 rows per working warp
-        u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
-        int k = 0, e = 0;
-        if (warp < nparts) e = det_list_partial(a.m, sm.targets, cnt, warp, nparts, acc_x, acc_x + Wp, lane, &k);
-        if (lane == 0) { sm.pe[warp] = e; sm.pk[warp] = k; }
-        __syncthreads();
-        if (warp == 0) {
-            int g = 0;
-            for (int t = 0; t < nparts; ++t) { et += sm.pe[t]; kt += sm.pk[t]; }
-            // fold partials 1..nparts-1 (and the running product of earlier slices, kept in slot 0 of acc... see below)
-            for (int w = lane; w < W; w += 32) {
-                u64 ax = sm.acc[w], az = sm.acc[Wp + w];
-                for (int t = 1; t < nparts; ++t) {
-                    u64 bx = sm.acc[(size_t)t * 2 * Wp + w], bz = sm.acc[(size_t)t * 2 * Wp + Wp + w];
-                    g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
-                }
-                if (base > 0) {               // multiply with the product of the previous slices (saved in P/D area)
-                    u64 bx = sm.P[w], bz = sm.P[Wp + w];
-                    g += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
-                }
-                sm.P[w] = ax; sm.P[Wp + w] = az;
-            }
-            et += warp_sum(g);
-        }
-        __syncthreads();
-        if (total <= kMaxTargets) break;
-    }
-    if (warp == 0 && lane == 0) {
+    if (tid == 0) {
+        int et = 0;
+        for (int t = 0; t < kMeasWarps; ++t) et += sm.pe[t];
         et &= 3;
         if (et & 1) atomicOr(&ws->err, 1u);
         a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
-        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)kt); atomicAdd(&ws->ncommit, 1u);
+        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)ktot); atomicAdd(&ws->ncommit, 1u);
     }
     __syncthreads();
 }
@@ -409,7 +409,7 @@ k_measure_block(MeasArgs a) {
     int pos = 0;
     u32 wave = 1;
     u32 commits_seen = 0;
-    int seqlen = 0;
+    int seqlen = 0, narrow = 0;
     u64 t_prof = gtime();
     while (pos < a.count) {
         const int wend = min(a.count, pos + WS);
@@ -529,7 +529,11 @@ k_measure_block(MeasArgs a) {
         {
             const u32 nc = __ldcg(&ws->ncommit);
             const u32 committed = (commits_seen == 0xffffffffu) ? 0xffffu : nc - commits_seen;
-            seqlen = (committed < (u32)a.seq_threshold) ? min(kSeqMax, max(kSeqMin, seqlen * 2)) : 0;
+            // a narrow wave is normal while the dependency frontier is still widening (round 1 of a
+            // memory experiment needs ~20 waves); only a long run of narrow waves means the block is
+            // inherently sequential
+            narrow = (committed < (u32)a.seq_threshold) ? narrow + 1 : 0;
+            seqlen = (narrow >= kNarrowWaves) ? min(kSeqMax, max(kSeqMin, seqlen * 2)) : 0;
         }
         if (seqlen > 0) {
             if (blockIdx.x == 0) {
