@@ -112,9 +112,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     args = ap.parse_args()
 
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from paper_2507_03092_b200 import dist as skdist
+    rank, local_rank, world = skdist.env_world()
     workload = f"rotated surface-code memory d={D}, {ROUNDS} rounds, final Z-basis data measurement (n=10081 qubits, 2132201 gates, 362881 measurements)"
 
     if args.impl == "reference":
@@ -133,26 +132,19 @@ def main():
 
     import numpy as np
     import torch
-    import torch.distributed as dist
     import paper_2507_03092_b200 as sk
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device; the stabilizer hot path has no CPU fallback")
     torch.cuda.set_device(local_rank)
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    skdist.init("nccl")
+    barrier = skdist.barrier
 
     sk.lib()
     ctx = sk.Context(local_rank)
     stream = torch.cuda.ExternalStream(ctx.stream)
     circ = sk.surface_code_circuit(D, ROUNDS, True)
-    seed = SEED ^ rank
+    seed = skdist.shot_seed(SEED, rank)
     prog = sk.Program(ctx, circ, mode=0)
     tab = sk.Tableau(ctx, circ.n)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")     # > 126 MB L2
@@ -179,11 +171,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     cnt = ctx.counters()
     out, det = prog.read_record()
-    ms_local = sum(step_ms) / len(step_ms)
-    t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item())
+    ms_per_step = skdist.max_over_ranks(sum(step_ms) / len(step_ms))
 
     # per-kernel-class device time (CUDA events around every launch) for the roofline lines
     tab.reset(); ctx.sync()
@@ -205,11 +193,7 @@ def main():
         if i > 0:
             e2e_times.append(dt)
     assert (o2 == out).all() and (d2 == det).all(), "e2e record differs from the resident-program record"
-    e2e_local = sum(e2e_times) / len(e2e_times)
-    t = torch.tensor([e2e_local], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_s = float(t.item())
+    e2e_s = skdist.max_over_ranks(sum(e2e_times) / len(e2e_times))
 
     if rank == 0:
         from oracle.oracle_py import algorithmic_bytes     # formula only; no oracle compute here
@@ -223,8 +207,17 @@ def main():
         peak, peak_src = peaks()
         kern = {"k_measure_block": (meas_bytes, cls["measure_ms"]), "k_layer": (gate_bytes, cls["layer_ms"])}
         dom = max(kern, key=lambda k: kern[k][1])
+        traffic = None
+        try:
+            import glob
+            tf = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
+            if tf:
+                with open(tf[-1]) as f:
+                    traffic = json.load(f).get(dom, {}).get("bytes")
+        except Exception:
+            traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom][0] / (kern[dom][1] * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "peak_source": peak_src,
                 "whole_step": {"algorithmic_bytes": total_bytes, "achieved": total_bytes / (ms_per_step * 1e-3) / 1e9,
                                "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
                 "kernels": {k: {"algorithmic_bytes": v[0], "ms_per_step": v[1], "achieved": v[0] / (v[1] * 1e-3) / 1e9,
@@ -246,9 +239,7 @@ def main():
             cb = cpu_reference(1, 0)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line))
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    skdist.finalize()
     return 0
 
 

@@ -46,6 +46,7 @@ struct MeasWs {
     u64 prof[8];        // block-0 wall time (ns) per phase: P1, barrier, P2, barrier, P3, barrier, sequential, window search
     u32 ncommit;        // measurements executed so far in this launch
     u32 pad;
+    u64 dbg[8];         // SK_DEBUG_PROF: cta_random ns in {stage+lists, B1, B2, B3+B4+record}, sums of nt, nmw, nsup, calls
     u64 seqprof[8];     // sequential mode, CTA 0: inspect, det, random, fence ns ; [4] det count, [5] random count, [6] SM cycles, [7] ns
 };
 
@@ -72,12 +73,13 @@ struct MeasArgs {
     u32* wpiv;          // [2][window] pivot of a window slot (0xffffffff = deterministic), by wave parity
     uint8_t* wrun;      // [2][window] 1 = runnable random measurement, by wave parity
     uint8_t* done;      // [count], zeroed before each launch
+    int prof;           // SK_DEBUG_PROF: extra barriers + timers inside cta_random (debug only)
     int use_tma;        // stage mask/P/D with cp.async.bulk (1) or ld.global.cg (0)
     int seq_threshold;  // a wave committing fewer measurements than this switches to sequential mode (0 = never)
 };
 
 __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
-#define SK_PROF(k) do { if (blockIdx.x == 0 && tid == 0) { u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
+#define SK_PROF(k) do { if (a.prof && blockIdx.x == 0 && tid == 0) { u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
 
 __device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
 
@@ -132,14 +134,19 @@ struct MeasSmem {
 };
 
 // K3: one random measurement (index jr, qubit q, pivot stabilizer row-bit p) by one CTA.
-__device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm, int jr, u32 q, int p, u32& tma_parity) {
+__device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm, int jr, u32 q, int p, u32& tma_parity, bool exclusive) {
     const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     MeasWs* ws = a.ws;
     const int pd = a.NS + p;
     const u64* qcol = a.m.cols + (size_t)(2 * q) * RW;
+    u64 tp_in = 0;
+    if (a.prof && tid == 0) tp_in = gtime();
     const int sp = sign_bit(a.m.sgn, p), sd = sign_bit(a.m.sgn, pd);
-    if (a.use_tma) {          // 1-D TMA bulk copies on one mbarrier (UBLKCP)
+    // one pass: stage mask | P | D into shared memory (contiguous) and, from the same registers,
+    // compact the work lists: target rows + non-zero mask words (pivot bits removed), support of P.
+    // sm.cnt[0..2] are zero on entry (reset at the end of the previous CTA-level operation).
+    if (a.use_tma) {          // 1-D TMA bulk copies on one mbarrier (UBLKCP); lists are built from smem afterwards
         if (tid == 0) {
             asm volatile("fence.proxy.async;" ::: "memory");
             mbar_expect_tx(sm.mbar, u32(RW * 8 + 4 * Wp * 8));
@@ -149,43 +156,71 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
         }
         if (!mbar_wait(sm.mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
         tma_parity ^= 1;
-    } else {                  // same bytes with ld.global.cg: lower latency for this 5 KB, latency-critical copy
+        __syncthreads();
+    }
+    {
         const u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
         const u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
-        for (int w = tid; w < RW + 4 * Wp; w += kMeasThreads) {
-            const u64 v = (w < RW) ? ldcg(qcol + w) : (w < RW + 2 * Wp ? ldcg(rp + (w - RW)) : ldcg(rd + (w - RW - 2 * Wp)));
-            sm.mask[w] = v;   // mask | P | D are contiguous in shared memory
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        sm.mask[p >> 6] &= ~(1ull << (p & 63)); sm.mask[pd >> 6] &= ~(1ull << (pd & 63));
-        sm.cnt[0] = 0; sm.cnt[1] = 0; sm.cnt[2] = 0;
-    }
-    __syncthreads();
-    // compact work lists (sparse case): target rows, non-zero mask words, support of P
-    for (int w = tid; w < RW; w += kMeasThreads) {
-        u64 bits = sm.mask[w];
-        if (!bits) continue;
-        const int mi = atomicAdd(&sm.cnt[1], 1);
-        if (mi < kMaxMaskWords) sm.mwords[mi] = (unsigned short)w;
-        while (bits) {
-            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            const int ti = atomicAdd(&sm.cnt[0], 1);
-            if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
-        }
-    }
-    for (int u = tid; u < 2 * W; u += kMeasThreads) {
-        const int h = u >= W, pw = h ? u - W : u;
-        u64 bits = sm.P[h * Wp + pw];
-        while (bits) {
-            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            const int pi = atomicAdd(&sm.cnt[2], 1);
-            if (pi < kMaxSupport) sm.support[pi] = (u32(pw * 64 + b) << 1) | u32(h);
+        const int total_words = RW + 4 * Wp;
+        for (int w0 = 0; w0 < total_words; w0 += kMeasThreads) {       // whole warps iterate together (w0 + tid may overrun)
+            const int w = w0 + tid;
+            u64 v = 0;
+            if (w < total_words)
+                v = a.use_tma ? sm.mask[w]
+                              : ((w < RW) ? ldcg(qcol + w) : (w < RW + 2 * Wp ? ldcg(rp + (w - RW)) : ldcg(rd + (w - RW - 2 * Wp))));
+            int kind = 2;                                               // 0 mask word, 1 word of P, 2 neither
+            if (w < RW) {
+                kind = 0;
+                if (w == (p >> 6)) v &= ~(1ull << (p & 63));
+                if (w == (pd >> 6)) v &= ~(1ull << (pd & 63));
+                sm.mask[w] = v;
+            } else if (w < total_words) {
+                if (!a.use_tma) sm.mask[w] = v;
+                if (w - RW < 2 * Wp) kind = 1;
+            }
+            // warp-aggregated appends: one shared-memory atomic per warp and list
+            const int pc = (kind == 2) ? 0 : __popcll(v);
+            const int pc_t = kind == 0 ? pc : 0, pc_s = kind == 1 ? pc : 0;
+            int in_t = pc_t, in_s = pc_s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int vt = __shfl_up_sync(0xffffffffu, in_t, o), vs = __shfl_up_sync(0xffffffffu, in_s, o);
+                if (lane >= o) { in_t += vt; in_s += vs; }
+            }
+            const u32 nzmask = __ballot_sync(0xffffffffu, kind == 0 && v != 0);
+            int base_t = 0, base_s = 0, base_m = 0;
+            if (lane == 31) {
+                if (in_t) base_t = atomicAdd(&sm.cnt[0], in_t);
+                if (in_s) base_s = atomicAdd(&sm.cnt[2], in_s);
+                if (nzmask) base_m = atomicAdd(&sm.cnt[1], __popc(nzmask));
+            }
+            base_t = __shfl_sync(0xffffffffu, base_t, 31); base_s = __shfl_sync(0xffffffffu, base_s, 31); base_m = __shfl_sync(0xffffffffu, base_m, 31);
+            if (kind == 0 && v) {
+                const int mi = base_m + __popc(nzmask & ((1u << lane) - 1u));
+                if (mi < kMaxMaskWords) sm.mwords[mi] = (unsigned short)w;
+                int ti = base_t + in_t - pc_t;
+                u64 bits = v;
+                while (bits) {
+                    const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                    if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
+                    ++ti;
+                }
+            } else if (kind == 1 && v) {
+                const int u = w - RW, h = u >= Wp, pw = h ? u - Wp : u;
+                int pi = base_s + in_s - pc_s;
+                u64 bits = v;
+                while (bits) {
+                    const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                    if (pi < kMaxSupport) sm.support[pi] = (u32(pw * 64 + b) << 1) | u32(h);
+                    ++pi;
+                }
+            }
         }
     }
     __syncthreads();
     const int nt = sm.cnt[0], nmw = sm.cnt[1], nsup = sm.cnt[2];
+    u64 tp0 = 0;
+    if (a.prof && tid == 0) { tp0 = gtime(); ws->dbg[0] += tp0 - tp_in; ws->dbg[4] += nt; ws->dbg[5] += nmw; ws->dbg[6] += nsup; }
     const bool sparse = nt <= kMaxTargets && nmw <= kMaxMaskWords && nsup <= kMaxSupport;
     // B1: rowsum(i, p) for every target row i (warp per row, P from smem)
     auto rowsum_into = [&](int i) {
@@ -217,11 +252,20 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
     };
     if (sparse) {
         for (int t = warp; t < nt; t += kMeasWarps) rowsum_into(int(sm.targets[t]));
+        if (a.prof) { __syncthreads(); if (tid == 0) { u64 t = gtime(); ws->dbg[1] += t - tp0; tp0 = t; } }
         // B2: C form, column_j ^= mask for j in supp(P): warp per support entry, lanes over the non-zero mask words
         for (int e = warp; e < nsup; e += kMeasWarps) {
             const u32 ent = sm.support[e];
             u64* col = a.m.cols + (size_t)ent * RW;           // ent == 2*qubit + half
-            for (int i = lane; i < nmw; i += 32) { const int w = sm.mwords[i]; atomicXor(col + w, sm.mask[w]); }
+            if (exclusive) {      // no other CTA touches C (sequential mode): plain RMW, except the two words B3 also updates
+                for (int i = lane; i < nmw; i += 32) {
+                    const int w = sm.mwords[i];
+                    if (w == (p >> 6) || w == (pd >> 6)) atomicXor(col + w, sm.mask[w]);
+                    else __stcg(col + w, ldcg(col + w) ^ sm.mask[w]);
+                }
+            } else {
+                for (int i = lane; i < nmw; i += 32) { const int w = sm.mwords[i]; atomicXor(col + w, sm.mask[w]); }
+            }
         }
     } else {
         for (int mw = warp; mw < RW; mw += kMeasWarps) {
@@ -238,6 +282,7 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
             }
         }
     }
+    if (a.prof) { __syncthreads(); if (tid == 0) { u64 t = gtime(); ws->dbg[2] += t - tp0; tp0 = t; } }
     // B3: C form, single-bit fixes for rows p (-> Z_q) and p+n (-> P); thread per (list, word)
     {
         const u64 pbit = 1ull << (p & 63), dbit = 1ull << (pd & 63);
@@ -282,55 +327,46 @@ __device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm
             atomicAdd(&ws->n_rand, 1ull); atomicAdd(&ws->k_rand, (u64)k); atomicAdd(&ws->ncommit, 1u);
         }
     }
+    if (tid == 0) { sm.cnt[0] = 0; sm.cnt[1] = 0; sm.cnt[2] = 0; }
     __syncthreads();      // smem is restaged by the next measurement
+    if (a.prof && tid == 0) { ws->dbg[3] += gtime() - tp0; ws->dbg[7] += 1; }
 }
 
-// K4 by a whole CTA: the partner list is compacted into shared memory, then thread w owns word w
-// of the product and multiplies the listed rows in (x, z, phase) word by word, 8 row loads in
-// flight; the per-word phase contributions are block-reduced (popcounts mod 4).  Word-parallel
-// evaluation is the same ordered product: g is a sum over qubit positions.
+// K4 by a whole CTA: the partner list is compacted into shared memory, then thread (w, g) owns
+// word w of the product for row group g and multiplies its share of the listed rows word by word,
+// 8 row loads in flight; groups are folded and the per-word phase contributions block-reduced
+// (popcounts mod 4).  Word-parallel evaluation is the same product: g is a sum over qubit
+// positions; the list order is irrelevant because stabilizer rows commute.
+// sm.cnt[0] is zero on entry and on exit.
 __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, int j, const u64* xcol) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     MeasWs* ws = a.ws;
-    if (tid == 0) sm.cnt[0] = 0;
-    __syncthreads();
-    int e = 0, ktot = 0;
-    u64 ax = 0, az = 0;                                   // this thread's word of the running product
-    // thread (w, g): word w = tid % Wq, row group g = tid / Wq  (Wq = W rounded up to 32)
-    const int Wq = (W + 31) & ~31;
-    const int ngroups = max(1, kMeasThreads / Wq);
-    const int myw = tid % Wq, myg = tid / Wq;
-    for (int base = 0; ; base += kMaxTargets) {           // column-order slices of at most kMaxTargets partners
-        // compact the partners with rank in [base, base + kMaxTargets) (rank = position in column order)
-        if (tid == 0) sm.cnt[1] = 0;
-        __syncthreads();
-        int seen = 0;
-        for (int w0 = 0; w0 < W; w0 += kMeasThreads) {    // block-wide exclusive prefix over words, chunk by chunk
-            const int w = w0 + tid;
-            const u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
-            const int pc = __popcll(bits);
-            int incl = pc;                                 // warp inclusive scan
+    for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
+        const int w = w0 + tid;
+        u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
+        const int pc = __popcll(bits);
+        int incl = pc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
-            if (lane == 31) sm.pk[warp] = incl;
-            __syncthreads();
-            int woff = 0;
-            for (int t = 0; t < warp; ++t) woff += sm.pk[t];
-            int chunk_total = 0;
-            for (int t = 0; t < kMeasWarps; ++t) chunk_total += sm.pk[t];
-            int rank = seen + woff + incl - pc;
-            u64 bb = bits;
-            while (bb) {
-                const int b = __ffsll((long long)bb) - 1; bb &= bb - 1;
-                if (rank >= base && rank < base + kMaxTargets) sm.targets[rank - base] = u32(w * 64 + b);
-                ++rank;
-            }
-            seen += chunk_total;
-            __syncthreads();
+        for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+        int base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&sm.cnt[0], incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int ti = base + incl - pc;
+        while (bits) {
+            const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
+            if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
+            ++ti;
         }
-        const int total = seen;
-        const int cnt = min(max(total - base, 0), kMaxTargets);
+    }
+    __syncthreads();
+    const int total = sm.cnt[0];
+    int e = 0;
+    u64 ax = 0, az = 0;                                   // this thread's word of the running product
+    const int Wq = (W + 31) & ~31;
+    const int ngroups = max(1, min(kMeasThreads / Wq, (total + 7) / 8));
+    const int myw = tid % Wq, myg = tid / Wq;
+    auto multiply_list = [&](int cnt) {
         if (myw < W && myg < ngroups) {
             for (int i0 = myg; i0 < cnt; i0 += 8 * ngroups) {
                 u64 sx[8], sz[8];
@@ -345,11 +381,39 @@ __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, i
             }
         }
         for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
-        ktot += cnt;
-        if (base + kMaxTargets >= total) break;
-        __syncthreads();
+    };
+    if (total <= kMaxTargets) {
+        multiply_list(total);
+    } else {
+        // more partners than list slots (dense tableaux): column-order slices selected by rank
+        for (int base = 0; base < total; base += kMaxTargets) {
+            __syncthreads();
+            int seen = 0;
+            for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
+                const int w = w0 + tid;
+                const u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
+                const int pc = __popcll(bits);
+                int incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+                if (lane == 31) sm.pk[warp] = incl;
+                __syncthreads();
+                int woff = 0, chunk_total = 0;
+                for (int t = 0; t < kMeasWarps; ++t) { if (t < warp) woff += sm.pk[t]; chunk_total += sm.pk[t]; }
+                int rank = seen + woff + incl - pc;
+                u64 bb = bits;
+                while (bb) {
+                    const int b = __ffsll((long long)bb) - 1; bb &= bb - 1;
+                    if (rank >= base && rank < base + kMaxTargets) sm.targets[rank - base] = u32(w * 64 + b);
+                    ++rank;
+                }
+                seen += chunk_total;
+                __syncthreads();
+            }
+            multiply_list(min(total - base, kMaxTargets));
+        }
     }
-    // combine the row groups (each holds a partial product of its word) and reduce the phase
+    // fold the row groups (each holds a partial product of its word) and reduce the phase
     if (ngroups > 1) {
         if (myw < W && myg > 0 && myg < ngroups) { sm.acc[(size_t)(myg - 1) * 2 * Wp + myw] = ax; sm.acc[(size_t)(myg - 1) * 2 * Wp + Wp + myw] = az; }
         __syncthreads();
@@ -368,7 +432,8 @@ __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, i
         et &= 3;
         if (et & 1) atomicOr(&ws->err, 1u);
         a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
-        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)ktot); atomicAdd(&ws->ncommit, 1u);
+        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)total); atomicAdd(&ws->ncommit, 1u);
+        sm.cnt[0] = 0;
     }
     __syncthreads();
 }
@@ -400,7 +465,7 @@ k_measure_block(MeasArgs a) {
     MeasWs* ws = a.ws;
     u32 epoch = 0;
     u32 tma_parity = 0;
-    if (tid == 0) mbar_init(&s_mbar, 1);
+    if (tid == 0) { mbar_init(&s_mbar, 1); s_cnt3[0] = 0; s_cnt3[1] = 0; s_cnt3[2] = 0; s_piv = 0xffffffffu; }
     __syncthreads();
 
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
@@ -410,7 +475,7 @@ k_measure_block(MeasArgs a) {
     u32 wave = 1;
     u32 commits_seen = 0;
     int seqlen = 0, narrow = 0;
-    u64 t_prof = gtime();
+    u64 t_prof = a.prof ? gtime() : 0;
     while (pos < a.count) {
         const int wend = min(a.count, pos + WS);
         const int par = int(wave & 1);
@@ -518,7 +583,7 @@ k_measure_block(MeasArgs a) {
         __syncthreads();
         for (int h = 0; h < s_nrun; ++h) {
             const int slot = s_run[h];
-            cta_random(a, sm, pos + slot, a.qubits[pos + slot], int(__ldcg(wpiv + slot)), tma_parity);
+            cta_random(a, sm, pos + slot, a.qubits[pos + slot], int(__ldcg(wpiv + slot)), tma_parity, false);
         }
         SK_PROF(4);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
@@ -538,14 +603,12 @@ k_measure_block(MeasArgs a) {
         if (seqlen > 0) {
             if (blockIdx.x == 0) {
                 int j = pos, ran = 0;
-                u64 t0s = gtime(); const long long c0 = clock64(); const u64 tseq0 = t0s;
+                u64 t0s = a.prof ? gtime() : 0; const long long c0 = clock64(); const u64 tseq0 = t0s;
                 for (; j < a.count && ran < seqlen; ++j) {
                     if (__ldcg(a.done + j)) continue;                   // uniform: every thread reads the same byte
                     const u32 q = a.qubits[j];
                     const u64* xcol = a.m.cols + (size_t)(2 * q) * RW;
-                    if (tid == 0) s_piv = 0xffffffffu;
-                    __syncthreads();
-                    u32 piv = 0xffffffffu;
+                    u32 piv = 0xffffffffu;                      // s_piv was reset at the end of the previous iteration
                     for (int w = tid; w < W; w += kMeasThreads) {
                         u64 v = ldcg(xcol + w);
                         if (v) piv = min(piv, u32(w * 64 + __ffsll((long long)v) - 1));
@@ -555,16 +618,17 @@ k_measure_block(MeasArgs a) {
                     __syncthreads();
                     piv = s_piv;
                     u64 t1 = 0, t2 = 0;
-                    if (tid == 0) { t1 = gtime(); ws->seqprof[0] += t1 - t0s; }
+                    if (a.prof && tid == 0) { t1 = gtime(); ws->seqprof[0] += t1 - t0s; }
                     if (piv == 0xffffffffu) cta_det(a, sm, j, xcol);
-                    else cta_random(a, sm, j, q, int(piv), tma_parity);
-                    if (tid == 0) { t2 = gtime(); ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
+                    else cta_random(a, sm, j, q, int(piv), tma_parity, true);
+                    if (a.prof && tid == 0) { t2 = gtime(); ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
                     __threadfence();                                    // this measurement's updates before the next column read
+                    if (tid == 0) s_piv = 0xffffffffu;                  // (everyone read s_piv before the CTA op's barriers)
                     __syncthreads();
-                    if (tid == 0) { t0s = gtime(); ws->seqprof[3] += t0s - t2; }
+                    if (a.prof && tid == 0) { t0s = gtime(); ws->seqprof[3] += t0s - t2; }
                     ++ran;
                 }
-                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - tseq0; }
+                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); if (a.prof) { ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - tseq0; } }
             }
             SK_PROF(6);
             if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;

@@ -35,6 +35,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("SK_SEQ_THRESHOLD")) c->seq_threshold = atoi(e);
     if (const char* e = getenv("SK_TMA")) c->use_tma = atoi(e);
+    if (getenv("SK_DEBUG_PROF") || getenv("SK_SEQPROF")) c->prof = 1;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
@@ -371,7 +372,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.claim = t->d_claim; a.wpiv = t->d_wpiv; a.wrun = t->d_wrun; a.done = t->d_done;
-    a.seq_threshold = c->seq_threshold; a.use_tma = c->use_tma;
+    a.seq_threshold = c->seq_threshold; a.use_tma = c->use_tma; a.prof = c->prof;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -434,7 +435,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
     SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 13 * 8, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->seqprof[0], 0, 8 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->dbg[0], 0, 16 * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -445,6 +446,7 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     *out = c->cnt;
     out->n_rand = h.n_rand; out->n_det = h.n_det; out->k_rand = h.k_rand; out->k_det = h.k_det; out->waves = h.waves;
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
+    if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "cta_random: calls %llu  stage+lists %.0f us  B1 %.0f us  B2 %.0f us  B3B4rec %.0f us  avg nt %.1f nmw %.1f nsup %.1f\n", (unsigned long long)h.dbg[7], h.dbg[0] / 1e3, h.dbg[1] / 1e3, h.dbg[2] / 1e3, h.dbg[3] / 1e3, double(h.dbg[4]) / (h.dbg[7] + 1e-9), double(h.dbg[5]) / (h.dbg[7] + 1e-9), double(h.dbg[6]) / (h.dbg[7] + 1e-9));
     if (getenv("SK_SEQPROF")) fprintf(stderr, "seqprof: inspect %.0f us det %.0f us (n=%llu) random %.0f us (n=%llu) fence %.0f us ; cycles %llu\n", h.seqprof[0] / 1e3, h.seqprof[1] / 1e3, (unsigned long long)h.seqprof[4], h.seqprof[2] / 1e3, (unsigned long long)h.seqprof[5], h.seqprof[3] / 1e3, (unsigned long long)h.seqprof[6]);
     return SK_OK;
 }
