@@ -3,33 +3,42 @@
 // Exact CHP semantics (Algorithm 1): the tableau, signs and
 // record are bit-identical to measuring one qubit at a time, in order.
 //
-// Out-of-order wave scheduler.  The FOOTPRINT of a pending measurement j in the current
-// state is the set of row slots F_j = {i mod n : x_iq = 1} (slot i = stabilizer i and its
-// destabilizer partner; the pivot and its partner are in it by construction).  Two
-// measurements with disjoint footprints act on disjoint rows, cannot change each other's
-// column x_q, pivot, branch or phases, and therefore commute bit-exactly -- also with
-// everything the earlier one may turn into once ITS predecessors have run (DESIGN.md,
-// "independence of measurements"; tools/proto_waves.py checks the rule against the oracle).
-// Per wave, over a window of pending measurements (kSlotsPerWarp per warp of the grid):
+// Two modes inside the kernel.
 //
+// WAVE mode (deterministic prefixes).  Over a window of pending measurements:
 //   P1  pivot search = scan of the stabilizer half of column x_q in the C form (contiguous;
-//       ffs + warp min) -- K2.  Every window member CLAIMS its slots with a 64-bit atomicMax
-//       of (wave, ~j); the first random index r0 is min-reduced.           -- grid barrier --
-//   P2  j < r0: deterministic and final (nothing before it writes).  j >= r0: runnable iff
-//       no slot of F_j is claimed by a smaller index.  Runnable deterministic measurements
-//       are evaluated at once from the read-only R form: ordered product of the stabilizer
-//       partners, phase by popcounts mod 4 -- K4.                           -- grid barrier --
-//   P3  runnable random measurements, one CTA each -- K3: column mask, pivot row P and old
-//       destabilizer row D staged in shared memory by 1-D TMA bulk copies, then
-//         B1 R form: rowsum(i, p) for every i in the mask (warp per row, P from smem)
-//         B2 C form: column_j ^= mask for j in supp(P)            (word parallel, atomicXor)
-//         B3 C form: bit fixes for the overwritten rows p and p+n ; sign bits ; record
-//         B4 R form: row p+n := P ; row p := Z_q                            -- grid barrier --
-//   A window without random measurements needs only the first barrier.  The first pending
-//   measurement is always runnable, so every wave makes progress; RNG ordinal and record
-//   slot are those of the measurement's position, never of its execution order.
-// Both forms stay valid throughout.  Row i = p+n is skipped in B1 (it is overwritten;
-// SURVEY.md section 7 "rowsum on the pivot's own destabilizer").
+//       ffs + warp min) -- K2; the index r0 of the first random measurement is min-reduced.
+//                                                                         -- grid barrier --
+//   P2  every j < r0 is deterministic and read-only: ordered product of the stabilizer
+//       partners from the R form, phase by popcounts mod 4 -- K4 (a warp per measurement, a
+//       whole CTA for long products).  A window without random measurements is done after
+//       this single barrier (rounds 2..d of a memory experiment: one wave per round).
+//
+// PANEL mode (from the first random measurement to the end of the block): blocked
+// elimination, the bit-matrix analogue of a right-looking LU panel factorisation.  A panel =
+// the next B <= 64 measurements (B * RW words must fit in shared memory).
+//   G   gather: the panel's B x-columns at the panel-start state, read from the R form.
+//   F   factorise (CTA 0, panel in shared memory): the B measurements are simulated IN ORDER
+//       on the panel's own bits only -- pivot (smallest stabilizer row), frozen
+//       target mask m_l, update of the later panel columns, the two overwritten rows -- which
+//       fixes, symbolically, every full-row operation sequential CHP would perform:
+//         hist_l  = steps k < l that multiplied the pivot row p_l before it was used,
+//         M_h     = steps l whose pivot is multiplied into row h,
+//         D_j     = partner set of a deterministic step j (split into rows that are still
+//                   panel-start stabilizers, N_j = parity of their histories, and rows that
+//                   earlier steps turned into +-Z).
+//   V   pivot values: P_l' = (prod_{k in hist_l} P_k') * row p_l  -- the value row p_l has when
+//       it is used; word-parallel (a thread owns one word of all B rows), phases reduced later.
+//   A   every touched row replays its own list   row_h := (prod_{l in M_h} P_l') * row_h
+//       independently (warp per row); destabilizer p_l + n starts from P_l'; row p_l := +-Z_q
+//       with the counter RNG bit of the measurement's ordinal.
+//   D   deterministic outcomes: sign of  prod_{i in D_j} row_i(panel start) * prod_{l in N_j} P_l'
+//       * prod (+-Z_{q_l}); equal to the sequential scratch-row product because all factors
+//       are commuting Hermitian operators (P^2 = +I cancels repeated factors).
+//   Every row undergoes exactly the multiplications of sequential CHP, in the same order;
+//   tools/proto_panel.py checks the scheme against the oracle.  Panel mode updates only the R
+//   form and raises ws->c_stale; the host re-derives C with a (flag-conditional) transpose.
+// Row i = p+n is never a rowsum target (SURVEY.md section 7 hazard): it is overwritten.
 //
 // Roofline: HBM/L2.  Algorithmic bytes: random  RW*8 + 16W + k*32W + 32W ;
 // deterministic  RW*8/2 + k*16W  -- reported from the k counters kept here.
@@ -38,29 +47,42 @@
 
 namespace skd {
 
+constexpr int kPanelMax = 64;
+
+struct PanelInfo {      // global scratch describing the current panel (written by CTA 0 in F)
+    u64 hist[kPanelMax];   // random step l: earlier random steps whose pivot was multiplied into row p_l
+    u64 dN[kPanelMax];     // deterministic step j: pivot values to multiply (parity of partner histories)
+    u64 dZ[kPanelMax];     // deterministic step j: earlier steps whose +-Z row is a partner
+    u32 piv[kPanelMax];    // pivot stabilizer row-bit, 0xffffffff = deterministic step
+    u32 eph[kPanelMax];    // V: sum over words of the g contributions of P_l' (atomic, mod 4 matters)
+    int dete[kPanelMax];   // D part 1: phase exponent of the panel-start partner product
+    u64 randmask;          // steps that are random
+    u64 osign;             // panel-start sign bits of the pivot rows
+    u32 nt;                // touched rows (entries of tlist / tM)
+    u32 pad;
+    uint8_t outc[kPanelMax];   // outcome of the random steps (counter RNG)
+};
+
 struct MeasWs {
     u32 bar;            // grid barrier counter (zeroed before each launch)
-    u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 tma timeout
+    u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout
     u32 r0[4];          // per-wave index of the first random measurement, min-reduced; 3 slots rotate
-    u64 n_rand, n_det, k_rand, k_det, waves;
-    u64 prof[8];        // block-0 wall time (ns) per phase: P1, barrier, P2, barrier, P3, barrier, sequential, window search
-    u32 ncommit;        // measurements executed so far in this launch
+    u32 c_stale;        // panel mode ran: the C form must be re-derived from R
     u32 pad;
-    u64 dbg[8];         // SK_DEBUG_PROF: cta_random ns in {stage+lists, B1, B2, B3+B4+record}, sums of nt, nmw, nsup, calls
-    u64 seqprof[8];     // sequential mode, CTA 0: inspect, det, random, fence ns ; [4] det count, [5] random count, [6] SM cycles, [7] ns
+    u64 n_rand, n_det, k_rand, k_det, waves;
+    u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
+    u64 panels;
 };
 
 constexpr int kMeasThreads = 512;
 constexpr int kMeasWarps = kMeasThreads / 32;
 constexpr int kSlotsPerWarp = 4;
 constexpr int kColChunk = 6;         // column words per lane loaded back-to-back (192 words per chunk)
-constexpr int kNarrowWaves = 32;      // consecutive narrow waves before switching to sequential mode
-constexpr int kSeqMin = 256, kSeqMax = 4096;   // sequential run length (doubles while waves stay narrow)
-constexpr int kMaxTargets = 2048, kMaxMaskWords = 512, kMaxSupport = 4096;   // sparse work-list capacities (dense fallback above)
-constexpr int kWarpList = 48;        // partner rows a single warp multiplies itself; longer products are tree-reduced by a CTA
+constexpr int kMaxTargets = 2048;    // partner-list capacity of the CTA-wide product (dense fallback above)
+constexpr int kWarpList = 64;        // rows a single warp multiplies from its list; longer products are tree-reduced by a CTA
 
 struct MeasArgs {
-    DMat m;             // tableau (C and R valid)
+    DMat m;             // tableau (C and R valid on entry)
     int n;              // qubits == rows per half
     int NS;             // row-bit offset of the destabilizer half (64*W)
     const u32* qubits;  // measurement list
@@ -69,282 +91,82 @@ struct MeasArgs {
     uint8_t* outcomes;  // [count]
     uint8_t* dets;      // [count]
     MeasWs* ws;
-    u64* claim;         // [64*W] slot claims, zeroed before each launch
     u32* wpiv;          // [2][window] pivot of a window slot (0xffffffff = deterministic), by wave parity
-    uint8_t* wrun;      // [2][window] 1 = runnable random measurement, by wave parity
-    uint8_t* done;      // [count], zeroed before each launch
-    int prof;           // SK_DEBUG_PROF: extra barriers + timers inside cta_random (debug only)
-    int use_tma;        // stage mask/P/D with cp.async.bulk (1) or ld.global.cg (0)
-    int seq_threshold;  // a wave committing fewer measurements than this switches to sequential mode (0 = never)
+    // panel mode scratch
+    int B;              // panel width (<= kPanelMax)
+    u64* pan;           // [B][RW] gathered panel ; after F: destabilizer halves of deterministic steps hold D_j
+    u64* pivbuf;        // [B] rows in R layout: P_l' x words then z words
+    u64* detacc;        // [B] rows in R layout: panel-start partner products of the deterministic steps
+    PanelInfo* info;
+    u32* tlist;         // [64*RW] touched rows
+    u64* tM;            // [64*RW] their step masks
+    int prof;           // device-side phase timers (SK_DEBUG_PROF)
 };
 
 __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
 #define SK_PROF(k) do { if (a.prof && blockIdx.x == 0 && tid == 0) { u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
 
 __device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
+__device__ __forceinline__ void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
+__device__ __forceinline__ u64 warp_xor64(u64 v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
-// K4: product of the stabilizer rows listed in `list` (entries part, part+nparts, ...), phase
-// exponent mod 4 returned warp-uniform.  Stabilizer rows commute and Pauli multiplication is
-// associative, so any grouping/order of the factors gives the same Hermitian product; 8 rows are
-// loaded per step so their latencies overlap.  acc_x/acc_z [Wp] are private to the warp
-// (lane-strided words).
-__device__ __forceinline__ int det_list_partial(const DMat& m, const u32* list, int cnt, int part, int nparts,
-                                                u64* acc_x, u64* acc_z, int lane, int* k_out) {
-    const int W = m.W, Wp = m.Wp;
-    for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
-    int e = 0, k = 0;
-    for (int i0 = part; i0 < cnt; i0 += 8 * nparts) {
+// Multiplies the rows listed in `list` (row indices into `base`, R layout: x words then z words,
+// Wp each) into the warp-private accumulator acc_x/acc_z [Wp] (lane-strided words), each as the
+// LEFT factor.  Returns this lane's share of the i-exponent (the caller adds the factors' sign
+// bits and reduces with warp_sum).  All factors commute, so any grouping/order gives the same
+// Hermitian product; 8 rows are loaded per step so their latencies overlap.
+__device__ __forceinline__ int warp_mul_list(const u64* base, int W, int Wp, const u32* list, int cnt,
+                                             u64* acc_x, u64* acc_z, int lane) {
+    int e = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 8) {
         int s[8]; int ns = 0;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) { const int i = i0 + t * nparts; if (i < cnt) { s[t] = int(list[i]); ns = t + 1; } else s[t] = 0; }
-        if (lane < ns) e += 2 * sign_bit(m.sgn, int(list[i0 + lane * nparts]));
+        for (int t = 0; t < 8; ++t) { const int i = i0 + t; if (i < cnt) { s[t] = int(list[i]); ns = t + 1; } else s[t] = 0; }
         for (int w = lane; w < W; w += 32) {
             u64 sx[8], sz[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) if (t < ns) {
-                const u64* rx = m.rows + (size_t)(2 * s[t]) * Wp;
+                const u64* rx = base + (size_t)(2 * s[t]) * Wp;
                 sx[t] = ldcg(rx + w); sz[t] = ldcg(rx + Wp + w);
             }
             u64 ax = acc_x[w], az = acc_z[w];
 #pragma unroll
             for (int t = 0; t < 8; ++t) if (t < ns) {
-                e += g_word(sx[t], sz[t], ax, az);      // rowsum(scratch, s): left factor = row s
+                e += g_word(sx[t], sz[t], ax, az);      // rowsum(acc, s): left factor = row s
                 ax ^= sx[t]; az ^= sz[t];
             }
             acc_x[w] = ax; acc_z[w] = az;
         }
-        k += ns;
     }
-    *k_out = k;
-    return warp_sum(e) & 3;
+    return e;
 }
 
 // ---- CTA-wide building blocks (all kMeasThreads threads call them together) -------------
 struct MeasSmem {
-    u64* mask;      // [RW]   column x_q (rows to update; pivot bits cleared)
-    u64* P;         // [2*Wp] pivot row
-    u64* D;         // [2*Wp] old destabilizer row of the pivot
-    u64* acc;       // [kMeasWarps][2*Wp] per-warp product accumulators
-    u64* mbar;
+    u64* acc;       // [kMeasWarps][2*Wp] per-warp product accumulators (start of the dynamic region)
     int* pe; int* pk;
-    int* cnt;                 // [3] list lengths
-    u32* targets;             // [kMaxTargets] rows to rowsum
-    unsigned short* mwords;   // [kMaxMaskWords] non-zero mask words
-    u32* support;             // [kMaxSupport] (2*qubit + half) entries of supp(P)
+    int* cnt;       // list length
+    u32* targets;   // [kMaxTargets] partner rows
 };
 
-// K3: one random measurement (index jr, qubit q, pivot stabilizer row-bit p) by one CTA.
-__device__ __forceinline__ void cta_random(const MeasArgs& a, const MeasSmem& sm, int jr, u32 q, int p, u32& tma_parity, bool exclusive) {
-    const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    MeasWs* ws = a.ws;
-    const int pd = a.NS + p;
-    const u64* qcol = a.m.cols + (size_t)(2 * q) * RW;
-    u64 tp_in = 0;
-    if (a.prof && tid == 0) tp_in = gtime();
-    const int sp = sign_bit(a.m.sgn, p), sd = sign_bit(a.m.sgn, pd);
-    // one pass: stage mask | P | D into shared memory (contiguous) and, from the same registers,
-    // compact the work lists: target rows + non-zero mask words (pivot bits removed), support of P.
-    // sm.cnt[0..2] are zero on entry (reset at the end of the previous CTA-level operation).
-    if (a.use_tma) {          // 1-D TMA bulk copies on one mbarrier (UBLKCP); lists are built from smem afterwards
-        if (tid == 0) {
-            asm volatile("fence.proxy.async;" ::: "memory");
-            mbar_expect_tx(sm.mbar, u32(RW * 8 + 4 * Wp * 8));
-            tma_load_1d(sm.mask, qcol, u32(RW * 8), sm.mbar);
-            tma_load_1d(sm.P, a.m.rows + (size_t)(2 * p) * Wp, u32(2 * Wp * 8), sm.mbar);
-            tma_load_1d(sm.D, a.m.rows + (size_t)(2 * pd) * Wp, u32(2 * Wp * 8), sm.mbar);
-        }
-        if (!mbar_wait(sm.mbar, tma_parity)) { if (tid == 0) atomicOr(&ws->err, 0x40000000u); }
-        tma_parity ^= 1;
-        __syncthreads();
-    }
-    {
-        const u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
-        const u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
-        const int total_words = RW + 4 * Wp;
-        for (int w0 = 0; w0 < total_words; w0 += kMeasThreads) {       // whole warps iterate together (w0 + tid may overrun)
-            const int w = w0 + tid;
-            u64 v = 0;
-            if (w < total_words)
-                v = a.use_tma ? sm.mask[w]
-                              : ((w < RW) ? ldcg(qcol + w) : (w < RW + 2 * Wp ? ldcg(rp + (w - RW)) : ldcg(rd + (w - RW - 2 * Wp))));
-            int kind = 2;                                               // 0 mask word, 1 word of P, 2 neither
-            if (w < RW) {
-                kind = 0;
-                if (w == (p >> 6)) v &= ~(1ull << (p & 63));
-                if (w == (pd >> 6)) v &= ~(1ull << (pd & 63));
-                sm.mask[w] = v;
-            } else if (w < total_words) {
-                if (!a.use_tma) sm.mask[w] = v;
-                if (w - RW < 2 * Wp) kind = 1;
-            }
-            // warp-aggregated appends: one shared-memory atomic per warp and list
-            const int pc = (kind == 2) ? 0 : __popcll(v);
-            const int pc_t = kind == 0 ? pc : 0, pc_s = kind == 1 ? pc : 0;
-            int in_t = pc_t, in_s = pc_s;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int vt = __shfl_up_sync(0xffffffffu, in_t, o), vs = __shfl_up_sync(0xffffffffu, in_s, o);
-                if (lane >= o) { in_t += vt; in_s += vs; }
-            }
-            const u32 nzmask = __ballot_sync(0xffffffffu, kind == 0 && v != 0);
-            int base_t = 0, base_s = 0, base_m = 0;
-            if (lane == 31) {
-                if (in_t) base_t = atomicAdd(&sm.cnt[0], in_t);
-                if (in_s) base_s = atomicAdd(&sm.cnt[2], in_s);
-                if (nzmask) base_m = atomicAdd(&sm.cnt[1], __popc(nzmask));
-            }
-            base_t = __shfl_sync(0xffffffffu, base_t, 31); base_s = __shfl_sync(0xffffffffu, base_s, 31); base_m = __shfl_sync(0xffffffffu, base_m, 31);
-            if (kind == 0 && v) {
-                const int mi = base_m + __popc(nzmask & ((1u << lane) - 1u));
-                if (mi < kMaxMaskWords) sm.mwords[mi] = (unsigned short)w;
-                int ti = base_t + in_t - pc_t;
-                u64 bits = v;
-                while (bits) {
-                    const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                    if (ti < kMaxTargets) sm.targets[ti] = u32(w * 64 + b);
-                    ++ti;
-                }
-            } else if (kind == 1 && v) {
-                const int u = w - RW, h = u >= Wp, pw = h ? u - Wp : u;
-                int pi = base_s + in_s - pc_s;
-                u64 bits = v;
-                while (bits) {
-                    const int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                    if (pi < kMaxSupport) sm.support[pi] = (u32(pw * 64 + b) << 1) | u32(h);
-                    ++pi;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const int nt = sm.cnt[0], nmw = sm.cnt[1], nsup = sm.cnt[2];
-    u64 tp0 = 0;
-    if (a.prof && tid == 0) { tp0 = gtime(); ws->dbg[0] += tp0 - tp_in; ws->dbg[4] += nt; ws->dbg[5] += nmw; ws->dbg[6] += nsup; }
-    const bool sparse = nt <= kMaxTargets && nmw <= kMaxMaskWords && nsup <= kMaxSupport;
-    // B1: rowsum(i, p) for every target row i (warp per row, P from smem)
-    auto rowsum_into = [&](int i) {
-        u64* tx = a.m.rows + (size_t)(2 * i) * Wp;
-        u64* tz = tx + Wp;
-        int e = 0;
-        for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {     // loads first, then phase + stores
-            u64 xv[kColChunk], zv[kColChunk];
-#pragma unroll
-            for (int t = 0; t < kColChunk; ++t) {
-                const int w = w0 + 32 * t + lane;
-                xv[t] = (w < W) ? ldcg(tx + w) : 0ull; zv[t] = (w < W) ? ldcg(tz + w) : 0ull;
-            }
-#pragma unroll
-            for (int t = 0; t < kColChunk; ++t) {
-                const int w = w0 + 32 * t + lane;
-                if (w >= W) continue;
-                const u64 px = sm.P[w], pz = sm.P[Wp + w];
-                e += g_word(px, pz, xv[t], zv[t]);             // left factor = pivot row
-                if (px) __stcg(tx + w, xv[t] ^ px);
-                if (pz) __stcg(tz + w, zv[t] ^ pz);
-            }
-        }
-        e = warp_sum(e) & 3;
-        if (lane == 0) {
-            if (e & 1) atomicOr(&ws->err, 1u);
-            if (sp ^ (e >> 1)) atomicXor(a.m.sgn + (i >> 6), 1ull << (i & 63));
-        }
-    };
-    if (sparse) {
-        for (int t = warp; t < nt; t += kMeasWarps) rowsum_into(int(sm.targets[t]));
-        if (a.prof) { __syncthreads(); if (tid == 0) { u64 t = gtime(); ws->dbg[1] += t - tp0; tp0 = t; } }
-        // B2: C form, column_j ^= mask for j in supp(P): warp per support entry, lanes over the non-zero mask words
-        for (int e = warp; e < nsup; e += kMeasWarps) {
-            const u32 ent = sm.support[e];
-            u64* col = a.m.cols + (size_t)ent * RW;           // ent == 2*qubit + half
-            if (exclusive) {      // no other CTA touches C (sequential mode): plain RMW, except the two words B3 also updates
-                for (int i = lane; i < nmw; i += 32) {
-                    const int w = sm.mwords[i];
-                    if (w == (p >> 6) || w == (pd >> 6)) atomicXor(col + w, sm.mask[w]);
-                    else __stcg(col + w, ldcg(col + w) ^ sm.mask[w]);
-                }
-            } else {
-                for (int i = lane; i < nmw; i += 32) { const int w = sm.mwords[i]; atomicXor(col + w, sm.mask[w]); }
-            }
-        }
-    } else {
-        for (int mw = warp; mw < RW; mw += kMeasWarps) {
-            u64 bits = sm.mask[mw];
-            while (bits) { int b = __ffsll((long long)bits) - 1; bits &= bits - 1; rowsum_into(mw * 64 + b); }
-        }
-        for (int u = warp; u < 2 * W; u += kMeasWarps) {
-            const int h = u >= W, pw = h ? u - W : u;
-            u64 bits = sm.P[h * Wp + pw];
-            while (bits) {
-                int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                u64* col = a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW;
-                for (int w = lane; w < RW; w += 32) { u64 mv = sm.mask[w]; if (mv) atomicXor(col + w, mv); }
-            }
-        }
-    }
-    if (a.prof) { __syncthreads(); if (tid == 0) { u64 t = gtime(); ws->dbg[2] += t - tp0; tp0 = t; } }
-    // B3: C form, single-bit fixes for rows p (-> Z_q) and p+n (-> P); thread per (list, word)
-    {
-        const u64 pbit = 1ull << (p & 63), dbit = 1ull << (pd & 63);
-        for (int u = tid; u < 4 * W; u += kMeasThreads) {
-            const int list = (u >= 2 * W) ? (u >= 3 * W ? 3 : 2) : (u >= W ? 1 : 0), pw = u - list * W;
-            const int h = list & 1;
-            u64 bits; int word; u64 bit;
-            if (list < 2) {          // row p: old P -> Z_q
-                bits = sm.P[h * Wp + pw];
-                if (h == 1 && pw == int(q >> 6)) bits ^= 1ull << (q & 63);
-                word = p >> 6; bit = pbit;
-            } else {                 // row p+n: old D -> P
-                bits = sm.D[h * Wp + pw] ^ sm.P[h * Wp + pw];
-                word = pd >> 6; bit = dbit;
-            }
-            while (bits) {
-                int b = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                atomicXor(a.m.cols + (size_t)(2 * (pw * 64 + b) + h) * RW + word, bit);
-            }
-        }
-    }
-    // B4: R form, row p+n := P ; row p := Z_q
-    {
-        u64* rp = a.m.rows + (size_t)(2 * p) * Wp;
-        u64* rd = a.m.rows + (size_t)(2 * pd) * Wp;
-        for (int w = tid; w < 2 * Wp; w += kMeasThreads) {
-            __stcg(rd + w, sm.P[w]);
-            u64 v = 0;
-            if (w == Wp + int(q >> 6)) v = 1ull << (q & 63);
-            __stcg(rp + w, v);
-        }
-    }
-    // signs, record, counters
-    if (warp == 0) {
-        const int k = nt;
-        if (lane == 0) {
-            const int out = counter_bit(a.seed, a.ordinal0 + (uint64_t)jr);
-            if (sp != out) atomicXor(a.m.sgn + (p >> 6), 1ull << (p & 63));
-            if (sd != sp) atomicXor(a.m.sgn + (pd >> 6), 1ull << (pd & 63));
-            a.outcomes[jr] = uint8_t(out);
-            a.dets[jr] = 0; a.done[jr] = 1;
-            atomicAdd(&ws->n_rand, 1ull); atomicAdd(&ws->k_rand, (u64)k); atomicAdd(&ws->ncommit, 1u);
-        }
-    }
-    if (tid == 0) { sm.cnt[0] = 0; sm.cnt[1] = 0; sm.cnt[2] = 0; }
-    __syncthreads();      // smem is restaged by the next measurement
-    if (a.prof && tid == 0) { ws->dbg[3] += gtime() - tp0; ws->dbg[7] += 1; }
-}
-
-// K4 by a whole CTA: the partner list is compacted into shared memory, then thread (w, g) owns
-// word w of the product for row group g and multiplies its share of the listed rows word by word,
-// 8 row loads in flight; groups are folded and the per-word phase contributions block-reduced
-// (popcounts mod 4).  Word-parallel evaluation is the same product: g is a sum over qubit
-// positions; the list order is irrelevant because stabilizer rows commute.
+// K4 by a whole CTA: the partner list (set bits of dcol[0..W), stabilizer indices) is compacted
+// into shared memory, then thread (w, g) owns word w of the product for row group g and
+// multiplies its share of the listed rows word by word, 8 row loads in flight; groups are folded
+// and the per-word phase contributions block-reduced (popcounts mod 4).  Word-parallel evaluation
+// is the same product: g is a sum over qubit positions; the list order is irrelevant because
+// stabilizer rows commute.  Returns (CTA-uniform) the phase exponent mod 4 including the rows'
+// signs; if out_x != nullptr the product words are stored there (R layout).  *total_out = #rows.
 // sm.cnt[0] is zero on entry and on exit.
-__device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, int j, const u64* xcol) {
+__device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, const u64* dcol, u64* out_x, int* total_out) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    MeasWs* ws = a.ws;
     for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
         const int w = w0 + tid;
-        u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
+        u64 bits = (w < W) ? ldcg(dcol + w) : 0ull;
         const int pc = __popcll(bits);
         int incl = pc;
 #pragma unroll
@@ -367,22 +189,54 @@ __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, i
     const int ngroups = max(1, min(kMeasThreads / Wq, (total + 7) / 8));
     const int myw = tid % Wq, myg = tid / Wq;
     auto multiply_list = [&](int cnt) {
-        if (myw < W && myg < ngroups) {
-            for (int i0 = myg; i0 < cnt; i0 += 8 * ngroups) {
-                u64 sx[8], sz[8];
+        if (Wq <= kMeasThreads) {
+            if (myw < W && myg < ngroups) {
+                for (int i0 = myg; i0 < cnt; i0 += 8 * ngroups) {
+                    u64 sx[8], sz[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int i = i0 + t * ngroups;
-                    if (i < cnt) { const u64* rx = a.m.rows + (size_t)(2 * sm.targets[i]) * Wp; sx[t] = ldcg(rx + myw); sz[t] = ldcg(rx + Wp + myw); }
-                    else { sx[t] = 0; sz[t] = 0; }
+                    for (int t = 0; t < 8; ++t) {
+                        const int i = i0 + t * ngroups;
+                        if (i < cnt) { const u64* rx = a.m.rows + (size_t)(2 * sm.targets[i]) * Wp; sx[t] = ldcg(rx + myw); sz[t] = ldcg(rx + Wp + myw); }
+                        else { sx[t] = 0; sz[t] = 0; }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) { e += g_word(sx[t], sz[t], ax, az); ax ^= sx[t]; az ^= sz[t]; }
                 }
-#pragma unroll
-                for (int t = 0; t < 8; ++t) { e += g_word(sx[t], sz[t], ax, az); ax ^= sx[t]; az ^= sz[t]; }
             }
         }
         for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
     };
-    if (total <= kMaxTargets) {
+    if (Wq > kMeasThreads) {
+        // very wide rows: a thread owns several words; the running product lives in out_x / sm.acc
+        // (not needed below 2^15 qubits; kept simple: one row at a time)
+        u64* px = out_x ? out_x : sm.acc;
+        for (int w = tid; w < 2 * Wp; w += kMeasThreads) px[w] = 0;
+        __syncthreads();
+        for (int base = 0; base < total; base += kMaxTargets) {
+            if (base) {     // refill the list with the next slice, in column order
+                __syncthreads();
+                if (tid == 0) {
+                    int rank = 0, fill = 0;
+                    for (int w = 0; w < W && fill < kMaxTargets; ++w) {
+                        u64 bits = ldcg(dcol + w);
+                        while (bits && fill < kMaxTargets) { const int b = __ffsll((long long)bits) - 1; bits &= bits - 1; if (rank >= base) sm.targets[fill++] = u32(w * 64 + b); ++rank; }
+                    }
+                }
+                __syncthreads();
+            }
+            const int cnt = min(total - base, kMaxTargets);
+            for (int w = tid; w < W; w += kMeasThreads) {
+                u64 bx = px[w], bz = px[Wp + w];
+                for (int i = 0; i < cnt; ++i) {
+                    const u64* rx = a.m.rows + (size_t)(2 * sm.targets[i]) * Wp;
+                    const u64 sx = ldcg(rx + w), sz = ldcg(rx + Wp + w);
+                    e += g_word(sx, sz, bx, bz); bx ^= sx; bz ^= sz;
+                }
+                px[w] = bx; px[Wp + w] = bz;
+            }
+            for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
+        }
+    } else if (total <= kMaxTargets) {
         multiply_list(total);
     } else {
         // more partners than list slots (dense tableaux): column-order slices selected by rank
@@ -391,7 +245,7 @@ __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, i
             int seen = 0;
             for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
                 const int w = w0 + tid;
-                const u64 bits = (w < W) ? ldcg(xcol + W + w) : 0ull;
+                const u64 bits = (w < W) ? ldcg(dcol + w) : 0ull;
                 const int pc = __popcll(bits);
                 int incl = pc;
 #pragma unroll
@@ -413,50 +267,189 @@ __device__ __forceinline__ void cta_det(const MeasArgs& a, const MeasSmem& sm, i
             multiply_list(min(total - base, kMaxTargets));
         }
     }
-    // fold the row groups (each holds a partial product of its word) and reduce the phase
-    if (ngroups > 1) {
-        if (myw < W && myg > 0 && myg < ngroups) { sm.acc[(size_t)(myg - 1) * 2 * Wp + myw] = ax; sm.acc[(size_t)(myg - 1) * 2 * Wp + Wp + myw] = az; }
-        __syncthreads();
-        if (myw < W && myg == 0)
-            for (int g = 1; g < ngroups; ++g) {
-                const u64 bx = sm.acc[(size_t)(g - 1) * 2 * Wp + myw], bz = sm.acc[(size_t)(g - 1) * 2 * Wp + Wp + myw];
-                e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
-            }
+    if (Wq <= kMeasThreads) {
+        // fold the row groups (each holds a partial product of its word) and reduce the phase
+        if (ngroups > 1) {
+            if (myw < W && myg > 0 && myg < ngroups) { sm.acc[(size_t)(myg - 1) * 2 * Wp + myw] = ax; sm.acc[(size_t)(myg - 1) * 2 * Wp + Wp + myw] = az; }
+            __syncthreads();
+            if (myw < W && myg == 0)
+                for (int g = 1; g < ngroups; ++g) {
+                    const u64 bx = sm.acc[(size_t)(g - 1) * 2 * Wp + myw], bz = sm.acc[(size_t)(g - 1) * 2 * Wp + Wp + myw];
+                    e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                }
+        }
+        if (out_x && myw < W && myg == 0) { __stcg(out_x + myw, ax); __stcg(out_x + Wp + myw, az); }
     }
     e = warp_sum(e);
     if (lane == 0) sm.pe[warp] = e;
     __syncthreads();
-    if (tid == 0) {
-        int et = 0;
-        for (int t = 0; t < kMeasWarps; ++t) et += sm.pe[t];
-        et &= 3;
-        if (et & 1) atomicOr(&ws->err, 1u);
-        a.outcomes[j] = uint8_t(et >> 1); a.dets[j] = 1; a.done[j] = 1;
-        atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)total); atomicAdd(&ws->ncommit, 1u);
-        sm.cnt[0] = 0;
-    }
+    int et = 0;
+    for (int t = 0; t < kMeasWarps; ++t) et += sm.pe[t];
+    *total_out = total;
     __syncthreads();
+    if (tid == 0) sm.cnt[0] = 0;
+    __syncthreads();
+    return et & 3;
 }
 
-// dynamic smem: mask[RW] | P[2*Wp] | D[2*Wp] | acc[kMeasWarps][2*Wp]   (u64 each)
+// ------------------------------------------------------------------ panel mode ------------
+// F: symbolic factorisation of one panel by CTA 0.  sp = dynamic smem: panel [Bn][RW] then the
+// pivot mask [W] (stabilizer rows used as pivots so far).
+struct PanelSmem {
+    u32 piv[kPanelMax]; u64 hist[kPanelMax], dN[kPanelMax], dZ[kPanelMax]; u32 kd[kPanelMax]; uint8_t outc[kPanelMax];
+    u32 full32[2], dfull32[2]; u32 nt; u32 krand; u64 psign; u32 podd;
+};
+
+__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, int pos, int Bn) {
+    const int RW = a.m.RW, W = a.m.W, NS = a.NS;
+    const int tid = threadIdx.x, lane = tid & 31;
+    u64* pivmask = sp + (size_t)Bn * RW;
+    for (int i = tid; i < Bn * RW; i += kMeasThreads) sp[i] = ldcg(a.pan + i);
+    for (int w = tid; w < W; w += kMeasThreads) pivmask[w] = 0;
+    if (tid < kPanelMax) { ps.piv[tid] = 0xffffffffu; ps.hist[tid] = 0; ps.dN[tid] = 0; ps.dZ[tid] = 0; ps.kd[tid] = 0; ps.outc[tid] = 0; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; }
+    __syncthreads();
+    const int nact = min(kMeasThreads, max(64, (RW + 31) & ~31));       // threads that own panel words (>= 64: one per panel column in the bit gathers)
+    u64 randmask = 0;
+    if (tid < nact) {
+        for (int j = 0; j < Bn; ++j) {
+            u64* cj = sp + (size_t)j * RW;
+            // pivot search over the stabilizer half (word-parallel; words ascend with the stride)
+            u32 cand = 0xffffffffu;
+            for (int w = tid; w < W; w += nact) { const u64 v = cj[w]; if (v && cand == 0xffffffffu) cand = u32(w * 64 + __ffsll((long long)v) - 1); }
+            cand = warp_min(cand);
+            if (lane == 0 && cand != 0xffffffffu) atomicMin(&ps.piv[j], cand);
+            named_bar(1, nact);
+            const u32 p = ps.piv[j];
+            if (p != 0xffffffffu) {
+                // ---------------- random step
+                const u32 pd = u32(NS) + p;
+                if (tid < 64) {       // bit p of every panel column: history (l < j) and pivot row (c > j); bit p+n likewise
+                    const u32 bit = (tid < Bn) ? u32((sp[(size_t)tid * RW + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
+                    const u32 dbit = (tid < Bn) ? u32((sp[(size_t)tid * RW + (pd >> 6)] >> (pd & 63)) & 1ull) : 0u;
+                    const u32 bal = __ballot_sync(0xffffffffu, bit), dbal = __ballot_sync(0xffffffffu, dbit);
+                    if (lane == 0) { ps.full32[tid >> 5] = bal; ps.dfull32[tid >> 5] = dbal; }
+                }
+                named_bar(1, nact);
+                const u64 full = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+                const u64 dfull = (u64)ps.dfull32[0] | ((u64)ps.dfull32[1] << 32);
+                const u64 below = (1ull << j) - 1ull;
+                const u64 above = (j < 63) ? ~((2ull << j) - 1ull) : 0ull;
+                const u64 pw = full & above;
+                for (int w = tid; w < RW; w += nact) {
+                    u64 m = cj[w];
+                    const bool isp = w == int(p >> 6), isd = w == int(pd >> 6);
+                    if (isp) m &= ~(1ull << (p & 63));
+                    if (isd) m &= ~(1ull << (pd & 63));
+                    cj[w] = m;                                   // frozen target mask of step j
+                    if (m) { u64 bits = pw; while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] ^= m; } }
+                    if (isp) {                                   // row p becomes +-Z_q: no x bits any more
+                        u64 bits = pw; while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] &= ~(1ull << (p & 63)); }
+                        pivmask[w] |= 1ull << (p & 63);
+                    }
+                    if (isd) {                                   // row p+n becomes the old pivot row: flip where it differs
+                        u64 bits = (dfull ^ full) & above;
+                        while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] ^= 1ull << (pd & 63); }
+                    }
+                }
+                if (tid == 0) { ps.hist[j] = full & randmask & below; ps.outc[j] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + j))); }
+                randmask |= 1ull << j;
+            } else {
+                // ---------------- deterministic step: partners D = destabilizer half of the column
+                if (tid < 64) {       // partners that earlier steps of this panel turned into +-Z
+                    u32 bit = 0;
+                    if (tid < j && ((randmask >> tid) & 1ull)) { const u32 pl = ps.piv[tid]; bit = u32((cj[W + (pl >> 6)] >> (pl & 63)) & 1ull); }
+                    const u32 bal = __ballot_sync(0xffffffffu, bit);
+                    if (lane == 0) ps.full32[tid >> 5] = bal;
+                }
+                named_bar(1, nact);
+                if (tid == 0) ps.dZ[j] = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+                u64 nb = 0; int kd = 0;
+                for (int w = tid; w < W; w += nact) {
+                    const u64 dw = cj[W + w];
+                    kd += __popcll(dw);
+                    const u64 nonpiv = dw & ~pivmask[w];
+                    cj[W + w] = nonpiv;
+                    if (nonpiv) { u64 bits = randmask; while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; nb ^= (u64)(__popcll(sp[(size_t)l * RW + w] & nonpiv) & 1) << l; } }
+                }
+                nb = warp_xor64(nb); kd = warp_sum(kd);
+                if (lane == 0) { if (nb) atomicXor(&ps.dN[j], nb); if (kd) atomicAdd(&ps.kd[j], (u32)kd); }
+            }
+        }
+    }
+    __syncthreads();
+    randmask = 0;
+    for (int j = 0; j < Bn; ++j) if (ps.piv[j] != 0xffffffffu) randmask |= 1ull << j;
+    // touched rows: targets of any random step, the pivots and their destabilizer partners
+    int kr = 0;
+    for (int w0 = 0; w0 < RW; w0 += kMeasThreads) {
+        const int w = w0 + tid;
+        u64 tw = 0;
+        if (w < RW) {
+            u64 bits = randmask;
+            while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; const u64 v = sp[(size_t)l * RW + w]; tw |= v; kr += __popcll(v); }
+            tw |= pivmask[w < W ? w : w - W];
+        }
+        const int pc = __popcll(tw);
+        int incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+        u32 base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&ps.nt, (u32)incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        u32 ti = base + incl - pc;
+        while (tw) { const int b = __ffsll((long long)tw) - 1; tw &= tw - 1; a.tlist[ti++] = u32(w * 64 + b); }
+    }
+    kr = warp_sum(kr);
+    if (lane == 0 && kr) atomicAdd(&ps.krand, (u32)kr);
+    // deterministic steps: partner sets (panel-start stabilizers only) for phase D
+    for (int j = 0; j < Bn; ++j)
+        if (!((randmask >> j) & 1ull))
+            for (int w = tid; w < W; w += kMeasThreads) __stcg(a.pan + (size_t)j * RW + W + w, sp[(size_t)j * RW + W + w]);
+    __syncthreads();
+    const u32 nt = ps.nt;
+    for (u32 i = tid; i < nt; i += kMeasThreads) {
+        const u32 h = __ldcg(a.tlist + i);
+        u64 M = 0, bits = randmask;
+        while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; M |= ((sp[(size_t)l * RW + (h >> 6)] >> (h & 63)) & 1ull) << l; }
+        __stcg(a.tM + i, M);
+    }
+    PanelInfo* info = a.info;
+    if (tid < kPanelMax) {
+        info->hist[tid] = ps.hist[tid]; info->dN[tid] = ps.dN[tid]; info->dZ[tid] = ps.dZ[tid];
+        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
+    }
+    if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
+        const u32 pl = ps.piv[tid];
+        const u32 bal = __ballot_sync(0xffffffffu, pl != 0xffffffffu && sign_bit(a.m.sgn, int(pl)));
+        if (lane == 0) ps.full32[tid >> 5] = bal;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        info->randmask = randmask; info->nt = nt; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        int nr = __popcll(randmask), kd = 0;
+        for (int j = 0; j < Bn; ++j) kd += ps.kd[j];
+        atomicAdd(&a.ws->n_rand, (u64)nr); atomicAdd(&a.ws->n_det, (u64)(Bn - nr));
+        atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)kd);
+        atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
+    }
+}
+
+// dynamic smem (u64): max( acc[kMeasWarps][2*Wp] + values scratch, panel [B][RW] + pivmask [W] )
 __global__ void __launch_bounds__(kMeasThreads, 1)
 k_measure_block(MeasArgs a) {
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ __align__(8) u64 s_mbar;
-    __shared__ int s_red[2];
-    __shared__ int s_nrun, s_run[kMeasWarps * kSlotsPerWarp];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
-    __shared__ u32 s_piv;
     __shared__ int s_wcnt[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
-    __shared__ int s_cnt3[3];
-    __shared__ u32 s_targets[kMaxTargets], s_support[kMaxSupport];
-    __shared__ unsigned short s_mwords[kMaxMaskWords];
+    __shared__ int s_cnt1;
+    __shared__ u32 s_targets[kMaxTargets];
+    __shared__ PanelSmem ps;
+    __shared__ PanelInfo s_info;
+    __shared__ u32 s_q[kPanelMax];
     const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
     MeasSmem sm;
-    sm.mask = smem; sm.P = sm.mask + RW; sm.D = sm.P + 2 * Wp; sm.acc = sm.D + 2 * Wp;
-    sm.mbar = &s_mbar; sm.pe = s_pe; sm.pk = s_pk;
-    sm.cnt = s_cnt3; sm.targets = s_targets; sm.mwords = s_mwords; sm.support = s_support;
+    sm.acc = smem; sm.pe = s_pe; sm.pk = s_pk; sm.cnt = &s_cnt1; sm.targets = s_targets;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int GW = G * kMeasWarps;
@@ -464,8 +457,7 @@ k_measure_block(MeasArgs a) {
     const int gw = blockIdx.x * kMeasWarps + warp;
     MeasWs* ws = a.ws;
     u32 epoch = 0;
-    u32 tma_parity = 0;
-    if (tid == 0) { mbar_init(&s_mbar, 1); s_cnt3[0] = 0; s_cnt3[1] = 0; s_cnt3[2] = 0; s_piv = 0xffffffffu; }
+    if (tid == 0) s_cnt1 = 0;
     __syncthreads();
 
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
@@ -473,34 +465,28 @@ k_measure_block(MeasArgs a) {
 
     int pos = 0;
     u32 wave = 1;
-    u32 commits_seen = 0;
-    int seqlen = 0, narrow = 0;
+    bool panel_mode = false;
     u64 t_prof = a.prof ? gtime() : 0;
+    // =============================================================== wave mode =====
     while (pos < a.count) {
         const int wend = min(a.count, pos + WS);
-        const int par = int(wave & 1);
-        u32* wpiv = a.wpiv + (size_t)par * WS;
-        uint8_t* wrun = a.wrun + (size_t)par * WS;
+        u32* wpiv = a.wpiv + (size_t)(wave & 1) * WS;
         // ------------------------------------------------------------ P1 -----
         if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0xffffffffu;
         for (int slot = gw; pos + slot < wend; slot += GW) {
             const int j = pos + slot;
-            if (__ldcg(a.done + j)) { if (lane == 0) wpiv[slot] = 0xfffffffeu; continue; }       // executed in an earlier wave
             const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
-            const u64 key = ((u64)wave << 32) | (u64)(0xffffffffu - (u32)j);
             u32 piv = 0xffffffffu;
-            for (int w0 = 0; w0 < RW; w0 += 32 * kColChunk) {        // loads first (one L2 round trip per chunk)
+            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {        // loads first (one L2 round trip per chunk)
                 u64 cv[kColChunk];
 #pragma unroll
-                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < RW) ? ldcg(xcol + w) : 0ull; }
+                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < W) ? ldcg(xcol + w) : 0ull; }
 #pragma unroll
                 for (int t = 0; t < kColChunk; ++t) {
                     const int w = w0 + 32 * t + lane;
-                    u64 v = cv[t];
-                    if (v && w < W) piv = min(piv, u32(w * 64 + __ffsll((long long)v) - 1));
-                    const int base = (w < W ? w : w - W) * 64;
-                    while (v) { int b = __ffsll((long long)v) - 1; v &= v - 1; atomicMax(a.claim + base + b, key); }
+                    if (cv[t]) piv = min(piv, u32(w * 64 + __ffsll((long long)cv[t]) - 1));
                 }
+                if (__any_sync(0xffffffffu, piv != 0xffffffffu)) break;
             }
             piv = warp_min(piv);
             if (lane == 0) {
@@ -510,141 +496,328 @@ k_measure_block(MeasArgs a) {
         }
         SK_PROF(0);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(1);
+        SK_PROF(6);
         const u32 r0 = __ldcg(&ws->r0[wave % 3]);
+        const int dend = (r0 == 0xffffffffu) ? wend : int(r0);      // [pos, dend) are deterministic and final
         if (tid == 0) s_nheavy = 0;
         __syncthreads();
-        // ------------------------------------------------------------ P2 (+K4) --
-        for (int slot = gw; pos + slot < wend; slot += GW) {
+        // ------------------------------------------------------------ P2 (K4) --
+        for (int slot = gw; pos + slot < dend; slot += GW) {
             const int j = pos + slot;
-            const u32 piv = __ldcg(wpiv + slot);      // written by this warp in P1
-            if (piv == 0xfffffffeu) { if (lane == 0) wrun[slot] = 0; continue; }
-            const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
-            bool blocked = false;
-            const bool isdet = piv == 0xffffffffu;
+            const u64* dcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW + W;     // destabilizer half
             if (lane == 0) s_wcnt[warp] = 0;
             __syncwarp();
-            for (int w0 = 0; w0 < RW; w0 += 32 * kColChunk) {
+            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {
                 u64 cv[kColChunk];
 #pragma unroll
-                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < RW) ? ldcg(xcol + w) : 0ull; }
+                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < W) ? ldcg(dcol + w) : 0ull; }
 #pragma unroll
                 for (int t = 0; t < kColChunk; ++t) {
                     const int w = w0 + 32 * t + lane;
                     u64 v = cv[t];
-                    const int base = (w < W ? w : w - W) * 64;
-                    const bool chk = (u32)j >= r0;
                     while (v) {
-                        int b = __ffsll((long long)v) - 1; v &= v - 1;
-                        if (isdet) { const int ti = atomicAdd(&s_wcnt[warp], 1); if (ti < kWarpList) s_wlist[warp][ti] = u32(base + b); }
-                        if (chk) {
-                            const u64 c = ldcg(a.claim + base + b);
-                            if ((u32)(c >> 32) == wave && (0xffffffffu - (u32)c) < (u32)j) blocked = true;
-                        }
+                        const int b = __ffsll((long long)v) - 1; v &= v - 1;
+                        const int ti = atomicAdd(&s_wcnt[warp], 1);
+                        if (ti < kWarpList) s_wlist[warp][ti] = u32(w * 64 + b);
                     }
                 }
             }
-            blocked = __any_sync(0xffffffffu, blocked);
-            if (lane == 0) wrun[slot] = uint8_t(!blocked && !isdet);
-            if (blocked || !isdet) continue;
             __syncwarp();
             const int npart = s_wcnt[warp];
             if (npart > kWarpList) {                  // tree-reduced by the whole CTA below
                 if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = slot; }
                 continue;
             }
-            int k;
-            const int e = det_list_partial(a.m, s_wlist[warp], npart, 0, 1, acc_x, acc_z, lane, &k);
+            for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
+            int e = warp_mul_list(a.m.rows, W, Wp, s_wlist[warp], npart, acc_x, acc_z, lane);
+            for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[warp][i]));
+            e = warp_sum(e) & 3;
             if (lane == 0) {
                 if (e & 1) atomicOr(&ws->err, 1u);
-                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1; a.done[j] = 1;
-                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)k); atomicAdd(&ws->ncommit, 1u);
+                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
+                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)npart);
             }
+            __syncwarp();
         }
         __syncthreads();
         for (int h = 0; h < s_nheavy; ++h) {
             const int j = pos + s_heavy[h];
-            cta_det(a, sm, j, a.m.cols + (size_t)(2 * a.qubits[j]) * RW);
+            int total;
+            const int e = cta_det(a, sm, a.m.cols + (size_t)(2 * a.qubits[j]) * RW + W, nullptr, &total);
+            if (tid == 0) {
+                if (e & 1) atomicOr(&ws->err, 1u);
+                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
+                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)total);
+            }
         }
         if (blockIdx.x == 0 && tid == 0) atomicAdd(&ws->waves, 1ull);
-        SK_PROF(2);
-        if (r0 == 0xffffffffu) { pos = wend; ++wave; commits_seen = 0xffffffffu; continue; }   // window was all deterministic: done
-        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;          // reads of the wave-start state done
-        SK_PROF(3);
+        SK_PROF(1);
+        ++wave;
+        pos = dend;
+        if (r0 != 0xffffffffu) { panel_mode = true; break; }
+    }
+    if (!panel_mode) return;
 
-        // ------------------------------------------------------------ P3: K3 ----
-        // this CTA owns window slots blockIdx.x, +G, +2G, ...: gather the runnable ones in parallel
-        if (tid == 0) s_nrun = 0;
+    // =============================================================== panel mode =====
+    // (the P2 reads above touch nothing that is written before the next grid barrier)
+    const int B = a.B;
+    PanelInfo* info = a.info;
+    const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs
+    while (pos < a.count) {
+        const int Bn = min(B, a.count - pos);
+        if (tid < kPanelMax) s_q[tid] = (tid < Bn) ? a.qubits[pos + tid] : 0xffffffffu;
         __syncthreads();
-        for (int i = tid; pos + blockIdx.x + i * G < wend; i += kMeasThreads) {
-            const int slot = blockIdx.x + i * G;
-            if (__ldcg(wrun + slot)) { int h = atomicAdd(&s_nrun, 1); s_run[h] = slot; }
+        // ---- G: gather the panel columns from the R form: warp per group of 32 row-bits
+        {
+            u32* pan32 = reinterpret_cast<u32*>(a.pan);
+            for (int g = gwi; g < 2 * RW; g += GW) {
+                const int h = 32 * g + lane;
+                const u64* rx = a.m.rows + (size_t)(2 * h) * Wp;
+                u32 lo = 0, hi = 0;
+                int lastw = -1; u64 lastv = 0;
+                for (int j0 = 0; j0 < Bn; j0 += 8) {
+                    u32 qq[8]; u64 v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) qq[t] = s_q[j0 + t];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const int wq = int(qq[t] >> 6), prev = t ? int(qq[t - 1] >> 6) : lastw;
+                        v[t] = (qq[t] != 0xffffffffu && wq != prev) ? ldcg(rx + wq) : 0ull;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        if (qq[t] == 0xffffffffu) continue;
+                        const int wq = int(qq[t] >> 6);
+                        if (wq == lastw) v[t] = lastv; else { lastv = v[t]; lastw = wq; }
+                        const u32 bal = __ballot_sync(0xffffffffu, (v[t] >> (qq[t] & 63)) & 1ull);
+                        const int j = j0 + t;
+                        if (lane == (j & 31)) { if (j < 32) lo = bal; else hi = bal; }
+                    }
+                }
+                if (lane < Bn) pan32[(size_t)lane * 2 * RW + g] = lo;
+                if (lane + 32 < Bn) pan32[(size_t)(lane + 32) * 2 * RW + g] = hi;
+            }
         }
+        SK_PROF(2);
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+        SK_PROF(7);
+        // ---- F: symbolic factorisation (CTA 0)
+        if (blockIdx.x == 0) panel_factorise(a, smem, ps, pos, Bn);
+        SK_PROF(3);
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+        SK_PROF(7);
+        // ---- V + D part 1
+        for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
         __syncthreads();
-        for (int h = 0; h < s_nrun; ++h) {
-            const int slot = s_run[h];
-            cta_random(a, sm, pos + slot, a.qubits[pos + slot], int(__ldcg(wpiv + slot)), tma_parity, false);
+        const u64 randmask = s_info.randmask;
+        const u64 allmask = (Bn < 64) ? ((1ull << Bn) - 1ull) : ~0ull;
+        const u64 detmask = ~randmask & allmask;
+        if (tid == 0) s_nheavy = 0;
+        __syncthreads();
+        {
+            // V: words [wlo, whi) of every pivot value belong to this CTA; thread t owns word wlo + t
+            const int wpc = (W + G - 1) / G;
+            const int wlo = min(W, blockIdx.x * wpc), whi = min(W, wlo + wpc);
+            const int nw = whi - wlo;
+            const int nvw = (nw + 31) / 32;                         // warps busy with V
+            u64* vs = smem + (size_t)kMeasWarps * 2 * Wp;           // [Bn][2][wpc] after the accumulators
+            if (warp < nvw) {
+                // stage the panel-start pivot rows' words: items (step k, word t), 4 items (8 loads) in flight per thread
+                const int nitems = Bn * nw, nvt = 32 * nvw;
+                for (int i0 = tid; i0 < nitems; i0 += 4 * nvt) {
+                    u64 lx[4], lz[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + u * nvt;
+                        lx[u] = 0; lz[u] = 0;
+                        if (i < nitems) {
+                            const int k = i / nw, t = i - k * nw;
+                            const u32 pk = s_info.piv[k];
+                            if (pk != 0xffffffffu) { const u64* rp = a.m.rows + (size_t)(2 * pk) * Wp + wlo + t; lx[u] = ldcg(rp); lz[u] = ldcg(rp + Wp); }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + u * nvt;
+                        if (i < nitems) { const int k = i / nw, t = i - k * nw; vs[(size_t)(2 * k) * wpc + t] = lx[u]; vs[(size_t)(2 * k + 1) * wpc + t] = lz[u]; }
+                    }
+                }
+                if (nvw == 1) __syncwarp(); else named_bar(2, 32 * nvw);
+                for (int t = tid; t < nw; t += nvt) {
+                    const int w = wlo + t;
+                    u64 bits = randmask;
+                    while (bits) {
+                        const int k = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                        u64 ax = vs[(size_t)(2 * k) * wpc + t], az = vs[(size_t)(2 * k + 1) * wpc + t];
+                        u64 hb = s_info.hist[k];
+                        int e = 0;
+                        while (hb) {
+                            const int l = __ffsll((long long)hb) - 1; hb &= hb - 1;
+                            const u64 bx = vs[(size_t)(2 * l) * wpc + t], bz = vs[(size_t)(2 * l + 1) * wpc + t];
+                            e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                        }
+                        vs[(size_t)(2 * k) * wpc + t] = ax; vs[(size_t)(2 * k + 1) * wpc + t] = az;
+                        __stcg(a.pivbuf + (size_t)(2 * k) * Wp + w, ax); __stcg(a.pivbuf + (size_t)(2 * k + 1) * Wp + w, az);
+                        if (e & 3) atomicAdd(&info->eph[k], (u32)(e & 3));
+                    }
+                }
+            } else {
+                // D part 1: product of the panel-start partner rows of every deterministic step; the idx-th
+                // deterministic step goes to CTA idx % G, warp (idx / G) % nwd of the non-V warps
+                const int nwd = kMeasWarps - nvw;
+                u64 bits = detmask; int idx = 0;
+                while (bits) {
+                    const int j = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                    const int my = idx++;
+                    if (my % G != int(blockIdx.x) || (my / G) % nwd != warp - nvw) continue;
+                    const u64* dcol = a.pan + (size_t)j * RW + W;
+                    if (lane == 0) s_wcnt[warp] = 0;
+                    __syncwarp();
+                    for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {
+                        u64 cv[kColChunk];
+#pragma unroll
+                        for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < W) ? ldcg(dcol + w) : 0ull; }
+#pragma unroll
+                        for (int t = 0; t < kColChunk; ++t) {
+                            const int w = w0 + 32 * t + lane;
+                            u64 v = cv[t];
+                            while (v) {
+                                const int b = __ffsll((long long)v) - 1; v &= v - 1;
+                                const int ti = atomicAdd(&s_wcnt[warp], 1);
+                                if (ti < kWarpList) s_wlist[warp][ti] = u32(w * 64 + b);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    const int npart = s_wcnt[warp];
+                    if (npart > kWarpList) {                  // tree-reduced by the whole CTA below
+                        if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = j; }
+                        continue;
+                    }
+                    for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
+                    int e = warp_mul_list(a.m.rows, W, Wp, s_wlist[warp], npart, acc_x, acc_z, lane);
+                    for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[warp][i]));
+                    e = warp_sum(e) & 3;
+                    u64* dx = a.detacc + (size_t)(2 * j) * Wp;
+                    for (int w = lane; w < W; w += 32) { __stcg(dx + w, acc_x[w]); __stcg(dx + Wp + w, acc_z[w]); }
+                    if (lane == 0) info->dete[j] = e;
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            for (int h = 0; h < s_nheavy; ++h) {
+                const int j = s_heavy[h];
+                int total;
+                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total);
+                if (tid == 0) info->dete[j] = e;
+            }
         }
         SK_PROF(4);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(5);
-        // ---- sequential mode: when a wave commits only a handful of measurements the block is
-        // dependency-limited; CTA 0 then runs the next `seqlen` measurements strictly in order
-        // with CTA-level synchronisation only (no grid barriers), the other CTAs wait.
-        {
-            const u32 nc = __ldcg(&ws->ncommit);
-            const u32 committed = (commits_seen == 0xffffffffu) ? 0xffffu : nc - commits_seen;
-            // a narrow wave is normal while the dependency frontier is still widening (round 1 of a
-            // memory experiment needs ~20 waves); only a long run of narrow waves means the block is
-            // inherently sequential
-            narrow = (committed < (u32)a.seq_threshold) ? narrow + 1 : 0;
-            seqlen = (narrow >= kNarrowWaves) ? min(kSeqMax, max(kSeqMin, seqlen * 2)) : 0;
-        }
-        if (seqlen > 0) {
-            if (blockIdx.x == 0) {
-                int j = pos, ran = 0;
-                u64 t0s = a.prof ? gtime() : 0; const long long c0 = clock64(); const u64 tseq0 = t0s;
-                for (; j < a.count && ran < seqlen; ++j) {
-                    if (__ldcg(a.done + j)) continue;                   // uniform: every thread reads the same byte
-                    const u32 q = a.qubits[j];
-                    const u64* xcol = a.m.cols + (size_t)(2 * q) * RW;
-                    u32 piv = 0xffffffffu;                      // s_piv was reset at the end of the previous iteration
-                    for (int w = tid; w < W; w += kMeasThreads) {
-                        u64 v = ldcg(xcol + w);
-                        if (v) piv = min(piv, u32(w * 64 + __ffsll((long long)v) - 1));
-                    }
-                    piv = warp_min(piv);
-                    if (lane == 0 && piv != 0xffffffffu) atomicMin(&s_piv, piv);
-                    __syncthreads();
-                    piv = s_piv;
-                    u64 t1 = 0, t2 = 0;
-                    if (a.prof && tid == 0) { t1 = gtime(); ws->seqprof[0] += t1 - t0s; }
-                    if (piv == 0xffffffffu) cta_det(a, sm, j, xcol);
-                    else cta_random(a, sm, j, q, int(piv), tma_parity, true);
-                    if (a.prof && tid == 0) { t2 = gtime(); ws->seqprof[piv == 0xffffffffu ? 1 : 2] += t2 - t1; ws->seqprof[piv == 0xffffffffu ? 4 : 5] += 1; }
-                    __threadfence();                                    // this measurement's updates before the next column read
-                    if (tid == 0) s_piv = 0xffffffffu;                  // (everyone read s_piv before the CTA op's barriers)
-                    __syncthreads();
-                    if (a.prof && tid == 0) { t0s = gtime(); ws->seqprof[3] += t0s - t2; }
-                    ++ran;
-                }
-                if (tid == 0) { atomicAdd(&ws->waves, (u64)ran); if (a.prof) { ws->seqprof[6] += (u64)(clock64() - c0); ws->seqprof[7] += gtime() - tseq0; } }
-            }
-            SK_PROF(6);
-            if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        }
-        commits_seen = __ldcg(&ws->ncommit);
-        // next window starts at the first measurement not yet executed (same value in every CTA)
-        int first = 0x7fffffff;
-        for (int jj = pos + tid; jj < wend; jj += kMeasThreads) if (!__ldcg(a.done + jj)) first = min(first, jj);   // no early exit: loads overlap
-        if (tid == 0) s_red[0] = 0x7fffffff;
-        __syncthreads();
-        if (first != 0x7fffffff) atomicMin(&s_red[0], first);
-        __syncthreads();
-        pos = min(s_red[0], wend);
-        ++wave;
         SK_PROF(7);
+        // ---- signs of the pivot values (triangular GF(2) recurrence; every CTA solves it itself)
+        if (tid == 0) {
+            u64 psign = 0; u32 odd = 0;
+            u64 bits = randmask;
+            while (bits) {
+                const int k = __ffsll((long long)bits) - 1; bits &= bits - 1;
+                const u32 ek = __ldcg(&info->eph[k]) + 2u * (u32)((s_info.osign >> k) & 1ull) + 2u * (u32)__popcll(s_info.hist[k] & psign);
+                odd |= ek & 1u;
+                psign |= (u64)((ek >> 1) & 1u) << k;
+            }
+            ps.psign = psign; ps.podd = odd;
+            if (odd) atomicOr(&ws->err, 1u);
+        }
+        __syncthreads();
+        const u64 psign = ps.psign;
+        // ---- D part 2 + A: items = deterministic steps, then touched rows; warp per item
+        {
+            const int nd = __popcll(detmask);
+            const int nt = int(s_info.nt);
+            for (int it = gwi; it < nd + nt; it += GW) {
+                if (it < nd) {
+                    // deterministic step: j = it-th set bit of detmask
+                    u64 bits = detmask; for (int s = 0; s < it; ++s) bits &= bits - 1;
+                    const int j = __ffsll((long long)bits) - 1;
+                    const u64* dx = a.detacc + (size_t)(2 * j) * Wp;
+                    for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(dx + w); acc_z[w] = ldcg(dx + Wp + w); }
+                    const u64 N = s_info.dN[j], Z = s_info.dZ[j];
+                    int cnt = 0;
+                    { u64 b = N; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
+                    __syncwarp();
+                    int e = warp_mul_list(a.pivbuf, W, Wp, s_wlist[warp], cnt, acc_x, acc_z, lane);
+                    __syncwarp();
+                    if (lane == 0) {
+                        e += __ldcg(&info->dete[j]) + 2 * __popcll(N & psign);
+                        u64 b = Z;
+                        while (b) {        // (+-Z_{q_l}) * acc
+                            const int l = __ffsll((long long)b) - 1; b &= b - 1;
+                            const u32 ql = s_q[l];
+                            const u64 zb = 1ull << (ql & 63);
+                            e += g_word(0ull, zb, acc_x[ql >> 6], acc_z[ql >> 6]) + 2 * int(s_info.outc[l]);
+                            acc_z[ql >> 6] ^= zb;
+                        }
+                    }
+                    e = warp_sum(e) & 3;
+                    if (lane == 0) {
+                        if (e & 1) atomicOr(&ws->err, 1u);
+                        a.outcomes[pos + j] = uint8_t(e >> 1); a.dets[pos + j] = 1;
+                    }
+                    __syncwarp();
+                } else {
+                    const int i = it - nd;
+                    const u32 h = __ldcg(a.tlist + i);
+                    u64 M = ldcg(a.tM + i);
+                    // is h a pivot of this panel, or the destabilizer partner of one?
+                    int kp = -1, ko = -1;
+                    {
+                        const u32 p0 = (lane < Bn) ? s_info.piv[lane] : 0xffffffffu, p1 = (lane + 32 < Bn) ? s_info.piv[lane + 32] : 0xffffffffu;
+                        const u32 b0 = __ballot_sync(0xffffffffu, p0 == h), b1 = __ballot_sync(0xffffffffu, p1 == h);
+                        const u32 c0 = __ballot_sync(0xffffffffu, p0 != 0xffffffffu && p0 + (u32)a.NS == h), c1 = __ballot_sync(0xffffffffu, p1 != 0xffffffffu && p1 + (u32)a.NS == h);
+                        if (b0) kp = __ffs(b0) - 1; else if (b1) kp = 32 + __ffs(b1) - 1;
+                        if (c0) ko = __ffs(c0) - 1; else if (c1) ko = 32 + __ffs(c1) - 1;
+                    }
+                    u64* tx = a.m.rows + (size_t)(2 * h) * Wp;
+                    u64* sg = a.m.sgn + (h >> 6);
+                    const u64 hb = 1ull << (h & 63);
+                    if (kp >= 0) {                // row p := +-Z_q
+                        const u32 q = s_q[kp];
+                        for (int w = lane; w < 2 * Wp; w += 32) __stcg(tx + w, (w == Wp + int(q >> 6)) ? (1ull << (q & 63)) : 0ull);
+                        if (lane == 0) { if (s_info.outc[kp]) atomicOr(sg, hb); else atomicAnd(sg, ~hb); a.outcomes[pos + kp] = s_info.outc[kp]; a.dets[pos + kp] = 0; }
+                        continue;
+                    }
+                    int e;
+                    if (ko >= 0) {                // row p+n := P_ko', then the later steps
+                        const u64* sx = a.pivbuf + (size_t)(2 * ko) * Wp;
+                        for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(sx + w); acc_z[w] = ldcg(sx + Wp + w); }
+                        M &= (ko < 63) ? ~((2ull << ko) - 1ull) : 0ull;
+                        e = (lane == 0) ? 2 * int((psign >> ko) & 1ull) : 0;
+                    } else {
+                        for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(tx + w); acc_z[w] = ldcg(tx + Wp + w); }
+                        e = (lane == 0) ? 2 * int((ldcg(sg) >> (h & 63)) & 1ull) : 0;
+                        if (M == 0) continue;
+                    }
+                    int cnt = 0;
+                    { u64 b = M; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
+                    __syncwarp();
+                    e += warp_mul_list(a.pivbuf, W, Wp, s_wlist[warp], cnt, acc_x, acc_z, lane);
+                    if (lane == 0) e += 2 * __popcll(M & psign);
+                    e = warp_sum(e) & 3;
+                    for (int w = lane; w < W; w += 32) { __stcg(tx + w, acc_x[w]); __stcg(tx + Wp + w, acc_z[w]); }
+                    if (lane == 0) {
+                        if (e & 1) atomicOr(&ws->err, 1u);
+                        if (e >> 1) atomicOr(sg, hb); else atomicAnd(sg, ~hb);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        SK_PROF(5);
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+        SK_PROF(7);
+        pos += Bn;
     }
+    if (blockIdx.x == 0 && tid == 0) ws->c_stale = 1u;
 }
 
 // SPEC:165-173 rowsum(h, i) on the R form + C form fix-up, single CTA (API parity helper).

@@ -16,12 +16,17 @@ __device__ __forceinline__ void bfly(u32& v, int j, u32 m, int lane) {
 }
 
 // All sizes in 32-bit words.  Loads outside [src_rows) x [src_words) read 0;
-// stores outside [dst_rows) x [dst_words) are dropped.
+// stores outside [dst_rows) x [dst_words) are dropped.  blockIdx.z selects one of gridDim.z
+// independent matrices (src + z*src_zoff -> dst + z*dst_zoff: the x and z halves of a store).
+// If `flag` is given the kernel is a no-op unless *flag != 0 (device-side "C form is stale").
 __global__ void __launch_bounds__(256)
 k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
-                 u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words) {
+                 u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                 size_t src_zoff, size_t dst_zoff, const u32* __restrict__ flag) {
     __shared__ u32 tin[256][9];    // [src row in tile][word], +1 pad: conflict-free column reads
     __shared__ u32 tout[256][9];   // [dst row in tile][word]
+    if (flag && __ldcg(flag) == 0u) return;
+    src += (size_t)blockIdx.z * src_zoff; dst += (size_t)blockIdx.z * dst_zoff;
     const int c0 = blockIdx.x * 256;          // first src row of the tile  (= dst bit offset)
     const int w0 = blockIdx.y * 8;            // first src word of the tile (= dst row offset / 32)
     const int t = threadIdx.x;

@@ -33,9 +33,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
     c->num_sms = prop.multiProcessorCount;
-    if (const char* e = getenv("SK_SEQ_THRESHOLD")) c->seq_threshold = atoi(e);
-    if (const char* e = getenv("SK_TMA")) c->use_tma = atoi(e);
-    if (getenv("SK_DEBUG_PROF") || getenv("SK_SEQPROF")) c->prof = 1;
+    if (getenv("SK_DEBUG_PROF")) c->prof = 1;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
@@ -96,14 +94,18 @@ struct sk_tableau {
     size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
     u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
     int meas_grid = 0; size_t meas_smem = 0;
-    u64* d_claim = nullptr; u32* d_wpiv = nullptr; uint8_t* d_wrun = nullptr; uint8_t* d_done = nullptr;
-    size_t claim_bytes = 0, done_cap = 0;
+    u32* d_wpiv = nullptr;
+    // panel-mode scratch (kernels_measure.cuh)
+    int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
+    u32* d_tlist = nullptr; u64* d_tM = nullptr;
 };
 
+// x and z halves in one launch (grid.z = 2); `flag` != nullptr makes the launch conditional on *flag
 static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int srows, int swords,
-                                u32* dst, size_t dstride, int drows, int dwords) {
-    dim3 grid((srows + 255) / 256, (swords + 7) / 8);
-    k_transpose_bits<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords);
+                                u32* dst, size_t dstride, int drows, int dwords,
+                                size_t src_zoff, size_t dst_zoff, const u32* flag) {
+    dim3 grid((srows + 255) / 256, (swords + 7) / 8, 2);
+    k_transpose_bits<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
     return SK_OK;
@@ -111,28 +113,22 @@ static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int s
 // C -> R
 static int32_t rows_from_cols(sk_tableau* t) {
     sk_ctx* c = t->ctx;
-    const u32* src = reinterpret_cast<const u32*>(t->m.cols);
-    u32* dst = reinterpret_cast<u32*>(t->m.rows);
-    for (int h = 0; h < 2; ++h) {
-        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * t->RW, (size_t)4 * t->RW, int(t->n), 2 * t->RW,
-                                      dst + (size_t)h * 2 * t->Wp, (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp);
-        if (rc) return rc;
-    }
+    int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(t->m.cols), (size_t)4 * t->RW, int(t->n), 2 * t->RW,
+                                  reinterpret_cast<u32*>(t->m.rows), (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp,
+                                  (size_t)2 * t->RW, (size_t)2 * t->Wp, nullptr);
+    if (rc) return rc;
     c->cnt.transposes++;
     t->r_valid = true;
     return SK_OK;
 }
-// R -> C
-static int32_t cols_from_rows(sk_tableau* t) {
+// R -> C ; with `flag` only if the device-side stale flag is raised
+static int32_t cols_from_rows(sk_tableau* t, const u32* flag = nullptr) {
     sk_ctx* c = t->ctx;
-    const u32* src = reinterpret_cast<const u32*>(t->m.rows);
-    u32* dst = reinterpret_cast<u32*>(t->m.cols);
-    for (int h = 0; h < 2; ++h) {
-        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * t->Wp, (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp,
-                                      dst + (size_t)h * 2 * t->RW, (size_t)4 * t->RW, int(t->n), 2 * t->RW);
-        if (rc) return rc;
-    }
-    c->cnt.transposes++;
+    int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(t->m.rows), (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp,
+                                  reinterpret_cast<u32*>(t->m.cols), (size_t)4 * t->RW, int(t->n), 2 * t->RW,
+                                  (size_t)2 * t->Wp, (size_t)2 * t->RW, flag);
+    if (rc) return rc;
+    if (!flag) c->cnt.transposes++;
     return SK_OK;
 }
 
@@ -161,20 +157,36 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     t->cols_bytes = (size_t)n * 2 * t->RW * 8;
     t->rows_bytes = (size_t)64 * t->RW * 2 * t->Wp * 8;
     t->sgn_bytes = (size_t)t->RW * 8;
-    t->meas_smem = (size_t)(t->RW + 4 * t->Wp + kMeasWarps * 2 * t->Wp) * 8;
-    if (t->meas_smem + 1024 > (size_t)c->max_smem_optin) {
-        size_t need = t->meas_smem; delete t;
-        SK_FAIL(c, SK_EDIM, "n=%llu needs %zu B of shared memory per CTA (limit %d)", (unsigned long long)n, need, c->max_smem_optin);
+    {
+        // dynamic shared memory of k_measure_block: per-warp accumulators + pivot-value scratch, or the panel
+        cudaFuncAttributes fa{};
+        SK_CUDA(c, cudaFuncGetAttributes(&fa, k_measure_block));
+        const size_t avail = (size_t)c->max_smem_optin - fa.sharedSizeBytes - 1024;
+        const size_t acc_words = (size_t)kMeasWarps * 2 * t->Wp;
+        const size_t col_words = (size_t)t->RW;
+        if ((acc_words + 2) * 8 > avail || (col_words + t->W) * 8 > avail) {
+            delete t;
+            SK_FAIL(c, SK_EDIM, "n=%llu needs more shared memory per CTA than the %zu B available", (unsigned long long)n, avail);
+        }
+        int B = int(std::min<size_t>(kPanelMax, (avail / 8 - t->W) / col_words));
+        if (const char* e = getenv("SK_PANEL")) B = std::max(1, std::min(B, atoi(e)));
+        const int wpc = (t->W + c->num_sms - 1) / c->num_sms;
+        while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
+        t->B = B;
+        t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + t->W) * 8;
     }
     cudaError_t e1 = cudaMalloc(&t->m.cols, t->cols_bytes);
     cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
     cudaError_t e3 = cudaMalloc(&t->m.sgn, t->sgn_bytes);
-    t->claim_bytes = (size_t)64 * t->W * 8;
     const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
-    cudaError_t e4 = cudaMalloc(&t->d_claim, t->claim_bytes);
-    cudaError_t e5 = cudaMalloc(&t->d_wpiv, 2 * window * 4);
-    cudaError_t e6 = cudaMalloc(&t->d_wrun, 2 * window);
-    if (e1 || e2 || e3 || e4 || e5 || e6) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
+    cudaError_t e4 = cudaMalloc(&t->d_wpiv, 2 * window * 4);
+    cudaError_t e5 = cudaMalloc(&t->d_pan, (size_t)t->B * t->RW * 8);
+    cudaError_t e6 = cudaMalloc(&t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
+    cudaError_t e7 = cudaMalloc(&t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
+    cudaError_t e8 = cudaMalloc(&t->d_info, sizeof(PanelInfo));
+    cudaError_t e9 = cudaMalloc(&t->d_tlist, (size_t)64 * t->RW * 4);
+    cudaError_t e10 = cudaMalloc(&t->d_tM, (size_t)64 * t->RW * 8);
+    if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
     if ((int)t->meas_smem > c->meas_smem_attr) {
         SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
         c->meas_smem_attr = (int)t->meas_smem;
@@ -193,7 +205,8 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     if (!t) return;
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
-    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_claim); cudaFree(t->d_wpiv); cudaFree(t->d_wrun); cudaFree(t->d_done);
+    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_wpiv);
+    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM);
     cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
     delete t;
 }
@@ -356,27 +369,21 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
     if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
-    // reset barrier counter and the three wave slots (counters persist)
+    // reset barrier counter, wave slots (0xffffffff = none) and the stale flag (counters persist)
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
     SK_CUDA(c, cudaMemsetAsync(&ws->r0[0], 0xFF, 16, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->ncommit, 0, 4, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(t->d_claim, 0, t->claim_bytes, c->stream));
-    if ((size_t)count > t->done_cap) {
-        SK_CUDA(c, cudaStreamSynchronize(c->stream));
-        cudaFree(t->d_done); t->d_done = nullptr; t->done_cap = 0;
-        SK_CUDA(c, cudaMalloc(&t->d_done, (size_t)count * 2));
-        t->done_cap = (size_t)count * 2;
-    }
-    SK_CUDA(c, cudaMemsetAsync(t->d_done, 0, (size_t)count, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->c_stale, 0, 4, c->stream));
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
-    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.claim = t->d_claim; a.wpiv = t->d_wpiv; a.wrun = t->d_wrun; a.done = t->d_done;
-    a.seq_threshold = c->seq_threshold; a.use_tma = c->use_tma; a.prof = c->prof;
+    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
+    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM;
+    a.prof = c->prof;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
-    return SK_OK;
+    // panel mode keeps only the R form current: re-derive C if (and only if) the kernel raised the flag
+    return cols_from_rows(t, &ws->c_stale);
 }
 
 static int32_t reserve_record(sk_tableau* t, size_t m) {
@@ -434,8 +441,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     if (!c) return SK_EARG;
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 13 * 8, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->dbg[0], 0, 16 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 14 * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -446,8 +452,8 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     *out = c->cnt;
     out->n_rand = h.n_rand; out->n_det = h.n_det; out->k_rand = h.k_rand; out->k_det = h.k_det; out->waves = h.waves;
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
-    if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "cta_random: calls %llu  stage+lists %.0f us  B1 %.0f us  B2 %.0f us  B3B4rec %.0f us  avg nt %.1f nmw %.1f nsup %.1f\n", (unsigned long long)h.dbg[7], h.dbg[0] / 1e3, h.dbg[1] / 1e3, h.dbg[2] / 1e3, h.dbg[3] / 1e3, double(h.dbg[4]) / (h.dbg[7] + 1e-9), double(h.dbg[5]) / (h.dbg[7] + 1e-9), double(h.dbg[6]) / (h.dbg[7] + 1e-9));
-    if (getenv("SK_SEQPROF")) fprintf(stderr, "seqprof: inspect %.0f us det %.0f us (n=%llu) random %.0f us (n=%llu) fence %.0f us ; cycles %llu\n", h.seqprof[0] / 1e3, h.seqprof[1] / 1e3, (unsigned long long)h.seqprof[4], h.seqprof[2] / 1e3, (unsigned long long)h.seqprof[5], h.seqprof[3] / 1e3, (unsigned long long)h.seqprof[6]);
+    if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "measure kernel CTA0 us: P1 %.0f P2 %.0f | gather %.0f factorise %.0f values+detA %.0f apply+detB %.0f | barriers wave %.0f panel %.0f | panels %llu\n",
+                                         h.prof[0] / 1e3, h.prof[1] / 1e3, h.prof[2] / 1e3, h.prof[3] / 1e3, h.prof[4] / 1e3, h.prof[5] / 1e3, h.prof[6] / 1e3, h.prof[7] / 1e3, (unsigned long long)h.panels);
     return SK_OK;
 }
 

@@ -16,10 +16,8 @@ struct sk_ctx {
     bool own_stream = false;
     int num_sms = 0;
     int max_smem_optin = 0;
-    int prof = 0;                           // SK_DEBUG_PROF / SK_SEQPROF: device-side phase timers (slows the kernel)
-    int use_tma = 0;                        // stage measurement operands with TMA bulk copies (SK_TMA=1) or ld.cg
+    int prof = 0;                           // SK_DEBUG_PROF: device-side phase timers (slows the kernel)
     int meas_grid_override = 0;             // SK_MEAS_GRID: CTAs of the measurement kernel (profiling aid)
-    int seq_threshold = 6;                  // measurement scheduler: sequential-mode trigger (SK_SEQ_THRESHOLD)
     int meas_smem_attr = 0;                 // largest dynamic-smem attribute set on k_measure_block
     std::string err;
     // growable device scratch

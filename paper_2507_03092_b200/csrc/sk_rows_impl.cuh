@@ -11,22 +11,18 @@
 static int32_t dm_transpose_c2r(sk_ctx* c, const DMat& m) {
     const u32* src = reinterpret_cast<const u32*>(m.cols);
     u32* dst = reinterpret_cast<u32*>(m.rows);
-    for (int h = 0; h < 2; ++h) {
-        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * m.RW, (size_t)4 * m.RW, int(m.n), 2 * m.RW,
-                                      dst + (size_t)h * 2 * m.Wp, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp);
-        if (rc) return rc;
-    }
+    int32_t rc = launch_transpose(c, src, (size_t)4 * m.RW, int(m.n), 2 * m.RW, dst, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp,
+                                  (size_t)2 * m.RW, (size_t)2 * m.Wp, nullptr);
+    if (rc) return rc;
     c->cnt.transposes++;
     return SK_OK;
 }
 static int32_t dm_transpose_r2c(sk_ctx* c, const DMat& m) {
     const u32* src = reinterpret_cast<const u32*>(m.rows);
     u32* dst = reinterpret_cast<u32*>(m.cols);
-    for (int h = 0; h < 2; ++h) {
-        int32_t rc = launch_transpose(c, src + (size_t)h * 2 * m.Wp, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp,
-                                      dst + (size_t)h * 2 * m.RW, (size_t)4 * m.RW, int(m.n), 2 * m.RW);
-        if (rc) return rc;
-    }
+    int32_t rc = launch_transpose(c, src, (size_t)4 * m.Wp, 64 * m.RW, 2 * m.Wp, dst, (size_t)4 * m.RW, int(m.n), 2 * m.RW,
+                                  (size_t)2 * m.Wp, (size_t)2 * m.RW, nullptr);
+    if (rc) return rc;
     c->cnt.transposes++;
     return SK_OK;
 }

@@ -24,5 +24,5 @@ for rep in range(reps):
     print(f"rep{rep}: device {e0.elapsed_time(e1):.3f} ms  enqueue {1e3*(w1-w0):.2f} ms  wall {1e3*(w2-w0):.2f} ms  "
           f"n_rand={c['n_rand']} n_det={c['n_det']} k_rand={c['k_rand']} k_det={c['k_det']} waves={c['waves']} layers={c['layers']} "
           f"transposes={c['transposes']} launches={c['kernel_launches']}")
-    print("   meas phases us [P1,bar,P2,bar,P3,bar,win]:", [round(v/1e3) for v in c["meas_phase_ns"][:7]])
+    print("   meas phases us [P1,P2,gather,factorise,values+detA,apply+detB,bar(wave),bar(panel)]:", [round(v/1e3) for v in c["meas_phase_ns"][:8]])
 print("outcome checksum", int(out.sum()), int(det.sum()))
