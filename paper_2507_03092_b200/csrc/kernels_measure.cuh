@@ -51,7 +51,7 @@ constexpr int kPanelMax = 64;
 
 struct PanelInfo {      // global scratch describing the current panel (written by CTA 0 in F)
     u64 hist[kPanelMax];   // random step l: earlier random steps whose pivot was multiplied into row p_l
-    u64 dN[kPanelMax];     // deterministic step j: pivot values to multiply (parity of partner histories)
+    u64 dN[kPanelMax];     // deterministic step j: pivot values to multiply (parity of partner histories; written by D part 1)
     u64 dZ[kPanelMax];     // deterministic step j: earlier steps whose +-Z row is a partner
     u32 piv[kPanelMax];    // pivot stabilizer row-bit, 0xffffffff = deterministic step
     u32 eph[kPanelMax];    // V: sum over words of the g contributions of P_l' (atomic, mod 4 matters)
@@ -65,13 +65,15 @@ struct PanelInfo {      // global scratch describing the current panel (written 
 
 struct MeasWs {
     u32 bar;            // grid barrier counter (zeroed before each launch)
-    u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout
+    u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
     u32 r0[4];          // per-wave index of the first random measurement, min-reduced; 3 slots rotate
     u32 c_stale;        // panel mode ran: the C form must be re-derived from R
     u32 pad;
     u64 n_rand, n_det, k_rand, k_det, waves;
     u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
     u64 panels;
+    u64 cprof[16];      // debug: SM cycles per step section, thread 0 [0..7] and thread 96 [8..15]: random {search+bar, gather+bar, update}, det {search+bar, gather+bar, rest}
+    u64 fprof[8];       // factorise (CTA 0) ns: load, random steps, deterministic steps, tail ; [4] random steps, [5] deterministic steps
 };
 
 constexpr int kMeasThreads = 512;
@@ -79,6 +81,7 @@ constexpr int kMeasWarps = kMeasThreads / 32;
 constexpr int kSlotsPerWarp = 4;
 constexpr int kColChunk = 6;         // column words per lane loaded back-to-back (192 words per chunk)
 constexpr int kMaxTargets = 2048;    // partner-list capacity of the CTA-wide product (dense fallback above)
+constexpr int kWarpDirect = 16;      // panel mode: longer partner products go to a whole CTA (<= 1 per CTA and panel)
 constexpr int kWarpList = 64;        // rows a single warp multiplies from its list; longer products are tree-reduced by a CTA
 
 struct MeasArgs {
@@ -100,6 +103,7 @@ struct MeasArgs {
     PanelInfo* info;
     u32* tlist;         // [64*RW] touched rows
     u64* tM;            // [64*RW] their step masks
+    u64* rowM;          // [64*RW] step mask by row-bit (zero for rows the current panel does not touch)
     int prof;           // device-side phase timers (SK_DEBUG_PROF)
 };
 
@@ -148,7 +152,7 @@ __device__ __forceinline__ int warp_mul_list(const u64* base, int W, int Wp, con
 // ---- CTA-wide building blocks (all kMeasThreads threads call them together) -------------
 struct MeasSmem {
     u64* acc;       // [kMeasWarps][2*Wp] per-warp product accumulators (start of the dynamic region)
-    int* pe; int* pk;
+    int* pe; int* pk; u64* pn;
     int* cnt;       // list length
     u32* targets;   // [kMaxTargets] partner rows
 };
@@ -161,7 +165,7 @@ struct MeasSmem {
 // stabilizer rows commute.  Returns (CTA-uniform) the phase exponent mod 4 including the rows'
 // signs; if out_x != nullptr the product words are stored there (R layout).  *total_out = #rows.
 // sm.cnt[0] is zero on entry and on exit.
-__device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, const u64* dcol, u64* out_x, int* total_out) {
+__device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, const u64* dcol, u64* out_x, int* total_out, const u64* rowM = nullptr, u64* n_out = nullptr) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
@@ -184,6 +188,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
     __syncthreads();
     const int total = sm.cnt[0];
     int e = 0;
+    u64 nx = 0;                                           // XOR of the listed rows' step masks (panel mode)
     u64 ax = 0, az = 0;                                   // this thread's word of the running product
     const int Wq = (W + 31) & ~31;
     const int ngroups = max(1, min(kMeasThreads / Wq, (total + 7) / 8));
@@ -204,7 +209,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
                 }
             }
         }
-        for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
+        for (int i = tid; i < cnt; i += kMeasThreads) { e += 2 * sign_bit(a.m.sgn, int(sm.targets[i])); if (rowM) nx ^= ldcg(rowM + sm.targets[i]); }
     };
     if (Wq > kMeasThreads) {
         // very wide rows: a thread owns several words; the running product lives in out_x / sm.acc
@@ -234,7 +239,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
                 }
                 px[w] = bx; px[Wp + w] = bz;
             }
-            for (int i = tid; i < cnt; i += kMeasThreads) e += 2 * sign_bit(a.m.sgn, int(sm.targets[i]));
+            for (int i = tid; i < cnt; i += kMeasThreads) { e += 2 * sign_bit(a.m.sgn, int(sm.targets[i])); if (rowM) nx ^= ldcg(rowM + sm.targets[i]); }
         }
     } else if (total <= kMaxTargets) {
         multiply_list(total);
@@ -282,9 +287,11 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
     }
     e = warp_sum(e);
     if (lane == 0) sm.pe[warp] = e;
+    if (rowM) { nx = warp_xor64(nx); if (lane == 0) sm.pn[warp] = nx; }
     __syncthreads();
     int et = 0;
     for (int t = 0; t < kMeasWarps; ++t) et += sm.pe[t];
+    if (rowM && n_out) { u64 nt = 0; for (int t = 0; t < kMeasWarps; ++t) nt ^= sm.pn[t]; *n_out = nt; }
     *total_out = total;
     __syncthreads();
     if (tid == 0) sm.cnt[0] = 0;
@@ -296,99 +303,156 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
 // F: symbolic factorisation of one panel by CTA 0.  sp = dynamic smem: panel [Bn][RW] then the
 // pivot mask [W] (stabilizer rows used as pivots so far).
 struct PanelSmem {
-    u32 piv[kPanelMax]; u64 hist[kPanelMax], dN[kPanelMax], dZ[kPanelMax]; u32 kd[kPanelMax]; uint8_t outc[kPanelMax];
-    u32 full32[2], dfull32[2]; u32 nt; u32 krand; u64 psign; u32 podd;
+    u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax]; uint8_t outc[kPanelMax];
+    u32 full32[2]; u32 nt; u32 krand; u32 kdet; u64 psign; u32 podd;
 };
 
-__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, int pos, int Bn) {
+// XOR of the frozen masks m_l[w] over the steps l in `bits` (column stride CS).  Few steps: chase the
+// bits; many (a "hot" word: the same rows are targets again and again): linear sweep, 8 loads in flight.
+__device__ __forceinline__ u64 xor_masks(const u64* sp, int CS, int w, u64 bits, int j) {
+    u64 acc = 0;
+    if (__popcll(bits) <= 3) {
+        while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; acc ^= sp[(size_t)l * CS + w]; }
+    } else {
+        const u64* col = sp + w;
+        for (int l0 = 0; l0 < j; l0 += 8, col += 8 * (size_t)CS, bits >>= 8) {
+            if ((bits & 0xffull) == 0) continue;
+            u64 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (l0 + u < j) ? col[(size_t)u * CS] : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc ^= ((bits >> u) & 1ull) ? v[u] : 0ull;
+        }
+    }
+    return acc;
+}
+
+// F: symbolic factorisation of one panel by CTA 0 (see the file header).
+// Shared-memory panel: column j = words [j*CS, j*CS + RW] with CS = RW + 2; word RW holds the VIRTUAL rows:
+// when random step l overwrites destabilizer p_l + n with the old pivot row, the old row-bit is retired and
+// the new content lives on as virtual row l (bit l of word RW), so overwritten rows need no special casing:
+// retired bits (pivots, which become +-Z_q and never carry an x again, and their old partners) are masked off.
+// Left-looking elimination: column j is brought up to date only when step j needs it,
+//   cur_j = (orig_j ^ XOR_{l in S_j} m_l) & ~retired,   S_j = earlier random steps whose pivot row has an x
+// in column j (S_j bit l = pw_l bit j; the virtual word starts as S_j itself), sparse in the word index
+// through nzm.  m_l = column l at step l minus the pivot and its partner = the rows step l multiplies.
+__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, u32* s_rows, u64* mbar, u32& tma_parity, int pos, int Bn) {
     const int RW = a.m.RW, W = a.m.W, NS = a.NS;
-    const int tid = threadIdx.x, lane = tid & 31;
-    u64* pivmask = sp + (size_t)Bn * RW;
-    for (int i = tid; i < Bn * RW; i += kMeasThreads) sp[i] = ldcg(a.pan + i);
-    for (int w = tid; w < W; w += kMeasThreads) pivmask[w] = 0;
-    if (tid < kPanelMax) { ps.piv[tid] = 0xffffffffu; ps.hist[tid] = 0; ps.dN[tid] = 0; ps.dZ[tid] = 0; ps.kd[tid] = 0; ps.outc[tid] = 0; }
-    if (tid == 0) { ps.nt = 0; ps.krand = 0; }
+    const int CS = RW + 2, RV = RW + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    u64* nzm = sp + (size_t)Bn * CS;            // [RV] steps l whose frozen mask has a non-zero word here
+    u64* ret = nzm + RV;                        // [RV] retired row-bits
+    u64 tf = a.prof ? gtime() : 0;
+#define SK_FPROF(k) do { if (a.prof && tid == 0) { u64 _n = gtime(); a.ws->fprof[k] += _n - tf; tf = _n; } } while (0)
+    // the gathered panel arrives by TMA bulk copies (UBLKCP), one per column, on one mbarrier
+    if (tid == 0) {
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_expect_tx(mbar, u32(Bn * RW * 8));
+        for (int j = 0; j < Bn; ++j) tma_load_1d(sp + (size_t)j * CS, a.pan + (size_t)j * RW, u32(RW * 8), mbar);
+    }
+    for (int w = tid; w < 2 * RV; w += kMeasThreads) nzm[w] = 0;      // nzm | ret are contiguous
+    if (tid < Bn) { sp[(size_t)tid * CS + RW] = 0; sp[(size_t)tid * CS + RW + 1] = 0; }
+    if (tid < kPanelMax) { ps.piv[tid] = 0xffffffffu; ps.hist[tid] = 0; ps.pw[tid] = 0; ps.dZ[tid] = 0; ps.outc[tid] = 0; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; }
+    if (!mbar_wait(mbar, tma_parity)) { if (tid == 0) atomicOr(&a.ws->err, 0x40000000u); }
+    tma_parity ^= 1;
     __syncthreads();
-    const int nact = min(kMeasThreads, max(64, (RW + 31) & ~31));       // threads that own panel words (>= 64: one per panel column in the bit gathers)
-    u64 randmask = 0;
+    SK_FPROF(0);
+    const int nact = min(kMeasThreads, max(64, (RV + 31) & ~31));       // threads that own panel words (>= 64: one per panel column in the bit gathers)
+    u64 randmask = 0, pw_prev = 0;
+    long long cp[6] = {0, 0, 0, 0, 0, 0};
     if (tid < nact) {
         for (int j = 0; j < Bn; ++j) {
-            u64* cj = sp + (size_t)j * RW;
-            // pivot search over the stabilizer half (word-parallel; words ascend with the stride)
+            const long long c0 = clock64();
+            u64* cj = sp + (size_t)j * CS;
+            // S_j: lane l holds pw of steps l and l+32 (step j-1 was published after the last barrier: take it from the register copy)
+            u64 S;
+            {
+                const u64 a0 = (lane < j - 1) ? ps.pw[lane] : 0ull, a1 = (lane + 32 < j - 1) ? ps.pw[lane + 32] : 0ull;
+                S = (u64)__ballot_sync(0xffffffffu, (a0 >> j) & 1ull) | ((u64)__ballot_sync(0xffffffffu, (a1 >> j) & 1ull) << 32);
+                if (j > 0) S |= ((pw_prev >> j) & 1ull) << (j - 1);
+            }
             u32 cand = 0xffffffffu;
-            for (int w = tid; w < W; w += nact) { const u64 v = cj[w]; if (v && cand == 0xffffffffu) cand = u32(w * 64 + __ffsll((long long)v) - 1); }
-            cand = warp_min(cand);
+            for (int w = tid; w < RV; w += nact) {
+                const u64 old = cj[w];
+                u64 cur = (w == RW) ? S : old;
+                const u64 bits = S & nzm[w];
+                if (bits) cur ^= xor_masks(sp, CS, w, bits, j);
+                cur &= ~ret[w];
+                if (cur != old) cj[w] = cur;
+                if (w < W && cur && cand == 0xffffffffu) cand = u32(w * 64 + __ffsll((long long)cur) - 1);   // words ascend with the stride
+            }
+            cand = __reduce_min_sync(0xffffffffu, cand);
             if (lane == 0 && cand != 0xffffffffu) atomicMin(&ps.piv[j], cand);
             named_bar(1, nact);
             const u32 p = ps.piv[j];
+            const long long c1 = clock64();
             if (p != 0xffffffffu) {
                 // ---------------- random step
                 const u32 pd = u32(NS) + p;
-                if (tid < 64) {       // bit p of every panel column: history (l < j) and pivot row (c > j); bit p+n likewise
-                    const u32 bit = (tid < Bn) ? u32((sp[(size_t)tid * RW + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
-                    const u32 dbit = (tid < Bn) ? u32((sp[(size_t)tid * RW + (pd >> 6)] >> (pd & 63)) & 1ull) : 0u;
-                    const u32 bal = __ballot_sync(0xffffffffu, bit), dbal = __ballot_sync(0xffffffffu, dbit);
-                    if (lane == 0) { ps.full32[tid >> 5] = bal; ps.dfull32[tid >> 5] = dbal; }
-                }
-                named_bar(1, nact);
-                const u64 full = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
-                const u64 dfull = (u64)ps.dfull32[0] | ((u64)ps.dfull32[1] << 32);
-                const u64 below = (1ull << j) - 1ull;
-                const u64 above = (j < 63) ? ~((2ull << j) - 1ull) : 0ull;
-                const u64 pw = full & above;
-                for (int w = tid; w < RW; w += nact) {
-                    u64 m = cj[w];
-                    const bool isp = w == int(p >> 6), isd = w == int(pd >> 6);
-                    if (isp) m &= ~(1ull << (p & 63));
-                    if (isd) m &= ~(1ull << (pd & 63));
-                    cj[w] = m;                                   // frozen target mask of step j
-                    if (m) { u64 bits = pw; while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] ^= m; } }
-                    if (isp) {                                   // row p becomes +-Z_q: no x bits any more
-                        u64 bits = pw; while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] &= ~(1ull << (p & 63)); }
-                        pivmask[w] |= 1ull << (p & 63);
-                    }
-                    if (isd) {                                   // row p+n becomes the old pivot row: flip where it differs
-                        u64 bits = (dfull ^ full) & above;
-                        while (bits) { const int c = __ffsll((long long)bits) - 1; bits &= bits - 1; sp[(size_t)c * RW + w] ^= 1ull << (pd & 63); }
-                    }
-                }
-                if (tid == 0) { ps.hist[j] = full & randmask & below; ps.outc[j] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + j))); }
-                randmask |= 1ull << j;
-            } else {
-                // ---------------- deterministic step: partners D = destabilizer half of the column
-                if (tid < 64) {       // partners that earlier steps of this panel turned into +-Z
-                    u32 bit = 0;
-                    if (tid < j && ((randmask >> tid) & 1ull)) { const u32 pl = ps.piv[tid]; bit = u32((cj[W + (pl >> 6)] >> (pl & 63)) & 1ull); }
+                if (tid < 64) {       // bit p of every panel column: frozen masks for c < j (history), panel-start bits for c > j
+                    const u32 bit = (tid < Bn) ? u32((sp[(size_t)tid * CS + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
                     const u32 bal = __ballot_sync(0xffffffffu, bit);
                     if (lane == 0) ps.full32[tid >> 5] = bal;
                 }
                 named_bar(1, nact);
-                if (tid == 0) ps.dZ[j] = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
-                u64 nb = 0; int kd = 0;
-                for (int w = tid; w < W; w += nact) {
-                    const u64 dw = cj[W + w];
-                    kd += __popcll(dw);
-                    const u64 nonpiv = dw & ~pivmask[w];
-                    cj[W + w] = nonpiv;
-                    if (nonpiv) { u64 bits = randmask; while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; nb ^= (u64)(__popcll(sp[(size_t)l * RW + w] & nonpiv) & 1) << l; } }
+                const long long c2 = clock64();
+                const u64 full = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+                const u64 above = (j < 63) ? ~((2ull << j) - 1ull) : 0ull;
+                const u64 hist = full & randmask & ((1ull << j) - 1ull);
+                // x bits of the pivot row at the later columns = its panel-start bits ^ those of the pivot rows multiplied into it
+                u64 pw = full;
+                { u64 bits = hist; while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; pw ^= (l == j - 1) ? pw_prev : ps.pw[l]; } }
+                pw &= above;
+                for (int w = tid; w < RV; w += nact) {
+                    const bool isp = w == int(p >> 6), isd = w == int(pd >> 6);
+                    u64 m = cj[w];
+                    if (isp | isd) {         // the pivot and its partner are not multiplied (SURVEY section 7 hazard); both row-bits retire
+                        const u64 bit = isp ? (1ull << (p & 63)) : (1ull << (pd & 63));
+                        m &= ~bit; cj[w] = m; ret[w] |= bit;
+                    }
+                    if (m) nzm[w] |= 1ull << j;
                 }
-                nb = warp_xor64(nb); kd = warp_sum(kd);
-                if (lane == 0) { if (nb) atomicXor(&ps.dN[j], nb); if (kd) atomicAdd(&ps.kd[j], (u32)kd); }
+                if (tid == 0) { ps.hist[j] = hist; ps.pw[j] = pw; }
+                pw_prev = pw;
+                randmask |= 1ull << j;
+                { const long long c3 = clock64(); cp[0] += c1 - c0; cp[1] += c2 - c1; cp[2] += c3 - c2; }
+                SK_FPROF(1); if (a.prof && tid == 0) a.ws->fprof[4]++;
+            } else {
+                // ---------------- deterministic step: nothing changes; its column (partners D = destabilizer half,
+                // partners that earlier steps turned into +-Z = virtual word) stays frozen for the tail
+                pw_prev = 0;
+                { const long long c3 = clock64(); cp[3] += c1 - c0; cp[5] += c3 - c1; }
+                SK_FPROF(2); if (a.prof && tid == 0) a.ws->fprof[5]++;
             }
         }
     }
+    if (a.prof && (tid == 0 || tid == 96)) for (int k = 0; k < 6; ++k) a.ws->cprof[(tid ? 8 : 0) + k] += (u64)cp[k];
     __syncthreads();
     randmask = 0;
     for (int j = 0; j < Bn; ++j) if (ps.piv[j] != 0xffffffffu) randmask |= 1ull << j;
-    // touched rows: targets of any random step, the pivots and their destabilizer partners
+    const int nrand = __popcll(randmask);
+    if (tid < Bn && ((randmask >> tid) & 1ull)) ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
+    // regular touched rows: targets of any random step that were not retired later
     int kr = 0;
-    for (int w0 = 0; w0 < RW; w0 += kMeasThreads) {
+    for (int w0 = 0; w0 < RV; w0 += kMeasThreads) {
         const int w = w0 + tid;
         u64 tw = 0;
-        if (w < RW) {
-            u64 bits = randmask;
-            while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; const u64 v = sp[(size_t)l * RW + w]; tw |= v; kr += __popcll(v); }
-            tw |= pivmask[w < W ? w : w - W];
+        if (w < RV) {
+            const u64 nz = nzm[w];
+            if (nz) {
+                const u64* col = sp + w;
+                u64 bits = nz;
+                for (int l0 = 0; l0 < Bn; l0 += 8, col += 8 * (size_t)CS, bits >>= 8) {
+                    if ((bits & 0xffull) == 0) continue;
+                    u64 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = (l0 + u < Bn && ((bits >> u) & 1ull)) ? col[(size_t)u * CS] : 0ull;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) { tw |= v[u]; kr += __popcll(v[u]); }
+                }
+            }
+            tw = (w < RW) ? (tw & ~ret[w]) : 0ull;        // virtual rows are listed with the overwritten destabilizers below
         }
         const int pc = __popcll(tw);
         int incl = pc;
@@ -398,41 +462,79 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
         if (lane == 31 && incl) base = atomicAdd(&ps.nt, (u32)incl);
         base = __shfl_sync(0xffffffffu, base, 31);
         u32 ti = base + incl - pc;
-        while (tw) { const int b = __ffsll((long long)tw) - 1; tw &= tw - 1; a.tlist[ti++] = u32(w * 64 + b); }
+        while (tw) {
+            const int b = __ffsll((long long)tw) - 1; tw &= tw - 1;
+            const u32 h = u32(w * 64 + b);
+            if (ti < (u32)kMaxTargets) s_rows[ti] = h;
+            __stcg(a.tlist + ti, h);
+            ++ti;
+        }
     }
     kr = warp_sum(kr);
     if (lane == 0 && kr) atomicAdd(&ps.krand, (u32)kr);
-    // deterministic steps: partner sets (panel-start stabilizers only) for phase D
-    for (int j = 0; j < Bn; ++j)
-        if (!((randmask >> j) & 1ull))
-            for (int w = tid; w < W; w += kMeasThreads) __stcg(a.pan + (size_t)j * RW + W + w, sp[(size_t)j * RW + W + w]);
-    __syncthreads();
-    const u32 nt = ps.nt;
-    for (u32 i = tid; i < nt; i += kMeasThreads) {
-        const u32 h = __ldcg(a.tlist + i);
-        u64 M = 0, bits = randmask;
-        while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; M |= ((sp[(size_t)l * RW + (h >> 6)] >> (h & 63)) & 1ull) << l; }
-        __stcg(a.tM + i, M);
-    }
-    PanelInfo* info = a.info;
-    if (tid < kPanelMax) {
-        info->hist[tid] = ps.hist[tid]; info->dN[tid] = ps.dN[tid]; info->dZ[tid] = ps.dZ[tid];
-        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
-    }
+    // deterministic steps: partner sets for phase D (real destabilizer words -> panel-start stabilizers; virtual word -> +-Z rows)
+    for (int j = warp; j < Bn; j += kMeasWarps)
+        if (!((randmask >> j) & 1ull)) {
+            int kd = 0;
+            for (int w = lane; w < W; w += 32) { const u64 v = sp[(size_t)j * CS + W + w]; kd += __popcll(v); __stcg(a.pan + (size_t)j * RW + W + w, v); }
+            kd = warp_sum(kd);
+            if (lane == 0) { const u64 z = sp[(size_t)j * CS + RW] & randmask; ps.dZ[j] = z; atomicAdd(&ps.kdet, (u32)(kd + __popcll(z))); }
+        }
     if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
         const u32 pl = ps.piv[tid];
         const u32 bal = __ballot_sync(0xffffffffu, pl != 0xffffffffu && sign_bit(a.m.sgn, int(pl)));
         if (lane == 0) ps.full32[tid >> 5] = bal;
     }
     __syncthreads();
+    // step masks M_h of the regular rows: warp-cooperative bit gather (lane l reads columns l and l+32)
+    const u32 ntr = ps.nt;
+    for (u32 i0 = u32(warp) * 32u; i0 < ntr; i0 += kMeasThreads) {
+        const u32 i = i0 + lane;
+        const u32 hh = (i < ntr) ? (i < (u32)kMaxTargets ? s_rows[i] : __ldcg(a.tlist + i)) : 0u;
+        const int cnt = int(min(32u, ntr - i0));
+        u64 myM = 0;
+        for (int r = 0; r < cnt; ++r) {
+            const u32 h = __shfl_sync(0xffffffffu, hh, r);
+            const u32 b0 = (lane < Bn) ? u32((sp[(size_t)lane * CS + (h >> 6)] >> (h & 63)) & 1ull) : 0u;
+            const u32 b1 = (lane + 32 < Bn) ? u32((sp[(size_t)(lane + 32) * CS + (h >> 6)] >> (h & 63)) & 1ull) : 0u;
+            const u64 M = ((u64)__ballot_sync(0xffffffffu, b0) | ((u64)__ballot_sync(0xffffffffu, b1) << 32)) & randmask;
+            if (lane == r) myM = M;
+        }
+        if (i < ntr) { __stcg(a.tM + i, myM); __stcg(a.rowM + hh, myM); }
+    }
+    // the two rows every random step l overwrites: pivot p_l (-> +-Z_q) and partner p_l + n (-> P_l', then the steps
+    // that multiply virtual row l)
+    if (tid < 64 && ((randmask >> tid) & 1ull)) {
+        const int l = tid;
+        const u32 pl = ps.piv[l];
+        u64 Mv = 0;
+        const u64* col = sp + RW;
+        for (int c0 = 0; c0 < Bn; c0 += 8, col += 8 * (size_t)CS) {
+            u64 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (c0 + u < Bn) ? col[(size_t)u * CS] : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) Mv |= ((v[u] >> l) & 1ull) << (c0 + u);
+        }
+        Mv &= randmask & ((l < 63) ? ~((2ull << l) - 1ull) : 0ull);
+        const u32 at = ntr + 2u * (u32)__popcll(randmask & ((1ull << l) - 1ull));
+        __stcg(a.tlist + at, pl); __stcg(a.tM + at, 0ull);
+        __stcg(a.rowM + pl, ps.hist[l]);     // a deterministic step before l may still have row p_l as a partner
+        __stcg(a.tlist + at + 1, u32(NS) + pl); __stcg(a.tM + at + 1, Mv);
+    }
+    PanelInfo* info = a.info;
+    if (tid < kPanelMax) {
+        info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid];
+        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
+    }
     if (tid == 0) {
-        info->randmask = randmask; info->nt = nt; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
-        int nr = __popcll(randmask), kd = 0;
-        for (int j = 0; j < Bn; ++j) kd += ps.kd[j];
-        atomicAdd(&a.ws->n_rand, (u64)nr); atomicAdd(&a.ws->n_det, (u64)(Bn - nr));
-        atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)kd);
+        info->randmask = randmask; info->nt = ntr + 2u * (u32)nrand; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        atomicAdd(&a.ws->n_rand, (u64)nrand); atomicAdd(&a.ws->n_det, (u64)(Bn - nrand));
+        atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)ps.kdet);
         atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
     }
+    SK_FPROF(3);
+#undef SK_FPROF
 }
 
 // dynamic smem (u64): max( acc[kMeasWarps][2*Wp] + values scratch, panel [B][RW] + pivmask [W] )
@@ -441,15 +543,17 @@ k_measure_block(MeasArgs a) {
     extern __shared__ __align__(16) u64 smem[];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
     __shared__ int s_wcnt[kMeasWarps];
+    __shared__ u64 s_pn[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
     __shared__ int s_cnt1;
     __shared__ u32 s_targets[kMaxTargets];
     __shared__ PanelSmem ps;
     __shared__ PanelInfo s_info;
     __shared__ u32 s_q[kPanelMax];
+    __shared__ __align__(8) u64 s_mbar;
     const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
     MeasSmem sm;
-    sm.acc = smem; sm.pe = s_pe; sm.pk = s_pk; sm.cnt = &s_cnt1; sm.targets = s_targets;
+    sm.acc = smem; sm.pe = s_pe; sm.pk = s_pk; sm.pn = s_pn; sm.cnt = &s_cnt1; sm.targets = s_targets;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int GW = G * kMeasWarps;
@@ -457,7 +561,8 @@ k_measure_block(MeasArgs a) {
     const int gw = blockIdx.x * kMeasWarps + warp;
     MeasWs* ws = a.ws;
     u32 epoch = 0;
-    if (tid == 0) s_cnt1 = 0;
+    u32 tma_parity = 0;
+    if (tid == 0) { s_cnt1 = 0; mbar_init(&s_mbar, 1); }
     __syncthreads();
 
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
@@ -602,7 +707,7 @@ k_measure_block(MeasArgs a) {
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
         // ---- F: symbolic factorisation (CTA 0)
-        if (blockIdx.x == 0) panel_factorise(a, smem, ps, pos, Bn);
+        if (blockIdx.x == 0) panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
         SK_PROF(3);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
@@ -669,7 +774,7 @@ k_measure_block(MeasArgs a) {
                 while (bits) {
                     const int j = __ffsll((long long)bits) - 1; bits &= bits - 1;
                     const int my = idx++;
-                    if (my % G != int(blockIdx.x) || (my / G) % nwd != warp - nvw) continue;
+                    if (G - 1 - my % G != int(blockIdx.x) || (my / G) % nwd != warp - nvw) continue;    // from the far end: V uses the first CTAs
                     const u64* dcol = a.pan + (size_t)j * RW + W;
                     if (lane == 0) s_wcnt[warp] = 0;
                     __syncwarp();
@@ -690,7 +795,7 @@ k_measure_block(MeasArgs a) {
                     }
                     __syncwarp();
                     const int npart = s_wcnt[warp];
-                    if (npart > kWarpList) {                  // tree-reduced by the whole CTA below
+                    if (npart > kWarpDirect) {                // tree-reduced by the whole CTA below
                         if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = j; }
                         continue;
                     }
@@ -698,9 +803,12 @@ k_measure_block(MeasArgs a) {
                     int e = warp_mul_list(a.m.rows, W, Wp, s_wlist[warp], npart, acc_x, acc_z, lane);
                     for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[warp][i]));
                     e = warp_sum(e) & 3;
+                    u64 N = 0;
+                    for (int i = lane; i < npart; i += 32) N ^= ldcg(a.rowM + s_wlist[warp][i]);
+                    N = warp_xor64(N) & randmask & ((1ull << j) - 1ull);
                     u64* dx = a.detacc + (size_t)(2 * j) * Wp;
                     for (int w = lane; w < W; w += 32) { __stcg(dx + w, acc_x[w]); __stcg(dx + Wp + w, acc_z[w]); }
-                    if (lane == 0) info->dete[j] = e;
+                    if (lane == 0) { info->dete[j] = e; info->dN[j] = N; }
                     __syncwarp();
                 }
             }
@@ -708,8 +816,9 @@ k_measure_block(MeasArgs a) {
             for (int h = 0; h < s_nheavy; ++h) {
                 const int j = s_heavy[h];
                 int total;
-                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total);
-                if (tid == 0) info->dete[j] = e;
+                u64 N = 0;
+                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total, a.rowM, &N);
+                if (tid == 0) { info->dete[j] = e; info->dN[j] = N & randmask & ((1ull << j) - 1ull); }
             }
         }
         SK_PROF(4);
@@ -741,7 +850,7 @@ k_measure_block(MeasArgs a) {
                     const int j = __ffsll((long long)bits) - 1;
                     const u64* dx = a.detacc + (size_t)(2 * j) * Wp;
                     for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(dx + w); acc_z[w] = ldcg(dx + Wp + w); }
-                    const u64 N = s_info.dN[j], Z = s_info.dZ[j];
+                    const u64 N = ldcg(&info->dN[j]), Z = s_info.dZ[j];
                     int cnt = 0;
                     { u64 b = N; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
                     __syncwarp();
@@ -768,6 +877,7 @@ k_measure_block(MeasArgs a) {
                     const int i = it - nd;
                     const u32 h = __ldcg(a.tlist + i);
                     u64 M = ldcg(a.tM + i);
+                    if (lane == 0) __stcg(a.rowM + h, 0ull);      // D part 1 (previous phase) was its last reader
                     // is h a pivot of this panel, or the destabilizer partner of one?
                     int kp = -1, ko = -1;
                     {

@@ -97,7 +97,7 @@ struct sk_tableau {
     u32* d_wpiv = nullptr;
     // panel-mode scratch (kernels_measure.cuh)
     int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
-    u32* d_tlist = nullptr; u64* d_tM = nullptr;
+    u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr;
 };
 
 // x and z halves in one launch (grid.z = 2); `flag` != nullptr makes the launch conditional on *flag
@@ -137,6 +137,7 @@ static int32_t tableau_identity(sk_tableau* t) {
     SK_CUDA(c, cudaMemsetAsync(t->m.cols, 0, t->cols_bytes, c->stream));
     SK_CUDA(c, cudaMemsetAsync(t->m.rows, 0, t->rows_bytes, c->stream));
     SK_CUDA(c, cudaMemsetAsync(t->m.sgn, 0, t->sgn_bytes, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->d_rowM, 0, (size_t)64 * t->RW * 8, c->stream));
     k_identity<<<(unsigned)((t->n + 255) / 256), 256, 0, c->stream>>>(t->m.cols, t->m.rows, int(t->n), t->RW, t->Wp, t->NS);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
@@ -163,17 +164,18 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         SK_CUDA(c, cudaFuncGetAttributes(&fa, k_measure_block));
         const size_t avail = (size_t)c->max_smem_optin - fa.sharedSizeBytes - 1024;
         const size_t acc_words = (size_t)kMeasWarps * 2 * t->Wp;
-        const size_t col_words = (size_t)t->RW;
-        if ((acc_words + 2) * 8 > avail || (col_words + t->W) * 8 > avail) {
+        const size_t col_words = (size_t)t->RW + 2;             // + virtual-row word + pad
+        const size_t aux_words = 2 * ((size_t)t->RW + 1);       // nzm | retired
+        if ((acc_words + 2) * 8 > avail || (col_words + aux_words) * 8 > avail) {
             delete t;
             SK_FAIL(c, SK_EDIM, "n=%llu needs more shared memory per CTA than the %zu B available", (unsigned long long)n, avail);
         }
-        int B = int(std::min<size_t>(kPanelMax, (avail / 8 - t->W) / col_words));
+        int B = int(std::min<size_t>(kPanelMax, (avail / 8 - aux_words) / col_words));
         if (const char* e = getenv("SK_PANEL")) B = std::max(1, std::min(B, atoi(e)));
         const int wpc = (t->W + c->num_sms - 1) / c->num_sms;
         while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
         t->B = B;
-        t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + t->W) * 8;
+        t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8;
     }
     cudaError_t e1 = cudaMalloc(&t->m.cols, t->cols_bytes);
     cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
@@ -184,9 +186,10 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e6 = cudaMalloc(&t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
     cudaError_t e7 = cudaMalloc(&t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
     cudaError_t e8 = cudaMalloc(&t->d_info, sizeof(PanelInfo));
-    cudaError_t e9 = cudaMalloc(&t->d_tlist, (size_t)64 * t->RW * 4);
-    cudaError_t e10 = cudaMalloc(&t->d_tM, (size_t)64 * t->RW * 8);
-    if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
+    cudaError_t e9 = cudaMalloc(&t->d_tlist, ((size_t)64 * t->RW + 2 * kPanelMax) * 4);
+    cudaError_t e10 = cudaMalloc(&t->d_tM, ((size_t)64 * t->RW + 2 * kPanelMax) * 8);
+    cudaError_t e11 = cudaMalloc(&t->d_rowM, (size_t)64 * t->RW * 8);
+    if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
     if ((int)t->meas_smem > c->meas_smem_attr) {
         SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
         c->meas_smem_attr = (int)t->meas_smem;
@@ -206,7 +209,7 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
     cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_wpiv);
-    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM);
+    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM); cudaFree(t->d_rowM);
     cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
     delete t;
 }
@@ -377,7 +380,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
-    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM;
+    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM;
     a.prof = c->prof;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
@@ -441,7 +444,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     if (!c) return SK_EARG;
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 14 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 38 * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -454,6 +457,9 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "measure kernel CTA0 us: P1 %.0f P2 %.0f | gather %.0f factorise %.0f values+detA %.0f apply+detB %.0f | barriers wave %.0f panel %.0f | panels %llu\n",
                                          h.prof[0] / 1e3, h.prof[1] / 1e3, h.prof[2] / 1e3, h.prof[3] / 1e3, h.prof[4] / 1e3, h.prof[5] / 1e3, h.prof[6] / 1e3, h.prof[7] / 1e3, (unsigned long long)h.panels);
+    if (getenv("SK_DEBUG_PROF")) { fprintf(stderr, "cprof cycles:"); for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", (unsigned long long)h.cprof[k]); fprintf(stderr, "\n"); }
+    if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "factorise us: load %.0f random steps %.0f (n=%llu) deterministic steps %.0f (n=%llu) tail %.0f\n",
+                                         h.fprof[0] / 1e3, h.fprof[1] / 1e3, (unsigned long long)h.fprof[4], h.fprof[2] / 1e3, (unsigned long long)h.fprof[5], h.fprof[3] / 1e3);
     return SK_OK;
 }
 
