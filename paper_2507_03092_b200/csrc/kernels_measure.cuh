@@ -48,6 +48,9 @@
 namespace skd {
 
 constexpr int kPanelMax = 64;
+constexpr int kRowK = 4, kRowThreads = 512;              // row-form factorisation: slots per thread, threads
+constexpr int kRowSlots = kRowK * kRowThreads;            // 2048 rows incl. up to kPanelMax virtual ones
+constexpr int kRowCap = kRowSlots - kPanelMax;
 
 struct PanelInfo {      // global scratch describing the current panel (written by CTA 0 in F)
     u64 hist[kPanelMax];   // random step l: earlier random steps whose pivot was multiplied into row p_l
@@ -59,7 +62,10 @@ struct PanelInfo {      // global scratch describing the current panel (written 
     u64 randmask;          // steps that are random
     u64 osign;             // panel-start sign bits of the pivot rows
     u32 nt;                // touched rows (entries of tlist / tM)
+    u32 acount;            // G: active rows of the panel being gathered (reset by F)
+    u32 dmode;             // partners of the deterministic steps: 0 = bit columns in pan, 1 = lists in dpart
     u32 pad;
+    u32 dcnt[kPanelMax];   // dmode 1: partners per deterministic step
     uint8_t outc[kPanelMax];   // outcome of the random steps (counter RNG)
 };
 
@@ -103,8 +109,12 @@ struct MeasArgs {
     PanelInfo* info;
     u32* tlist;         // [64*RW] touched rows
     u64* tM;            // [64*RW] their step masks
+    u32* alist_h;       // [64*RW] G: active rows (row-bits) of the panel, row form
+    u64* alist_b;       // [64*RW]    and their bits in the panel columns
+    u32* dpart;         // [B][kRowSlots] row form: partner stabilizers of the deterministic steps
     u64* rowM;          // [64*RW] step mask by row-bit (zero for rows the current panel does not touch)
     int prof;           // device-side phase timers (SK_DEBUG_PROF)
+    int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
 };
 
 __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
@@ -165,10 +175,15 @@ struct MeasSmem {
 // stabilizer rows commute.  Returns (CTA-uniform) the phase exponent mod 4 including the rows'
 // signs; if out_x != nullptr the product words are stored there (R layout).  *total_out = #rows.
 // sm.cnt[0] is zero on entry and on exit.
-__device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, const u64* dcol, u64* out_x, int* total_out, const u64* rowM = nullptr, u64* n_out = nullptr) {
+__device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, const u64* dcol, u64* out_x, int* total_out, const u64* rowM = nullptr, u64* n_out = nullptr,
+                                       const u32* glist = nullptr, int gcount = 0) {
     const int Wp = a.m.Wp, W = a.m.W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int w0 = 0; w0 < W; w0 += kMeasThreads) {
+    if (glist) {          // partners given as a list (<= kMaxTargets entries) instead of a bit column
+        for (int i = tid; i < gcount; i += kMeasThreads) sm.targets[i] = __ldcg(glist + i);
+        if (tid == 0) sm.cnt[0] = gcount;
+    }
+    for (int w0 = 0; w0 < (glist ? 0 : W); w0 += kMeasThreads) {
         const int w = w0 + tid;
         u64 bits = (w < W) ? ldcg(dcol + w) : 0ull;
         const int pc = __popcll(bits);
@@ -303,9 +318,161 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
 // F: symbolic factorisation of one panel by CTA 0.  sp = dynamic smem: panel [Bn][RW] then the
 // pivot mask [W] (stabilizer rows used as pivots so far).
 struct PanelSmem {
-    u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax]; uint8_t outc[kPanelMax];
-    u32 full32[2]; u32 nt; u32 krand; u32 kdet; u64 psign; u32 podd;
+    u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax], S[kPanelMax]; uint8_t outc[kPanelMax];
+    u32 full32[2]; u32 nt; u32 krand; u32 kdet;
+    u32 dcnt[kPanelMax]; u32 wmin[2][kRowThreads / 32]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd;
 };
+
+// F, row form (the common case: <= kRowCap rows have an x in any of the panel's columns).  The active rows
+// live in REGISTERS of kRowThreads/32 warps as (row-bit, panel bits, step mask M); sequential CHP on them is then
+//   pivot  = min row-bit among stabilizer rows with bit j            (scan + REDUX, one smem hop across the warps)
+//   random: every other row with bit j:  bits ^= bits_p ; M |= 1<<j  ; the pivot and its old partner retire;
+//           the partner's new content (the old pivot row) becomes a fresh VIRTUAL row (born at step j)
+//   deterministic: partners = destabilizer rows with bit j (virtual ones stand for the +-Z rows of earlier steps)
+// which yields the same schedule (pivots, histories, step masks, partner sets) as the column form below.
+__device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A) {
+    const int NS = a.NS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr u32 kInf = 0xffffffffu;
+    long long tc = clock64();
+#define SK_RPROF(k) do { if (a.prof && tid == 0) { const long long _c = clock64(); a.ws->cprof[k] += (u64)(_c - tc); tc = _c; } } while (0)
+    if (tid < kPanelMax) { ps.piv[tid] = kInf; ps.hist[tid] = 0; ps.dZ[tid] = 0; ps.outc[tid] = 0; ps.dcnt[tid] = 0; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; }
+    __syncthreads();
+    u64 randmask = 0;
+    // only as many warps as the rows (plus the virtual rows still to come) need take part: the per-step cost is issue-bound
+    const int Tact = min(kRowThreads, int(((A + kPanelMax + kRowK - 1) / kRowK + 31) & ~31u));
+    if (tid < Tact) {
+        // slot state in scalars (kRowK == 4), so that it stays in registers: row-bit | (born step + 1) << 24 (kInf = empty), bits, M
+        static_assert(kRowK == 4, "slot macros below are written for 4 slots per thread");
+        u32 hh0 = kInf, hh1 = kInf, hh2 = kInf, hh3 = kInf; u64 bb0 = 0, bb1 = 0, bb2 = 0, bb3 = 0, mm0 = 0, mm1 = 0, mm2 = 0, mm3 = 0;
+#define SK_SLOTS(X) X(0, hh0, bb0, mm0) X(1, hh1, bb1, mm1) X(2, hh2, bb2, mm2) X(3, hh3, bb3, mm3)
+        int Kact = int((A + Tact - 1) / Tact);
+#define SK_LOAD(k, hh, bb, mm) { const u32 i = u32(k) * Tact + tid; if (i < A) { hh = __ldcg(a.alist_h + i); bb = ldcg(a.alist_b + i); } }
+        SK_SLOTS(SK_LOAD)
+#undef SK_LOAD
+        int ntarget = 0;
+        int vt = int(A % (u32)Tact), vk = int(A / (u32)Tact);      // slot (thread, k) of the next virtual row
+        const int nw = Tact >> 5;
+        SK_RPROF(0);
+        for (int j = 0; j < Bn; ++j) {
+            // which of this thread's slots have an x in column j
+            u32 hit = 0;
+#define SK_HIT(k, hh, bb, mm) hit |= (u32(bb >> j) & 1u) << k;
+            SK_SLOTS(SK_HIT)
+#undef SK_HIT
+            // pivot candidate: smallest stabilizer row-bit among the hits, carried with its bits and step mask
+            u32 mymin = kInf; u64 cb = 0, cm = 0;
+            if (hit) {
+#define SK_SCAN(k, hh, bb, mm) if (((hit >> k) & 1u) && hh < mymin && hh < (u32)NS) { mymin = hh; cb = bb; cm = mm; }
+                SK_SLOTS(SK_SCAN)
+#undef SK_SCAN
+            }
+            const u32 wm = __reduce_min_sync(0xffffffffu, mymin);
+            if (mymin == wm && (wm != kInf || lane == 0)) { ps.wmin[j & 1][warp] = wm; ps.wbp[j & 1][warp] = cb; ps.wmp[j & 1][warp] = cm; }   // row-bits are unique: one writer
+            named_bar(1, Tact);
+            // minimum over the warps and the warp that holds it (row-bits are unique)
+            const u32 wv = (lane < nw) ? ps.wmin[j & 1][lane] : kInf;
+            const u32 p = __reduce_min_sync(0xffffffffu, wv);
+            const int tw = __ffs(__ballot_sync(0xffffffffu, wv == p)) - 1;
+            if (p == kInf) {
+                // ---------------- deterministic step: partners = destabilizer rows with an x (virtual ones stand for +-Z rows)
+                if (hit) {
+                    u32 dzlo = 0, dzhi = 0;
+#define SK_DET(k, hh, bb, mm) if ((hit >> k) & 1u) { \
+                        const u32 born = hh >> 24; \
+                        if (born) { if (born <= 32) dzlo |= 1u << (born - 1); else dzhi |= 1u << (born - 33); } \
+                        else { const u32 at = atomicAdd(&ps.dcnt[j], 1u); __stcg(a.dpart + (size_t)j * kRowSlots + at, hh - (u32)NS); } }
+                    SK_SLOTS(SK_DET)
+#undef SK_DET
+                    if (dzlo | dzhi) atomicOr(&ps.dZ[j], (u64)dzlo | ((u64)dzhi << 32));
+                }
+                continue;
+            }
+            // ---------------- random step
+            const u32 pd = (u32)NS + p;
+            const u64 bp = ps.wbp[j & 1][tw], Mp = ps.wmp[j & 1][tw];
+            const u64 above = (j < 63) ? ~((2ull << j) - 1ull) : 0ull;
+            // pivot -> +-Z_q (history kept for earlier deterministic steps); others with bit j: multiplied by the pivot row
+            if (hit) {
+#define SK_UPD(k, hh, bb, mm) if ((hit >> k) & 1u) { \
+                    if (hh == p) { __stcg(a.rowM + p, mm); hh = kInf; bb = 0; } \
+                    else if (hh != pd) { bb ^= bp; mm |= 1ull << j; ++ntarget; } }
+                SK_SLOTS(SK_UPD)
+#undef SK_UPD
+            }
+            // the old partner row is overwritten: its past is void (it may or may not have had an x in column j)
+#define SK_RET(k, hh, bb, mm) if (hh == pd) { hh = kInf; bb = 0; }
+            SK_SLOTS(SK_RET)
+#undef SK_RET
+            if (tid == vt) {                        // ... and its new content, the old pivot row, is a fresh virtual row
+#define SK_NEW(k, hh, bb, mm) if (k == vk) { hh = pd | (u32(j + 1) << 24); bb = bp & above; mm = 0; }
+                SK_SLOTS(SK_NEW)
+#undef SK_NEW
+            }
+            Kact = max(Kact, vk + 1);
+            if (++vt == Tact) { vt = 0; ++vk; }
+            if (tid == 0) { ps.piv[j] = p; ps.hist[j] = Mp; }
+            randmask |= 1ull << j;
+        }
+        SK_RPROF(1);
+        // emit the touched rows (regular rows that were multiplied at least once, and every virtual row)
+        int cnt = 0;
+#define SK_CNT(k, hh, bb, mm) if (k < Kact && hh != kInf && (mm || (hh >> 24))) ++cnt;
+        SK_SLOTS(SK_CNT)
+#undef SK_CNT
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
+        if (lane == 31) ps.wcnt[warp] = incl;
+        ntarget = warp_sum(ntarget);
+        if (lane == 0 && ntarget) atomicAdd(&ps.krand, (u32)ntarget);
+        named_bar(1, Tact);
+        u32 at = incl - cnt;
+        for (int t = 0; t < warp; ++t) at += ps.wcnt[t];
+#define SK_EMIT(k, hh, bb, mm) if (k < Kact && hh != kInf && (mm || (hh >> 24))) { \
+                const u32 row = hh & 0xffffffu; \
+                __stcg(a.tlist + at, row); __stcg(a.tM + at, mm); \
+                if (!(hh >> 24) && row < (u32)NS) __stcg(a.rowM + row, mm); \
+                ++at; }
+        SK_SLOTS(SK_EMIT)
+#undef SK_EMIT
+#undef SK_SLOTS
+        if (tid == Tact - 1) ps.nt = at;
+        SK_RPROF(2);
+    }
+    __syncthreads();
+    SK_RPROF(3);
+    randmask = 0;
+    for (int j = 0; j < Bn; ++j) if (ps.piv[j] != kInf) randmask |= 1ull << j;
+    const int nrand = __popcll(randmask);
+    const u32 ntr = ps.nt;
+    if (tid < Bn && ((randmask >> tid) & 1ull)) {
+        ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
+        const u32 at = ntr + (u32)__popcll(randmask & ((1ull << tid) - 1ull));
+        __stcg(a.tlist + at, ps.piv[tid]); __stcg(a.tM + at, 0ull);          // the pivot itself: -> +-Z_q
+    }
+    if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
+        const u32 pl = ps.piv[tid];
+        const u32 bal = __ballot_sync(0xffffffffu, pl != kInf && sign_bit(a.m.sgn, int(pl)));
+        if (lane == 0) ps.full32[tid >> 5] = bal;
+        if (tid < Bn && pl == kInf) atomicAdd(&ps.kdet, ps.dcnt[tid] + (u32)__popcll(ps.dZ[tid]));
+    }
+    __syncthreads();
+    PanelInfo* info = a.info;
+    if (tid < kPanelMax) {
+        info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid]; info->dcnt[tid] = ps.dcnt[tid];
+        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
+    }
+    if (tid == 0) {
+        info->randmask = randmask; info->nt = ntr + (u32)nrand; info->dmode = 1; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        atomicAdd(&a.ws->n_rand, (u64)nrand); atomicAdd(&a.ws->n_det, (u64)(Bn - nrand));
+        atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)ps.kdet);
+        atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
+    }
+    SK_RPROF(4);
+#undef SK_RPROF
+}
 
 // XOR of the frozen masks m_l[w] over the steps l in `bits` (column stride CS).  Few steps: chase the
 // bits; many (a "hot" word: the same rows are targets again and again): linear sweep, 8 loads in flight.
@@ -345,10 +512,10 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     u64 tf = a.prof ? gtime() : 0;
 #define SK_FPROF(k) do { if (a.prof && tid == 0) { u64 _n = gtime(); a.ws->fprof[k] += _n - tf; tf = _n; } } while (0)
     // the gathered panel arrives by TMA bulk copies (UBLKCP), one per column, on one mbarrier
-    if (tid == 0) {
+    if (warp == 0) {
         asm volatile("fence.proxy.async;" ::: "memory");
-        mbar_expect_tx(mbar, u32(Bn * RW * 8));
-        for (int j = 0; j < Bn; ++j) tma_load_1d(sp + (size_t)j * CS, a.pan + (size_t)j * RW, u32(RW * 8), mbar);
+        if (lane == 0) mbar_expect_tx(mbar, u32(Bn * RW * 8));
+        for (int j = lane; j < Bn; j += 32) tma_load_1d(sp + (size_t)j * CS, a.pan + (size_t)j * RW, u32(RW * 8), mbar);
     }
     for (int w = tid; w < 2 * RV; w += kMeasThreads) nzm[w] = 0;      // nzm | ret are contiguous
     if (tid < Bn) { sp[(size_t)tid * CS + RW] = 0; sp[(size_t)tid * CS + RW + 1] = 0; }
@@ -358,80 +525,121 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     tma_parity ^= 1;
     __syncthreads();
     SK_FPROF(0);
-    const int nact = min(kMeasThreads, max(64, (RV + 31) & ~31));       // threads that own panel words (>= 64: one per panel column in the bit gathers)
-    u64 randmask = 0, pw_prev = 0;
+    // ---- control warp: the serial recurrence lives on the STABILIZER half only (pivots, pivot-row bits pw, histories);
+    // warp-synchronous, no CTA barriers.  Lane owns words lane, lane+32, ...
     long long cp[6] = {0, 0, 0, 0, 0, 0};
-    if (tid < nact) {
+    if (warp == 0) {
+        u64 randmask = 0;
         for (int j = 0; j < Bn; ++j) {
             const long long c0 = clock64();
             u64* cj = sp + (size_t)j * CS;
-            // S_j: lane l holds pw of steps l and l+32 (step j-1 was published after the last barrier: take it from the register copy)
-            u64 S;
-            {
-                const u64 a0 = (lane < j - 1) ? ps.pw[lane] : 0ull, a1 = (lane + 32 < j - 1) ? ps.pw[lane + 32] : 0ull;
-                S = (u64)__ballot_sync(0xffffffffu, (a0 >> j) & 1ull) | ((u64)__ballot_sync(0xffffffffu, (a1 >> j) & 1ull) << 32);
-                if (j > 0) S |= ((pw_prev >> j) & 1ull) << (j - 1);
-            }
+            // S_j: lane l holds pw of steps l and l+32
+            const u64 a0 = (lane < j) ? ps.pw[lane] : 0ull, a1 = (lane + 32 < j) ? ps.pw[lane + 32] : 0ull;
+            const u64 S = (u64)__ballot_sync(0xffffffffu, (a0 >> j) & 1ull) | ((u64)__ballot_sync(0xffffffffu, (a1 >> j) & 1ull) << 32);
             u32 cand = 0xffffffffu;
-            for (int w = tid; w < RV; w += nact) {
-                const u64 old = cj[w];
-                u64 cur = (w == RW) ? S : old;
-                const u64 bits = S & nzm[w];
-                if (bits) cur ^= xor_masks(sp, CS, w, bits, j);
-                cur &= ~ret[w];
-                if (cur != old) cj[w] = cur;
-                if (w < W && cur && cand == 0xffffffffu) cand = u32(w * 64 + __ffsll((long long)cur) - 1);   // words ascend with the stride
+            u64 nzw = 0;                 // which of this lane's words are non-zero in the materialised column
+            int k = 0;
+            for (int w0 = 0; w0 < W; w0 += 32, ++k) {
+                const int w = w0 + lane;
+                const bool valid = w < W;
+                const u64 old = valid ? cj[w] : 0ull;
+                u64 cur = old;
+                const u64 bits = valid ? (S & nzm[w]) : 0ull;
+                const int nb = __popcll(bits);
+                if (nb && nb <= 3) { u64 b = bits; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; cur ^= sp[(size_t)l * CS + w]; } }
+                // hot words (the same rows are targets again and again): the whole warp reduces one word at a time,
+                // lane l loading the masks of steps l and l+32; 32-bit halves combined with REDUX
+                u32 hot = __ballot_sync(0xffffffffu, nb > 3);
+                while (hot) {
+                    const int src = __ffs(hot) - 1; hot &= hot - 1;
+                    const u64 sb = __shfl_sync(0xffffffffu, bits, src);
+                    const int ws = w0 + src;
+                    u64 x = 0;
+                    if ((sb >> lane) & 1ull) x ^= sp[(size_t)lane * CS + ws];
+                    if ((sb >> (lane + 32)) & 1ull) x ^= sp[(size_t)(lane + 32) * CS + ws];
+                    const u32 lo = __reduce_xor_sync(0xffffffffu, (u32)x), hi = __reduce_xor_sync(0xffffffffu, (u32)(x >> 32));
+                    if (lane == src) cur ^= (u64)lo | ((u64)hi << 32);
+                }
+                if (valid) {
+                    cur &= ~ret[w];
+                    if (cur != old) cj[w] = cur;
+                    if (cur) { if (k < 64) nzw |= 1ull << k; if (cand == 0xffffffffu) cand = u32(w * 64 + __ffsll((long long)cur) - 1); }   // words ascend with k
+                }
             }
-            cand = __reduce_min_sync(0xffffffffu, cand);
-            if (lane == 0 && cand != 0xffffffffu) atomicMin(&ps.piv[j], cand);
-            named_bar(1, nact);
-            const u32 p = ps.piv[j];
+            const u32 p = __reduce_min_sync(0xffffffffu, cand);
+            if (lane == 0) ps.S[j] = S;
             const long long c1 = clock64();
             if (p != 0xffffffffu) {
                 // ---------------- random step
-                const u32 pd = u32(NS) + p;
-                if (tid < 64) {       // bit p of every panel column: frozen masks for c < j (history), panel-start bits for c > j
-                    const u32 bit = (tid < Bn) ? u32((sp[(size_t)tid * CS + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
-                    const u32 bal = __ballot_sync(0xffffffffu, bit);
-                    if (lane == 0) ps.full32[tid >> 5] = bal;
-                }
-                named_bar(1, nact);
-                const long long c2 = clock64();
-                const u64 full = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+                __syncwarp();         // the materialised column is visible to the bit gather
+                const u32 b0 = (lane < Bn) ? u32((sp[(size_t)lane * CS + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
+                const u32 b1 = (lane + 32 < Bn) ? u32((sp[(size_t)(lane + 32) * CS + (p >> 6)] >> (p & 63)) & 1ull) : 0u;
+                // bit p of every panel column: frozen masks for c < j (history), panel-start bits for c > j
+                const u64 full = (u64)__ballot_sync(0xffffffffu, b0) | ((u64)__ballot_sync(0xffffffffu, b1) << 32);
                 const u64 above = (j < 63) ? ~((2ull << j) - 1ull) : 0ull;
                 const u64 hist = full & randmask & ((1ull << j) - 1ull);
                 // x bits of the pivot row at the later columns = its panel-start bits ^ those of the pivot rows multiplied into it
-                u64 pw = full;
-                { u64 bits = hist; while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; pw ^= (l == j - 1) ? pw_prev : ps.pw[l]; } }
-                pw &= above;
-                for (int w = tid; w < RV; w += nact) {
-                    const bool isp = w == int(p >> 6), isd = w == int(pd >> 6);
-                    u64 m = cj[w];
-                    if (isp | isd) {         // the pivot and its partner are not multiplied (SURVEY section 7 hazard); both row-bits retire
-                        const u64 bit = isp ? (1ull << (p & 63)) : (1ull << (pd & 63));
-                        m &= ~bit; cj[w] = m; ret[w] |= bit;
+                u64 x = 0;
+                if ((hist >> lane) & 1ull) x ^= ps.pw[lane];
+                if ((hist >> (lane + 32)) & 1ull) x ^= ps.pw[lane + 32];
+                const u32 lo = __reduce_xor_sync(0xffffffffu, (u32)x), hi = __reduce_xor_sync(0xffffffffu, (u32)(x >> 32));
+                const u64 pw = (full ^ ((u64)lo | ((u64)hi << 32))) & above;
+                const long long c2 = clock64();
+                // freeze m_j (stabilizer half): the pivot is not multiplied into itself; its row-bit retires
+                k = 0;
+                for (int w0 = 0; w0 < W; w0 += 32, ++k) {
+                    const int w = w0 + lane;
+                    if (k < 64 ? !((nzw >> k) & 1ull) : (w >= W || cj[w] == 0)) continue;     // (beyond 2048 words per half: re-read)
+                    if (w == int(p >> 6)) {
+                        const u64 bit = 1ull << (p & 63);
+                        const u64 m = cj[w] & ~bit;
+                        cj[w] = m; ret[w] |= bit;
+                        if (!m) continue;
                     }
-                    if (m) nzm[w] |= 1ull << j;
+                    nzm[w] |= 1ull << j;
                 }
-                if (tid == 0) { ps.hist[j] = hist; ps.pw[j] = pw; }
-                pw_prev = pw;
+                if (lane == 0) { ps.piv[j] = p; ps.hist[j] = hist; ps.pw[j] = pw; }
                 randmask |= 1ull << j;
                 { const long long c3 = clock64(); cp[0] += c1 - c0; cp[1] += c2 - c1; cp[2] += c3 - c2; }
-                SK_FPROF(1); if (a.prof && tid == 0) a.ws->fprof[4]++;
             } else {
-                // ---------------- deterministic step: nothing changes; its column (partners D = destabilizer half,
-                // partners that earlier steps turned into +-Z = virtual word) stays frozen for the tail
-                pw_prev = 0;
                 { const long long c3 = clock64(); cp[3] += c1 - c0; cp[5] += c3 - c1; }
-                SK_FPROF(2); if (a.prof && tid == 0) a.ws->fprof[5]++;
             }
+            __syncwarp();
         }
     }
-    if (a.prof && (tid == 0 || tid == 96)) for (int k = 0; k < 6; ++k) a.ws->cprof[(tid ? 8 : 0) + k] += (u64)cp[k];
+    if (a.prof && tid == 0) for (int k = 0; k < 6; ++k) a.ws->cprof[k] += (u64)cp[k];
     __syncthreads();
+    SK_FPROF(1);
+    // ---- destabilizer half + virtual word: they never influence the recurrence, so every word replays the B steps
+    // on its own (thread per word, no synchronisation): same materialise / freeze rule with S_j and p_j from above
+    for (int w = W + tid; w < RV; w += kMeasThreads) {
+        u64 nz = 0, rt = 0;
+        for (int j = 0; j < Bn; ++j) {
+            const u64 S = ps.S[j];
+            const u32 p = ps.piv[j];
+            u64* cj = sp + (size_t)j * CS;
+            const u64 old = cj[w];
+            u64 cur = (w == RW) ? S : old;
+            u64 bits = S & nz;
+            while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; cur ^= sp[(size_t)l * CS + w]; }
+            cur &= ~rt;
+            if (p != 0xffffffffu) {
+                const u32 pd = u32(NS) + p;
+                if (w == int(pd >> 6)) { const u64 bit = 1ull << (pd & 63); cur &= ~bit; rt |= bit; }
+                if (cur) nz |= 1ull << j;
+            }
+            if (cur != old) cj[w] = cur;
+        }
+        nzm[w] = nz; ret[w] = rt;
+    }
+    __syncthreads();
+    SK_FPROF(2);
+    u64 randmask;
     randmask = 0;
     for (int j = 0; j < Bn; ++j) if (ps.piv[j] != 0xffffffffu) randmask |= 1ull << j;
     const int nrand = __popcll(randmask);
+    long long tc0 = clock64();
+#define SK_TPROF(k) do { if (a.prof && tid == 0) { const long long _c = clock64(); a.ws->cprof[k] += (u64)(_c - tc0); tc0 = _c; } } while (0)
     if (tid < Bn && ((randmask >> tid) & 1ull)) ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
     // regular touched rows: targets of any random step that were not retired later
     int kr = 0;
@@ -472,6 +680,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     }
     kr = warp_sum(kr);
     if (lane == 0 && kr) atomicAdd(&ps.krand, (u32)kr);
+    SK_TPROF(6);
     // deterministic steps: partner sets for phase D (real destabilizer words -> panel-start stabilizers; virtual word -> +-Z rows)
     for (int j = warp; j < Bn; j += kMeasWarps)
         if (!((randmask >> j) & 1ull)) {
@@ -486,22 +695,26 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
         if (lane == 0) ps.full32[tid >> 5] = bal;
     }
     __syncthreads();
-    // step masks M_h of the regular rows: warp-cooperative bit gather (lane l reads columns l and l+32)
+    SK_TPROF(7);
+    // step masks M_h of the regular rows: a lane per row sweeps the random steps, 8 loads in flight
     const u32 ntr = ps.nt;
-    for (u32 i0 = u32(warp) * 32u; i0 < ntr; i0 += kMeasThreads) {
-        const u32 i = i0 + lane;
-        const u32 hh = (i < ntr) ? (i < (u32)kMaxTargets ? s_rows[i] : __ldcg(a.tlist + i)) : 0u;
-        const int cnt = int(min(32u, ntr - i0));
-        u64 myM = 0;
-        for (int r = 0; r < cnt; ++r) {
-            const u32 h = __shfl_sync(0xffffffffu, hh, r);
-            const u32 b0 = (lane < Bn) ? u32((sp[(size_t)lane * CS + (h >> 6)] >> (h & 63)) & 1ull) : 0u;
-            const u32 b1 = (lane + 32 < Bn) ? u32((sp[(size_t)(lane + 32) * CS + (h >> 6)] >> (h & 63)) & 1ull) : 0u;
-            const u64 M = ((u64)__ballot_sync(0xffffffffu, b0) | ((u64)__ballot_sync(0xffffffffu, b1) << 32)) & randmask;
-            if (lane == r) myM = M;
+    if (a.prof && tid == 0) { a.ws->cprof[4] += ntr; a.ws->cprof[12] += ps.krand; }
+    for (u32 i = tid; i < ntr; i += kMeasThreads) {
+        const u32 h = (i < (u32)kMaxTargets) ? s_rows[i] : __ldcg(a.tlist + i);
+        const u64* col = sp + (h >> 6);
+        const int sh = int(h & 63);
+        u64 M = 0, bits = randmask;
+        for (int l0 = 0; l0 < Bn; l0 += 8, col += 8 * (size_t)CS, bits >>= 8) {
+            if ((bits & 0xffull) == 0) continue;
+            u64 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (l0 + u < Bn) ? col[(size_t)u * CS] : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) M |= ((v[u] >> sh) & (bits >> u) & 1ull) << (l0 + u);
         }
-        if (i < ntr) { __stcg(a.tM + i, myM); __stcg(a.rowM + hh, myM); }
+        __stcg(a.tM + i, M); __stcg(a.rowM + h, M);
     }
+    SK_TPROF(14);
     // the two rows every random step l overwrites: pivot p_l (-> +-Z_q) and partner p_l + n (-> P_l', then the steps
     // that multiply virtual row l)
     if (tid < 64 && ((randmask >> tid) & 1ull)) {
@@ -528,11 +741,13 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
         info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
     }
     if (tid == 0) {
-        info->randmask = randmask; info->nt = ntr + 2u * (u32)nrand; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        info->randmask = randmask; info->nt = ntr + 2u * (u32)nrand; info->dmode = 0; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
         atomicAdd(&a.ws->n_rand, (u64)nrand); atomicAdd(&a.ws->n_det, (u64)(Bn - nrand));
         atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)ps.kdet);
         atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
     }
+    SK_TPROF(15);
+#undef SK_TPROF
     SK_FPROF(3);
 #undef SK_FPROF
 }
@@ -679,6 +894,7 @@ k_measure_block(MeasArgs a) {
                 const int h = 32 * g + lane;
                 const u64* rx = a.m.rows + (size_t)(2 * h) * Wp;
                 u32 lo = 0, hi = 0;
+                u64 rb = 0;                       // this lane's row: its bits in the panel columns (row form)
                 int lastw = -1; u64 lastv = 0;
                 for (int j0 = 0; j0 < Bn; j0 += 8) {
                     u32 qq[8]; u64 v[8];
@@ -694,20 +910,36 @@ k_measure_block(MeasArgs a) {
                         if (qq[t] == 0xffffffffu) continue;
                         const int wq = int(qq[t] >> 6);
                         if (wq == lastw) v[t] = lastv; else { lastv = v[t]; lastw = wq; }
-                        const u32 bal = __ballot_sync(0xffffffffu, (v[t] >> (qq[t] & 63)) & 1ull);
+                        const u64 bit = (v[t] >> (qq[t] & 63)) & 1ull;
+                        const u32 bal = __ballot_sync(0xffffffffu, bit);
                         const int j = j0 + t;
+                        rb |= bit << j;
                         if (lane == (j & 31)) { if (j < 32) lo = bal; else hi = bal; }
                     }
                 }
                 if (lane < Bn) pan32[(size_t)lane * 2 * RW + g] = lo;
                 if (lane + 32 < Bn) pan32[(size_t)(lane + 32) * 2 * RW + g] = hi;
+                // active rows (any x bit in the panel's columns), compacted in arbitrary order
+                const u32 am = __ballot_sync(0xffffffffu, rb != 0);
+                if (am) {
+                    u32 base = 0;
+                    if (lane == 0) base = atomicAdd(&info->acount, (u32)__popc(am));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (rb) { const u32 at = base + __popc(am & ((1u << lane) - 1u)); __stcg(a.alist_h + at, (u32)h); __stcg(a.alist_b + at, rb); }
+                }
             }
         }
         SK_PROF(2);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
         // ---- F: symbolic factorisation (CTA 0)
-        if (blockIdx.x == 0) panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
+        if (blockIdx.x == 0) {
+            const u32 A = __ldcg(&info->acount);
+            __syncthreads();
+            if (tid == 0) { info->acount = 0; if (a.prof) { ws->cprof[8] += A; if (A > ws->cprof[9]) ws->cprof[9] = A; } }
+            if (A <= (u32)kRowCap && !a.force_columns) panel_factorise_rows(a, ps, pos, Bn, A);
+            else panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
+        }
         SK_PROF(3);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
@@ -778,6 +1010,12 @@ k_measure_block(MeasArgs a) {
                     const u64* dcol = a.pan + (size_t)j * RW + W;
                     if (lane == 0) s_wcnt[warp] = 0;
                     __syncwarp();
+                    if (s_info.dmode) {          // partner list written by the row-form factorisation
+                        const int n = int(s_info.dcnt[j]);
+                        const u32* gl = a.dpart + (size_t)j * kRowSlots;
+                        if (n <= kWarpDirect) for (int i = lane; i < n; i += 32) s_wlist[warp][i] = __ldcg(gl + i);
+                        if (lane == 0) s_wcnt[warp] = n;
+                    } else
                     for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {
                         u64 cv[kColChunk];
 #pragma unroll
@@ -817,7 +1055,8 @@ k_measure_block(MeasArgs a) {
                 const int j = s_heavy[h];
                 int total;
                 u64 N = 0;
-                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total, a.rowM, &N);
+                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total, a.rowM, &N,
+                                      s_info.dmode ? a.dpart + (size_t)j * kRowSlots : nullptr, int(s_info.dcnt[j]));
                 if (tid == 0) { info->dete[j] = e; info->dN[j] = N & randmask & ((1ull << j) - 1ull); }
             }
         }

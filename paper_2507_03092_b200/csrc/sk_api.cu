@@ -34,6 +34,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
     c->num_sms = prop.multiProcessorCount;
     if (getenv("SK_DEBUG_PROF")) c->prof = 1;
+    if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
@@ -97,7 +98,7 @@ struct sk_tableau {
     u32* d_wpiv = nullptr;
     // panel-mode scratch (kernels_measure.cuh)
     int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
-    u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr;
+    u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr; u32* d_alist_h = nullptr; u64* d_alist_b = nullptr; u32* d_dpart = nullptr;
 };
 
 // x and z halves in one launch (grid.z = 2); `flag` != nullptr makes the launch conditional on *flag
@@ -189,7 +190,11 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e9 = cudaMalloc(&t->d_tlist, ((size_t)64 * t->RW + 2 * kPanelMax) * 4);
     cudaError_t e10 = cudaMalloc(&t->d_tM, ((size_t)64 * t->RW + 2 * kPanelMax) * 8);
     cudaError_t e11 = cudaMalloc(&t->d_rowM, (size_t)64 * t->RW * 8);
-    if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
+    cudaError_t e12 = cudaMalloc(&t->d_alist_h, (size_t)64 * t->RW * 4);
+    cudaError_t e13 = cudaMalloc(&t->d_alist_b, (size_t)64 * t->RW * 8);
+    cudaError_t e14 = cudaMalloc(&t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
+    if (!e8) e8 = cudaMemset(t->d_info, 0, sizeof(PanelInfo));
+    if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11 || e12 || e13 || e14) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
     if ((int)t->meas_smem > c->meas_smem_attr) {
         SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
         c->meas_smem_attr = (int)t->meas_smem;
@@ -209,7 +214,7 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
     cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_wpiv);
-    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM); cudaFree(t->d_rowM);
+    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM); cudaFree(t->d_rowM); cudaFree(t->d_alist_h); cudaFree(t->d_alist_b); cudaFree(t->d_dpart);
     cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
     delete t;
 }
@@ -380,8 +385,8 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
-    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM;
-    a.prof = c->prof;
+    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
+    a.prof = c->prof; a.force_columns = c->force_columns;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
