@@ -164,6 +164,8 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         cudaFuncAttributes fa{};
         SK_CUDA(c, cudaFuncGetAttributes(&fa, k_measure_block));
         const size_t avail = (size_t)c->max_smem_optin - fa.sharedSizeBytes - 1024;
+        // the attribute belongs to the function (per device), not to a context: always opt in to the device maximum
+        SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c->max_smem_optin - fa.sharedSizeBytes)));
         const size_t acc_words = (size_t)kMeasWarps * 2 * t->Wp;
         const size_t col_words = (size_t)t->RW + 2;             // + virtual-row word + pad
         const size_t aux_words = 2 * ((size_t)t->RW + 1);       // nzm | retired
@@ -195,10 +197,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e14 = cudaMalloc(&t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
     if (!e8) e8 = cudaMemset(t->d_info, 0, sizeof(PanelInfo));
     if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11 || e12 || e13 || e14) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
-    if ((int)t->meas_smem > c->meas_smem_attr) {
-        SK_CUDA(c, cudaFuncSetAttribute(k_measure_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t->meas_smem));
-        c->meas_smem_attr = (int)t->meas_smem;
-    }
+
     int per_sm = 0;
     SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_measure_block, kMeasThreads, t->meas_smem));
     if (per_sm < 1) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "measurement kernel does not fit on an SM"); }

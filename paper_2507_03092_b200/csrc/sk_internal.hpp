@@ -19,7 +19,6 @@ struct sk_ctx {
     int prof = 0;                           // SK_DEBUG_PROF: device-side phase timers (slows the kernel)
     int force_columns = 0;                  // SK_PANEL_COLUMNS=1: column-form panel factorisation only (testing aid)
     int meas_grid_override = 0;             // SK_MEAS_GRID: CTAs of the measurement kernel (profiling aid)
-    int meas_smem_attr = 0;                 // largest dynamic-smem attribute set on k_measure_block
     std::string err;
     // growable device scratch
     void* d_gates = nullptr; size_t d_gates_cap = 0;

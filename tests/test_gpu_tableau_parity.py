@@ -1,4 +1,6 @@
 """-m gpu: bit-exact parity of the CUDA tableau path (through the C ABI) against the CPU oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -238,3 +240,43 @@ def test_surface_code_d71_oracle_rounds_and_full_properties(sk, ctx, orc):   # B
     # idempotence at scale: measuring every qubit again is deterministic and repeats
     again, adet = t.measure_batch(np.arange(d * d, dtype=np.uint32), SEED, ordinal0=len(out))
     assert (adet == 1).all() and (again == data).all()
+
+
+@pytest.mark.parametrize("columns,width", [(1, 64), (1, 5), (1, 1), (0, 7), (0, 1)])
+def test_panel_factorisation_variants(sk, orc, columns, width):
+    """Panel mode (kernels_measure.cuh) has two factorisations -- row form in registers and the
+    column form in shared memory (TMA staged) used when too many rows are active -- and any panel
+    width 1..64.  Every variant must reproduce sequential CHP bit for bit."""
+    old = {k: os.environ.get(k) for k in ("SK_PANEL_COLUMNS", "SK_PANEL")}
+    os.environ["SK_PANEL_COLUMNS"] = str(columns); os.environ["SK_PANEL"] = str(width)
+    try:
+        c2 = sk.Context(0)
+        circs = [(sk.surface_code_circuit(7, 3, True), SEED), (sk.random_layered_circuit(256, 5), 11)]
+        rng = np.random.default_rng(99)
+        for n, count, pm in ((9, 300, 0.3), (70, 900, 0.15), (130, 800, 0.3)):
+            circs.append((sk.Circuit(n, rand_gates(rng, n, count, pm=pm)), int(rng.integers(0, 2**63))))
+        for circ, seed in circs:
+            c2.reset_counters()
+            t, out, det, _ = c2.sim(circ, seed)
+            o = orc.Tableau(circ.n); oo, od, rc = o.sim(circ.gates, seed, workers=8)
+            assert rc == 0 and (out == oo).all() and (det == od).all()
+            assert_same_tableau(t, o)
+            dc, oc = c2.counters(), o.counters()
+            for k in ("n_rand", "n_det", "k_rand", "k_det"):
+                assert dc[k] == oc[k], k
+            t.close()
+        c2.close()
+    finally:
+        for k, v in old.items():
+            if v is None: os.environ.pop(k, None)
+            else: os.environ[k] = v
+
+
+def test_dense_tableau_falls_back_to_column_form(sk, ctx, orc):
+    """n = 4096 random layered circuit: more than 1984 rows carry an x in a panel's columns, so the
+    kernel itself switches to the column-form factorisation."""
+    c = sk.random_layered_circuit(4096, 3)
+    t, out, det, _ = ctx.sim(c, 17)
+    o = orc.Tableau(c.n); oo, od, rc = o.sim(c.gates, 17, workers=8)
+    assert rc == 0 and (out == oo).all() and (det == od).all()
+    assert_same_tableau(t, o)
