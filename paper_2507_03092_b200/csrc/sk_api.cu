@@ -1,6 +1,9 @@
 // sk_api.cu -- C ABI (include/stabkit_b200.h): context, tableau, engine.
 // Host orchestration only; all arithmetic is in the kernels_*.cuh files.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -41,6 +44,10 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     else {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return SK_ECUDA; }
         c->own_stream = true;
+    }
+    {
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) { uint64_t keep = ~0ull; cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep); }
     }
     if (cudaMalloc(&c->d_err, 256) != cudaSuccess) { delete c; return SK_ECUDA; }
     cudaMemsetAsync(c->d_err, 0, 256, c->stream);
@@ -84,6 +91,11 @@ int32_t sk_ctx_reserve_tmp(sk_ctx* c, size_t bytes) {
     c->d_tmp_cap = cap;
     return SK_OK;
 }
+
+// Stream-ordered allocations from the device's default memory pool (kept resident: release threshold = max), so that
+// creating / destroying tableaux and programs inside sk_sim costs microseconds after the first call.
+template <class T> static cudaError_t dmalloc(sk_ctx* c, T** p, size_t bytes) { return cudaMallocAsync((void**)p, bytes ? bytes : 16, c->stream); }
+static void dfree(sk_ctx* c, void* p) { if (p) cudaFreeAsync(p, c->stream); }
 
 // ------------------------------------------------------------------ tableau --
 struct sk_tableau {
@@ -180,22 +192,22 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         t->B = B;
         t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8;
     }
-    cudaError_t e1 = cudaMalloc(&t->m.cols, t->cols_bytes);
-    cudaError_t e2 = cudaMalloc(&t->m.rows, t->rows_bytes);
-    cudaError_t e3 = cudaMalloc(&t->m.sgn, t->sgn_bytes);
+    cudaError_t e1 = dmalloc(c, &t->m.cols, t->cols_bytes);
+    cudaError_t e2 = dmalloc(c, &t->m.rows, t->rows_bytes);
+    cudaError_t e3 = dmalloc(c, &t->m.sgn, t->sgn_bytes);
     const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
-    cudaError_t e4 = cudaMalloc(&t->d_wpiv, 2 * window * 4);
-    cudaError_t e5 = cudaMalloc(&t->d_pan, (size_t)t->B * t->RW * 8);
-    cudaError_t e6 = cudaMalloc(&t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
-    cudaError_t e7 = cudaMalloc(&t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
-    cudaError_t e8 = cudaMalloc(&t->d_info, sizeof(PanelInfo));
-    cudaError_t e9 = cudaMalloc(&t->d_tlist, ((size_t)64 * t->RW + 2 * kPanelMax) * 4);
-    cudaError_t e10 = cudaMalloc(&t->d_tM, ((size_t)64 * t->RW + 2 * kPanelMax) * 8);
-    cudaError_t e11 = cudaMalloc(&t->d_rowM, (size_t)64 * t->RW * 8);
-    cudaError_t e12 = cudaMalloc(&t->d_alist_h, (size_t)64 * t->RW * 4);
-    cudaError_t e13 = cudaMalloc(&t->d_alist_b, (size_t)64 * t->RW * 8);
-    cudaError_t e14 = cudaMalloc(&t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
-    if (!e8) e8 = cudaMemset(t->d_info, 0, sizeof(PanelInfo));
+    cudaError_t e4 = dmalloc(c, &t->d_wpiv, 2 * window * 4);
+    cudaError_t e5 = dmalloc(c, &t->d_pan, (size_t)t->B * t->RW * 8);
+    cudaError_t e6 = dmalloc(c, &t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
+    cudaError_t e7 = dmalloc(c, &t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
+    cudaError_t e8 = dmalloc(c, &t->d_info, sizeof(PanelInfo));
+    cudaError_t e9 = dmalloc(c, &t->d_tlist, ((size_t)64 * t->RW + 2 * kPanelMax) * 4);
+    cudaError_t e10 = dmalloc(c, &t->d_tM, ((size_t)64 * t->RW + 2 * kPanelMax) * 8);
+    cudaError_t e11 = dmalloc(c, &t->d_rowM, (size_t)64 * t->RW * 8);
+    cudaError_t e12 = dmalloc(c, &t->d_alist_h, (size_t)64 * t->RW * 4);
+    cudaError_t e13 = dmalloc(c, &t->d_alist_b, (size_t)64 * t->RW * 8);
+    cudaError_t e14 = dmalloc(c, &t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
+    if (!e8) e8 = cudaMemsetAsync(t->d_info, 0, sizeof(PanelInfo), c->stream);
     if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11 || e12 || e13 || e14) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
 
     int per_sm = 0;
@@ -210,11 +222,12 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
 
 extern "C" void sk_tableau_destroy(sk_tableau* t) {
     if (!t) return;
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
-    cudaFree(t->m.cols); cudaFree(t->m.rows); cudaFree(t->m.sgn); cudaFree(t->d_wpiv);
-    cudaFree(t->d_pan); cudaFree(t->d_pivbuf); cudaFree(t->d_detacc); cudaFree(t->d_info); cudaFree(t->d_tlist); cudaFree(t->d_tM); cudaFree(t->d_rowM); cudaFree(t->d_alist_h); cudaFree(t->d_alist_b); cudaFree(t->d_dpart);
-    cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
+    sk_ctx* c = t->ctx;
+    cudaSetDevice(c->device);
+    for (void* p : {(void*)t->m.cols, (void*)t->m.rows, (void*)t->m.sgn, (void*)t->d_wpiv, (void*)t->d_pan, (void*)t->d_pivbuf, (void*)t->d_detacc,
+                    (void*)t->d_info, (void*)t->d_tlist, (void*)t->d_tM, (void*)t->d_rowM, (void*)t->d_alist_h, (void*)t->d_alist_b, (void*)t->d_dpart,
+                    (void*)t->d_q, (void*)t->d_out, (void*)t->d_det})
+        dfree(c, p);          // stream-ordered: queued behind the work that still uses the buffers
     delete t;
 }
 extern "C" int32_t sk_tableau_reset(sk_tableau* t) { return t ? tableau_identity(t) : SK_EARG; }
@@ -396,13 +409,12 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
 static int32_t reserve_record(sk_tableau* t, size_t m) {
     sk_ctx* c = t->ctx;
     if (m <= t->rec_cap) return SK_OK;
-    SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(t->d_q); cudaFree(t->d_out); cudaFree(t->d_det);
+    dfree(c, t->d_q); dfree(c, t->d_out); dfree(c, t->d_det);
     t->d_q = nullptr; t->d_out = nullptr; t->d_det = nullptr; t->rec_cap = 0;
     size_t cap = std::max<size_t>(m * 2, 1024);
-    SK_CUDA(c, cudaMalloc(&t->d_q, cap * 4));
-    SK_CUDA(c, cudaMalloc(&t->d_out, cap));
-    SK_CUDA(c, cudaMalloc(&t->d_det, cap));
+    SK_CUDA(c, dmalloc(c, &t->d_q, cap * 4));
+    SK_CUDA(c, dmalloc(c, &t->d_out, cap));
+    SK_CUDA(c, dmalloc(c, &t->d_det, cap));
     t->rec_cap = cap;
     return SK_OK;
 }
@@ -482,8 +494,7 @@ struct sk_program {
 extern "C" void sk_program_destroy(sk_program* p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
-    cudaStreamSynchronize(p->ctx->stream);
-    cudaFree(p->d_gates); cudaFree(p->d_mq); cudaFree(p->d_out); cudaFree(p->d_det);
+    dfree(p->ctx, p->d_gates); dfree(p->ctx, p->d_mq); dfree(p->ctx, p->d_out); dfree(p->ctx, p->d_det);
     delete p;
 }
 extern "C" uint64_t sk_program_measurements(const sk_program* p) { return p ? p->nmeas : 0; }
@@ -495,11 +506,31 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     *out = nullptr;
     if (warnings) *warnings = 0;
     if (n == 0) SK_FAIL(c, SK_EDIM, "circuit has zero qubits");
-    for (size_t i = 0; i < ngates; ++i) {
-        int32_t rc = validate_gate(c, gates[i], n, i);
-        if (rc) return rc;
-        if (gates[i].kind == SK_T || gates[i].kind == SK_TDG)
-            SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
+    // validation: threads look for any offending gate; the (rare) error path re-runs in order to report the first one
+    const unsigned nthreads = ngates > (1u << 16) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+    auto parallel_for = [&](size_t count, auto&& fn) {          // fn(begin, end, thread)
+        if (nthreads == 1 || count < nthreads) { fn(size_t(0), count, 0u); return; }
+        std::vector<std::thread> th;
+        for (unsigned k = 0; k < nthreads; ++k) th.emplace_back([&, k] { fn(count * k / nthreads, count * (k + 1) / nthreads, k); });
+        for (auto& t : th) t.join();
+    };
+    {
+        std::atomic<bool> bad{false};
+        parallel_for(ngates, [&](size_t lo, size_t hi, unsigned) {
+            bool b = false;
+            for (size_t i = lo; i < hi; ++i) {
+                const sk_gate& g = gates[i];
+                b |= g.kind >= SK_T || g.q0 >= n || (sk_is_two_qubit(g.kind) && (g.q1 >= n || g.q0 == g.q1));
+            }
+            if (b) bad = true;
+        });
+        if (bad)
+            for (size_t i = 0; i < ngates; ++i) {
+                int32_t rc = validate_gate(c, gates[i], n, i);
+                if (rc) return rc;
+                if (gates[i].kind == SK_T || gates[i].kind == SK_TDG)
+                    SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
+            }
     }
     for (size_t k = 0; k < nmarks; ++k)
         if (marks[k] >= ngates || (k && marks[k] <= marks[k - 1])) SK_FAIL(c, SK_EARG, "chunk_marks must be strictly increasing and < gate count (SPEC:238)");
@@ -530,7 +561,48 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
         }
     };
     if (mode == 0 || nmarks == 0) {
-        emit_sequential(0, ngates);
+        // sim semantics on the whole circuit: maximal runs of M gates are measurement blocks, the Clifford runs between
+        // them are layered independently (per-qubit order preserved) -- one task per run, spread over host threads
+        struct Seg { size_t lo, hi; bool meas; size_t out; std::vector<uint32_t> sizes; };
+        std::vector<Seg> segs;
+        for (size_t i = 0; i < ngates;) {
+            const bool m = gates[i].kind == SK_M;
+            size_t j = i;
+            while (j < ngates && (gates[j].kind == SK_M) == m) ++j;
+            segs.push_back({i, j, m, 0, {}});
+            i = j;
+        }
+        size_t ng = 0, nm = 0;
+        for (Seg& sg : segs) { if (sg.meas) { sg.out = nm; nm += sg.hi - sg.lo; } else { sg.out = ng; ng += sg.hi - sg.lo; } }
+        ordered.resize(ng); mq.resize(nm);
+        std::atomic<size_t> next{0};
+        parallel_for(nthreads, [&](size_t, size_t, unsigned) {
+            std::vector<uint32_t> level(n, 0), lay, start;
+            for (size_t si = next++; si < segs.size(); si = next++) {
+                Seg& sg = segs[si];
+                const sk_gate* g = gates + sg.lo; const size_t cnt = sg.hi - sg.lo;
+                if (sg.meas) { for (size_t i = 0; i < cnt; ++i) mq[sg.out + i] = g[i].q0; continue; }
+                lay.resize(cnt);
+                uint32_t depth = 0;
+                for (size_t i = 0; i < cnt; ++i) {
+                    uint32_t l = level[g[i].q0];
+                    const bool two = sk_is_two_qubit(g[i].kind);
+                    if (two) l = std::max(l, level[g[i].q1]);
+                    lay[i] = l; level[g[i].q0] = l + 1; if (two) level[g[i].q1] = l + 1;
+                    depth = std::max(depth, l + 1);
+                }
+                for (size_t i = 0; i < cnt; ++i) { level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) level[g[i].q1] = 0; }
+                start.assign(depth + 1, 0);
+                for (size_t i = 0; i < cnt; ++i) start[lay[i] + 1]++;
+                sg.sizes.resize(depth);
+                for (uint32_t d = 0; d < depth; ++d) { sg.sizes[d] = start[d + 1]; start[d + 1] += start[d]; }
+                for (size_t i = 0; i < cnt; ++i) ordered[sg.out + start[lay[i]]++] = g[i];
+            }
+        });
+        for (const Seg& sg : segs) {
+            if (sg.meas) p->ops.push_back({1, uint32_t(sg.out), uint32_t(sg.hi - sg.lo)});
+            else { size_t base = sg.out; for (uint32_t sz : sg.sizes) { p->ops.push_back({0, uint32_t(base), sz}); base += sz; } }
+        }
     } else {
         if (c->q_epoch.size() < n) c->q_epoch.assign(n, 0);
         size_t lo = 0;
@@ -562,8 +634,8 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     for (size_t i = 0; i < ngates; ++i) p->hist[gates[i].kind]++;
     p->ngates = ordered.size(); p->nmeas = mq.size();
     cudaError_t e = cudaSuccess;
-    if (p->ngates) { e = cudaMalloc(&p->d_gates, p->ngates * sizeof(sk_gate)); }
-    if (!e && p->nmeas) { e = cudaMalloc(&p->d_mq, p->nmeas * 4); if (!e) e = cudaMalloc(&p->d_out, p->nmeas); if (!e) e = cudaMalloc(&p->d_det, p->nmeas); }
+    if (p->ngates) { e = dmalloc(c, &p->d_gates, p->ngates * sizeof(sk_gate)); }
+    if (!e && p->nmeas) { e = dmalloc(c, &p->d_mq, p->nmeas * 4); if (!e) e = dmalloc(c, &p->d_out, p->nmeas); if (!e) e = dmalloc(c, &p->d_det, p->nmeas); }
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
     if (p->ngates) e = cudaMemcpyAsync(p->d_gates, ordered.data(), p->ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
     if (!e && p->nmeas) e = cudaMemcpyAsync(p->d_mq, mq.data(), p->nmeas * 4, cudaMemcpyHostToDevice, c->stream);
@@ -634,12 +706,22 @@ extern "C" int32_t sk_sim(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ng
     if (!c || !out_t) return SK_EARG;
     *out_t = nullptr;
     sk_program* p = nullptr; sk_tableau* t = nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     int32_t rc = sk_program_create(c, n, gates, ngates, marks, nmarks, mode, &p, warnings);
     if (rc) return rc;
+    const auto t1 = now();
     rc = sk_tableau_create(c, n, &t);
+    const auto t2 = now();
     if (!rc) rc = sk_program_run(p, t, seed);
+    const auto t3 = now();
     if (!rc) rc = sk_program_read_record(p, outcomes, deterministic);
+    const auto t4 = now();
     sk_program_destroy(p);
+    const auto t5 = now();
+    if (c->prof) fprintf(stderr, "sk_sim host ms: program_create %.2f tableau_create %.2f enqueue %.2f wait+record %.2f program_destroy %.2f\n",
+                         ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out_t = t;
     return SK_OK;

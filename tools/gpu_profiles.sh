@@ -20,8 +20,12 @@ with open('gpurun_out/launches_bench_${R}_summary.txt', 'w') as f:
         f.write(f"{k:40s} launches={len(v):5d} total_us={sum(v):12.1f} share={100*sum(v)/tot:6.2f}% mean_us={sum(v)/len(v):10.1f} max_us={max(v):10.1f}\n")
 print(open('gpurun_out/launches_bench_${R}_summary.txt').read())
 PY
-# full captures: one k_layer launch (CX layer), one transpose, the round-2 (all-deterministic) measurement block
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_layer -s 10 -c 2 -f -o gpurun_out/k_layer_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_transpose -s 2 -c 1 -f -o gpurun_out/k_transpose_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+# full captures: one k_layer launch (CX layer), one transpose, measurement block #0 (round 1: panel mode) and #1 (round 2: one deterministic wave)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_layer -s 10 -c 1 -f -o gpurun_out/k_layer_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_transpose -s 0 -c 1 -f -o gpurun_out/k_transpose_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_measure_block -s 0 -c 1 -f -o gpurun_out/k_measure_panel_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_measure_block -s 1 -c 1 -f -o gpurun_out/k_measure_det_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
-ls -la gpurun_out/*.ncu-rep
+for k in k_layer k_transpose k_measure_panel k_measure_det; do
+  ncu -i gpurun_out/${k}_${R}.ncu-rep --page raw --csv > gpurun_out/${k}_${R}_raw.csv 2>/dev/null
+done
+ls -la gpurun_out/
