@@ -62,6 +62,7 @@ extern "C" void sk_ctx_destroy(sk_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     cudaFree(c->d_gates); cudaFree(c->d_tmp); cudaFree(c->d_err); cudaFree(c->d_ws);
+    if (c->h_pin) cudaFreeHost(c->h_pin);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -499,6 +500,98 @@ extern "C" void sk_program_destroy(sk_program* p) {
 }
 extern "C" uint64_t sk_program_measurements(const sk_program* p) { return p ? p->nmeas : 0; }
 
+
+// ---- host-side compilation of a circuit with sim semantics -------------------------------
+// Maximal runs of M gates are measurement blocks; the Clifford runs between them are layered independently
+// (gates on disjoint qubits share a layer, per-qubit order preserved => same tableau as gate by gate).
+struct Seg {
+    size_t lo = 0, hi = 0; bool meas = false; size_t out = 0;   // gates [lo, hi) ; offset into the ordered gates / the qubit list
+    std::vector<uint32_t> sizes;                               // layer sizes of a Clifford run
+    std::atomic<int> done{0};
+};
+static unsigned host_threads(size_t ngates) {
+    return ngates > (1u << 16) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+}
+template <class F> static void parallel_for(unsigned nthreads, size_t count, F&& fn) {          // fn(begin, end, thread)
+    if (nthreads <= 1 || count < nthreads) { fn(size_t(0), count, 0u); return; }
+    std::vector<std::thread> th;
+    for (unsigned k = 0; k < nthreads; ++k) th.emplace_back([&, k] { fn(count * k / nthreads, count * (k + 1) / nthreads, k); });
+    for (auto& t : th) t.join();
+}
+// threads look for any offending gate; the (rare) error path re-runs in order to report the first one
+static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, unsigned nthreads) {
+    std::atomic<bool> bad{false};
+    parallel_for(nthreads, ngates, [&](size_t lo, size_t hi, unsigned) {
+        bool b = false;
+        for (size_t i = lo; i < hi; ++i) {
+            const sk_gate& g = gates[i];
+            b |= g.kind >= SK_T || g.q0 >= n || (sk_is_two_qubit(g.kind) && (g.q1 >= n || g.q0 == g.q1));
+        }
+        if (b) bad = true;
+    });
+    if (bad)
+        for (size_t i = 0; i < ngates; ++i) {
+            int32_t rc = validate_gate(c, gates[i], n, i);
+            if (rc) return rc;
+            if (gates[i].kind == SK_T || gates[i].kind == SK_TDG)
+                SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
+        }
+    return SK_OK;
+}
+static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_t& ng, size_t& nm) {
+    std::vector<std::pair<size_t, size_t>> b;
+    for (size_t i = 0; i < ngates;) {
+        const bool m = gates[i].kind == SK_M;
+        size_t j = i;
+        while (j < ngates && (gates[j].kind == SK_M) == m) ++j;
+        b.emplace_back(i, j);
+        i = j;
+    }
+    std::vector<Seg> segs(b.size());
+    ng = nm = 0;
+    for (size_t k = 0; k < b.size(); ++k) {
+        Seg& sg = segs[k];
+        sg.lo = b[k].first; sg.hi = b[k].second; sg.meas = gates[sg.lo].kind == SK_M;
+        if (sg.meas) { sg.out = nm; nm += sg.hi - sg.lo; } else { sg.out = ng; ng += sg.hi - sg.lo; }
+    }
+    return segs;
+}
+struct SegScratch { std::vector<uint32_t> level, lay, start; };
+static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* ordered, uint32_t* mq, SegScratch& sc) {
+    const sk_gate* g = gates + sg.lo; const size_t cnt = sg.hi - sg.lo;
+    if (sg.meas) { for (size_t i = 0; i < cnt; ++i) mq[sg.out + i] = g[i].q0; }
+    else {
+        if (sc.level.size() < n) sc.level.assign(n, 0);
+        sc.lay.resize(cnt);
+        uint32_t depth = 0;
+        for (size_t i = 0; i < cnt; ++i) {
+            uint32_t l = sc.level[g[i].q0];
+            const bool two = sk_is_two_qubit(g[i].kind);
+            if (two) l = std::max(l, sc.level[g[i].q1]);
+            sc.lay[i] = l; sc.level[g[i].q0] = l + 1; if (two) sc.level[g[i].q1] = l + 1;
+            depth = std::max(depth, l + 1);
+        }
+        for (size_t i = 0; i < cnt; ++i) { sc.level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) sc.level[g[i].q1] = 0; }
+        sc.start.assign(depth + 1, 0);
+        for (size_t i = 0; i < cnt; ++i) sc.start[sc.lay[i] + 1]++;
+        sg.sizes.resize(depth);
+        for (uint32_t d = 0; d < depth; ++d) { sg.sizes[d] = sc.start[d + 1]; sc.start[d + 1] += sc.start[d]; }
+        for (size_t i = 0; i < cnt; ++i) ordered[sg.out + sc.start[sc.lay[i]]++] = g[i];
+    }
+    sg.done.store(1, std::memory_order_release);
+}
+// pinned host staging owned by the context (grown on demand): ordered gates then the measured-qubit list
+static int32_t reserve_pinned(sk_ctx* c, size_t bytes) {
+    if (bytes <= c->h_pin_cap) return SK_OK;
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->h_pin) cudaFreeHost(c->h_pin);
+    c->h_pin = nullptr; c->h_pin_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, 1 << 20);
+    SK_CUDA(c, cudaHostAlloc(&c->h_pin, cap, cudaHostAllocDefault));
+    c->h_pin_cap = cap;
+    return SK_OK;
+}
+
 extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates,
                                      const uint32_t* marks, size_t nmarks, int mode,
                                      sk_program** out, uint32_t* warnings) {
@@ -506,32 +599,8 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     *out = nullptr;
     if (warnings) *warnings = 0;
     if (n == 0) SK_FAIL(c, SK_EDIM, "circuit has zero qubits");
-    // validation: threads look for any offending gate; the (rare) error path re-runs in order to report the first one
-    const unsigned nthreads = ngates > (1u << 16) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
-    auto parallel_for = [&](size_t count, auto&& fn) {          // fn(begin, end, thread)
-        if (nthreads == 1 || count < nthreads) { fn(size_t(0), count, 0u); return; }
-        std::vector<std::thread> th;
-        for (unsigned k = 0; k < nthreads; ++k) th.emplace_back([&, k] { fn(count * k / nthreads, count * (k + 1) / nthreads, k); });
-        for (auto& t : th) t.join();
-    };
-    {
-        std::atomic<bool> bad{false};
-        parallel_for(ngates, [&](size_t lo, size_t hi, unsigned) {
-            bool b = false;
-            for (size_t i = lo; i < hi; ++i) {
-                const sk_gate& g = gates[i];
-                b |= g.kind >= SK_T || g.q0 >= n || (sk_is_two_qubit(g.kind) && (g.q1 >= n || g.q0 == g.q1));
-            }
-            if (b) bad = true;
-        });
-        if (bad)
-            for (size_t i = 0; i < ngates; ++i) {
-                int32_t rc = validate_gate(c, gates[i], n, i);
-                if (rc) return rc;
-                if (gates[i].kind == SK_T || gates[i].kind == SK_TDG)
-                    SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
-            }
-    }
+    const unsigned nthreads = host_threads(ngates);
+    { int32_t rc = validate_circuit(c, n, gates, ngates, nthreads); if (rc) return rc; }
     for (size_t k = 0; k < nmarks; ++k)
         if (marks[k] >= ngates || (k && marks[k] <= marks[k - 1])) SK_FAIL(c, SK_EARG, "chunk_marks must be strictly increasing and < gate count (SPEC:238)");
 
@@ -561,43 +630,13 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
         }
     };
     if (mode == 0 || nmarks == 0) {
-        // sim semantics on the whole circuit: maximal runs of M gates are measurement blocks, the Clifford runs between
-        // them are layered independently (per-qubit order preserved) -- one task per run, spread over host threads
-        struct Seg { size_t lo, hi; bool meas; size_t out; std::vector<uint32_t> sizes; };
-        std::vector<Seg> segs;
-        for (size_t i = 0; i < ngates;) {
-            const bool m = gates[i].kind == SK_M;
-            size_t j = i;
-            while (j < ngates && (gates[j].kind == SK_M) == m) ++j;
-            segs.push_back({i, j, m, 0, {}});
-            i = j;
-        }
         size_t ng = 0, nm = 0;
-        for (Seg& sg : segs) { if (sg.meas) { sg.out = nm; nm += sg.hi - sg.lo; } else { sg.out = ng; ng += sg.hi - sg.lo; } }
+        std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
         ordered.resize(ng); mq.resize(nm);
         std::atomic<size_t> next{0};
-        parallel_for(nthreads, [&](size_t, size_t, unsigned) {
-            std::vector<uint32_t> level(n, 0), lay, start;
-            for (size_t si = next++; si < segs.size(); si = next++) {
-                Seg& sg = segs[si];
-                const sk_gate* g = gates + sg.lo; const size_t cnt = sg.hi - sg.lo;
-                if (sg.meas) { for (size_t i = 0; i < cnt; ++i) mq[sg.out + i] = g[i].q0; continue; }
-                lay.resize(cnt);
-                uint32_t depth = 0;
-                for (size_t i = 0; i < cnt; ++i) {
-                    uint32_t l = level[g[i].q0];
-                    const bool two = sk_is_two_qubit(g[i].kind);
-                    if (two) l = std::max(l, level[g[i].q1]);
-                    lay[i] = l; level[g[i].q0] = l + 1; if (two) level[g[i].q1] = l + 1;
-                    depth = std::max(depth, l + 1);
-                }
-                for (size_t i = 0; i < cnt; ++i) { level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) level[g[i].q1] = 0; }
-                start.assign(depth + 1, 0);
-                for (size_t i = 0; i < cnt; ++i) start[lay[i] + 1]++;
-                sg.sizes.resize(depth);
-                for (uint32_t d = 0; d < depth; ++d) { sg.sizes[d] = start[d + 1]; start[d + 1] += start[d]; }
-                for (size_t i = 0; i < cnt; ++i) ordered[sg.out + start[lay[i]]++] = g[i];
-            }
+        parallel_for(nthreads, nthreads, [&](size_t, size_t, unsigned) {
+            SegScratch sc;
+            for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], ordered.data(), mq.data(), sc);
         });
         for (const Seg& sg : segs) {
             if (sg.meas) p->ops.push_back({1, uint32_t(sg.out), uint32_t(sg.hi - sg.lo)});
@@ -700,28 +739,84 @@ extern "C" int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint
     return SK_OK;
 }
 
+// sim with host buffers, mode 0: compilation, upload and execution are pipelined.  Worker threads compile the
+// segments in order into pinned staging; the calling thread uploads each finished segment (async copy) and enqueues
+// its launches, so the device runs round r while the host still compiles round r+1.
+static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, uint64_t seed,
+                             sk_tableau** out_t, uint8_t* outcomes, uint8_t* deterministic) {
+    const unsigned nthreads = host_threads(ngates);
+    int32_t rc = validate_circuit(c, n, gates, ngates, nthreads);
+    if (rc) return rc;
+    size_t ng = 0, nm = 0;
+    std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
+    rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + 64);
+    if (rc) return rc;
+    sk_gate* h_gates = (sk_gate*)c->h_pin;
+    uint32_t* h_mq = (uint32_t*)((char*)c->h_pin + ((ng * sizeof(sk_gate) + 15) & ~size_t(15)));
+    sk_program* p = new sk_program();
+    p->ctx = c; p->n = n; p->ngates = ng; p->nmeas = nm;
+    cudaError_t e = cudaSuccess;
+    if (ng) e = dmalloc(c, &p->d_gates, ng * sizeof(sk_gate));
+    if (!e && nm) { e = dmalloc(c, &p->d_mq, nm * 4); if (!e) e = dmalloc(c, &p->d_out, nm); if (!e) e = dmalloc(c, &p->d_det, nm); }
+    if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
+    sk_tableau* t = nullptr;
+    rc = sk_tableau_create(c, n, &t);
+    if (rc) { sk_program_destroy(p); return rc; }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> workers;
+    auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc); };
+    for (unsigned k = 1; k < nthreads; ++k) workers.emplace_back(work);
+    SegScratch mine;
+    for (size_t si = 0; si < segs.size() && !rc; ++si) {
+        Seg& sg = segs[si];
+        while (!sg.done.load(std::memory_order_acquire)) {
+            if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine); }
+            else std::this_thread::yield();
+        }
+        const size_t cnt = sg.hi - sg.lo;
+        if (sg.meas) {
+            e = cudaMemcpyAsync(p->d_mq + sg.out, h_mq + sg.out, cnt * 4, cudaMemcpyHostToDevice, c->stream);
+            if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
+            rc = launch_measure(t, p->d_mq + sg.out, int(cnt), seed, sg.out, p->d_out + sg.out, p->d_det + sg.out);
+        } else {
+            e = cudaMemcpyAsync(p->d_gates + sg.out, h_gates + sg.out, cnt * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
+            if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
+            size_t base = sg.out;
+            for (uint32_t sz : sg.sizes) { launch_layer(t, p->d_gates + base, int(sz)); base += sz; }
+        }
+    }
+    next = segs.size();
+    for (auto& w : workers) w.join();
+    if (!rc) {
+        uint64_t hist[12] = {0};
+        for (size_t i = 0; i < ngates; ++i) hist[gates[i].kind]++;
+        for (int k = 0; k < 12; ++k) c->cnt.gate_hist[k] += hist[k];
+        p->last_t = t;
+        rc = sk_program_read_record(p, outcomes, deterministic);
+    } else cudaStreamSynchronize(c->stream);
+    sk_program_destroy(p);
+    if (rc) { sk_tableau_destroy(t); return rc; }
+    *out_t = t;
+    return SK_OK;
+}
+
 extern "C" int32_t sk_sim(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates,
                           const uint32_t* marks, size_t nmarks, int mode, uint64_t seed,
                           sk_tableau** out_t, uint8_t* outcomes, uint8_t* deterministic, uint32_t* warnings) {
-    if (!c || !out_t) return SK_EARG;
+    if (!c || !out_t || (!gates && ngates) || (!marks && nmarks)) return SK_EARG;
     *out_t = nullptr;
+    if (warnings) *warnings = 0;
+    if (n == 0) SK_FAIL(c, SK_EDIM, "circuit has zero qubits");
+    for (size_t k = 0; k < nmarks; ++k)
+        if (marks[k] >= ngates || (k && marks[k] <= marks[k - 1])) SK_FAIL(c, SK_EARG, "chunk_marks must be strictly increasing and < gate count (SPEC:238)");
+    if (mode == 0 || nmarks == 0) return sim_pipelined(c, n, gates, ngates, seed, out_t, outcomes, deterministic);
     sk_program* p = nullptr; sk_tableau* t = nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    const auto t0 = now();
     int32_t rc = sk_program_create(c, n, gates, ngates, marks, nmarks, mode, &p, warnings);
     if (rc) return rc;
-    const auto t1 = now();
     rc = sk_tableau_create(c, n, &t);
-    const auto t2 = now();
     if (!rc) rc = sk_program_run(p, t, seed);
-    const auto t3 = now();
     if (!rc) rc = sk_program_read_record(p, outcomes, deterministic);
-    const auto t4 = now();
     sk_program_destroy(p);
-    const auto t5 = now();
-    if (c->prof) fprintf(stderr, "sk_sim host ms: program_create %.2f tableau_create %.2f enqueue %.2f wait+record %.2f program_destroy %.2f\n",
-                         ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out_t = t;
     return SK_OK;

@@ -23,6 +23,7 @@ struct sk_ctx {
     // growable device scratch
     void* d_gates = nullptr; size_t d_gates_cap = 0;
     void* d_tmp = nullptr; size_t d_tmp_cap = 0;
+    void* h_pin = nullptr; size_t h_pin_cap = 0;   // pinned host staging (sk_sim: ordered gates + measured qubits)
     skd::u32* d_err = nullptr;              // generic error word for small kernels
     void* d_ws = nullptr;                   // skd::MeasWs: barrier, wave slots, device-side counters
     // host-side counters (device-side ones live in MeasWs)
