@@ -330,6 +330,7 @@ struct PanelSmem {
 //           the partner's new content (the old pivot row) becomes a fresh VIRTUAL row (born at step j)
 //   deterministic: partners = destabilizer rows with bit j (virtual ones stand for the +-Z rows of earlier steps)
 // which yields the same schedule (pivots, histories, step masks, partner sets) as the column form below.
+template <int KT>       // slots per thread actually used (1, 2 or 4): fewer slots = fewer dependent instructions per step
 __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A) {
     const int NS = a.NS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -341,12 +342,12 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     __syncthreads();
     u64 randmask = 0;
     // only as many warps as the rows (plus the virtual rows still to come) need take part: the per-step cost is issue-bound
-    const int Tact = min(kRowThreads, int(((A + kPanelMax + kRowK - 1) / kRowK + 31) & ~31u));
+    const int Tact = min(kRowThreads, int(((A + kPanelMax + KT - 1) / KT + 31) & ~31u));
     if (tid < Tact) {
         // slot state in scalars (kRowK == 4), so that it stays in registers: row-bit | (born step + 1) << 24 (kInf = empty), bits, M
         static_assert(kRowK == 4, "slot macros below are written for 4 slots per thread");
         u32 hh0 = kInf, hh1 = kInf, hh2 = kInf, hh3 = kInf; u64 bb0 = 0, bb1 = 0, bb2 = 0, bb3 = 0, mm0 = 0, mm1 = 0, mm2 = 0, mm3 = 0;
-#define SK_SLOTS(X) X(0, hh0, bb0, mm0) X(1, hh1, bb1, mm1) X(2, hh2, bb2, mm2) X(3, hh3, bb3, mm3)
+#define SK_SLOTS(X) X(0, hh0, bb0, mm0) if (KT > 1) { X(1, hh1, bb1, mm1) } if (KT > 2) { X(2, hh2, bb2, mm2) X(3, hh3, bb3, mm3) }
         int Kact = int((A + Tact - 1) / Tact);
 #define SK_LOAD(k, hh, bb, mm) { const u32 i = u32(k) * Tact + tid; if (i < A) { hh = __ldcg(a.alist_h + i); bb = ldcg(a.alist_b + i); } }
         SK_SLOTS(SK_LOAD)
@@ -937,7 +938,11 @@ k_measure_block(MeasArgs a) {
             const u32 A = __ldcg(&info->acount);
             __syncthreads();
             if (tid == 0) { info->acount = 0; if (a.prof) { ws->cprof[8] += A; if (A > ws->cprof[9]) ws->cprof[9] = A; } }
-            if (A <= (u32)kRowCap && !a.force_columns) panel_factorise_rows(a, ps, pos, Bn, A);
+            if (A <= (u32)kRowCap && !a.force_columns) {
+                if (A + kPanelMax <= (u32)kRowThreads) panel_factorise_rows<1>(a, ps, pos, Bn, A);
+                else if (A + kPanelMax <= 2u * kRowThreads) panel_factorise_rows<2>(a, ps, pos, Bn, A);
+                else panel_factorise_rows<4>(a, ps, pos, Bn, A);
+            }
             else panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
         }
         SK_PROF(3);
