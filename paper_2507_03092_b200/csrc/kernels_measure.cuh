@@ -74,11 +74,12 @@ struct MeasWs {
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
     u32 r0[4];          // per-wave index of the first random measurement, min-reduced; 3 slots rotate
     u32 c_stale;        // panel mode ran: the C form must be re-derived from R
-    u32 pad;
+    u32 progress;       // panel mode: measurements of this launch whose factorisation step is published (zeroed before each launch)
     u64 n_rand, n_det, k_rand, k_det, waves;
     u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
     u64 panels;
     u64 cprof[16];      // debug: SM cycles per step section, thread 0 [0..7] and thread 96 [8..15]: random {search+bar, gather+bar, update}, det {search+bar, gather+bar, rest}
+    u64 ctaphase[160 * 4];   // debug: per-CTA own time (ns) in panel phases G, F, V+D1, A+D2 (excluding barrier waits)
     u64 fprof[8];       // factorise (CTA 0) ns: load, random steps, deterministic steps, tail ; [4] random steps, [5] deterministic steps
 };
 
@@ -122,6 +123,15 @@ __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globa
 
 __device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
 __device__ __forceinline__ void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
+__device__ __forceinline__ void st_release(u32* p, u32 v) { asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+// bounded wait until *p >= target (monotone counter); false on timeout
+__device__ __forceinline__ bool wait_geq(const u32* p, u32 target) {
+    for (unsigned long long spins = 0; spins < (1ull << 22); ++spins) {
+        if (int(ld_acquire(p) - target) >= 0) return true;
+        __nanosleep(100);            // keep the polling traffic away from the producer's stores
+    }
+    return false;
+}
 __device__ __forceinline__ u64 warp_xor64(u64 v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
@@ -319,7 +329,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
 // pivot mask [W] (stabilizer rows used as pivots so far).
 struct PanelSmem {
     u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax], S[kPanelMax]; uint8_t outc[kPanelMax];
-    u32 full32[2]; u32 nt; u32 krand; u32 kdet;
+    u32 full32[2]; u32 nt; u32 krand; u32 kdet; int steps;
     u32 dcnt[kPanelMax]; u32 wmin[2][kRowThreads / 32]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd;
 };
 
@@ -338,11 +348,23 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     long long tc = clock64();
 #define SK_RPROF(k) do { if (a.prof && tid == 0) { const long long _c = clock64(); a.ws->cprof[k] += (u64)(_c - tc); tc = _c; } } while (0)
     if (tid < kPanelMax) { ps.piv[tid] = kInf; ps.hist[tid] = 0; ps.dZ[tid] = 0; ps.outc[tid] = 0; ps.dcnt[tid] = 0; }
-    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; ps.steps = 0; a.info->dmode = 1; }
     __syncthreads();
     u64 randmask = 0;
-    // only as many warps as the rows (plus the virtual rows still to come) need take part: the per-step cost is issue-bound
+    // Lookahead: every finished step is published at once (pivot, history, partner list, then a release store of the
+    // progress counter), so the other CTAs compute pivot values and partner products while the recurrence continues.
+    // only as many warps as the rows (plus the virtual rows still to come) need take part
     const int Tact = min(kRowThreads, int(((A + kPanelMax + KT - 1) / KT + 31) & ~31u));
+    // Steps are published in groups of 8: the release (a fence) is paid once per group -- and by a helper warp (the
+    // last one, when the recurrence does not need it), so that the fence latency stays off the recurrence's critical path.
+    const bool helper = Tact <= kMeasThreads - 32;
+    int published = 0;
+    auto publish = [&](int upto) {        // steps [published, upto)
+        PanelInfo* info = a.info;
+        for (int jj = published; jj < upto; ++jj) { info->piv[jj] = ps.piv[jj]; info->hist[jj] = ps.hist[jj]; info->dcnt[jj] = ps.dcnt[jj]; info->dZ[jj] = ps.dZ[jj]; }
+        st_release(&a.ws->progress, u32(pos + upto));
+        published = upto;
+    };
     if (tid < Tact) {
         // slot state in scalars (kRowK == 4), so that it stays in registers: row-bit | (born step + 1) << 24 (kInf = empty), bits, M
         static_assert(kRowK == 4, "slot macros below are written for 4 slots per thread");
@@ -372,6 +394,10 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
             const u32 wm = __reduce_min_sync(0xffffffffu, mymin);
             if (mymin == wm && (wm != kInf || lane == 0)) { ps.wmin[j & 1][warp] = wm; ps.wbp[j & 1][warp] = cb; ps.wmp[j & 1][warp] = cm; }   // row-bits are unique: one writer
             named_bar(1, Tact);
+            if (tid == 0) {                                    // all warps' writes of the steps before j precede this barrier
+                if (helper) { __threadfence_block(); *(volatile int*)&ps.steps = j; }
+                else if (j - published >= 8) publish(j);
+            }
             // minimum over the warps and the warp that holds it (row-bits are unique)
             const u32 wv = (lane < nw) ? ps.wmin[j & 1][lane] : kInf;
             const u32 p = __reduce_min_sync(0xffffffffu, wv);
@@ -416,6 +442,8 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
             if (tid == 0) { ps.piv[j] = p; ps.hist[j] = Mp; }
             randmask |= 1ull << j;
         }
+        named_bar(1, Tact);
+        if (tid == 0) { if (helper) { __threadfence_block(); *(volatile int*)&ps.steps = Bn; } else publish(Bn); }
         SK_RPROF(1);
         // emit the touched rows (regular rows that were multiplied at least once, and every virtual row)
         int cnt = 0;
@@ -441,6 +469,12 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 #undef SK_SLOTS
         if (tid == Tact - 1) ps.nt = at;
         SK_RPROF(2);
+    } else if (helper && tid == kMeasThreads - 32) {
+        while (published < Bn) {
+            const int st = *(volatile int*)&ps.steps;
+            if (st - published >= 8 || (st == Bn && st > published)) { __threadfence_block(); publish(st); }
+            else __nanosleep(200);
+        }
     }
     __syncthreads();
     SK_RPROF(3);
@@ -463,7 +497,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     PanelInfo* info = a.info;
     if (tid < kPanelMax) {
         info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid]; info->dcnt[tid] = ps.dcnt[tid];
-        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
+        info->piv[tid] = ps.piv[tid]; info->outc[tid] = ps.outc[tid];
     }
     if (tid == 0) {
         info->randmask = randmask; info->nt = ntr + (u32)nrand; info->dmode = 1; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
@@ -739,7 +773,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     PanelInfo* info = a.info;
     if (tid < kPanelMax) {
         info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid];
-        info->piv[tid] = ps.piv[tid]; info->eph[tid] = 0; info->dete[tid] = 0; info->outc[tid] = ps.outc[tid];
+        info->piv[tid] = ps.piv[tid]; info->outc[tid] = ps.outc[tid];
     }
     if (tid == 0) {
         info->randmask = randmask; info->nt = ntr + 2u * (u32)nrand; info->dmode = 0; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
@@ -749,6 +783,8 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     }
     SK_TPROF(15);
 #undef SK_TPROF
+    __syncthreads();
+    if (tid == 0) { __threadfence(); st_release(&a.ws->progress, u32(pos + Bn)); }      // column form: everything is published at the end
     SK_FPROF(3);
 #undef SK_FPROF
 }
@@ -761,7 +797,7 @@ k_measure_block(MeasArgs a) {
     __shared__ int s_wcnt[kMeasWarps];
     __shared__ u64 s_pn[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
-    __shared__ int s_cnt1;
+    __shared__ int s_cnt1, s_flag;
     __shared__ u32 s_targets[kMaxTargets];
     __shared__ PanelSmem ps;
     __shared__ PanelInfo s_info;
@@ -884,9 +920,17 @@ k_measure_block(MeasArgs a) {
     const int B = a.B;
     PanelInfo* info = a.info;
     const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs
+    u32 prev_nt = 0;
+    u64 t_cta = 0;
+#define SK_CSTART() do { if (a.prof && tid == 0) t_cta = gtime(); } while (0)
+#define SK_CPROF(k) do { if (a.prof && tid == 0 && blockIdx.x < 160) ws->ctaphase[blockIdx.x * 4 + k] += gtime() - t_cta; } while (0)
     while (pos < a.count) {
         const int Bn = min(B, a.count - pos);
+        SK_CSTART();
         if (tid < kPanelMax) s_q[tid] = (tid < Bn) ? a.qubits[pos + tid] : 0xffffffffu;
+        // housekeeping for the panel that just finished: its step-mask entries (D part 2 was their last reader) and phase sums
+        for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(a.rowM + __ldcg(a.tlist + i), 0ull);
+        if (blockIdx.x == 0 && tid < kPanelMax) info->eph[tid] = 0;
         __syncthreads();
         // ---- G: gather the panel columns from the R form: warp per group of 32 row-bits
         {
@@ -930,9 +974,9 @@ k_measure_block(MeasArgs a) {
                 }
             }
         }
-        SK_PROF(2);
+        SK_PROF(2); SK_CPROF(0);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(7);
+        SK_PROF(7); SK_CSTART();
         // ---- F: symbolic factorisation (CTA 0)
         if (blockIdx.x == 0) {
             const u32 A = __ldcg(&info->acount);
@@ -945,10 +989,91 @@ k_measure_block(MeasArgs a) {
             }
             else panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
         }
-        SK_PROF(3);
-        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(7);
-        // ---- V + D part 1
+        SK_PROF(3); SK_CPROF(1);
+        // ---- consumers (every CTA but 0, which is busy factorising): V pivot values + D part 1, fed step by step
+        const int nC = max(1, G - 1);
+        const int cidx = (G == 1) ? 0 : int(blockIdx.x) - 1;
+        if (G == 1 || blockIdx.x != 0) {
+        SK_CSTART();
+        if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + 1)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
+        __syncthreads();
+        if (!s_flag) return;
+        const u32 dmode = __ldcg(&info->dmode);         // written before the first publication
+        const int wpc = (W + nC - 1) / nC;
+        const int wlo = min(W, cidx * wpc), whi = min(W, wlo + wpc);
+        const int nw = whi - wlo;
+        const int nvw = min(kMeasWarps - 1, (nw + 31) / 32);    // warps busy with V (a thread may own several words)
+        u64* vs = smem + (size_t)kMeasWarps * 2 * Wp;           // [Bn][2][wpc] after the accumulators
+        if (dmode == 1) {
+            // ---------- streaming: V consumes the published steps in chunks of 8 (two L2 round trips per chunk)
+            if (warp < nvw) {
+                const int nvt = 32 * nvw;
+                for (int done = 0; done < Bn;) {
+                    const int target = min(Bn, done + 8);
+                    if (!wait_geq(&ws->progress, u32(pos + target))) { atomicOr(&ws->err, 0x80000000u); break; }
+                    for (int t = tid; t < nw; t += nvt) {
+                        const int w = wlo + t;
+                        u32 pk[8]; u64 hk[8], lx[8], lz[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) pk[u] = (done + u < target) ? __ldcg(&info->piv[done + u]) : 0xffffffffu;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            lx[u] = 0; lz[u] = 0; hk[u] = 0;
+                            if (pk[u] != 0xffffffffu) { const u64* rp = a.m.rows + (size_t)(2 * pk[u]) * Wp + w; lx[u] = ldcg(rp); lz[u] = ldcg(rp + Wp); hk[u] = ldcg(&info->hist[done + u]); }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (pk[u] == 0xffffffffu) continue;
+                            const int k = done + u;
+                            u64 ax = lx[u], az = lz[u], hb = hk[u];
+                            int e = 0;
+                            while (hb) {
+                                const int l = __ffsll((long long)hb) - 1; hb &= hb - 1;
+                                const u64 bx = vs[(size_t)(2 * l) * wpc + t], bz = vs[(size_t)(2 * l + 1) * wpc + t];
+                                e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                            }
+                            vs[(size_t)(2 * k) * wpc + t] = ax; vs[(size_t)(2 * k + 1) * wpc + t] = az;
+                            __stcg(a.pivbuf + (size_t)(2 * k) * Wp + w, ax); __stcg(a.pivbuf + (size_t)(2 * k + 1) * Wp + w, az);
+                            if (e & 3) atomicAdd(&info->eph[k], (u32)(e & 3));
+                        }
+                    }
+                    done = target;
+                }
+            }
+            if (nvw) __syncthreads();
+            // ---------- streaming D part 1: step j belongs to consumer nC-1 - j % nC (from the far end: V uses the first ones);
+            // the step masks N_j are taken in D part 2, when the factorisation has finished
+            for (int j = nC - 1 - cidx; j < Bn; j += nC) {
+                if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + j + 1)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
+                __syncthreads();
+                if (!s_flag) return;
+                if (__ldcg(&info->piv[j]) != 0xffffffffu) continue;
+                const int cnt = int(__ldcg(&info->dcnt[j]));
+                const u32* gl = a.dpart + (size_t)j * kRowSlots;
+                u64* dx = a.detacc + (size_t)(2 * j) * Wp;
+                if (cnt <= kWarpDirect) {
+                    if (warp == 0) {
+                        for (int i = lane; i < cnt; i += 32) s_wlist[0][i] = __ldcg(gl + i);
+                        for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
+                        __syncwarp();
+                        int e = warp_mul_list(a.m.rows, W, Wp, s_wlist[0], cnt, acc_x, acc_z, lane);
+                        for (int i = lane; i < cnt; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[0][i]));
+                        e = warp_sum(e) & 3;
+                        for (int w = lane; w < W; w += 32) { __stcg(dx + w, acc_x[w]); __stcg(dx + Wp + w, acc_z[w]); }
+                        if (lane == 0) info->dete[j] = e;
+                    }
+                } else {
+                    int total;
+                    const int e = cta_det(a, sm, a.pan, dx, &total, nullptr, nullptr, gl, cnt);
+                    if (tid == 0) info->dete[j] = e;
+                }
+                __syncthreads();
+            }
+        } else {
+        // ---------- column form: nothing is published before the end; V and D part 1 (with N_j) as one phase
+        if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + Bn)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
+        __syncthreads();
+        if (!s_flag) return;
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
         __syncthreads();
         const u64 randmask = s_info.randmask;
@@ -958,11 +1083,6 @@ k_measure_block(MeasArgs a) {
         __syncthreads();
         {
             // V: words [wlo, whi) of every pivot value belong to this CTA; thread t owns word wlo + t
-            const int wpc = (W + G - 1) / G;
-            const int wlo = min(W, blockIdx.x * wpc), whi = min(W, wlo + wpc);
-            const int nw = whi - wlo;
-            const int nvw = (nw + 31) / 32;                         // warps busy with V
-            u64* vs = smem + (size_t)kMeasWarps * 2 * Wp;           // [Bn][2][wpc] after the accumulators
             if (warp < nvw) {
                 // stage the panel-start pivot rows' words: items (step k, word t), 4 items (8 loads) in flight per thread
                 const int nitems = Bn * nw, nvt = 32 * nvw;
@@ -1005,13 +1125,13 @@ k_measure_block(MeasArgs a) {
                 }
             } else {
                 // D part 1: product of the panel-start partner rows of every deterministic step; the idx-th
-                // deterministic step goes to CTA idx % G, warp (idx / G) % nwd of the non-V warps
+                // deterministic step goes to consumer nC-1 - idx % nC, warp (idx / nC) % nwd of the non-V warps
                 const int nwd = kMeasWarps - nvw;
                 u64 bits = detmask; int idx = 0;
                 while (bits) {
                     const int j = __ffsll((long long)bits) - 1; bits &= bits - 1;
                     const int my = idx++;
-                    if (G - 1 - my % G != int(blockIdx.x) || (my / G) % nwd != warp - nvw) continue;    // from the far end: V uses the first CTAs
+                    if (nC - 1 - my % nC != cidx || (my / nC) % nwd != warp - nvw) continue;    // from the far end: V uses the first consumers
                     const u64* dcol = a.pan + (size_t)j * RW + W;
                     if (lane == 0) s_wcnt[warp] = 0;
                     __syncwarp();
@@ -1065,16 +1185,25 @@ k_measure_block(MeasArgs a) {
                 if (tid == 0) { info->dete[j] = e; info->dN[j] = N & randmask & ((1ull << j) - 1ull); }
             }
         }
+        }   // column form
+        SK_CPROF(2);
+        }   // consumers
         SK_PROF(4);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(7);
-        // ---- signs of the pivot values (triangular GF(2) recurrence; every CTA solves it itself)
+        SK_PROF(7); SK_CSTART();
+        // ---- the finished panel description (one round trip), then the signs of the pivot values
+        // (triangular GF(2) recurrence; every CTA solves it itself)
+        for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
+        __syncthreads();
+        const u64 randmask = s_info.randmask;
+        const u64 allmask = (Bn < 64) ? ((1ull << Bn) - 1ull) : ~0ull;
+        const u64 detmask = ~randmask & allmask;
         if (tid == 0) {
             u64 psign = 0; u32 odd = 0;
             u64 bits = randmask;
             while (bits) {
                 const int k = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                const u32 ek = __ldcg(&info->eph[k]) + 2u * (u32)((s_info.osign >> k) & 1ull) + 2u * (u32)__popcll(s_info.hist[k] & psign);
+                const u32 ek = s_info.eph[k] + 2u * (u32)((s_info.osign >> k) & 1ull) + 2u * (u32)__popcll(s_info.hist[k] & psign);
                 odd |= ek & 1u;
                 psign |= (u64)((ek >> 1) & 1u) << k;
             }
@@ -1094,7 +1223,15 @@ k_measure_block(MeasArgs a) {
                     const int j = __ffsll((long long)bits) - 1;
                     const u64* dx = a.detacc + (size_t)(2 * j) * Wp;
                     for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(dx + w); acc_z[w] = ldcg(dx + Wp + w); }
-                    const u64 N = ldcg(&info->dN[j]), Z = s_info.dZ[j];
+                    u64 N;
+                    if (s_info.dmode) {        // XOR of the partners' step masks, restricted to the steps before j
+                        N = 0;
+                        const int cnt = int(s_info.dcnt[j]);
+                        const u32* gl = a.dpart + (size_t)j * kRowSlots;
+                        for (int i = lane; i < cnt; i += 32) N ^= ldcg(a.rowM + __ldcg(gl + i));
+                        N = warp_xor64(N) & randmask & ((1ull << j) - 1ull);
+                    } else N = ldcg(&info->dN[j]);
+                    const u64 Z = s_info.dZ[j];
                     int cnt = 0;
                     { u64 b = N; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
                     __syncwarp();
@@ -1121,7 +1258,6 @@ k_measure_block(MeasArgs a) {
                     const int i = it - nd;
                     const u32 h = __ldcg(a.tlist + i);
                     u64 M = ldcg(a.tM + i);
-                    if (lane == 0) __stcg(a.rowM + h, 0ull);      // D part 1 (previous phase) was its last reader
                     // is h a pivot of this panel, or the destabilizer partner of one?
                     int kp = -1, ko = -1;
                     {
@@ -1166,11 +1302,14 @@ k_measure_block(MeasArgs a) {
                 }
             }
         }
-        SK_PROF(5);
+        SK_PROF(5); SK_CPROF(3);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
+        prev_nt = s_info.nt;
         pos += Bn;
     }
+    for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(a.rowM + __ldcg(a.tlist + i), 0ull);
+    if (blockIdx.x == 0 && tid < kPanelMax) info->eph[tid] = 0;
     if (blockIdx.x == 0 && tid == 0) ws->c_stale = 1u;
 }
 

@@ -188,7 +188,9 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         }
         int B = int(std::min<size_t>(kPanelMax, (avail / 8 - aux_words) / col_words));
         if (const char* e = getenv("SK_PANEL")) B = std::max(1, std::min(B, atoi(e)));
-        const int wpc = (t->W + c->num_sms - 1) / c->num_sms;
+        t->meas_grid = c->meas_grid_override > 0 ? std::min(c->meas_grid_override, c->num_sms) : c->num_sms;
+        const int ncons = std::max(1, t->meas_grid - 1);         // consumer CTAs of the pivot-value phase
+        const int wpc = (t->W + ncons - 1) / ncons;
         while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
         t->B = B;
         t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8;
@@ -214,7 +216,6 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     int per_sm = 0;
     SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_measure_block, kMeasThreads, t->meas_smem));
     if (per_sm < 1) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "measurement kernel does not fit on an SM"); }
-    t->meas_grid = c->meas_grid_override > 0 ? std::min(c->meas_grid_override, c->num_sms) : c->num_sms;
     int32_t rc = tableau_identity(t);
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out = t;
@@ -394,7 +395,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasWs* ws = (MeasWs*)c->d_ws;
     SK_CUDA(c, cudaMemsetAsync(&ws->r0[0], 0xFF, 16, c->stream));
     SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->c_stale, 0, 4, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->c_stale, 0, 8, c->stream));      // c_stale + progress
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
@@ -461,7 +462,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     if (!c) return SK_EARG;
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, 38 * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, (38 + 640) * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -474,6 +475,14 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "measure kernel CTA0 us: P1 %.0f P2 %.0f | gather %.0f factorise %.0f values+detA %.0f apply+detB %.0f | barriers wave %.0f panel %.0f | panels %llu\n",
                                          h.prof[0] / 1e3, h.prof[1] / 1e3, h.prof[2] / 1e3, h.prof[3] / 1e3, h.prof[4] / 1e3, h.prof[5] / 1e3, h.prof[6] / 1e3, h.prof[7] / 1e3, (unsigned long long)h.panels);
+    if (getenv("SK_DEBUG_PROF")) {
+        const char* nm[4] = {"G", "F", "V+D1", "A+D2"};
+        for (int ph = 0; ph < 4; ++ph) {
+            double mx = 0, sum = 0; int arg = 0, cnt = 0;
+            for (int b = 0; b < 160; ++b) { double v = h.ctaphase[b * 4 + ph] / 1e3; if (v > 0) { sum += v; ++cnt; } if (v > mx) { mx = v; arg = b; } }
+            fprintf(stderr, "panel phase %-5s own time per CTA (us): avg %.0f max %.0f (CTA %d) cta0 %.0f\n", nm[ph], cnt ? sum / cnt : 0.0, mx, arg, h.ctaphase[ph] / 1e3);
+        }
+    }
     if (getenv("SK_DEBUG_PROF")) { fprintf(stderr, "cprof cycles:"); for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", (unsigned long long)h.cprof[k]); fprintf(stderr, "\n"); }
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "factorise us: load %.0f random steps %.0f (n=%llu) deterministic steps %.0f (n=%llu) tail %.0f\n",
                                          h.fprof[0] / 1e3, h.fprof[1] / 1e3, (unsigned long long)h.fprof[4], h.fprof[2] / 1e3, (unsigned long long)h.fprof[5], h.fprof[3] / 1e3);
