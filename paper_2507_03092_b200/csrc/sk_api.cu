@@ -37,6 +37,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return SK_ECUDA; }
     c->num_sms = prop.multiProcessorCount;
     if (getenv("SK_DEBUG_PROF")) c->prof = 1;
+    if (const char* e = getenv("SK_NO_GRAPH")) c->no_graph = atoi(e);
     if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
@@ -110,6 +111,7 @@ struct sk_tableau {
     int meas_grid = 0; size_t meas_smem = 0;
     u32* d_wpiv = nullptr;
     // panel-mode scratch (kernels_measure.cuh)
+    uint64_t uid = 0;               // distinguishes tableaux that reuse a host address (graph cache key)
     int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
     u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr; u32* d_alist_h = nullptr; u64* d_alist_b = nullptr; u32* d_dpart = nullptr;
 };
@@ -166,7 +168,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     if (n > (1u << 20)) SK_FAIL(c, SK_EDIM, "n=%llu exceeds the supported 2^20 qubits", (unsigned long long)n);
     SK_CUDA(c, cudaSetDevice(c->device));
     sk_tableau* t = new sk_tableau();
-    t->ctx = c; t->n = n;
+    t->ctx = c; t->n = n; t->uid = ++c->tableau_uid;
     t->W = int((n + 63) / 64); t->Wp = (t->W + 1) & ~1; t->RW = 2 * t->W; t->NS = 64 * t->W;
     t->m.n = n; t->m.W = t->W; t->m.Wp = t->Wp; t->m.RW = t->RW;
     t->cols_bytes = (size_t)n * 2 * t->RW * 8;
@@ -499,11 +501,15 @@ struct sk_program {
     u32* d_mq = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t nmeas = 0;
     uint64_t hist[12] = {0};
     sk_tableau* last_t = nullptr;
+    // the whole launch sequence of a run as a CUDA graph, replayed while (tableau, seed, entry state) stay the same
+    cudaGraphExec_t gexec = nullptr; uint64_t g_tab_uid = 0, g_seed = 0; bool g_r_in = false, g_r_out = false, g_disabled = false;
+    uint64_t g_launches = 0, g_layers = 0, g_transposes = 0;
 };
 
 extern "C" void sk_program_destroy(sk_program* p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
+    if (p->gexec) { cudaStreamSynchronize(p->ctx->stream); cudaGraphExecDestroy(p->gexec); }
     dfree(p->ctx, p->d_gates); dfree(p->ctx, p->d_mq); dfree(p->ctx, p->d_out); dfree(p->ctx, p->d_det);
     delete p;
 }
@@ -706,17 +712,53 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         if (!class_ms) return;
         cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->stream); ev.push_back(e); cls.push_back(k);
     };
-    mark(-1);
-    for (const ProgOp& op : p->ops) {
-        if (op.type == 0) {
-            launch_layer(t, p->d_gates + op.off, int(op.count));
-            mark(0);
-        } else {
-            if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; mark(1); }
-            int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
-            if (rc) return rc;
-            mark(2);
+    auto enqueue_all = [&]() -> int32_t {
+        mark(-1);
+        for (const ProgOp& op : p->ops) {
+            if (op.type == 0) {
+                launch_layer(t, p->d_gates + op.off, int(op.count));
+                mark(0);
+            } else {
+                if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; mark(1); }
+                int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
+                if (rc) return rc;
+                mark(2);
+            }
         }
+        return SK_OK;
+    };
+    const bool want_graph = !class_ms && !p->g_disabled && !c->no_graph && p->ops.size() >= 8;
+    if (want_graph && p->gexec && p->g_tab_uid == t->uid && p->g_seed == seed && p->g_r_in == t->r_valid) {
+        SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));                     // replay
+        t->r_valid = p->g_r_out;
+        c->cnt.kernel_launches += p->g_launches; c->cnt.layers += p->g_layers; c->cnt.transposes += p->g_transposes;
+    } else if (want_graph) {
+        if (p->gexec) { cudaStreamSynchronize(c->stream); cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        const bool r_in = t->r_valid;
+        const sk_counters before = c->cnt;
+        cudaGraph_t graph = nullptr;
+        int32_t rc = SK_OK;
+        if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            rc = enqueue_all();
+            cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+            if (!rc && e == cudaSuccess && graph && cudaGraphInstantiate(&p->gexec, graph, 0) == cudaSuccess) {
+                p->g_tab_uid = t->uid; p->g_seed = seed; p->g_r_in = r_in; p->g_r_out = t->r_valid;
+                p->g_launches = c->cnt.kernel_launches - before.kernel_launches; p->g_layers = c->cnt.layers - before.layers;
+                p->g_transposes = c->cnt.transposes - before.transposes;
+            } else { p->gexec = nullptr; p->g_disabled = true; }
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+        } else { p->g_disabled = true; cudaGetLastError(); }
+        if (rc) return rc;
+        if (p->gexec) SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));
+        else {                              // capture is not possible here: plain stream launches
+            t->r_valid = r_in; c->cnt = before;
+            rc = enqueue_all();
+            if (rc) return rc;
+        }
+    } else {
+        int32_t rc = enqueue_all();
+        if (rc) return rc;
     }
     SK_CUDA(c, cudaGetLastError());
     for (int k = 0; k < 12; ++k) c->cnt.gate_hist[k] += p->hist[k];

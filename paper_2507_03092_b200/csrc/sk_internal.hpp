@@ -17,6 +17,8 @@ struct sk_ctx {
     int num_sms = 0;
     int max_smem_optin = 0;
     int prof = 0;                           // SK_DEBUG_PROF: device-side phase timers (slows the kernel)
+    int no_graph = 0;                       // SK_NO_GRAPH=1: sk_program_run enqueues plain launches instead of replaying a CUDA graph
+    uint64_t tableau_uid = 0;
     int force_columns = 0;                  // SK_PANEL_COLUMNS=1: column-form panel factorisation only (testing aid)
     int meas_grid_override = 0;             // SK_MEAS_GRID: CTAs of the measurement kernel (profiling aid)
     std::string err;
