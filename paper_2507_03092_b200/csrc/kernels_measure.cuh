@@ -44,6 +44,7 @@
 // deterministic  RW*8/2 + k*16W  -- reported from the k counters kept here.
 #pragma once
 #include "common.cuh"
+#include "kernels_transpose.cuh"
 
 namespace skd {
 
@@ -115,6 +116,7 @@ struct MeasArgs {
     u32* dpart;         // [B][kRowSlots] row form: partner stabilizers of the deterministic steps
     u64* rowM;          // [64*RW] step mask by row-bit (zero for rows the current panel does not touch)
     int prof;           // device-side phase timers (SK_DEBUG_PROF)
+    int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
 };
 
@@ -917,6 +919,22 @@ k_measure_block(MeasArgs a) {
 
     // =============================================================== panel mode =====
     // (the P2 reads above touch nothing that is written before the next grid barrier)
+    if (a.destab_stale) {
+        // The host transposed only the stabilizer half C -> R (all a deterministic block needs).  Panel mode works on whole
+        // rows: derive the destabilizer rows now, two 256 x 256-bit tiles per CTA at a time (same tile move as k_transpose_bits).
+        const int half = tid >> 8, t = tid & 255;
+        u32 (*tin)[9] = reinterpret_cast<u32 (*)[9]>(smem) + (size_t)half * 512;
+        u32 (*tout)[9] = tin + 256;
+        const int nbx = (a.n + 255) / 256, by_lo = RW / 8, nby = (2 * RW + 7) / 8 - by_lo;      // u32 words [RW, 2*RW) of a column = destabilizer rows
+        const int ntiles = nbx * nby * 2;
+        for (int tile = blockIdx.x * 2 + half; tile < ntiles; tile += 2 * G) {
+            const int z = tile / (nbx * nby), r = tile - z * nbx * nby, by = by_lo + r / nbx, bx = r - (r / nbx) * nbx;
+            transpose_tile_256(reinterpret_cast<const u32*>(a.m.cols) + (size_t)z * 2 * RW, (size_t)4 * RW, a.n, 2 * RW,
+                               reinterpret_cast<u32*>(a.m.rows) + (size_t)z * 2 * Wp, (size_t)4 * Wp, 64 * RW, 2 * Wp,
+                               bx * 256, by * 8, t, 2 + half, tin, tout);
+        }
+        if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
+    }
     const int B = a.B;
     PanelInfo* info = a.info;
     const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs

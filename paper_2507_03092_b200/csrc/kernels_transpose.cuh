@@ -61,6 +61,38 @@ k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, i
     }
 }
 
+// The same tile move as a device function for use inside a persistent kernel: `nthr` = 256 threads of one half-CTA
+// (thread index t in [0,256)), synchronised with the named barrier `bar_id`; tin/tout = 2 x 256 x 9 words of shared memory.
+__device__ __forceinline__ void transpose_tile_256(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                                                   u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                                                   int c0, int w0, int t, int bar_id, u32 (*tin)[9], u32 (*tout)[9]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        int rr = k * 32 + (t >> 3), ww = t & 7;
+        int gr = c0 + rr, gw = w0 + ww;
+        u32 v = 0;
+        if (gr < src_rows && gw < src_words) v = __ldcg(src + (size_t)gr * src_stride + gw);
+        tin[rr][ww] = v;
+    }
+    asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
+    const int warp = t >> 5, lane = t & 31;
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) {
+        u32 v = tin[warp * 32 + lane][bj];
+        bfly(v, 16, 0x0000ffffu, lane); bfly(v, 8, 0x00ff00ffu, lane); bfly(v, 4, 0x0f0f0f0fu, lane);
+        bfly(v, 2, 0x33333333u, lane); bfly(v, 1, 0x55555555u, lane);
+        tout[bj * 32 + lane][warp] = v;
+    }
+    asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        int rr = k * 32 + (t >> 3), ww = t & 7;
+        int gr = w0 * 32 + rr, gw = (c0 >> 5) + ww;
+        if (gr < dst_rows && gw < dst_words) __stcg(dst + (size_t)gr * dst_stride + gw, tout[rr][ww]);
+    }
+    asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");      // tin/tout are reused by the next tile
+}
+
 // sign bit-vector <-> one byte per row (host ABI); rowbit = map of tableau row index
 __global__ void k_signs_to_bytes(const u64* __restrict__ sgn, uint8_t* __restrict__ out, int nrows, int split, int NS) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;

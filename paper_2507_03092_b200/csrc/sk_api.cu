@@ -106,6 +106,7 @@ struct sk_tableau {
     int W = 0, Wp = 0, RW = 0, NS = 0;
     DMat m;
     bool r_valid = false;           // C form is always valid; R form on demand
+    bool r_destab_stale = false;    // R holds the stabilizer rows only (C -> R was restricted to that half)
     size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
     u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
     int meas_grid = 0; size_t meas_smem = 0;
@@ -126,17 +127,19 @@ static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int s
     SK_CUDA(c, cudaGetLastError());
     return SK_OK;
 }
-// C -> R
-static int32_t rows_from_cols(sk_tableau* t) {
+// C -> R ; stab_only: just the stabilizer rows (all an all-deterministic measurement block reads; the measurement kernel
+// derives the destabilizer rows itself if it has to enter panel mode)
+static int32_t rows_from_cols(sk_tableau* t, bool stab_only = false) {
     sk_ctx* c = t->ctx;
-    int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(t->m.cols), (size_t)4 * t->RW, int(t->n), 2 * t->RW,
-                                  reinterpret_cast<u32*>(t->m.rows), (size_t)4 * t->Wp, 64 * t->RW, 2 * t->Wp,
+    int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(t->m.cols), (size_t)4 * t->RW, int(t->n), stab_only ? t->RW : 2 * t->RW,
+                                  reinterpret_cast<u32*>(t->m.rows), (size_t)4 * t->Wp, stab_only ? t->NS : 64 * t->RW, 2 * t->Wp,
                                   (size_t)2 * t->RW, (size_t)2 * t->Wp, nullptr);
     if (rc) return rc;
     c->cnt.transposes++;
-    t->r_valid = true;
+    t->r_valid = true; t->r_destab_stale = stab_only;
     return SK_OK;
 }
+static int32_t rows_full(sk_tableau* t) { return (!t->r_valid || t->r_destab_stale) ? rows_from_cols(t, false) : SK_OK; }
 // R -> C ; with `flag` only if the device-side stale flag is raised
 static int32_t cols_from_rows(sk_tableau* t, const u32* flag = nullptr) {
     sk_ctx* c = t->ctx;
@@ -157,7 +160,7 @@ static int32_t tableau_identity(sk_tableau* t) {
     k_identity<<<(unsigned)((t->n + 255) / 256), 256, 0, c->stream>>>(t->m.cols, t->m.rows, int(t->n), t->RW, t->Wp, t->NS);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
-    t->r_valid = true;
+    t->r_valid = true; t->r_destab_stale = false;
     return SK_OK;
 }
 
@@ -195,7 +198,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         const int wpc = (t->W + ncons - 1) / ncons;
         while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
         t->B = B;
-        t->meas_smem = std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8;
+        t->meas_smem = std::max<size_t>(std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8, 2 * 512 * 9 * 4);   // >= the in-kernel transpose tiles
     }
     cudaError_t e1 = dmalloc(c, &t->m.cols, t->cols_bytes);
     cudaError_t e2 = dmalloc(c, &t->m.rows, t->rows_bytes);
@@ -253,7 +256,7 @@ extern "C" int32_t sk_tableau_upload(sk_tableau* t, const uint64_t* x, const uin
     k_bytes_to_signs<<<(unsigned)((nrows + 255) / 256), 256, 0, c->stream>>>(ds, t->m.sgn, int(nrows), int(t->n), t->NS);
     c->cnt.kernel_launches += 2;
     SK_CUDA(c, cudaGetLastError());
-    t->r_valid = true;
+    t->r_valid = true; t->r_destab_stale = false;
     rc = cols_from_rows(t);
     if (rc) return rc;
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -278,7 +281,7 @@ static int32_t check_ws(sk_ctx* c) {
 extern "C" int32_t sk_tableau_download(sk_tableau* t, uint64_t* x, uint64_t* z, uint8_t* sign) {
     if (!t || !x || !z || !sign) return SK_EARG;
     sk_ctx* c = t->ctx;
-    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    { int32_t rc0 = rows_full(t); if (rc0) return rc0; }
     const size_t nrows = 2 * t->n, words = nrows * t->W;
     int32_t rc = sk_ctx_reserve_tmp(c, words * 16 + nrows + 64);
     if (rc) return rc;
@@ -392,7 +395,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
                               uint8_t* d_out, uint8_t* d_det) {
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
-    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; }
     // reset barrier counter, wave slots (0xffffffff = none) and the stale flag (counters persist)
     MeasWs* ws = (MeasWs*)c->d_ws;
     SK_CUDA(c, cudaMemsetAsync(&ws->r0[0], 0xFF, 16, c->stream));
@@ -402,7 +405,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
     a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
-    a.prof = c->prof; a.force_columns = c->force_columns;
+    a.prof = c->prof; a.force_columns = c->force_columns; a.destab_stale = t->r_destab_stale ? 1 : 0;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -450,7 +453,7 @@ extern "C" int32_t sk_tableau_rowsum(sk_tableau* t, uint64_t h, uint64_t i) {
     if (!t) return SK_EARG;
     sk_ctx* c = t->ctx;
     if (h >= 2 * t->n || i >= 2 * t->n || h == i) SK_FAIL(c, SK_EDIM, "rowsum(%llu,%llu): rows must differ and be < 2n (SPEC:167)", (unsigned long long)h, (unsigned long long)i);
-    if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; }
+    { int32_t rc = rows_full(t); if (rc) return rc; }
     int hb = h < t->n ? int(h) : t->NS + int(h - t->n);
     int ib = i < t->n ? int(i) : t->NS + int(i - t->n);
     k_rowsum_single<<<1, 256, 0, c->stream>>>(t->m, hb, ib, c->d_err);
@@ -502,7 +505,7 @@ struct sk_program {
     uint64_t hist[12] = {0};
     sk_tableau* last_t = nullptr;
     // the whole launch sequence of a run as a CUDA graph, replayed while (tableau, seed, entry state) stay the same
-    cudaGraphExec_t gexec = nullptr; uint64_t g_tab_uid = 0, g_seed = 0; bool g_r_in = false, g_r_out = false, g_disabled = false;
+    cudaGraphExec_t gexec = nullptr; uint64_t g_tab_uid = 0, g_seed = 0; bool g_r_in = false, g_r_out = false, g_d_in = false, g_d_out = false, g_disabled = false;
     uint64_t g_launches = 0, g_layers = 0, g_transposes = 0;
 };
 
@@ -719,7 +722,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
                 launch_layer(t, p->d_gates + op.off, int(op.count));
                 mark(0);
             } else {
-                if (!t->r_valid) { int32_t rc = rows_from_cols(t); if (rc) return rc; mark(1); }
+                if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; mark(1); }
                 int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
                 if (rc) return rc;
                 mark(2);
@@ -728,13 +731,13 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         return SK_OK;
     };
     const bool want_graph = !class_ms && !p->g_disabled && !c->no_graph && p->ops.size() >= 8;
-    if (want_graph && p->gexec && p->g_tab_uid == t->uid && p->g_seed == seed && p->g_r_in == t->r_valid) {
+    if (want_graph && p->gexec && p->g_tab_uid == t->uid && p->g_seed == seed && p->g_r_in == t->r_valid && p->g_d_in == t->r_destab_stale) {
         SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));                     // replay
-        t->r_valid = p->g_r_out;
+        t->r_valid = p->g_r_out; t->r_destab_stale = p->g_d_out;
         c->cnt.kernel_launches += p->g_launches; c->cnt.layers += p->g_layers; c->cnt.transposes += p->g_transposes;
     } else if (want_graph) {
         if (p->gexec) { cudaStreamSynchronize(c->stream); cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
-        const bool r_in = t->r_valid;
+        const bool r_in = t->r_valid, d_in = t->r_destab_stale;
         const sk_counters before = c->cnt;
         cudaGraph_t graph = nullptr;
         int32_t rc = SK_OK;
@@ -742,7 +745,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
             rc = enqueue_all();
             cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
             if (!rc && e == cudaSuccess && graph && cudaGraphInstantiate(&p->gexec, graph, 0) == cudaSuccess) {
-                p->g_tab_uid = t->uid; p->g_seed = seed; p->g_r_in = r_in; p->g_r_out = t->r_valid;
+                p->g_tab_uid = t->uid; p->g_seed = seed; p->g_r_in = r_in; p->g_r_out = t->r_valid; p->g_d_in = d_in; p->g_d_out = t->r_destab_stale;
                 p->g_launches = c->cnt.kernel_launches - before.kernel_launches; p->g_layers = c->cnt.layers - before.layers;
                 p->g_transposes = c->cnt.transposes - before.transposes;
             } else { p->gexec = nullptr; p->g_disabled = true; }
@@ -752,7 +755,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         if (rc) return rc;
         if (p->gexec) SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));
         else {                              // capture is not possible here: plain stream launches
-            t->r_valid = r_in; c->cnt = before;
+            t->r_valid = r_in; t->r_destab_stale = d_in; c->cnt = before;
             rc = enqueue_all();
             if (rc) return rc;
         }
