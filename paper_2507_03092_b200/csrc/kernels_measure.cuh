@@ -472,6 +472,8 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
         if (tid == Tact - 1) ps.nt = at;
         SK_RPROF(2);
     } else if (helper && tid == kMeasThreads - 32) {
+        // lock-free hand-off through ps.steps (volatile + __threadfence_block on both sides): deliberate, and the only
+        // shared-memory access pattern compute-sanitizer's racecheck reports for this kernel
         while (published < Bn) {
             const int st = *(volatile int*)&ps.steps;
             if (st - published >= 8 || (st == Bn && st > published)) { __threadfence_block(); publish(st); }
@@ -799,7 +801,7 @@ k_measure_block(MeasArgs a) {
     __shared__ int s_wcnt[kMeasWarps];
     __shared__ u64 s_pn[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
-    __shared__ int s_cnt1, s_flag;
+    __shared__ int s_cnt1;
     __shared__ u32 s_targets[kMaxTargets];
     __shared__ PanelSmem ps;
     __shared__ PanelInfo s_info;
@@ -1013,9 +1015,8 @@ k_measure_block(MeasArgs a) {
         const int cidx = (G == 1) ? 0 : int(blockIdx.x) - 1;
         if (G == 1 || blockIdx.x != 0) {
         SK_CSTART();
-        if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + 1)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
-        __syncthreads();
-        if (!s_flag) return;
+        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+          if (__syncthreads_or(bad)) return; }
         const u32 dmode = __ldcg(&info->dmode);         // written before the first publication
         const int wpc = (W + nC - 1) / nC;
         const int wlo = min(W, cidx * wpc), whi = min(W, wlo + wpc);
@@ -1062,9 +1063,8 @@ k_measure_block(MeasArgs a) {
             // ---------- streaming D part 1: step j belongs to consumer nC-1 - j % nC (from the far end: V uses the first ones);
             // the step masks N_j are taken in D part 2, when the factorisation has finished
             for (int j = nC - 1 - cidx; j < Bn; j += nC) {
-                if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + j + 1)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
-                __syncthreads();
-                if (!s_flag) return;
+                { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + j + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+                  if (__syncthreads_or(bad)) return; }
                 if (__ldcg(&info->piv[j]) != 0xffffffffu) continue;
                 const int cnt = int(__ldcg(&info->dcnt[j]));
                 const u32* gl = a.dpart + (size_t)j * kRowSlots;
@@ -1089,9 +1089,8 @@ k_measure_block(MeasArgs a) {
             }
         } else {
         // ---------- column form: nothing is published before the end; V and D part 1 (with N_j) as one phase
-        if (tid == 0) { s_flag = wait_geq(&ws->progress, u32(pos + Bn)) ? 1 : 0; if (!s_flag) atomicOr(&ws->err, 0x80000000u); }
-        __syncthreads();
-        if (!s_flag) return;
+        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + Bn)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+          if (__syncthreads_or(bad)) return; }
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
         __syncthreads();
         const u64 randmask = s_info.randmask;
