@@ -30,13 +30,16 @@ __device__ __forceinline__ ulonglong2 operator^(ulonglong2 a, ulonglong2 b) { re
 __device__ __forceinline__ ulonglong2 operator&(ulonglong2 a, ulonglong2 b) { return make_ulonglong2(a.x & b.x, a.y & b.y); }
 __device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulonglong2(~a.x, ~a.y); }
 
-// gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb); thread v owns
-// 128-bit row-vector v of every column it visits.
+// gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb), or [block_off[b], block_off[b+1]) when the host
+// supplies chunk boundaries; thread v owns 128-bit row-vector v of every column it visits.
+// Merged layers: a launch may hold several consecutive layers provided every set of gates that share qubits (a
+// "cluster", e.g. H a ; CX a d) sits inside ONE chunk in program order -- the same thread then applies them in order to
+// its row-vector (its own store is visible to its own later load), and no other CTA touches those columns.
 __global__ void __launch_bounds__(256)
 k_layer(u64* __restrict__ cols, u64* __restrict__ sgn, const sk_gate* __restrict__ gates,
-        int ngates, int RW, int gpb) {
-    const int g0 = blockIdx.x * gpb;
-    const int g1 = min(ngates, g0 + gpb);
+        int ngates, int RW, int gpb, const u32* __restrict__ block_off) {
+    const int g0 = block_off ? int(block_off[blockIdx.x]) : blockIdx.x * gpb;
+    const int g1 = block_off ? int(block_off[blockIdx.x + 1]) : min(ngates, g0 + gpb);
     const int RW2 = RW >> 1;
     for (int v = threadIdx.x; v < RW2; v += blockDim.x) {
         ulonglong2 s = make_ulonglong2(0, 0);

@@ -307,15 +307,20 @@ static int32_t validate_gate(sk_ctx* c, const sk_gate& g, uint64_t n, size_t idx
     return SK_OK;
 }
 
-static void launch_layer(sk_tableau* t, const sk_gate* d_gates, int ngates) {
+static int layer_threads(const sk_tableau* t) { return std::min(256, std::max(32, (t->RW / 2 + 31) & ~31)); }
+static int layer_target_ctas(const sk_ctx* c, int threads) { return c->num_sms * std::max(1, 1536 / threads); }
+// one launch = one layer, or several merged layers with host-made chunk boundaries (d_boff[0..nblocks], relative to d_gates)
+static void launch_layer(sk_tableau* t, const sk_gate* d_gates, int ngates, const u32* d_boff = nullptr, int nblocks = 0, int nlayers = 1) {
     sk_ctx* c = t->ctx;
-    const int RW2 = t->RW / 2;
-    int threads = std::min(256, std::max(32, (RW2 + 31) & ~31));
-    int target_ctas = c->num_sms * std::max(1, 1536 / threads);
-    int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
-    int grid = (ngates + gpb - 1) / gpb;
-    k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb);
-    c->cnt.kernel_launches++; c->cnt.layers++;
+    const int threads = layer_threads(t);
+    if (d_boff) k_layer<<<nblocks, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, 0, d_boff);
+    else {
+        const int target_ctas = layer_target_ctas(c, threads);
+        const int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
+        const int grid = (ngates + gpb - 1) / gpb;
+        k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb, nullptr);
+    }
+    c->cnt.kernel_launches++; c->cnt.layers += (uint64_t)nlayers;
     t->r_valid = false;
 }
 
@@ -495,12 +500,13 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
 }
 
 // ------------------------------------------------------------------ engine --
-struct ProgOp { uint8_t type; uint32_t off, count; };   // 0 = layer, 1 = measurement block
+struct ProgOp { uint8_t type; uint32_t off, count; uint32_t boff = 0, nblocks = 0, nlayers = 1; };   // 0 = one k_layer launch (a layer, or merged layers with a chunk table d_boff[boff .. boff+nblocks]), 1 = measurement block
 struct sk_program {
     sk_ctx* ctx = nullptr;
     uint64_t n = 0;
     std::vector<ProgOp> ops;
     sk_gate* d_gates = nullptr; size_t ngates = 0;
+    u32* d_boff = nullptr;          // chunk tables of the merged-layer launches
     u32* d_mq = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t nmeas = 0;
     uint64_t hist[12] = {0};
     sk_tableau* last_t = nullptr;
@@ -513,7 +519,7 @@ extern "C" void sk_program_destroy(sk_program* p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
     if (p->gexec) { cudaStreamSynchronize(p->ctx->stream); cudaGraphExecDestroy(p->gexec); }
-    dfree(p->ctx, p->d_gates); dfree(p->ctx, p->d_mq); dfree(p->ctx, p->d_out); dfree(p->ctx, p->d_det);
+    dfree(p->ctx, p->d_gates); dfree(p->ctx, p->d_boff); dfree(p->ctx, p->d_mq); dfree(p->ctx, p->d_out); dfree(p->ctx, p->d_det);
     delete p;
 }
 extern "C" uint64_t sk_program_measurements(const sk_program* p) { return p ? p->nmeas : 0; }
@@ -524,9 +530,18 @@ extern "C" uint64_t sk_program_measurements(const sk_program* p) { return p ? p-
 // (gates on disjoint qubits share a layer, per-qubit order preserved => same tableau as gate by gate).
 struct Seg {
     size_t lo = 0, hi = 0; bool meas = false; size_t out = 0;   // gates [lo, hi) ; offset into the ordered gates / the qubit list
-    std::vector<uint32_t> sizes;                               // layer sizes of a Clifford run
+    std::vector<uint32_t> sizes;                               // Clifford run: gates per launch group (one layer, or merged layers)
+    std::vector<uint32_t> glayers;                             //   logical layers in each group
+    std::vector<uint32_t> gblocks;                             //   chunks in each group (0 = uniform chunks, no table)
+    std::vector<uint32_t> boff;                                //   chunk tables of the merged groups, concatenated (nblocks+1 entries each, relative to the group)
+    size_t bslot = 0;                                          //   first entry of this run's block in the chunk-table staging
     std::atomic<int> done{0};
 };
+static int target_ctas_for(const sk_ctx* c, uint64_t n) {
+    const int W = int((n + 63) / 64);
+    const int threads = std::min(256, std::max(32, (W + 31) & ~31));
+    return layer_target_ctas(c, threads);
+}
 static unsigned host_threads(size_t ngates) {
     return ngates > (1u << 16) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
 }
@@ -567,19 +582,25 @@ static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_
     }
     std::vector<Seg> segs(b.size());
     ng = nm = 0;
+    size_t nruns = 0;
     for (size_t k = 0; k < b.size(); ++k) {
         Seg& sg = segs[k];
         sg.lo = b[k].first; sg.hi = b[k].second; sg.meas = gates[sg.lo].kind == SK_M;
-        if (sg.meas) { sg.out = nm; nm += sg.hi - sg.lo; } else { sg.out = ng; ng += sg.hi - sg.lo; }
+        if (sg.meas) { sg.out = nm; nm += sg.hi - sg.lo; } else { sg.out = ng; sg.bslot = 2 * ng + 2 * nruns; ++nruns; ng += sg.hi - sg.lo; }
     }
     return segs;
 }
-struct SegScratch { std::vector<uint32_t> level, lay, start; };
-static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* ordered, uint32_t* mq, SegScratch& sc) {
+struct SegScratch { std::vector<uint32_t> level, lay, start, parent, csize, cid, corder, cstart; std::vector<sk_gate> tmp; };
+constexpr uint32_t kMaxCluster = 4;      // gates that share qubits across merged layers (e.g. H a ; CX a d) -- kept small so chunks stay balanced
+// Layering of one Clifford run + merging of consecutive layers into launch groups.  Layers l and l+1 may share a launch
+// when the gates that share qubits form small clusters: each cluster is then placed whole, in program order, inside one
+// chunk of the launch (k_layer applies a chunk's gates in order per row-vector).  Surface-code rounds: H | CX | CX | CX | CX | H
+// becomes {H,CX} {CX} {CX} {CX,H} -- 4 launches instead of 6.
+static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* ordered, uint32_t* mq, SegScratch& sc, int target_ctas) {
     const sk_gate* g = gates + sg.lo; const size_t cnt = sg.hi - sg.lo;
     if (sg.meas) { for (size_t i = 0; i < cnt; ++i) mq[sg.out + i] = g[i].q0; }
     else {
-        if (sc.level.size() < n) sc.level.assign(n, 0);
+        if (sc.level.size() < n) { sc.level.assign(n, 0); sc.parent.assign(n, 0xffffffffu); sc.csize.assign(n, 0); }
         sc.lay.resize(cnt);
         uint32_t depth = 0;
         for (size_t i = 0; i < cnt; ++i) {
@@ -592,9 +613,72 @@ static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* 
         for (size_t i = 0; i < cnt; ++i) { sc.level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) sc.level[g[i].q1] = 0; }
         sc.start.assign(depth + 1, 0);
         for (size_t i = 0; i < cnt; ++i) sc.start[sc.lay[i] + 1]++;
-        sg.sizes.resize(depth);
-        for (uint32_t d = 0; d < depth; ++d) { sg.sizes[d] = sc.start[d + 1]; sc.start[d + 1] += sc.start[d]; }
-        for (size_t i = 0; i < cnt; ++i) ordered[sg.out + sc.start[sc.lay[i]]++] = g[i];
+        std::vector<uint32_t> lsize(depth);
+        for (uint32_t d = 0; d < depth; ++d) { lsize[d] = sc.start[d + 1]; sc.start[d + 1] += sc.start[d]; }
+        sk_gate* og = ordered + sg.out;
+        for (size_t i = 0; i < cnt; ++i) og[sc.start[sc.lay[i]]++] = g[i];        // level-sorted, order within a level preserved
+        // ---- merge consecutive levels into launch groups
+        auto find = [&](uint32_t q) { while (sc.parent[q] != q) { sc.parent[q] = sc.parent[sc.parent[q]]; q = sc.parent[q]; } return q; };
+        auto touch = [&](uint32_t q) { if (sc.parent[q] == 0xffffffffu) { sc.parent[q] = q; sc.csize[q] = 0; } };
+        auto reset = [&](size_t lo, size_t hi) { for (size_t i = lo; i < hi; ++i) { sc.parent[og[i].q0] = 0xffffffffu; if (sk_is_two_qubit(og[i].kind)) sc.parent[og[i].q1] = 0xffffffffu; } };
+        auto add_gate = [&](const sk_gate& G) -> uint32_t {       // returns the gate count of the cluster the gate joins
+            touch(G.q0);
+            uint32_t r = find(G.q0);
+            if (sk_is_two_qubit(G.kind)) {
+                touch(G.q1);
+                uint32_t r1 = find(G.q1);
+                if (r1 != r) { sc.parent[r1] = r; sc.csize[r] += sc.csize[r1]; }
+            }
+            return ++sc.csize[r];
+        };
+        sg.sizes.clear(); sg.glayers.clear(); sg.gblocks.clear(); sg.boff.clear();
+        size_t lo = 0;                      // group = og[lo, hi)
+        uint32_t d = 0;
+        while (d < depth) {
+            size_t hi = lo + lsize[d];
+            uint32_t nl = 1, maxc = 0;
+            for (size_t i = lo; i < hi; ++i) maxc = std::max(maxc, add_gate(og[i]));
+            while (d + nl < depth) {        // try to take the next level in
+                const size_t nhi = hi + lsize[d + nl];
+                uint32_t m2 = maxc;
+                for (size_t i = hi; i < nhi && m2 <= kMaxCluster; ++i) m2 = std::max(m2, add_gate(og[i]));
+                if (m2 > kMaxCluster) {     // no: rebuild the union-find of the group without that level
+                    reset(lo, nhi);
+                    for (size_t i = lo; i < hi; ++i) add_gate(og[i]);
+                    break;
+                }
+                maxc = m2; hi = nhi; ++nl;
+            }
+            const uint32_t gcount = uint32_t(hi - lo);
+            uint32_t nblocks = 0;
+            if (nl > 1) {
+                // order the group's gates cluster by cluster (first appearance), keeping program order inside a cluster
+                sc.cid.resize(gcount); sc.corder.clear();
+                for (size_t i = lo; i < hi; ++i) {
+                    const uint32_t r = find(og[i].q0);
+                    if (!(sc.csize[r] & 0x80000000u)) { sc.csize[r] = 0x80000000u | uint32_t(sc.corder.size()); sc.corder.push_back(0); }
+                    const uint32_t c = sc.csize[r] & 0x7fffffffu;
+                    sc.cid[i - lo] = c; sc.corder[c]++;
+                }
+                sc.cstart.assign(sc.corder.size() + 1, 0);
+                for (size_t c = 0; c < sc.corder.size(); ++c) sc.cstart[c + 1] = sc.cstart[c] + sc.corder[c];
+                sc.tmp.resize(gcount);
+                { std::vector<uint32_t>& pos = sc.corder; for (size_t c = 0; c < pos.size(); ++c) pos[c] = sc.cstart[c];
+                  for (size_t i = 0; i < gcount; ++i) sc.tmp[pos[sc.cid[i]]++] = og[lo + i]; }
+                for (size_t i = 0; i < gcount; ++i) og[lo + i] = sc.tmp[i];
+                // chunks of about gcount / target_ctas gates, closed at cluster boundaries
+                const uint32_t gpb = std::max<uint32_t>(1, (gcount + target_ctas - 1) / target_ctas);
+                sg.boff.push_back(0);
+                uint32_t open = 0;
+                for (size_t c = 0; c + 1 < sc.cstart.size(); ++c) {
+                    if (sc.cstart[c + 1] - open >= gpb) { sg.boff.push_back(sc.cstart[c + 1]); open = sc.cstart[c + 1]; ++nblocks; }
+                }
+                if (open != gcount) { sg.boff.push_back(gcount); ++nblocks; }
+            }
+            reset(lo, hi);
+            sg.sizes.push_back(gcount); sg.glayers.push_back(nl); sg.gblocks.push_back(nblocks);
+            lo = hi; d += nl;
+        }
     }
     sg.done.store(1, std::memory_order_release);
 }
@@ -625,7 +709,7 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     sk_program* p = new sk_program();
     p->ctx = c; p->n = n;
     std::vector<sk_gate> ordered; ordered.reserve(ngates);
-    std::vector<uint32_t> mq; std::vector<uint32_t> scratch, sizes;
+    std::vector<uint32_t> mq; std::vector<uint32_t> scratch, sizes, h_boff;
     uint32_t warn = 0;
 
     auto emit_sequential = [&](size_t lo, size_t hi) {      // sim semantics on gates [lo, hi)
@@ -652,13 +736,21 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
         std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
         ordered.resize(ng); mq.resize(nm);
         std::atomic<size_t> next{0};
+        const int tctas = target_ctas_for(c, n);
         parallel_for(nthreads, nthreads, [&](size_t, size_t, unsigned) {
             SegScratch sc;
-            for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], ordered.data(), mq.data(), sc);
+            for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], ordered.data(), mq.data(), sc, tctas);
         });
         for (const Seg& sg : segs) {
-            if (sg.meas) p->ops.push_back({1, uint32_t(sg.out), uint32_t(sg.hi - sg.lo)});
-            else { size_t base = sg.out; for (uint32_t sz : sg.sizes) { p->ops.push_back({0, uint32_t(base), sz}); base += sz; } }
+            if (sg.meas) { p->ops.push_back({1, uint32_t(sg.out), uint32_t(sg.hi - sg.lo)}); continue; }
+            size_t base = sg.out, bo = 0;
+            for (size_t k = 0; k < sg.sizes.size(); ++k) {
+                ProgOp op{0, uint32_t(base), sg.sizes[k]};
+                op.nlayers = sg.glayers[k]; op.nblocks = sg.gblocks[k];
+                if (op.nblocks) { op.boff = uint32_t(h_boff.size()); h_boff.insert(h_boff.end(), sg.boff.begin() + bo, sg.boff.begin() + bo + op.nblocks + 1); bo += op.nblocks + 1; }
+                p->ops.push_back(op);
+                base += sg.sizes[k];
+            }
         }
     } else {
         if (c->q_epoch.size() < n) c->q_epoch.assign(n, 0);
@@ -692,9 +784,11 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     p->ngates = ordered.size(); p->nmeas = mq.size();
     cudaError_t e = cudaSuccess;
     if (p->ngates) { e = dmalloc(c, &p->d_gates, p->ngates * sizeof(sk_gate)); }
+    if (!e && !h_boff.empty()) e = dmalloc(c, &p->d_boff, h_boff.size() * 4);
     if (!e && p->nmeas) { e = dmalloc(c, &p->d_mq, p->nmeas * 4); if (!e) e = dmalloc(c, &p->d_out, p->nmeas); if (!e) e = dmalloc(c, &p->d_det, p->nmeas); }
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
     if (p->ngates) e = cudaMemcpyAsync(p->d_gates, ordered.data(), p->ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
+    if (!e && !h_boff.empty()) e = cudaMemcpyAsync(p->d_boff, h_boff.data(), h_boff.size() * 4, cudaMemcpyHostToDevice, c->stream);
     if (!e && p->nmeas) e = cudaMemcpyAsync(p->d_mq, mq.data(), p->nmeas * 4, cudaMemcpyHostToDevice, c->stream);
     if (!e) e = cudaStreamSynchronize(c->stream);     // host vectors die at return
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "program upload failed: %s", cudaGetErrorString(e)); }
@@ -719,7 +813,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         mark(-1);
         for (const ProgOp& op : p->ops) {
             if (op.type == 0) {
-                launch_layer(t, p->d_gates + op.off, int(op.count));
+                launch_layer(t, p->d_gates + op.off, int(op.count), op.nblocks ? p->d_boff + op.boff : nullptr, int(op.nblocks), int(op.nlayers));
                 mark(0);
             } else {
                 if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; mark(1); }
@@ -803,14 +897,17 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     if (rc) return rc;
     size_t ng = 0, nm = 0;
     std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
-    rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + 64);
+    const size_t nboff = 2 * ng + 2 * segs.size() + 2;       // chunk tables: a run of k gates needs at most 2k + 2 entries
+    rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + nboff * 4 + 64);
     if (rc) return rc;
     sk_gate* h_gates = (sk_gate*)c->h_pin;
     uint32_t* h_mq = (uint32_t*)((char*)c->h_pin + ((ng * sizeof(sk_gate) + 15) & ~size_t(15)));
+    uint32_t* h_boff = h_mq + ((nm + 3) & ~size_t(3));
+    const int tctas = target_ctas_for(c, n);
     sk_program* p = new sk_program();
     p->ctx = c; p->n = n; p->ngates = ng; p->nmeas = nm;
     cudaError_t e = cudaSuccess;
-    if (ng) e = dmalloc(c, &p->d_gates, ng * sizeof(sk_gate));
+    if (ng) { e = dmalloc(c, &p->d_gates, ng * sizeof(sk_gate)); if (!e) e = dmalloc(c, &p->d_boff, nboff * 4); }
     if (!e && nm) { e = dmalloc(c, &p->d_mq, nm * 4); if (!e) e = dmalloc(c, &p->d_out, nm); if (!e) e = dmalloc(c, &p->d_det, nm); }
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
     sk_tableau* t = nullptr;
@@ -818,13 +915,13 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     if (rc) { sk_program_destroy(p); return rc; }
     std::atomic<size_t> next{0};
     std::vector<std::thread> workers;
-    auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc); };
+    auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc, tctas); };
     for (unsigned k = 1; k < nthreads; ++k) workers.emplace_back(work);
     SegScratch mine;
     for (size_t si = 0; si < segs.size() && !rc; ++si) {
         Seg& sg = segs[si];
         while (!sg.done.load(std::memory_order_acquire)) {
-            if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine); }
+            if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine, tctas); }
             else std::this_thread::yield();
         }
         const size_t cnt = sg.hi - sg.lo;
@@ -835,8 +932,18 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
         } else {
             e = cudaMemcpyAsync(p->d_gates + sg.out, h_gates + sg.out, cnt * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
             if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
-            size_t base = sg.out;
-            for (uint32_t sz : sg.sizes) { launch_layer(t, p->d_gates + base, int(sz)); base += sz; }
+            if (!sg.boff.empty()) {
+                std::memcpy(h_boff + sg.bslot, sg.boff.data(), sg.boff.size() * 4);
+                e = cudaMemcpyAsync(p->d_boff + sg.bslot, h_boff + sg.bslot, sg.boff.size() * 4, cudaMemcpyHostToDevice, c->stream);
+                if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
+            }
+            size_t base = sg.out, bo = 0;
+            for (size_t k = 0; k < sg.sizes.size(); ++k) {
+                const uint32_t nb = sg.gblocks[k];
+                launch_layer(t, p->d_gates + base, int(sg.sizes[k]), nb ? p->d_boff + sg.bslot + bo : nullptr, int(nb), int(sg.glayers[k]));
+                if (nb) bo += nb + 1;
+                base += sg.sizes[k];
+            }
         }
     }
     next = segs.size();

@@ -32,7 +32,7 @@ static void dm_launch_layer(sk_ctx* c, const DMat& m, const sk_gate* d_gates, in
     int target_ctas = c->num_sms * std::max(1, 1536 / threads);
     int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
     int grid = (ngates + gpb - 1) / gpb;
-    k_layer<<<grid, threads, 0, c->stream>>>(m.cols, m.sgn, d_gates, ngates, m.RW, gpb);
+    k_layer<<<grid, threads, 0, c->stream>>>(m.cols, m.sgn, d_gates, ngates, m.RW, gpb, nullptr);
     c->cnt.kernel_launches++; c->cnt.layers++;
 }
 template <class... A> static void launch_push(sk_ctx* c, int W, int nrows, A... args) {
