@@ -513,26 +513,6 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 #undef SK_RPROF
 }
 
-// XOR of the frozen masks m_l[w] over the steps l in `bits` (column stride CS).  Few steps: chase the
-// bits; many (a "hot" word: the same rows are targets again and again): linear sweep, 8 loads in flight.
-__device__ __forceinline__ u64 xor_masks(const u64* sp, int CS, int w, u64 bits, int j) {
-    u64 acc = 0;
-    if (__popcll(bits) <= 3) {
-        while (bits) { const int l = __ffsll((long long)bits) - 1; bits &= bits - 1; acc ^= sp[(size_t)l * CS + w]; }
-    } else {
-        const u64* col = sp + w;
-        for (int l0 = 0; l0 < j; l0 += 8, col += 8 * (size_t)CS, bits >>= 8) {
-            if ((bits & 0xffull) == 0) continue;
-            u64 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = (l0 + u < j) ? col[(size_t)u * CS] : 0ull;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc ^= ((bits >> u) & 1ull) ? v[u] : 0ull;
-        }
-    }
-    return acc;
-}
-
 // F: symbolic factorisation of one panel by CTA 0 (see the file header).
 // Shared-memory panel: column j = words [j*CS, j*CS + RW] with CS = RW + 2; word RW holds the VIRTUAL rows:
 // when random step l overwrites destabilizer p_l + n with the old pivot row, the old row-bit is retired and
