@@ -397,7 +397,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
             if (mymin == wm && (wm != kInf || lane == 0)) { ps.wmin[j & 1][warp] = wm; ps.wbp[j & 1][warp] = cb; ps.wmp[j & 1][warp] = cm; }   // row-bits are unique: one writer
             named_bar(1, Tact);
             if (tid == 0) {                                    // all warps' writes of the steps before j precede this barrier
-                if (helper) { __threadfence_block(); *(volatile int*)&ps.steps = j; }
+                if (helper) { if ((j & 7) == 0) { __threadfence_block(); *(volatile int*)&ps.steps = j; } }     // the helper publishes in groups of 8
                 else if (j - published >= 8) publish(j);
             }
             // minimum over the warps and the warp that holds it (row-bits are unique)

@@ -272,11 +272,22 @@ def test_panel_factorisation_variants(sk, orc, columns, width):
             else: os.environ[k] = v
 
 
-def test_dense_tableau_falls_back_to_column_form(sk, ctx, orc):
-    """n = 4096 random layered circuit: more than 1984 rows carry an x in a panel's columns, so the
-    kernel itself switches to the column-form factorisation."""
-    c = sk.random_layered_circuit(4096, 3)
-    t, out, det, _ = ctx.sim(c, 17)
-    o = orc.Tableau(c.n); oo, od, rc = o.sim(c.gates, 17, workers=8)
+def test_dense_tableau_falls_back_to_column_form(sk, orc):
+    """A deep random Clifford circuit on 2304 qubits: nearly every row has an x in any 64 measured columns, i.e. more
+    than the 1984 active rows the register-resident factorisation holds, so the kernel itself switches to the
+    column-form (shared-memory, TMA-staged) factorisation -- checked through the panel counters."""
+    n = 2304
+    rng = np.random.default_rng(31)
+    gates = rand_gates(rng, n, 10 * n, kinds=(H, S, CX, CX))
+    gates += [(M, int(q), 0) for q in rng.integers(0, n, 150)]
+    circ = sk.Circuit(n, gates)
+    c2 = sk.Context(0)
+    t, out, det, _ = c2.sim(circ, 17)
+    o = orc.Tableau(n); oo, od, rc = o.sim(circ.gates, 17, workers=8)
     assert rc == 0 and (out == oo).all() and (det == od).all()
     assert_same_tableau(t, o)
+    dc, oc = c2.counters(), o.counters()
+    for k in ("n_rand", "n_det", "k_rand", "k_det"):
+        assert dc[k] == oc[k], k
+    assert dc["k_rand"] > 1984 * 10          # dense indeed: thousands of rows multiplied per random measurement
+    t.close(); c2.close()
