@@ -58,7 +58,7 @@ struct PanelInfo {      // global scratch describing the current panel (written 
     u64 dN[kPanelMax];     // deterministic step j: pivot values to multiply (parity of partner histories; written by D part 1)
     u64 dZ[kPanelMax];     // deterministic step j: earlier steps whose +-Z row is a partner
     u32 piv[kPanelMax];    // pivot stabilizer row-bit, 0xffffffff = deterministic step
-    u32 eph[kPanelMax];    // V: sum over words of the g contributions of P_l' (atomic, mod 4 matters)
+    u32 eph[2][kPanelMax]; // V: sum over words of the g contributions of P_l' (atomic, mod 4 matters); double-buffered by panel parity
     int dete[kPanelMax];   // D part 1: phase exponent of the panel-start partner product
     u64 randmask;          // steps that are random
     u64 osign;             // panel-start sign bits of the pivot rows
@@ -109,13 +109,17 @@ struct MeasArgs {
     u64* pivbuf;        // [B] rows in R layout: P_l' x words then z words
     u64* detacc;        // [B] rows in R layout: panel-start partner products of the deterministic steps
     PanelInfo* info;
-    u32* tlist;         // [64*RW] touched rows
-    u64* tM;            // [64*RW] their step masks
+    u32* tlist;         // [2][tcap] touched rows            } double-buffered by panel parity: the apply phase of panel k
+    u64* tM;            // [2][tcap] their step masks        } retires the entries of panel k-1 while panel k+1 is prepared
+    u32 tcap;           // entries per buffer
     u32* alist_h;       // [64*RW] G: active rows (row-bits) of the panel, row form
     u64* alist_b;       // [64*RW]    and their bits in the panel columns
     u32* dpart;         // [B][kRowSlots] row form: partner stabilizers of the deterministic steps
-    u64* rowM;          // [64*RW] step mask by row-bit (zero for rows the current panel does not touch)
+    u64* rowM;          // [2][64*RW] step mask by row-bit (zero for rows the panel does not touch), double-buffered likewise
     int prof;           // device-side phase timers (SK_DEBUG_PROF)
+    u64* tbits;         // [RW] row-bits listed in tlist of the panel just factorised (the folded gather skips them)
+    int fold;           // gather of the next panel folded into the apply phase (SK_NO_FOLD=1 disables)
+    int row_cap;        // most active rows the row-form factorisation takes (kRowCap; SK_ROW_CAP lowers it for tests)
     int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
 };
@@ -343,7 +347,7 @@ struct PanelSmem {
 //   deterministic: partners = destabilizer rows with bit j (virtual ones stand for the +-Z rows of earlier steps)
 // which yields the same schedule (pivots, histories, step masks, partner sets) as the column form below.
 template <int KT>       // slots per thread actually used (1, 2 or 4): fewer slots = fewer dependent instructions per step
-__device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A) {
+__device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
     const int NS = a.NS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr u32 kInf = 0xffffffffu;
@@ -364,7 +368,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     auto publish = [&](int upto) {        // steps [published, upto)
         PanelInfo* info = a.info;
         for (int jj = published; jj < upto; ++jj) { info->piv[jj] = ps.piv[jj]; info->hist[jj] = ps.hist[jj]; info->dcnt[jj] = ps.dcnt[jj]; info->dZ[jj] = ps.dZ[jj]; }
-        st_release(&a.ws->progress, u32(pos + upto));
+        st_release(&a.ws->progress, pbase + u32(upto));
         published = upto;
     };
     if (tid < Tact) {
@@ -425,7 +429,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
             // pivot -> +-Z_q (history kept for earlier deterministic steps); others with bit j: multiplied by the pivot row
             if (hit) {
 #define SK_UPD(k, hh, bb, mm) if ((hit >> k) & 1u) { \
-                    if (hh == p) { __stcg(a.rowM + p, mm); hh = kInf; bb = 0; } \
+                    if (hh == p) { __stcg(rowM + p, mm); hh = kInf; bb = 0; } \
                     else if (hh != pd) { bb ^= bp; mm |= 1ull << j; ++ntarget; } }
                 SK_SLOTS(SK_UPD)
 #undef SK_UPD
@@ -463,8 +467,8 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
         for (int t = 0; t < warp; ++t) at += ps.wcnt[t];
 #define SK_EMIT(k, hh, bb, mm) if (k < Kact && hh != kInf && (mm || (hh >> 24))) { \
                 const u32 row = hh & 0xffffffu; \
-                __stcg(a.tlist + at, row); __stcg(a.tM + at, mm); \
-                if (!(hh >> 24) && row < (u32)NS) __stcg(a.rowM + row, mm); \
+                __stcg(tlist + at, row); __stcg(tM + at, mm); atomicOr(a.tbits + (row >> 6), 1ull << (row & 63)); \
+                if (!(hh >> 24) && row < (u32)NS) __stcg(rowM + row, mm); \
                 ++at; }
         SK_SLOTS(SK_EMIT)
 #undef SK_EMIT
@@ -489,7 +493,8 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     if (tid < Bn && ((randmask >> tid) & 1ull)) {
         ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
         const u32 at = ntr + (u32)__popcll(randmask & ((1ull << tid) - 1ull));
-        __stcg(a.tlist + at, ps.piv[tid]); __stcg(a.tM + at, 0ull);          // the pivot itself: -> +-Z_q
+        __stcg(tlist + at, ps.piv[tid]); __stcg(tM + at, 0ull);          // the pivot itself: -> +-Z_q
+        atomicOr(a.tbits + (ps.piv[tid] >> 6), 1ull << (ps.piv[tid] & 63));
     }
     if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
         const u32 pl = ps.piv[tid];
@@ -522,7 +527,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 //   cur_j = (orig_j ^ XOR_{l in S_j} m_l) & ~retired,   S_j = earlier random steps whose pivot row has an x
 // in column j (S_j bit l = pw_l bit j; the virtual word starts as S_j itself), sparse in the word index
 // through nzm.  m_l = column l at step l minus the pivot and its partner = the rows step l multiplies.
-__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, u32* s_rows, u64* mbar, u32& tma_parity, int pos, int Bn) {
+__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, u32* s_rows, u64* mbar, u32& tma_parity, int pos, int Bn, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
     const int RW = a.m.RW, W = a.m.W, NS = a.NS;
     const int CS = RW + 2, RV = RW + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -693,7 +698,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
             const int b = __ffsll((long long)tw) - 1; tw &= tw - 1;
             const u32 h = u32(w * 64 + b);
             if (ti < (u32)kMaxTargets) s_rows[ti] = h;
-            __stcg(a.tlist + ti, h);
+            __stcg(tlist + ti, h); atomicOr(a.tbits + (h >> 6), 1ull << (h & 63));
             ++ti;
         }
     }
@@ -719,7 +724,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     const u32 ntr = ps.nt;
     if (a.prof && tid == 0) { a.ws->cprof[4] += ntr; a.ws->cprof[12] += ps.krand; }
     for (u32 i = tid; i < ntr; i += kMeasThreads) {
-        const u32 h = (i < (u32)kMaxTargets) ? s_rows[i] : __ldcg(a.tlist + i);
+        const u32 h = (i < (u32)kMaxTargets) ? s_rows[i] : __ldcg(tlist + i);
         const u64* col = sp + (h >> 6);
         const int sh = int(h & 63);
         u64 M = 0, bits = randmask;
@@ -731,7 +736,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
 #pragma unroll
             for (int u = 0; u < 8; ++u) M |= ((v[u] >> sh) & (bits >> u) & 1ull) << (l0 + u);
         }
-        __stcg(a.tM + i, M); __stcg(a.rowM + h, M);
+        __stcg(tM + i, M); __stcg(rowM + h, M);
     }
     SK_TPROF(14);
     // the two rows every random step l overwrites: pivot p_l (-> +-Z_q) and partner p_l + n (-> P_l', then the steps
@@ -750,9 +755,10 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
         }
         Mv &= randmask & ((l < 63) ? ~((2ull << l) - 1ull) : 0ull);
         const u32 at = ntr + 2u * (u32)__popcll(randmask & ((1ull << l) - 1ull));
-        __stcg(a.tlist + at, pl); __stcg(a.tM + at, 0ull);
-        __stcg(a.rowM + pl, ps.hist[l]);     // a deterministic step before l may still have row p_l as a partner
-        __stcg(a.tlist + at + 1, u32(NS) + pl); __stcg(a.tM + at + 1, Mv);
+        __stcg(tlist + at, pl); __stcg(tM + at, 0ull);
+        __stcg(rowM + pl, ps.hist[l]);     // a deterministic step before l may still have row p_l as a partner
+        __stcg(tlist + at + 1, u32(NS) + pl); __stcg(tM + at + 1, Mv);
+        atomicOr(a.tbits + (pl >> 6), 1ull << (pl & 63)); atomicOr(a.tbits + ((u32(NS) + pl) >> 6), 1ull << ((u32(NS) + pl) & 63));
     }
     PanelInfo* info = a.info;
     if (tid < kPanelMax) {
@@ -768,7 +774,7 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
     SK_TPROF(15);
 #undef SK_TPROF
     __syncthreads();
-    if (tid == 0) { __threadfence(); st_release(&a.ws->progress, u32(pos + Bn)); }      // column form: everything is published at the end
+    if (tid == 0) { __threadfence(); st_release(&a.ws->progress, pbase + u32(Bn)); }      // column form: everything is published at the end
     SK_FPROF(3);
 #undef SK_FPROF
 }
@@ -785,7 +791,7 @@ k_measure_block(MeasArgs a) {
     __shared__ u32 s_targets[kMaxTargets];
     __shared__ PanelSmem ps;
     __shared__ PanelInfo s_info;
-    __shared__ u32 s_q[kPanelMax];
+    __shared__ u32 s_q[kPanelMax], s_q2[kPanelMax];
     __shared__ __align__(8) u64 s_mbar;
     const int RW = a.m.RW, Wp = a.m.Wp, W = a.m.W;
     MeasSmem sm;
@@ -921,17 +927,22 @@ k_measure_block(MeasArgs a) {
     PanelInfo* info = a.info;
     const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs
     u32 prev_nt = 0;
+    u32 pbase = 0;                      // progress counter value at the start of this panel attempt (monotone across attempts)
+    int kpar = 0;                       // parity of the panel being processed: selects tlist / tM / rowM / eph buffers
+    bool have_list = false;             // the active-row list of this panel was already built by the previous apply phase
+    const size_t rowcap = (size_t)64 * RW;
     u64 t_cta = 0;
 #define SK_CSTART() do { if (a.prof && tid == 0) t_cta = gtime(); } while (0)
 #define SK_CPROF(k) do { if (a.prof && tid == 0 && blockIdx.x < 160) ws->ctaphase[blockIdx.x * 4 + k] += gtime() - t_cta; } while (0)
     while (pos < a.count) {
         const int Bn = min(B, a.count - pos);
         SK_CSTART();
+        u64* rowM = a.rowM + (size_t)kpar * rowcap;
+        u32* tlist = a.tlist + (size_t)kpar * a.tcap;
+        u64* tM = a.tM + (size_t)kpar * a.tcap;
         if (tid < kPanelMax) s_q[tid] = (tid < Bn) ? a.qubits[pos + tid] : 0xffffffffu;
-        // housekeeping for the panel that just finished: its step-mask entries (D part 2 was their last reader) and phase sums
-        for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(a.rowM + __ldcg(a.tlist + i), 0ull);
-        if (blockIdx.x == 0 && tid < kPanelMax) info->eph[tid] = 0;
         __syncthreads();
+        if (!have_list) {
         // ---- G: gather the panel columns from the R form: warp per group of 32 row-bits
         {
             u32* pan32 = reinterpret_cast<u32*>(a.pan);
@@ -977,17 +988,23 @@ k_measure_block(MeasArgs a) {
         SK_PROF(2); SK_CPROF(0);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7); SK_CSTART();
+        }   // standalone gather
         // ---- F: symbolic factorisation (CTA 0)
         if (blockIdx.x == 0) {
             const u32 A = __ldcg(&info->acount);
+            for (int w = tid; w < RW; w += kMeasThreads) a.tbits[w] = 0;
             __syncthreads();
             if (tid == 0) { info->acount = 0; if (a.prof) { ws->cprof[8] += A; if (A > ws->cprof[9]) ws->cprof[9] = A; } }
-            if (A <= (u32)kRowCap && !a.force_columns) {
-                if (A + kPanelMax <= (u32)kRowThreads) panel_factorise_rows<1>(a, ps, pos, Bn, A);
-                else if (A + kPanelMax <= 2u * kRowThreads) panel_factorise_rows<2>(a, ps, pos, Bn, A);
-                else panel_factorise_rows<4>(a, ps, pos, Bn, A);
+            if (A <= (u32)a.row_cap && !a.force_columns) {
+                if (A + kPanelMax <= (u32)kRowThreads) panel_factorise_rows<1>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
+                else if (A + kPanelMax <= 2u * kRowThreads) panel_factorise_rows<2>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
+                else panel_factorise_rows<4>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
             }
-            else panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn);
+            else if (!have_list) panel_factorise(a, smem, ps, s_targets, &s_mbar, tma_parity, pos, Bn, rowM, tlist, tM, pbase);
+            else {
+                // too many active rows for the row form, and the folded gather made no bit columns: ask for a full gather
+                if (tid == 0) { info->dmode = 2; __threadfence(); st_release(&ws->progress, pbase + u32(Bn)); }
+            }
         }
         SK_PROF(3); SK_CPROF(1);
         // ---- consumers (every CTA but 0, which is busy factorising): V pivot values + D part 1, fed step by step
@@ -995,7 +1012,7 @@ k_measure_block(MeasArgs a) {
         const int cidx = (G == 1) ? 0 : int(blockIdx.x) - 1;
         if (G == 1 || blockIdx.x != 0) {
         SK_CSTART();
-        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + 1u) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
           if (__syncthreads_or(bad)) return; }
         const u32 dmode = __ldcg(&info->dmode);         // written before the first publication
         const int wpc = (W + nC - 1) / nC;
@@ -1009,7 +1026,7 @@ k_measure_block(MeasArgs a) {
                 const int nvt = 32 * nvw;
                 for (int done = 0; done < Bn;) {
                     const int target = min(Bn, done + 8);
-                    if (!wait_geq(&ws->progress, u32(pos + target))) { atomicOr(&ws->err, 0x80000000u); break; }
+                    if (!wait_geq(&ws->progress, pbase + u32(target))) { atomicOr(&ws->err, 0x80000000u); break; }
                     for (int t = tid; t < nw; t += nvt) {
                         const int w = wlo + t;
                         u32 pk[8]; u64 hk[8], lx[8], lz[8];
@@ -1033,7 +1050,7 @@ k_measure_block(MeasArgs a) {
                             }
                             vs[(size_t)(2 * k) * wpc + t] = ax; vs[(size_t)(2 * k + 1) * wpc + t] = az;
                             __stcg(a.pivbuf + (size_t)(2 * k) * Wp + w, ax); __stcg(a.pivbuf + (size_t)(2 * k + 1) * Wp + w, az);
-                            if (e & 3) atomicAdd(&info->eph[k], (u32)(e & 3));
+                            if (e & 3) atomicAdd(&info->eph[kpar][k], (u32)(e & 3));
                         }
                     }
                     done = target;
@@ -1043,7 +1060,7 @@ k_measure_block(MeasArgs a) {
             // ---------- streaming D part 1: step j belongs to consumer nC-1 - j % nC (from the far end: V uses the first ones);
             // the step masks N_j are taken in D part 2, when the factorisation has finished
             for (int j = nC - 1 - cidx; j < Bn; j += nC) {
-                { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + j + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+                { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + u32(j + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
                   if (__syncthreads_or(bad)) return; }
                 if (__ldcg(&info->piv[j]) != 0xffffffffu) continue;
                 const int cnt = int(__ldcg(&info->dcnt[j]));
@@ -1067,9 +1084,9 @@ k_measure_block(MeasArgs a) {
                 }
                 __syncthreads();
             }
-        } else {
+        } else if (dmode == 0) {
         // ---------- column form: nothing is published before the end; V and D part 1 (with N_j) as one phase
-        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, u32(pos + Bn)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+        { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + u32(Bn)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
           if (__syncthreads_or(bad)) return; }
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
         __syncthreads();
@@ -1117,7 +1134,7 @@ k_measure_block(MeasArgs a) {
                         }
                         vs[(size_t)(2 * k) * wpc + t] = ax; vs[(size_t)(2 * k + 1) * wpc + t] = az;
                         __stcg(a.pivbuf + (size_t)(2 * k) * Wp + w, ax); __stcg(a.pivbuf + (size_t)(2 * k + 1) * Wp + w, az);
-                        if (e & 3) atomicAdd(&info->eph[k], (u32)(e & 3));
+                        if (e & 3) atomicAdd(&info->eph[kpar][k], (u32)(e & 3));
                     }
                 }
             } else {
@@ -1164,7 +1181,7 @@ k_measure_block(MeasArgs a) {
                     for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[warp][i]));
                     e = warp_sum(e) & 3;
                     u64 N = 0;
-                    for (int i = lane; i < npart; i += 32) N ^= ldcg(a.rowM + s_wlist[warp][i]);
+                    for (int i = lane; i < npart; i += 32) N ^= ldcg(rowM + s_wlist[warp][i]);
                     N = warp_xor64(N) & randmask & ((1ull << j) - 1ull);
                     u64* dx = a.detacc + (size_t)(2 * j) * Wp;
                     for (int w = lane; w < W; w += 32) { __stcg(dx + w, acc_x[w]); __stcg(dx + Wp + w, acc_z[w]); }
@@ -1177,7 +1194,7 @@ k_measure_block(MeasArgs a) {
                 const int j = s_heavy[h];
                 int total;
                 u64 N = 0;
-                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total, a.rowM, &N,
+                const int e = cta_det(a, sm, a.pan + (size_t)j * RW + W, a.detacc + (size_t)(2 * j) * Wp, &total, rowM, &N,
                                       s_info.dmode ? a.dpart + (size_t)j * kRowSlots : nullptr, int(s_info.dcnt[j]));
                 if (tid == 0) { info->dete[j] = e; info->dN[j] = N & randmask & ((1ull << j) - 1ull); }
             }
@@ -1192,15 +1209,28 @@ k_measure_block(MeasArgs a) {
         // (triangular GF(2) recurrence; every CTA solves it itself)
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
         __syncthreads();
+        if (s_info.dmode == 2) { have_list = false; pbase += u32(Bn); continue; }      // regather: same panel again, with the full (row + column) gather
         const u64 randmask = s_info.randmask;
         const u64 allmask = (Bn < 64) ? ((1ull << Bn) - 1ull) : ~0ull;
         const u64 detmask = ~randmask & allmask;
+        // The gather of the NEXT panel is folded into this phase when the row form is in use: touched rows emit their new
+        // bits as they are written, the untouched ones (not in tbits) are read here -- no separate phase, no grid barrier.
+        const int Bn2 = min(B, a.count - pos - Bn);
+        const bool do_fold = a.fold && s_info.dmode == 1 && Bn2 > 0;
+        if (tid < kPanelMax) s_q2[tid] = (do_fold && tid < Bn2) ? a.qubits[pos + Bn + tid] : 0xffffffffu;
+        // housekeeping: retire the previous panel's step-mask entries (its D part 2 was their last reader) and phase sums
+        {
+            const u32* ptl = a.tlist + (size_t)(kpar ^ 1) * a.tcap;
+            u64* prm = a.rowM + (size_t)(kpar ^ 1) * rowcap;
+            for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(prm + __ldcg(ptl + i), 0ull);
+            if (blockIdx.x == 0 && tid < kPanelMax) info->eph[kpar ^ 1][tid] = 0;
+        }
         if (tid == 0) {
             u64 psign = 0; u32 odd = 0;
             u64 bits = randmask;
             while (bits) {
                 const int k = __ffsll((long long)bits) - 1; bits &= bits - 1;
-                const u32 ek = s_info.eph[k] + 2u * (u32)((s_info.osign >> k) & 1ull) + 2u * (u32)__popcll(s_info.hist[k] & psign);
+                const u32 ek = s_info.eph[kpar][k] + 2u * (u32)((s_info.osign >> k) & 1ull) + 2u * (u32)__popcll(s_info.hist[k] & psign);
                 odd |= ek & 1u;
                 psign |= (u64)((ek >> 1) & 1u) << k;
             }
@@ -1213,6 +1243,17 @@ k_measure_block(MeasArgs a) {
         {
             const int nd = __popcll(detmask);
             const int nt = int(s_info.nt);
+            // next panel's bits of a row whose new x words sit in this warp's accumulator
+            auto emit_next = [&](u32 h) {
+                if (!do_fold) return;
+                __syncwarp();
+                const u32 q0 = s_q2[lane], q1 = s_q2[lane + 32];
+                const u32 b0 = (q0 != 0xffffffffu) ? u32((acc_x[q0 >> 6] >> (q0 & 63)) & 1ull) : 0u;
+                const u32 b1 = (q1 != 0xffffffffu) ? u32((acc_x[q1 >> 6] >> (q1 & 63)) & 1ull) : 0u;
+                const u64 rb = (u64)__ballot_sync(0xffffffffu, b0) | ((u64)__ballot_sync(0xffffffffu, b1) << 32);
+                if (rb && lane == 0) { const u32 at = atomicAdd(&info->acount, 1u); __stcg(a.alist_h + at, h); __stcg(a.alist_b + at, rb); }
+                __syncwarp();
+            };
             for (int it = gwi; it < nd + nt; it += GW) {
                 if (it < nd) {
                     // deterministic step: j = it-th set bit of detmask
@@ -1225,7 +1266,7 @@ k_measure_block(MeasArgs a) {
                         N = 0;
                         const int cnt = int(s_info.dcnt[j]);
                         const u32* gl = a.dpart + (size_t)j * kRowSlots;
-                        for (int i = lane; i < cnt; i += 32) N ^= ldcg(a.rowM + __ldcg(gl + i));
+                        for (int i = lane; i < cnt; i += 32) N ^= ldcg(rowM + __ldcg(gl + i));
                         N = warp_xor64(N) & randmask & ((1ull << j) - 1ull);
                     } else N = ldcg(&info->dN[j]);
                     const u64 Z = s_info.dZ[j];
@@ -1253,8 +1294,8 @@ k_measure_block(MeasArgs a) {
                     __syncwarp();
                 } else {
                     const int i = it - nd;
-                    const u32 h = __ldcg(a.tlist + i);
-                    u64 M = ldcg(a.tM + i);
+                    const u32 h = __ldcg(tlist + i);
+                    u64 M = ldcg(tM + i);
                     // is h a pivot of this panel, or the destabilizer partner of one?
                     int kp = -1, ko = -1;
                     {
@@ -1282,7 +1323,7 @@ k_measure_block(MeasArgs a) {
                     } else {
                         for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(tx + w); acc_z[w] = ldcg(tx + Wp + w); }
                         e = (lane == 0) ? 2 * int((ldcg(sg) >> (h & 63)) & 1ull) : 0;
-                        if (M == 0) continue;
+                        if (M == 0) { emit_next(h); continue; }
                     }
                     int cnt = 0;
                     { u64 b = M; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
@@ -1295,7 +1336,42 @@ k_measure_block(MeasArgs a) {
                         if (e & 1) atomicOr(&ws->err, 1u);
                         if (e >> 1) atomicOr(sg, hb); else atomicAnd(sg, ~hb);
                     }
-                    __syncwarp();
+                    emit_next(h);
+                }
+            }
+            // folded gather, untouched rows: a lane per row, rows listed in tbits are skipped (their warps emitted them above)
+            if (do_fold) {
+                for (int g = gwi; g < 2 * RW; g += GW) {
+                    const int h = 32 * g + lane;
+                    const bool skip = (ldcg(a.tbits + (h >> 6)) >> (h & 63)) & 1ull;
+                    const u64* rx = a.m.rows + (size_t)(2 * h) * Wp;
+                    u64 rb = 0;
+                    int lastw = -1; u64 lastv = 0;
+                    for (int j0 = 0; j0 < Bn2; j0 += 8) {
+                        u32 qq[8]; u64 v[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) qq[t] = s_q2[j0 + t];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const int wq = int(qq[t] >> 6), prev = t ? int(qq[t - 1] >> 6) : lastw;
+                            v[t] = (!skip && qq[t] != 0xffffffffu && wq != prev) ? ldcg(rx + wq) : 0ull;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            if (qq[t] == 0xffffffffu) continue;
+                            const int wq = int(qq[t] >> 6);
+                            if (wq == lastw) v[t] = lastv; else { lastv = v[t]; lastw = wq; }
+                            rb |= ((v[t] >> (qq[t] & 63)) & 1ull) << (j0 + t);
+                        }
+                    }
+                    if (skip) rb = 0;
+                    const u32 am = __ballot_sync(0xffffffffu, rb != 0);
+                    if (am) {
+                        u32 base = 0;
+                        if (lane == 0) base = atomicAdd(&info->acount, (u32)__popc(am));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (rb) { const u32 at = base + __popc(am & ((1u << lane) - 1u)); __stcg(a.alist_h + at, (u32)h); __stcg(a.alist_b + at, rb); }
+                    }
                 }
             }
         }
@@ -1303,10 +1379,17 @@ k_measure_block(MeasArgs a) {
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(7);
         prev_nt = s_info.nt;
+        have_list = do_fold;
+        kpar ^= 1;
+        pbase += u32(Bn);
         pos += Bn;
     }
-    for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(a.rowM + __ldcg(a.tlist + i), 0ull);
-    if (blockIdx.x == 0 && tid < kPanelMax) info->eph[tid] = 0;
+    {   // the last panel's entries (buffers of parity kpar ^ 1 after the final toggle)
+        const u32* ptl = a.tlist + (size_t)(kpar ^ 1) * a.tcap;
+        u64* prm = a.rowM + (size_t)(kpar ^ 1) * rowcap;
+        for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(prm + __ldcg(ptl + i), 0ull);
+        if (blockIdx.x == 0 && tid < kPanelMax) { info->eph[0][tid] = 0; info->eph[1][tid] = 0; }
+    }
     if (blockIdx.x == 0 && tid == 0) ws->c_stale = 1u;
 }
 

@@ -38,6 +38,8 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (getenv("SK_DEBUG_PROF")) c->prof = 1;
     if (const char* e = getenv("SK_NO_GRAPH")) c->no_graph = atoi(e);
+    if (const char* e = getenv("SK_NO_FOLD")) c->no_fold = atoi(e);
+    if (const char* e = getenv("SK_ROW_CAP")) c->row_cap = atoi(e);
     if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
@@ -114,7 +116,7 @@ struct sk_tableau {
     // panel-mode scratch (kernels_measure.cuh)
     uint64_t uid = 0;               // distinguishes tableaux that reuse a host address (graph cache key)
     int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
-    u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr; u32* d_alist_h = nullptr; u64* d_alist_b = nullptr; u32* d_dpart = nullptr;
+    u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr; u64* d_tbits = nullptr; u32 tcap = 0; u32* d_alist_h = nullptr; u64* d_alist_b = nullptr; u32* d_dpart = nullptr;
 };
 
 // x and z halves in one launch (grid.z = 2); `flag` != nullptr makes the launch conditional on *flag
@@ -156,7 +158,8 @@ static int32_t tableau_identity(sk_tableau* t) {
     SK_CUDA(c, cudaMemsetAsync(t->m.cols, 0, t->cols_bytes, c->stream));
     SK_CUDA(c, cudaMemsetAsync(t->m.rows, 0, t->rows_bytes, c->stream));
     SK_CUDA(c, cudaMemsetAsync(t->m.sgn, 0, t->sgn_bytes, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(t->d_rowM, 0, (size_t)64 * t->RW * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->d_rowM, 0, (size_t)2 * 64 * t->RW * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(t->d_tbits, 0, (size_t)t->RW * 8, c->stream));
     k_identity<<<(unsigned)((t->n + 255) / 256), 256, 0, c->stream>>>(t->m.cols, t->m.rows, int(t->n), t->RW, t->Wp, t->NS);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
@@ -209,9 +212,11 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e6 = dmalloc(c, &t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
     cudaError_t e7 = dmalloc(c, &t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
     cudaError_t e8 = dmalloc(c, &t->d_info, sizeof(PanelInfo));
-    cudaError_t e9 = dmalloc(c, &t->d_tlist, ((size_t)64 * t->RW + 2 * kPanelMax) * 4);
-    cudaError_t e10 = dmalloc(c, &t->d_tM, ((size_t)64 * t->RW + 2 * kPanelMax) * 8);
-    cudaError_t e11 = dmalloc(c, &t->d_rowM, (size_t)64 * t->RW * 8);
+    t->tcap = u32(64 * t->RW + 2 * kPanelMax);
+    cudaError_t e9 = dmalloc(c, &t->d_tlist, (size_t)2 * t->tcap * 4);
+    cudaError_t e10 = dmalloc(c, &t->d_tM, (size_t)2 * t->tcap * 8);
+    cudaError_t e11 = dmalloc(c, &t->d_rowM, (size_t)2 * 64 * t->RW * 8);
+    if (!e11) e11 = dmalloc(c, &t->d_tbits, (size_t)t->RW * 8);
     cudaError_t e12 = dmalloc(c, &t->d_alist_h, (size_t)64 * t->RW * 4);
     cudaError_t e13 = dmalloc(c, &t->d_alist_b, (size_t)64 * t->RW * 8);
     cudaError_t e14 = dmalloc(c, &t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
@@ -232,7 +237,7 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     sk_ctx* c = t->ctx;
     cudaSetDevice(c->device);
     for (void* p : {(void*)t->m.cols, (void*)t->m.rows, (void*)t->m.sgn, (void*)t->d_wpiv, (void*)t->d_pan, (void*)t->d_pivbuf, (void*)t->d_detacc,
-                    (void*)t->d_info, (void*)t->d_tlist, (void*)t->d_tM, (void*)t->d_rowM, (void*)t->d_alist_h, (void*)t->d_alist_b, (void*)t->d_dpart,
+                    (void*)t->d_info, (void*)t->d_tlist, (void*)t->d_tM, (void*)t->d_rowM, (void*)t->d_tbits, (void*)t->d_alist_h, (void*)t->d_alist_b, (void*)t->d_dpart,
                     (void*)t->d_q, (void*)t->d_out, (void*)t->d_det})
         dfree(c, p);          // stream-ordered: queued behind the work that still uses the buffers
     delete t;
@@ -409,7 +414,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
-    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
+    a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.tbits = t->d_tbits; a.tcap = t->tcap; a.fold = c->no_fold ? 0 : 1; a.row_cap = c->row_cap > 0 ? std::min(c->row_cap, kRowCap) : kRowCap; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
     a.prof = c->prof; a.force_columns = c->force_columns; a.destab_stale = t->r_destab_stale ? 1 : 0;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));

@@ -18,6 +18,8 @@ struct sk_ctx {
     int max_smem_optin = 0;
     int prof = 0;                           // SK_DEBUG_PROF: device-side phase timers (slows the kernel)
     int no_graph = 0;                       // SK_NO_GRAPH=1: sk_program_run enqueues plain launches instead of replaying a CUDA graph
+    int no_fold = 0;                        // SK_NO_FOLD=1: the measurement kernel gathers every panel in a phase of its own
+    int row_cap = 0;                        // SK_ROW_CAP=<k>: row-form factorisation only up to k active rows (tests: exercises the regather path)
     uint64_t tableau_uid = 0;
     int force_columns = 0;                  // SK_PANEL_COLUMNS=1: column-form panel factorisation only (testing aid)
     int meas_grid_override = 0;             // SK_MEAS_GRID: CTAs of the measurement kernel (profiling aid)
