@@ -1341,7 +1341,8 @@ k_measure_block(MeasArgs a) {
             }
             // folded gather, untouched rows: a lane per row, rows listed in tbits are skipped (their warps emitted them above)
             if (do_fold) {
-                for (int g = gwi; g < 2 * RW; g += GW) {
+                // groups are handed out from the far end of the warp index space: the item loop above keeps the first warps busy
+                for (int g = GW - 1 - gwi; g < 2 * RW; g += GW) {
                     const int h = 32 * g + lane;
                     const bool skip = (ldcg(a.tbits + (h >> 6)) >> (h & 63)) & 1ull;
                     const u64* rx = a.m.rows + (size_t)(2 * h) * Wp;
