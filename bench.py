@@ -39,42 +39,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons.  The sampler runs from before the warm-up (nvidia-smi needs a moment to
+    start) at 20 ms; stop(t0, t1) keeps the samples whose timestamps fall inside the timed region [t0, t1] (wall clock),
+    or, if the region was shorter than the sampling period, the samples closest to it."""
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
 
     def start(self):
-        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+        q = "timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            c = [x.strip() for x in line.split(",")]
+            try:
+                ts = datetime.datetime.strptime(c[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                ts = time.time()
+            self.rows.append((ts, c[1:]))
 
-    def stop(self) -> dict:
+    def stop(self, t0: float = 0.0, t1: float = float("inf")) -> dict:
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 pass
-        sm = sorted(int(r[0]) for r in self.rows if r and r[0].isdigit())
-        mx = [int(r[1]) for r in self.rows if len(r) > 1 and r[1].isdigit()]
+        rows = [r for ts, r in self.rows if t0 <= ts <= t1]
+        where = "inside the timed region"
+        if not rows and self.rows:          # region shorter than the sampling period: nearest samples
+            mid = 0.5 * (t0 + t1) if t1 != float("inf") else t0
+            rows = [r for _, r in sorted(self.rows, key=lambda x: abs(x[0] - mid))[:3]]
+            where = "nearest to the timed region"
+        sm = sorted(int(r[0]) for r in rows if r and r[0].isdigit())
+        mx = [int(r[1]) for r in rows if len(r) > 1 and r[1].isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in rows:
             for k, nme in enumerate(names):
                 if len(r) > 2 + k and r[2 + k].lower().startswith("active"):
                     reasons.add(nme)
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampled": where}
 
 
 def cpu_reference(steps: int, warmup: int, rounds_sample: int = 6):
@@ -113,7 +128,7 @@ def cpu_reference(steps: int, warmup: int, rounds_sample: int = 6):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -167,15 +182,18 @@ def main():
         e1.record(stream)
         return e0, e1
 
+    sampler = ClockSampler(local_rank); sampler.start()
     for _ in range(max(args.warmup, 3)):
         one_step(False)
     ctx.sync()
     ctx.reset_counters()
-    sampler = ClockSampler(local_rank); sampler.start()
     barrier()
+    t_region0 = time.time()
     evs = [one_step(True) for _ in range(args.steps)]
+    ctx.sync()
+    t_region1 = time.time()
     barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop(t_region0, t_region1)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     cnt = ctx.counters()
     out, det = prog.read_record()

@@ -2,7 +2,7 @@
 # Evidence for profiles/: bench line, ncu launch list of the bench command, one full capture of the top kernels.
 mkdir -p gpurun_out
 R=${ROUND:-r01}
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_${R}.json 2> gpurun_out/bench_${R}.err
+timeout 900 python bench.py > gpurun_out/bench_${R}.json 2> gpurun_out/bench_${R}.err
 tail -c 600 gpurun_out/bench_${R}.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_bench_${R}.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_bench_${R}.log 2>&1
 python - <<PY
