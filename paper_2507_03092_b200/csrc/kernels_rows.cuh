@@ -152,15 +152,24 @@ k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
     }
     __syncthreads();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= t0) return;
-    const u64* mx = rows + (size_t)(2 * m) * Wp; const u64* mz = mx + Wp;
-    const u32 g = group_of[m];
+    const bool live = m < t0;                       // whole warps stay for the warp-level aggregation below
+    const int mm = live ? m : 0;
+    const u64* mx = rows + (size_t)(2 * mm) * Wp; const u64* mz = mx + Wp;
+    const u32 g = live ? group_of[mm] : 0u;
+    const u32 widx = g >> 5, gbit = 1u << (g & 31);
     for (int k = 0; k < Bt && tb + k < t0 + B; ++k) {
         const u64* bx = s_blk + (size_t)k * 2 * W; const u64* bz = bx + W;
-        if (conflict_words(bx, bz, mx, mz, W, mode)) {
-            u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + (g >> 5);
-            const u32 bit = 1u << (g & 31);
-            if (!(__ldcg(word) & bit)) atomicOr(word, bit);
+        const bool c = live && conflict_words(bx, bz, mx, mz, W, mode);
+        // lanes whose group falls into the same bitmap word merge their bits (MATCH.ANY + REDUX.OR) and one lane per word
+        // issues one atomic -- instead of a load + atomic per conflicting pair
+        const u32 act = __ballot_sync(0xffffffffu, c);
+        if (c) {
+            const u32 peers = __match_any_sync(act, widx);
+            const u32 bits = __reduce_or_sync(peers, gbit);
+            if (int(threadIdx.x & 31) == __ffs(peers) - 1) {
+                u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + widx;
+                if ((__ldcg(word) & bits) != bits) atomicOr(word, bits);
+            }
         }
     }
 }
