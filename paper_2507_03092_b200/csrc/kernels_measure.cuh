@@ -37,7 +37,7 @@
 //       are commuting Hermitian operators (P^2 = +I cancels repeated factors).
 //   Every row undergoes exactly the multiplications of sequential CHP, in the same order;
 //   tools/proto_panel.py checks the scheme against the oracle.  Panel mode updates only the R
-//   form and raises ws->c_stale; the host re-derives C with a (flag-conditional) transpose.
+//   form; before the kernel exits it re-derives the C form itself (tile transpose over all CTAs).
 // Row i = p+n is never a rowsum target (SURVEY.md section 7 hazard): it is overwritten.
 //
 // Roofline: HBM/L2.  Algorithmic bytes: random  RW*8 + 16W + k*32W + 32W ;
@@ -71,11 +71,14 @@ struct PanelInfo {      // global scratch describing the current panel (written 
 };
 
 struct MeasWs {
-    u32 bar;            // grid barrier counter (zeroed before each launch)
+    // ---- first 32 bytes: zeroed by ONE memset before each launch
+    u32 bar;            // grid barrier counter
+    u32 progress;       // panel mode: factorisation steps published so far in this launch (monotone)
+    u32 r0[4];          // per-wave ~index of the first random measurement (0 = none), max-reduced; 3 slots rotate
+    u32 pad0[2];
+    // ---- persistent
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
-    u32 r0[4];          // per-wave index of the first random measurement, min-reduced; 3 slots rotate
-    u32 c_stale;        // panel mode ran: the C form must be re-derived from R
-    u32 progress;       // panel mode: measurements of this launch whose factorisation step is published (zeroed before each launch)
+    u32 pad1;
     u64 n_rand, n_det, k_rand, k_det, waves;
     u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
     u64 panels;
@@ -819,7 +822,7 @@ k_measure_block(MeasArgs a) {
         const int wend = min(a.count, pos + WS);
         u32* wpiv = a.wpiv + (size_t)(wave & 1) * WS;
         // ------------------------------------------------------------ P1 -----
-        if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0xffffffffu;
+        if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0u;
         for (int slot = gw; pos + slot < wend; slot += GW) {
             const int j = pos + slot;
             const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
@@ -838,13 +841,13 @@ k_measure_block(MeasArgs a) {
             piv = warp_min(piv);
             if (lane == 0) {
                 wpiv[slot] = piv;
-                if (piv != 0xffffffffu) atomicMin(&ws->r0[wave % 3], (u32)j);
+                if (piv != 0xffffffffu) atomicMax(&ws->r0[wave % 3], ~(u32)j);      // stored inverted: zero-initialised, max = smallest index
             }
         }
         SK_PROF(0);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(6);
-        const u32 r0 = __ldcg(&ws->r0[wave % 3]);
+        const u32 r0 = ~__ldcg(&ws->r0[wave % 3]);                               // 0xffffffff = no random measurement in the window
         const int dend = (r0 == 0xffffffffu) ? wend : int(r0);      // [pos, dend) are deterministic and final
         if (tid == 0) s_nheavy = 0;
         __syncthreads();
@@ -1391,7 +1394,23 @@ k_measure_block(MeasArgs a) {
         for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(prm + __ldcg(ptl + i), 0ull);
         if (blockIdx.x == 0 && tid < kPanelMax) { info->eph[0][tid] = 0; info->eph[1][tid] = 0; }
     }
-    if (blockIdx.x == 0 && tid == 0) ws->c_stale = 1u;
+    // Panel mode kept only the R form current: re-derive the C form here (same tile move as k_transpose_bits, two tiles per
+    // CTA at a time), so that the host never needs a conditional transpose after a measurement block.  Every row was final at
+    // the last grid barrier.
+    {
+        const int half = tid >> 8, t = tid & 255;
+        u32 (*tin)[9] = reinterpret_cast<u32 (*)[9]>(smem) + (size_t)half * 512;
+        u32 (*tout)[9] = tin + 256;
+        const int nbx = (64 * RW + 255) / 256, nby = (2 * Wp + 7) / 8;
+        const int ntiles = nbx * nby * 2;
+        __syncthreads();
+        for (int tile = blockIdx.x * 2 + half; tile < ntiles; tile += 2 * G) {
+            const int z = tile / (nbx * nby), r = tile - z * nbx * nby, by = r / nbx, bx = r - by * nbx;
+            transpose_tile_256(reinterpret_cast<const u32*>(a.m.rows) + (size_t)z * 2 * Wp, (size_t)4 * Wp, 64 * RW, 2 * Wp,
+                               reinterpret_cast<u32*>(a.m.cols) + (size_t)z * 2 * RW, (size_t)4 * RW, a.n, 2 * RW,
+                               bx * 256, by * 8, t, 2 + half, tin, tout);
+        }
+    }
 }
 
 // SPEC:165-173 rowsum(h, i) on the R form + C form fix-up, single CTA (API parity helper).

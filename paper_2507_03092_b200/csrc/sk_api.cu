@@ -406,11 +406,9 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
     if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; }
-    // reset barrier counter, wave slots (0xffffffff = none) and the stale flag (counters persist)
+    // one memset resets the launch-scoped words (barrier counter, progress counter, wave slots); counters and err persist
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->r0[0], 0xFF, 16, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->bar, 0, 4, c->stream));
-    SK_CUDA(c, cudaMemsetAsync(&ws->c_stale, 0, 8, c->stream));      // c_stale + progress
+    SK_CUDA(c, cudaMemsetAsync(ws, 0, 32, c->stream));
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
@@ -419,8 +417,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
-    // panel mode keeps only the R form current: re-derive C if (and only if) the kernel raised the flag
-    return cols_from_rows(t, &ws->c_stale);
+    return SK_OK;          // (a block that entered panel mode re-derives the C form itself before it exits)
 }
 
 static int32_t reserve_record(sk_tableau* t, size_t m) {
