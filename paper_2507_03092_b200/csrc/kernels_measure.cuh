@@ -75,7 +75,8 @@ struct MeasWs {
     u32 bar;            // grid barrier counter
     u32 progress;       // panel mode: factorisation steps published so far in this launch (monotone)
     u32 r0[4];          // per-wave ~index of the first random measurement (0 = none), max-reduced; 3 slots rotate
-    u32 pad0[2];
+    u32 exitcnt;        // CTAs that have left the kernel: the last one re-zeroes this block for the next launch
+    u32 pad0;
     // ---- persistent
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
     u32 pad1;
@@ -128,6 +129,10 @@ struct MeasArgs {
 };
 
 __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+// normal kernel exit: the last CTA to leave (every other one is past all grid barriers) re-zeroes the launch-scoped words,
+// so the host needs no memset between measurement blocks (it zeroes them itself after an error)
+#define SK_MEAS_EXIT() do { __syncthreads(); if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(&ws->exitcnt, 1u) == gridDim.x - 1) { \
+        ws->bar = 0; ws->progress = 0; ws->r0[0] = 0; ws->r0[1] = 0; ws->r0[2] = 0; ws->r0[3] = 0; __threadfence(); ws->exitcnt = 0; } } } while (0)
 #define SK_PROF(k) do { if (a.prof && blockIdx.x == 0 && tid == 0) { u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
 
 __device__ __forceinline__ int sign_bit(const u64* sgn, int r) { return int((ldcg(sgn + (r >> 6)) >> (r & 63)) & 1ull); }
@@ -906,7 +911,7 @@ k_measure_block(MeasArgs a) {
         pos = dend;
         if (r0 != 0xffffffffu) { panel_mode = true; break; }
     }
-    if (!panel_mode) return;
+    if (!panel_mode) { SK_MEAS_EXIT(); return; }
 
     // =============================================================== panel mode =====
     // (the P2 reads above touch nothing that is written before the next grid barrier)
@@ -1411,6 +1416,7 @@ k_measure_block(MeasArgs a) {
                                bx * 256, by * 8, t, 2 + half, tin, tout);
         }
     }
+    SK_MEAS_EXIT();
 }
 
 // SPEC:165-173 rowsum(h, i) on the R form + C form fix-up, single CTA (API parity helper).

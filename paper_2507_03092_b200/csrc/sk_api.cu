@@ -275,7 +275,10 @@ static int32_t check_ws(sk_ctx* c) {
     u32 e2 = 0;
     SK_CUDA(c, cudaMemcpyAsync(&e2, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    if ((h.err & 0xC0000000u)) SK_FAIL(c, SK_ECUDA, "measurement kernel timed out (err=0x%x)", h.err);
+    if ((h.err & 0xC0000000u)) {
+        cudaMemsetAsync(ws, 0, 32, c->stream); cudaMemsetAsync(&ws->err, 0, 4, c->stream);      // an aborted launch leaves its words behind
+        SK_FAIL(c, SK_ECUDA, "measurement kernel timed out (err=0x%x)", h.err);
+    }
     if ((h.err & 1u) || (e2 & 1u)) {
         cudaMemsetAsync(&ws->err, 0, 4, c->stream); cudaMemsetAsync(c->d_err, 0, 4, c->stream);
         SK_FAIL(c, SK_EINVARIANT, "rowsum produced an odd mod-4 phase (SPEC:169)");
@@ -406,9 +409,9 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
     if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; }
-    // one memset resets the launch-scoped words (barrier counter, progress counter, wave slots); counters and err persist
+    // the launch-scoped words (barrier counter, progress counter, wave slots) are zero: the previous launch's last CTA
+    // re-zeroed them on its way out (check_ws does it after an error)
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(ws, 0, 32, c->stream));
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
