@@ -157,19 +157,23 @@ k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
     const u64* mx = rows + (size_t)(2 * mm) * Wp; const u64* mz = mx + Wp;
     const u32 g = live ? group_of[mm] : 0u;
     const u32 widx = g >> 5, gbit = 1u << (g & 31);
+    // Do all lanes of this warp point into the same bitmap word?  (Neighbouring earlier terms sit in neighbouring groups
+    // when nearly every term opens its own group -- QWC on random strings.)  Then the warp merges its bits with one REDUX.OR
+    // and issues one atomic per block term instead of a load + atomic per conflicting pair; otherwise lanes go one by one.
+    const u32 w_first = __shfl_sync(0xffffffffu, widx, 0);
+    const bool one_word = __all_sync(0xffffffffu, !live || widx == w_first);
     for (int k = 0; k < Bt && tb + k < t0 + B; ++k) {
         const u64* bx = s_blk + (size_t)k * 2 * W; const u64* bz = bx + W;
         const bool c = live && conflict_words(bx, bz, mx, mz, W, mode);
-        // lanes whose group falls into the same bitmap word merge their bits (MATCH.ANY + REDUX.OR) and one lane per word
-        // issues one atomic -- instead of a load + atomic per conflicting pair
-        const u32 act = __ballot_sync(0xffffffffu, c);
-        if (c) {
-            const u32 peers = __match_any_sync(act, widx);
-            const u32 bits = __reduce_or_sync(peers, gbit);
-            if (int(threadIdx.x & 31) == __ffs(peers) - 1) {
-                u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + widx;
+        if (one_word) {
+            const u32 bits = __reduce_or_sync(0xffffffffu, c ? gbit : 0u);
+            if ((threadIdx.x & 31) == 0 && bits) {
+                u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + w_first;
                 if ((__ldcg(word) & bits) != bits) atomicOr(word, bits);
             }
+        } else if (c) {
+            u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + widx;
+            if (!(__ldcg(word) & gbit)) atomicOr(word, gbit);
         }
     }
 }
