@@ -576,15 +576,17 @@ static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
         }
     return SK_OK;
 }
-static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_t& ng, size_t& nm) {
+static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_t& ng, size_t& nm, unsigned nthreads = 1) {
+    // boundaries = positions where "is a measurement" changes; found chunk-parallel, concatenated in order
+    std::vector<std::vector<size_t>> cuts(std::max(1u, nthreads));
+    parallel_for(nthreads, ngates, [&](size_t lo, size_t hi, unsigned k) {
+        std::vector<size_t>& c = cuts[k];
+        for (size_t i = std::max<size_t>(lo, 1); i < hi; ++i) if ((gates[i].kind == SK_M) != (gates[i - 1].kind == SK_M)) c.push_back(i);
+    });
     std::vector<std::pair<size_t, size_t>> b;
-    for (size_t i = 0; i < ngates;) {
-        const bool m = gates[i].kind == SK_M;
-        size_t j = i;
-        while (j < ngates && (gates[j].kind == SK_M) == m) ++j;
-        b.emplace_back(i, j);
-        i = j;
-    }
+    size_t start = 0;
+    for (const auto& c : cuts) for (size_t i : c) { b.emplace_back(start, i); start = i; }
+    if (ngates) b.emplace_back(start, ngates);
     std::vector<Seg> segs(b.size());
     ng = nm = 0;
     size_t nruns = 0;
@@ -738,7 +740,7 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
     };
     if (mode == 0 || nmarks == 0) {
         size_t ng = 0, nm = 0;
-        std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
+        std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm, nthreads);
         ordered.resize(ng); mq.resize(nm);
         std::atomic<size_t> next{0};
         const int tctas = target_ctas_for(c, n);
@@ -901,7 +903,7 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     int32_t rc = validate_circuit(c, n, gates, ngates, nthreads);
     if (rc) return rc;
     size_t ng = 0, nm = 0;
-    std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm);
+    std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm, nthreads);
     const size_t nboff = 2 * ng + 2 * segs.size() + 2;       // chunk tables: a run of k gates needs at most 2k + 2 entries
     rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + nboff * 4 + 64);
     if (rc) return rc;
