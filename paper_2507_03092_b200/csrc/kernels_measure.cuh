@@ -344,7 +344,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
 struct PanelSmem {
     u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax], S[kPanelMax]; uint8_t outc[kPanelMax];
     u32 full32[2]; u32 nt; u32 krand; u32 kdet; int steps;
-    u32 dcnt[kPanelMax]; u32 wmin[2][kRowThreads / 32]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd;
+    u32 dcnt[kPanelMax]; u32 gmin[3]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd;
 };
 
 // F, row form (the common case: <= kRowCap rows have an x in any of the panel's columns).  The active rows
@@ -362,7 +362,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     long long tc = clock64();
 #define SK_RPROF(k) do { if (a.prof && tid == 0) { const long long _c = clock64(); a.ws->cprof[k] += (u64)(_c - tc); tc = _c; } } while (0)
     if (tid < kPanelMax) { ps.piv[tid] = kInf; ps.hist[tid] = 0; ps.dZ[tid] = 0; ps.outc[tid] = 0; ps.dcnt[tid] = 0; }
-    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; ps.steps = 0; a.info->dmode = 1; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; ps.steps = 0; ps.gmin[0] = kInf; ps.gmin[1] = kInf; ps.gmin[2] = kInf; a.info->dmode = 1; }
     __syncthreads();
     u64 randmask = 0;
     // Lookahead: every finished step is published at once (pivot, history, partner list, then a release store of the
@@ -406,16 +406,18 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 #undef SK_SCAN
             }
             const u32 wm = __reduce_min_sync(0xffffffffu, mymin);
-            if (mymin == wm && (wm != kInf || lane == 0)) { ps.wmin[j & 1][warp] = wm; ps.wbp[j & 1][warp] = cb; ps.wmp[j & 1][warp] = cm; }   // row-bits are unique: one writer
+            // the CTA-wide minimum and the warp that holds it in ONE shared word: atomicMin of (row-bit << 5 | warp); row-bits are
+            // unique, so exactly one lane of the CTA ends up as the owner.  Three slots rotate (the next one is re-armed here).
+            if (mymin == wm && wm != kInf) { atomicMin(&ps.gmin[j % 3], (wm << 5) | (u32)warp); ps.wbp[j & 1][warp] = cb; ps.wmp[j & 1][warp] = cm; }
+            if (tid == 0) ps.gmin[(j + 1) % 3] = kInf;
             named_bar(1, Tact);
             if (tid == 0) {                                    // all warps' writes of the steps before j precede this barrier
                 if (helper) { if ((j & 7) == 0) { __threadfence_block(); *(volatile int*)&ps.steps = j; } }     // the helper publishes in groups of 8
                 else if (j - published >= 8) publish(j);
             }
-            // minimum over the warps and the warp that holds it (row-bits are unique)
-            const u32 wv = (lane < nw) ? ps.wmin[j & 1][lane] : kInf;
-            const u32 p = __reduce_min_sync(0xffffffffu, wv);
-            const int tw = __ffs(__ballot_sync(0xffffffffu, wv == p)) - 1;
+            const u32 gm = ps.gmin[j % 3];
+            const u32 p = (gm == kInf) ? kInf : (gm >> 5);
+            const int tw = int(gm & 31u);
             if (p == kInf) {
                 // ---------------- deterministic step: partners = destabilizer rows with an x (virtual ones stand for +-Z rows)
                 if (hit) {
