@@ -344,7 +344,7 @@ __device__ __forceinline__ int cta_det(const MeasArgs& a, const MeasSmem& sm, co
 struct PanelSmem {
     u32 piv[kPanelMax]; u64 hist[kPanelMax], pw[kPanelMax], dZ[kPanelMax], S[kPanelMax]; uint8_t outc[kPanelMax];
     u32 full32[2]; u32 nt; u32 krand; u32 kdet; int steps;
-    u32 dcnt[kPanelMax]; u32 gmin[3]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd;
+    u32 dcnt[kPanelMax]; u32 gmin[3]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd; u32 pready;
 };
 
 // F, row form (the common case: <= kRowCap rows have an x in any of the panel's columns).  The active rows
@@ -814,7 +814,7 @@ k_measure_block(MeasArgs a) {
     MeasWs* ws = a.ws;
     u32 epoch = 0;
     u32 tma_parity = 0;
-    if (tid == 0) { s_cnt1 = 0; mbar_init(&s_mbar, 1); }
+    if (tid == 0) { s_cnt1 = 0; mbar_init(&s_mbar, 1); ps.pready = 0; }
     __syncthreads();
 
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
@@ -1218,6 +1218,11 @@ k_measure_block(MeasArgs a) {
         // ---- the finished panel description (one round trip), then the signs of the pivot values
         // (triangular GF(2) recurrence; every CTA solves it itself)
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
+        const int Bn2 = min(B, a.count - pos - Bn);
+        if (tid < kPanelMax) {        // next panel's qubits for the folded gather (same round trip as the description above)
+            const bool f = a.fold && Bn2 > 0 && __ldcg(&info->dmode) == 1u;
+            s_q2[tid] = (f && tid < Bn2) ? a.qubits[pos + Bn + tid] : 0xffffffffu;
+        }
         __syncthreads();
         if (s_info.dmode == 2) { have_list = false; pbase += u32(Bn); continue; }      // regather: same panel again, with the full (row + column) gather
         const u64 randmask = s_info.randmask;
@@ -1225,9 +1230,7 @@ k_measure_block(MeasArgs a) {
         const u64 detmask = ~randmask & allmask;
         // The gather of the NEXT panel is folded into this phase when the row form is in use: touched rows emit their new
         // bits as they are written, the untouched ones (not in tbits) are read here -- no separate phase, no grid barrier.
-        const int Bn2 = min(B, a.count - pos - Bn);
         const bool do_fold = a.fold && s_info.dmode == 1 && Bn2 > 0;
-        if (tid < kPanelMax) s_q2[tid] = (do_fold && tid < Bn2) ? a.qubits[pos + Bn + tid] : 0xffffffffu;
         // housekeeping: retire the previous panel's step-mask entries (its D part 2 was their last reader) and phase sums
         {
             const u32* ptl = a.tlist + (size_t)(kpar ^ 1) * a.tcap;
@@ -1235,6 +1238,7 @@ k_measure_block(MeasArgs a) {
             for (u32 i = blockIdx.x * kMeasThreads + tid; i < prev_nt; i += G * kMeasThreads) __stcg(prm + __ldcg(ptl + i), 0ull);
             if (blockIdx.x == 0 && tid < kPanelMax) info->eph[kpar ^ 1][tid] = 0;
         }
+        const u32 pseq = pbase + u32(Bn);            // unique per panel attempt, never 0
         if (tid == 0) {
             u64 psign = 0; u32 odd = 0;
             u64 bits = randmask;
@@ -1245,10 +1249,19 @@ k_measure_block(MeasArgs a) {
                 psign |= (u64)((ek >> 1) & 1u) << k;
             }
             ps.psign = psign; ps.podd = odd;
+            __threadfence_block();
+            *(volatile u32*)&ps.pready = pseq;          // the warps pick the signs up when they first need them (end of their first item)
             if (odd) atomicOr(&ws->err, 1u);
         }
-        __syncthreads();
-        const u64 psign = ps.psign;
+        bool ps_have = false; u64 ps_val = 0;
+        auto get_psign = [&]() -> u64 {
+            if (!ps_have) {
+                if (lane == 0) { while (*(volatile u32*)&ps.pready != pseq) {} }
+                __syncwarp();
+                ps_val = *(volatile u64*)&ps.psign; ps_have = true;
+            }
+            return ps_val;
+        };
         // ---- D part 2 + A: items = deterministic steps, then touched rows; warp per item
         {
             const int nd = __popcll(detmask);
@@ -1285,8 +1298,9 @@ k_measure_block(MeasArgs a) {
                     __syncwarp();
                     int e = warp_mul_list(a.pivbuf, W, Wp, s_wlist[warp], cnt, acc_x, acc_z, lane);
                     __syncwarp();
+                    const u64 sgd = get_psign();
                     if (lane == 0) {
-                        e += __ldcg(&info->dete[j]) + 2 * __popcll(N & psign);
+                        e += __ldcg(&info->dete[j]) + 2 * __popcll(N & sgd);
                         u64 b = Z;
                         while (b) {        // (+-Z_{q_l}) * acc
                             const int l = __ffsll((long long)b) - 1; b &= b - 1;
@@ -1329,7 +1343,7 @@ k_measure_block(MeasArgs a) {
                         const u64* sx = a.pivbuf + (size_t)(2 * ko) * Wp;
                         for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(sx + w); acc_z[w] = ldcg(sx + Wp + w); }
                         M &= (ko < 63) ? ~((2ull << ko) - 1ull) : 0ull;
-                        e = (lane == 0) ? 2 * int((psign >> ko) & 1ull) : 0;
+                        e = 0;                       // (+ the sign of P_ko', added with the other pivot signs below)
                     } else {
                         for (int w = lane; w < W; w += 32) { acc_x[w] = ldcg(tx + w); acc_z[w] = ldcg(tx + Wp + w); }
                         e = (lane == 0) ? 2 * int((ldcg(sg) >> (h & 63)) & 1ull) : 0;
@@ -1339,7 +1353,7 @@ k_measure_block(MeasArgs a) {
                     { u64 b = M; while (b) { const int l = __ffsll((long long)b) - 1; b &= b - 1; if (lane == 0) s_wlist[warp][cnt] = u32(l); ++cnt; } }
                     __syncwarp();
                     e += warp_mul_list(a.pivbuf, W, Wp, s_wlist[warp], cnt, acc_x, acc_z, lane);
-                    if (lane == 0) e += 2 * __popcll(M & psign);
+                    { const u64 sg_ = get_psign(); if (lane == 0) e += 2 * __popcll(M & sg_) + (ko >= 0 ? 2 * int((sg_ >> ko) & 1ull) : 0); }
                     e = warp_sum(e) & 3;
                     for (int w = lane; w < W; w += 32) { __stcg(tx + w, acc_x[w]); __stcg(tx + Wp + w, acc_z[w]); }
                     if (lane == 0) {
