@@ -390,7 +390,6 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 #undef SK_LOAD
         int ntarget = 0;
         int vt = int(A % (u32)Tact), vk = int(A / (u32)Tact);      // slot (thread, k) of the next virtual row
-        const int nw = Tact >> 5;
         SK_RPROF(0);
         for (int j = 0; j < Bn; ++j) {
             // which of this thread's slots have an x in column j
