@@ -198,6 +198,41 @@ int32_t sk_pbc_layer_download(sk_pbc* p, uint64_t layer, uint64_t* x, uint64_t* 
 /* final M_tab, 2n rows row-major (measurement_rows are rows 0..n-1) */
 int32_t sk_pbc_mtab_download(sk_pbc* p, uint64_t* x, uint64_t* z, uint8_t* sign);
 
+/* ---- row sharding of one tableau across GPUs ------ */
+/* A shard owns the slots [slot_lo, slot_hi): stabilizer i AND destabilizer i for every i in the
+ * range (the deterministic branch of SPEC:183 then needs no remote row).  One shard per GPU /
+ * process; Clifford gates never communicate (rows are independent).  A measurement is
+ * assembled by the host driver from the calls below plus three small exchanges:
+ *   pivot search  -> allreduce-min of d_cand over the shards
+ *   random branch -> owner's pivot row broadcast, every shard rowsums
+ *   deterministic -> allgather of the partial products, multiplied in shard order
+ * Every d_* argument is a DEVICE pointer supplied by the caller (the exchange buffers of its
+ * communication library), used on the context's stream; results are bit-identical to the unsharded
+ * sk_measure_batch. */
+typedef struct sk_shard sk_shard;
+int32_t sk_shard_create(sk_ctx* ctx, uint64_t n, uint64_t slot_lo, uint64_t slot_hi, sk_shard** out);  /* identity rows */
+void sk_shard_destroy(sk_shard* s);
+int32_t sk_shard_reset(sk_shard* s);
+/* Any ordered Clifford sequence on this shard's rows (same kernel and layering as sk_apply_gates). */
+int32_t sk_shard_apply_gates(sk_shard* s, const sk_gate* gates, size_t ngates);
+/* d_cand[j] (int32) = smallest GLOBAL stabilizer index in this shard with an x on qubits[j], else 0x7f7f7f7f. */
+int32_t sk_shard_pivot_search(sk_shard* s, const uint32_t* qubits, size_t m, int32_t* d_cand);
+/* 64-bit words per partial product / pivot row buffer: x[Wp] z[Wp] phase pad, Wp = W rounded up to even. */
+uint64_t sk_shard_partial_words(const sk_shard* s);
+/* d_part[j] = product of this shard's partner stabilizers of measurement j (identity if none). */
+int32_t sk_shard_det_partial(sk_shard* s, const uint32_t* qubits, size_t m, uint64_t* d_part);
+/* d_gathered = [nshards][m][partial_words] in shard order -> outcome bytes (host). Synchronises. */
+int32_t sk_shard_det_combine(sk_shard* s, const uint64_t* d_gathered, uint32_t nshards, size_t m, uint8_t* outcomes);
+/* Owner only: stabilizer p (global index) -> d_row[partial_words]. */
+int32_t sk_shard_pivot_row(sk_shard* s, uint64_t p, uint64_t* d_row);
+/* Every shard: rowsum(h, pivot) on its rows with an x on q (ref: proj/src/pauli.cpp:189-205 phase sum);
+ * the owner then stores destabilizer p := pivot row and stabilizer p := (-1)^outcome Z_q. */
+int32_t sk_shard_random_update(sk_shard* s, uint32_t q, uint64_t p, const uint64_t* d_row, uint8_t outcome);
+/* This shard's rows, row-major: stabilizers slot_lo..slot_hi-1, then their destabilizers. Synchronises. */
+int32_t sk_shard_download(sk_shard* s, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* rowsums performed: out2[0] random branch, out2[1] deterministic branch. Synchronises. */
+int32_t sk_shard_counters(sk_shard* s, uint64_t out2[2]);
+
 #ifdef __cplusplus
 }
 #endif

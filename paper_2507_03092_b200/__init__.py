@@ -110,6 +110,18 @@ def lib() -> C.CDLL:
             "sk_pbc_layer_rows": (u64, [vp, u64]),
             "sk_pbc_layer_download": (i32, [vp, u64, vp, vp, vp]),
             "sk_pbc_mtab_download": (i32, [vp, vp, vp, vp]),
+            "sk_shard_create": (i32, [vp, u64, u64, u64, P(vp)]),
+            "sk_shard_destroy": (None, [vp]),
+            "sk_shard_reset": (i32, [vp]),
+            "sk_shard_apply_gates": (i32, [vp, vp, sz]),
+            "sk_shard_pivot_search": (i32, [vp, vp, sz, vp]),
+            "sk_shard_partial_words": (u64, [vp]),
+            "sk_shard_det_partial": (i32, [vp, vp, sz, vp]),
+            "sk_shard_det_combine": (i32, [vp, vp, u32, sz, vp]),
+            "sk_shard_pivot_row": (i32, [vp, u64, vp]),
+            "sk_shard_random_update": (i32, [vp, u32, u64, vp, C.c_uint8]),
+            "sk_shard_download": (i32, [vp, vp, vp, vp]),
+            "sk_shard_counters": (i32, [vp, P(u64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)      # AttributeError here == header/library mismatch: fail loudly
@@ -130,6 +142,9 @@ EXPORTS = [
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",
     "sk_group_first_fit", "sk_verify_grouping", "sk_transpile", "sk_pbc_destroy", "sk_pbc_stats",
     "sk_pbc_layer_rows", "sk_pbc_layer_download", "sk_pbc_mtab_download",
+    "sk_shard_create", "sk_shard_destroy", "sk_shard_reset", "sk_shard_apply_gates", "sk_shard_pivot_search",
+    "sk_shard_partial_words", "sk_shard_det_partial", "sk_shard_det_combine", "sk_shard_pivot_row",
+    "sk_shard_random_update", "sk_shard_download", "sk_shard_counters",
 ]
 
 

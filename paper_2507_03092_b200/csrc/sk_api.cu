@@ -991,3 +991,4 @@ extern "C" int32_t sk_sim(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ng
 }
 
 #include "sk_rows_impl.cuh"
+#include "sk_shard_impl.cuh"

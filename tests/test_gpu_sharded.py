@@ -1,0 +1,89 @@
+"""-m gpu: the row-sharded tableau (sk_shard_* C ABI + paper_2507_03092_b200/sharded.py) against the CPU oracle.
+Several shards live on the one GPU of the test box (`local_shards`), so the whole protocol -- pivot candidates
+min-reduced over shards, pivot row handed from its owner to every shard, partial products multiplied in shard
+order -- runs through the CUDA kernels; with torch.distributed the same calls go over NCCL."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+H, S, SDG, X, Y, Z, CX, CZ, SWAP, M, T, TDG = range(12)
+SEED = 20250703
+
+
+def run_both(sk, orc, circ, seed, local_shards):
+    from paper_2507_03092_b200.sharded import ShardedTableau
+    t = ShardedTableau.create_cuda(circ.n, local_shards=local_shards, device_index=0)
+    try:
+        out, det = t.sim(circ, seed)
+        x, z, r = t.gather_tableau()
+        stats = dict(t.stats)
+        k = [s.counters() for s in t.shards]
+    finally:
+        t.close()
+    o = orc.Tableau(circ.n)
+    oo, od, rc = o.sim(circ.gates, seed)
+    assert rc == 0
+    ox, oz, orr = o.get()
+    assert (det == od).all(), "deterministic flags differ"
+    assert (out == oo).all(), "outcomes differ"
+    assert (x == ox).all() and (z == oz).all(), "tableau bits differ"
+    assert (r == orr).all(), "signs differ"
+    assert stats["n_rand"] == int((od == 0).sum()) and stats["n_det"] == int((od == 1).sum())
+    return stats, k
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8])
+@pytest.mark.parametrize("d", [3, 5, 7])
+def test_surface_code_sharded_matches_oracle(sk, orc, d, shards):
+    run_both(sk, orc, sk.surface_code_circuit(d, d, True), SEED, shards)
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+@pytest.mark.parametrize("n", [64, 200])
+def test_random_layered_sharded_matches_oracle(sk, orc, n, shards):
+    run_both(sk, orc, sk.random_layered_circuit(n, 11 + n), 7, shards)
+
+
+@pytest.mark.parametrize("n,shards", [(1, 1), (5, 2), (65, 2), (130, 3), (257, 4), (300, 8)])
+def test_random_circuits_with_measurements_sharded(sk, orc, n, shards):
+    rng = np.random.default_rng(1000 + n)
+    gates = []
+    for _ in range(300 + 4 * n):
+        if rng.random() < 0.2:
+            gates.append((M, int(rng.integers(0, n)), 0)); continue
+        k = int(rng.choice([H, S, SDG, X, Y, Z, CX, CZ, SWAP]))
+        a = int(rng.integers(0, n)); b = 0
+        if k in (CX, CZ, SWAP):
+            if n == 1: k = H
+            else: b = int(rng.integers(0, n - 1)); b += b >= a
+        gates.append((k, a, b))
+    run_both(sk, orc, sk.Circuit(n, gates), 99, shards)
+
+
+def test_sharded_equals_unsharded_engine_d25_first_round(sk, ctx, orc):
+    """config C2's circuit cut to 2 rounds: sharded record == single-GPU sk_sim record (and the oracle's)."""
+    circ = sk.surface_code_circuit(25, 2, True)
+    t1, out1, det1, _ = ctx.sim(circ, SEED)
+    t1.close()
+    from paper_2507_03092_b200.sharded import ShardedTableau
+    t = ShardedTableau.create_cuda(circ.n, local_shards=4, device_index=0)
+    try:
+        out, det = t.sim(circ, SEED)
+    finally:
+        t.close()
+    assert (out == out1).all() and (det == det1).all()
+
+
+def test_shard_argument_errors(sk, ctx):
+    import ctypes as C
+    L = sk.lib()
+    h = C.c_void_p()
+    assert L.sk_shard_create(ctx._h, 0, 0, 0, C.byref(h)) == sk.SK_EDIM
+    assert L.sk_shard_create(ctx._h, 10, 4, 11, C.byref(h)) == sk.SK_EDIM
+    assert L.sk_shard_create(ctx._h, 100, 64, 100, C.byref(h)) == sk.SK_OK
+    buf = (C.c_uint64 * 64)()
+    assert L.sk_shard_pivot_row(h, 3, buf) == sk.SK_EDIM          # stabilizer 3 lives in another shard
+    g = sk.gates_array([(T, 0, 0)])
+    assert L.sk_shard_apply_gates(h, g.ctypes.data_as(C.c_void_p), 1) == sk.SK_EUNSUPPORTED
+    L.sk_shard_destroy(h)
