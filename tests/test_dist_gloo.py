@@ -51,3 +51,63 @@ def test_world_size_2_gloo_replicas():
     outs = [p.communicate(timeout=180)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
     assert "rank 0 ok" in outs[0] and "rank 1 ok" in outs[1]
+
+
+def _run_two_ranks(script):
+    port = free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, "-c", script], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=300)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    assert "rank 0 ok" in outs[0] and "rank 1 ok" in outs[1], outs
+
+
+def test_world_size_2_gloo_row_sharded_protocol():
+    """The row-sharded driver (paper_2507_03092_b200/sharded.py) over a real 2-rank process group: allreduce-min of
+    the pivot candidates, broadcast of the pivot row, allgather of the partial products.  The per-shard arithmetic
+    is tests/shard_stub.py here (no GPU in this container); on the GPU box the same driver runs on CudaShard
+    (tests/test_gpu_sharded.py).  2 ranks x 2 local shards = 4 global shards; record and tableau == oracle."""
+    script = textwrap.dedent("""
+        import os, sys
+        sys.path.insert(0, %r)
+        import numpy as np
+        import paper_2507_03092_b200 as sk
+        from paper_2507_03092_b200 import dist
+        from paper_2507_03092_b200.sharded import ShardedTableau, Exchange, counter_bit
+        from tests.shard_stub import StubShard
+        from oracle import oracle_py as orc
+        rank, local_rank, world = dist.init("gloo")
+        assert world == 2
+        rng = np.random.default_rng(5)
+        n = 70
+        gates = []
+        for _ in range(500):
+            u = rng.random()
+            if u < 0.2: gates.append((9, int(rng.integers(0, n)), 0)); continue
+            k = int(rng.choice([0, 1, 2, 3, 4, 5, 6, 7, 8])); a = int(rng.integers(0, n)); b = 0
+            if k >= 6: b = int(rng.integers(0, n - 1)); b += b >= a
+            gates.append((k, a, b))
+        for circ, seed in ((sk.surface_code_circuit(3, 3, True), 20250703), (sk.surface_code_circuit(5, 2, True), 1), (sk.Circuit(n, gates), 99)):
+            ex = Exchange(2)
+            assert ex.nshards == 4
+            shards = [StubShard(circ.n, *dist.slot_range(circ.n, rank * 2 + l, 4)) for l in range(2)]
+            t = ShardedTableau(circ.n, shards, ex)
+            out, det = t.sim(circ, seed)
+            x, z, r = t.gather_tableau()
+            o = orc.Tableau(circ.n)
+            oo, od, rc = o.sim(circ.gates, seed)
+            ox, oz, orr = o.get()
+            assert rc == 0 and (out == oo).all() and (det == od).all(), "record differs from the oracle"
+            assert (x == ox).all() and (z == oz).all() and (r == orr).all(), "tableau differs from the oracle"
+            assert ex.calls["allreduce_min"] >= 1 and ex.calls["allgather"] >= 1
+            if (od == 0).any(): assert ex.calls["broadcast"] == int((od == 0).sum())
+        # CounterRng bits (ref: rng.hpp:33-39; SURVEY 8c probe values)
+        assert "".join(str(counter_bit(0, i)) for i in range(32)) == "01111010000000100000010000111101"
+        assert "".join(str(counter_bit(7, i)) for i in range(32)) == "01010011011101100101001001101001"
+        dist.finalize()
+        print("rank", rank, "ok")
+    """ % ROOT)
+    _run_two_ranks(script)
