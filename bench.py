@@ -9,8 +9,11 @@ One JSON line on stdout (rank 0).  `value` = seconds per full simulation with th
 and tableau already resident in HBM (CUDA events on the library's stream, max over ranks);
 `e2e` = the same simulation through the C-ABI call `sk_sim` with HOST buffers (circuit in pinned
 host memory -> compile -> upload -> simulate -> measurement record back to the host).
-N > 1: every rank simulates the whole circuit (independent shots, seed ^ rank) -- "replicas";
-row sharding of one tableau is described in DESIGN.md section 7 and is not enabled here.
+N > 1: every rank simulates the whole circuit (independent shots, seed ^ rank) -- "replicas", the
+layout that is fastest for a 102 MB working set.  `--sharding rows` instead runs ONE simulation whose
+tableau is row-sharded over the N ranks (paper_2507_03092_b200/sharded.py; NCCL allreduce-min /
+broadcast / allgather per measurement window) and reports it as strong scaling; `--local-shards L` puts L
+shards on each GPU (how the protocol is exercised on a single B200).
 """
 from __future__ import annotations
 
@@ -125,6 +128,49 @@ def cpu_reference(steps: int, warmup: int, rounds_sample: int = 6):
             "sample_seconds": t_hi + t_lo}
 
 
+def bench_row_sharded(args, sk, skdist, torch, rank, local_rank, world, workload):
+    """One d=71 simulation with the tableau row-sharded over the ranks (x local shards per GPU).  The circuit is a host
+    buffer, so the timed region is end to end by construction (gates H2D per Clifford run, candidates / outcomes D2H)."""
+    from paper_2507_03092_b200.sharded import ShardedTableau
+    circ = sk.surface_code_circuit(D, ROUNDS, True)
+    sampler = ClockSampler(local_rank); sampler.start()
+    times, rec, stats, calls, xbytes, launches = [], None, None, None, 0, 0
+    steps, warm = max(1, min(args.steps, 3)), 1
+    t_region0 = time.time()
+    for i in range(warm + steps):
+        if i == warm:
+            t_region0 = time.time()
+        t = ShardedTableau.create_cuda(circ.n, local_shards=args.local_shards, device_index=local_rank)
+        t.ctx.reset_counters()
+        skdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(t.stream)
+        out, det = t.sim(circ, SEED)
+        e1.record(t.stream); t.stream.synchronize()
+        skdist.barrier()
+        if i >= warm:
+            times.append(e0.elapsed_time(e1))
+            launches += t.ctx.counters()["kernel_launches"]
+        rec, stats, calls, xbytes = (int(out.sum()), int(det.sum())), dict(t.stats), dict(t.ex.calls), t.ex.bytes
+        t.close()
+    clocks = sampler.stop(t_region0, time.time())
+    ms = skdist.max_over_ranks(sum(times) / len(times))
+    if rank == 0:
+        G = world * args.local_shards
+        line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": workload, "seed": SEED, "parallelism": f"tableau row-sharded over {world} rank(s) x {args.local_shards} local shard(s) = {G} shards",
+                           "timing": "CUDA events on the library stream around the whole simulation, mean of steps, max over ranks"},
+                "e2e": {"value": ms * 1e-3, "unit": "s", "h2d_bytes_per_step": int(len(circ.gates) * 12 * args.local_shards + 4 * 2 * circ.num_measurements),
+                        "d2h_bytes_per_step": int(5 * circ.num_measurements), "call": "ShardedTableau.sim(circuit in host memory, seed)"},
+                "gpu_launches": int(launches), "clocks": clocks, "record_checksum": list(rec),
+                "sharding": {"global_shards": G, "n_rand": stats["n_rand"], "n_det": stats["n_det"], "pivot_search_windows": stats["searches"],
+                             "collectives_per_step": calls, "exchange_bytes_per_step": xbytes}}
+        print(json.dumps(line))
+    skdist.finalize()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -133,6 +179,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sharding", default="replicas", choices=["replicas", "rows"])
+    ap.add_argument("--local-shards", type=int, default=1)
     args = ap.parse_args()
 
     from paper_2507_03092_b200 import dist as skdist
@@ -164,6 +212,8 @@ def main():
     barrier = skdist.barrier
 
     sk.lib()
+    if args.sharding == "rows":
+        return bench_row_sharded(args, sk, skdist, torch, rank, local_rank, world, workload)
     ctx = sk.Context(local_rank)
     stream = torch.cuda.ExternalStream(ctx.stream)
     circ = sk.surface_code_circuit(D, ROUNDS, True)

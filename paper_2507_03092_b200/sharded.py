@@ -126,11 +126,17 @@ class Exchange:
         self.nshards = self.world * self.local
         self.calls = {"allreduce_min": 0, "allgather": 0, "broadcast": 0}
         self.bytes = 0
+        # gloo has no CUDA all_gather: with that backend device buffers are staged through the host (used by the
+        # 2-process test that shares one GPU, where NCCL refuses two ranks on a device)
+        self.stage = self.on and td.get_backend() == "gloo"
+
+    def _to_wire(self, t):
+        return t.cpu() if (self.stage and t.is_cuda) else t
 
     def allreduce_min(self, tensors) -> np.ndarray:
         t = tensors[0] if len(tensors) == 1 else self.torch.stack(list(tensors)).amin(dim=0)
         if self.on and self.world > 1:
-            t = t.contiguous()
+            t = self._to_wire(t.contiguous())
             self.td.all_reduce(t, op=self.td.ReduceOp.MIN)
             self.calls["allreduce_min"] += 1
             self.bytes += t.numel() * 4
@@ -140,17 +146,21 @@ class Exchange:
         loc = self.torch.stack(list(tensors))                      # [local, m, PW]
         if not (self.on and self.world > 1):
             return loc.contiguous()
-        outs = [self.torch.empty_like(loc) for _ in range(self.world)]
-        self.td.all_gather(outs, loc.contiguous())
+        wire = self._to_wire(loc.contiguous())
+        outs = [self.torch.empty_like(wire) for _ in range(self.world)]
+        self.td.all_gather(outs, wire)
         self.calls["allgather"] += 1
         self.bytes += loc.numel() * 8 * self.world
-        return self.torch.cat(outs, dim=0).contiguous()            # [world * local, m, PW], shard order
+        return self.torch.cat(outs, dim=0).to(loc.device).contiguous()   # [world * local, m, PW], shard order
 
     def broadcast(self, row, owner_shard: int, empty):
         owner_rank = owner_shard // self.local
         buf = row if self.rank == owner_rank else empty()
         if self.on and self.world > 1:
-            self.td.broadcast(buf, src=owner_rank)
+            wire = self._to_wire(buf)
+            self.td.broadcast(wire, src=owner_rank)
+            if wire is not buf:
+                buf.copy_(wire)
             self.calls["broadcast"] += 1
             self.bytes += buf.numel() * 8
         return buf

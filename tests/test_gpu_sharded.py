@@ -87,3 +87,43 @@ def test_shard_argument_errors(sk, ctx):
     g = sk.gates_array([(T, 0, 0)])
     assert L.sk_shard_apply_gates(h, g.ctypes.data_as(C.c_void_p), 1) == sk.SK_EUNSUPPORTED
     L.sk_shard_destroy(h)
+
+
+def test_two_processes_one_shard_each_over_a_process_group(sk, orc):
+    """Two OS processes, one CudaShard each (both on GPU 0), exchanging through torch.distributed.  NCCL refuses two
+    ranks on one device, so the group is gloo with the device buffers staged through the host; the driver code and
+    every kernel are the ones an NCCL job runs."""
+    import os, socket, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = textwrap.dedent("""
+        import sys
+        sys.path.insert(0, %r)
+        import numpy as np
+        import paper_2507_03092_b200 as sk
+        from paper_2507_03092_b200 import dist
+        from paper_2507_03092_b200.sharded import ShardedTableau
+        from oracle import oracle_py as orc
+        rank, local_rank, world = dist.init("gloo")
+        for circ, seed in ((sk.surface_code_circuit(7, 7, True), 20250703), (sk.random_layered_circuit(128, 3), 5)):
+            t = ShardedTableau.create_cuda(circ.n, local_shards=1, device_index=0)
+            out, det = t.sim(circ, seed)
+            x, z, r = t.gather_tableau()
+            calls = dict(t.ex.calls)
+            t.close()
+            o = orc.Tableau(circ.n)
+            oo, od, rc = o.sim(circ.gates, seed)
+            ox, oz, orr = o.get()
+            assert rc == 0 and (out == oo).all() and (det == od).all(), "record differs from the oracle"
+            assert (x == ox).all() and (z == oz).all() and (r == orr).all(), "tableau differs from the oracle"
+            assert calls["broadcast"] == int((od == 0).sum()) and calls["allgather"] >= 1 and calls["allreduce_min"] >= 1
+        dist.finalize()
+        print("rank", rank, "ok")
+    """ % root)
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK="0", WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", script], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=280)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    assert "rank 0 ok" in outs[0] and "rank 1 ok" in outs[1], outs
