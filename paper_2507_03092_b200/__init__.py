@@ -191,7 +191,9 @@ class Circuit:
 
     @property
     def num_measurements(self) -> int:
-        return int((self.gates["kind"] == M).sum())
+        if getattr(self, "_nm", None) is None:             # counted once: a pass over the gate array costs milliseconds at d=71
+            self._nm = int((self.gates["kind"] == M).sum())
+        return self._nm
 
     def emit_native(self) -> str:
         """.stab text (SPEC:273 round trip)."""

@@ -900,10 +900,16 @@ extern "C" int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint
 static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, uint64_t seed,
                              sk_tableau** out_t, uint8_t* outcomes, uint8_t* deterministic) {
     const unsigned nthreads = host_threads(ngates);
+    static const bool dbg = getenv("SK_DEBUG_E2E") != nullptr;           // host-side stage times on stderr
+    const auto tp0 = std::chrono::steady_clock::now();
+    auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count(); };
+    double ts_val = 0, ts_scan = 0, ts_alloc = 0, ts_first = 0, ts_enq = 0, ts_join = 0;
     int32_t rc = validate_circuit(c, n, gates, ngates, nthreads);
     if (rc) return rc;
+    ts_val = since();
     size_t ng = 0, nm = 0;
     std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm, nthreads);
+    ts_scan = since();
     const size_t nboff = 2 * ng + 2 * segs.size() + 2;       // chunk tables: a run of k gates needs at most 2k + 2 entries
     rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + nboff * 4 + 64);
     if (rc) return rc;
@@ -920,11 +926,13 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     sk_tableau* t = nullptr;
     rc = sk_tableau_create(c, n, &t);
     if (rc) { sk_program_destroy(p); return rc; }
+    ts_alloc = since();
     std::atomic<size_t> next{0};
     std::vector<std::thread> workers;
     auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc, tctas); };
     for (unsigned k = 1; k < nthreads; ++k) workers.emplace_back(work);
     SegScratch mine;
+    size_t uploaded = 0, nbatches = 0;          // segments [0, uploaded) are on the device
     for (size_t si = 0; si < segs.size() && !rc; ++si) {
         Seg& sg = segs[si];
         while (!sg.done.load(std::memory_order_acquire)) {
@@ -932,18 +940,33 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             else std::this_thread::yield();
         }
         const size_t cnt = sg.hi - sg.lo;
-        if (sg.meas) {
-            e = cudaMemcpyAsync(p->d_mq + sg.out, h_mq + sg.out, cnt * 4, cudaMemcpyHostToDevice, c->stream);
+        if (si == 0) ts_first = since();
+        if (si >= uploaded) {
+            // one copy per array for every segment the workers have finished by now (they run ahead while the device is busy
+            // with a measurement block): the ordered gates and the measured qubits are contiguous across segments
+            size_t e_seg = si + 1;
+            while (e_seg < segs.size() && segs[e_seg].done.load(std::memory_order_acquire)) ++e_seg;
+            size_t g_lo = ~size_t(0), g_hi = 0, m_lo = ~size_t(0), m_hi = 0, b_lo = ~size_t(0), b_hi = 0;
+            for (size_t k = si; k < e_seg; ++k) {
+                const Seg& q = segs[k]; const size_t qc = q.hi - q.lo;
+                if (q.meas) { m_lo = std::min(m_lo, q.out); m_hi = std::max(m_hi, q.out + qc); }
+                else {
+                    g_lo = std::min(g_lo, q.out); g_hi = std::max(g_hi, q.out + qc);
+                    if (!q.boff.empty()) {
+                        std::memcpy(h_boff + q.bslot, q.boff.data(), q.boff.size() * 4);
+                        b_lo = std::min(b_lo, q.bslot); b_hi = std::max(b_hi, q.bslot + q.boff.size());
+                    }
+                }
+            }
+            if (!e && m_hi > m_lo) e = cudaMemcpyAsync(p->d_mq + m_lo, h_mq + m_lo, (m_hi - m_lo) * 4, cudaMemcpyHostToDevice, c->stream);
+            if (!e && g_hi > g_lo) e = cudaMemcpyAsync(p->d_gates + g_lo, h_gates + g_lo, (g_hi - g_lo) * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
+            if (!e && b_hi > b_lo) e = cudaMemcpyAsync(p->d_boff + b_lo, h_boff + b_lo, (b_hi - b_lo) * 4, cudaMemcpyHostToDevice, c->stream);
             if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
+            uploaded = e_seg; ++nbatches;
+        }
+        if (sg.meas) {
             rc = launch_measure(t, p->d_mq + sg.out, int(cnt), seed, sg.out, p->d_out + sg.out, p->d_det + sg.out);
         } else {
-            e = cudaMemcpyAsync(p->d_gates + sg.out, h_gates + sg.out, cnt * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
-            if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
-            if (!sg.boff.empty()) {
-                std::memcpy(h_boff + sg.bslot, sg.boff.data(), sg.boff.size() * 4);
-                e = cudaMemcpyAsync(p->d_boff + sg.bslot, h_boff + sg.bslot, sg.boff.size() * 4, cudaMemcpyHostToDevice, c->stream);
-                if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
-            }
             size_t base = sg.out, bo = 0;
             for (size_t k = 0; k < sg.sizes.size(); ++k) {
                 const uint32_t nb = sg.gblocks[k];
@@ -953,14 +976,19 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             }
         }
     }
+    ts_enq = since();
     next = segs.size();
     for (auto& w : workers) w.join();
+    ts_join = since();
     if (!rc) {
         uint64_t hist[12] = {0};
         for (size_t i = 0; i < ngates; ++i) hist[gates[i].kind]++;
         for (int k = 0; k < 12; ++k) c->cnt.gate_hist[k] += hist[k];
         p->last_t = t;
+        const double ts_hist = since();
         rc = sk_program_read_record(p, outcomes, deterministic);
+        if (dbg) fprintf(stderr, "sk_sim host ms: validate %.2f scan %.2f alloc+tableau %.2f first segment ready %.2f all enqueued %.2f workers joined %.2f histogram %.2f record read (device done) %.2f | %u threads, %zu segments in %zu uploads\n",
+                         ts_val, ts_scan, ts_alloc, ts_first, ts_enq, ts_join, ts_hist, since(), nthreads, segs.size(), nbatches);
     } else cudaStreamSynchronize(c->stream);
     sk_program_destroy(p);
     if (rc) { sk_tableau_destroy(t); return rc; }
