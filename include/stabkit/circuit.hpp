@@ -59,6 +59,16 @@ inline Circuit parse_native(std::string_view text) {
     return detail::take_circuit(n, g, ng, marks, nm);
 }
 
+// SPEC:252-260
+inline Circuit parse_qasm2_subset(std::string_view text) {
+    uint64_t n = 0; sk_gate* g = nullptr; size_t ng = 0, nm = 0, line = 0; uint32_t* marks = nullptr; char msg[256] = {0};
+    const int rc = sk_circuit_parse_qasm2(text.data(), text.size(), &n, &g, &ng, &marks, &nm, &line, msg, sizeof msg);
+    if (rc == SK_EPARSE) throw ParseError(line, msg);
+    if (rc == SK_EUNSUPPORTED) throw UnsupportedError(msg);
+    if (rc != SK_OK) throw Error("parse_qasm2_subset failed");
+    return detail::take_circuit(n, g, ng, marks, nm);
+}
+
 // inverse of parse_native
 inline std::string emit_native(const Circuit& c) {
     static const char* names[] = {"h", "s", "sdg", "x", "y", "z", "cx", "cz", "swap", "m", "t", "tdg"};

@@ -40,4 +40,25 @@ inline SimResult sim(const Circuit& c, const EngineConfig& cfg) { return detail:
 // SPEC:320-328; chunk_size_hint is advisory
 inline SimResult sim2d(const Circuit& c, size_t /*chunk_size_hint*/, const EngineConfig& cfg) { return detail::run(c, cfg, 1); }
 
+// per-measurement-site counts of outcome 1 over `shots` runs, shot s seeded cfg.seed ^ s.
+// The circuit is compiled once and stays on the device; counts are accumulated there.
+struct ShotHistogram { uint64_t shots = 0; std::vector<uint32_t> ones; std::vector<std::vector<uint8_t>> records; };
+inline ShotHistogram run_shots(const Circuit& c, uint64_t shots, const EngineConfig& cfg, bool keep_records = false) {
+    if (shots < 1) throw Error("run_shots: shots must be >= 1 (SPEC:332)");
+    Device& d = Device::instance();
+    sk_program* p = nullptr; sk_tableau* t = nullptr; uint32_t warn = 0;
+    d.check(sk_program_create(d.ctx(), c.n, c.raw(), c.gates.size(), c.chunk_marks.data(), c.chunk_marks.size(), 0, &p, &warn));
+    const int32_t rc_t = sk_tableau_create(d.ctx(), c.n, &t);
+    if (rc_t) { sk_program_destroy(p); d.check(rc_t); }
+    const size_t nm = c.num_measurements();
+    ShotHistogram h; h.shots = shots; h.ones.assign(nm + 1, 0);
+    std::vector<uint8_t> flat(keep_records ? shots * nm + 1 : 0);
+    const int32_t rc = sk_program_run_shots(p, t, shots, cfg.seed, h.ones.data(), keep_records ? flat.data() : nullptr);
+    sk_tableau_destroy(t); sk_program_destroy(p);
+    d.check(rc);
+    h.ones.resize(nm);
+    if (keep_records) for (uint64_t s = 0; s < shots; ++s) h.records.emplace_back(flat.begin() + s * nm, flat.begin() + (s + 1) * nm);
+    return h;
+}
+
 }  // namespace stabkit

@@ -133,6 +133,12 @@ int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed);
 /* Same, with CUDA events around every launch: class_ms = device ms spent in {fused layers,
  * transposes, measurement blocks}.  Synchronises; for roofline reporting, not for timing runs. */
 int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[3]);
+/* SPEC:330-338 run_shots: `shots` runs from the identity tableau with seeds seed ^ shot_index.
+ * ones[i] = number of shots in which measurement site i gave 1 (accumulated on the device);
+ * records (optional, may be NULL) receives every shot's outcome bytes, [shots][measurements].
+ * t ends in the state of the last shot.  shots == 0 -> SK_EARG.  Synchronises. */
+int32_t sk_program_run_shots(sk_program* p, sk_tableau* t, uint64_t shots, uint64_t seed,
+                             uint32_t* ones, uint8_t* records);
 /* outcome / deterministic byte per M gate in circuit order (MeasurementRecord). */
 int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic);
 /* Convenience: identity tableau -> run -> record.  *out_t receives the final tableau. */
@@ -155,6 +161,12 @@ int32_t sk_circuit_random_layered(uint64_t n, uint64_t seed, sk_gate** gates, si
 int32_t sk_circuit_parse_native(const char* text, size_t len, uint64_t* n, sk_gate** gates,
                                 size_t* ngates, uint32_t** chunk_marks, size_t* nmarks,
                                 size_t* err_line, char* err_msg, size_t err_cap);
+/* SPEC:252-260 parse_qasm2_subset (OPENQASM 2.0 header, one qreg, optional cregs, h s sdg x y z cx cz swap t tdg,
+ * `measure q[i] -> c[j];` -> M, `barrier` -> chunk mark).  Unsupported constructs (second qreg, parameterised or unknown
+ * gates, `if`, `gate`, `reset`) -> SK_EUNSUPPORTED, malformed text -> SK_EPARSE; err_msg names the construct and line. */
+int32_t sk_circuit_parse_qasm2(const char* text, size_t len, uint64_t* n, sk_gate** gates,
+                               size_t* ngates, uint32_t** chunk_marks, size_t* nmarks,
+                               size_t* err_line, char* err_msg, size_t err_cap);
 /* SPEC:262-270.  violations: pairs (chunk index, gate index); kind bit 0 = collision, bit 1 = measurement. */
 int32_t sk_circuit_validate_chunks(uint64_t n, const sk_gate* gates, size_t ngates,
                                    const uint32_t* chunk_marks, size_t nmarks,

@@ -86,11 +86,13 @@ def lib() -> C.CDLL:
             "sk_program_run": (i32, [vp, vp, u64]),
             "sk_program_run_profiled": (i32, [vp, vp, u64, P(C.c_float)]),
             "sk_program_read_record": (i32, [vp, vp, vp]),
+            "sk_program_run_shots": (i32, [vp, vp, u64, u64, vp, vp]),
             "sk_sim": (i32, [vp, u64, vp, sz, vp, sz, C.c_int, u64, P(vp), vp, vp, P(u32)]),
             "sk_free": (None, [vp]),
             "sk_circuit_surface_code": (i32, [u32, u32, C.c_int, P(u64), P(vp), P(sz), P(vp), P(sz)]),
             "sk_circuit_random_layered": (i32, [u64, u64, P(vp), P(sz), P(vp), P(sz)]),
             "sk_circuit_parse_native": (i32, [C.c_char_p, sz, P(u64), P(vp), P(sz), P(vp), P(sz), P(sz), C.c_char_p, sz]),
+            "sk_circuit_parse_qasm2": (i32, [C.c_char_p, sz, P(u64), P(vp), P(sz), P(vp), P(sz), P(sz), C.c_char_p, sz]),
             "sk_circuit_validate_chunks": (i32, [u64, vp, sz, vp, sz, P(vp), P(vp), P(vp), P(sz)]),
             "sk_rows_create": (i32, [vp, u64, u64, P(vp)]),
             "sk_rows_destroy": (None, [vp]),
@@ -135,8 +137,8 @@ EXPORTS = [
     "sk_get_counters", "sk_reset_counters", "sk_tableau_create", "sk_tableau_destroy", "sk_tableau_reset",
     "sk_tableau_qubits", "sk_tableau_upload", "sk_tableau_download", "sk_apply_layer", "sk_apply_gates",
     "sk_measure_z", "sk_measure_batch", "sk_tableau_rowsum", "sk_program_create", "sk_program_destroy",
-    "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_sim", "sk_free",
-    "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native",
+    "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_program_run_shots", "sk_sim", "sk_free",
+    "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native", "sk_circuit_parse_qasm2",
     "sk_circuit_validate_chunks", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
     "sk_rows_download", "sk_rows_conj_layer", "sk_commutation_vector",
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",
@@ -239,6 +241,21 @@ def parse_native(text: str) -> Circuit:
         e.line = line.value
         raise e
     _check_noctx(rc, "parse_native")
+    return Circuit(n.value, _take(g, ng.value, GATE_DTYPE), _take(mk, nmk.value, np.uint32))
+
+
+def parse_qasm2_subset(text: str) -> Circuit:
+    """SPEC:252-260.  Unsupported constructs raise UnsupportedError, malformed text ParseError (both carry .line)."""
+    L = lib()
+    raw = text.encode()
+    n, g, ng, mk, nmk, line = C.c_uint64(), C.c_void_p(), C.c_size_t(), C.c_void_p(), C.c_size_t(), C.c_size_t()
+    msg = C.create_string_buffer(256)
+    rc = L.sk_circuit_parse_qasm2(raw, len(raw), C.byref(n), C.byref(g), C.byref(ng), C.byref(mk), C.byref(nmk), C.byref(line), msg, 256)
+    if rc in (SK_EPARSE, SK_EUNSUPPORTED):
+        e = (ParseError if rc == SK_EPARSE else UnsupportedError)(rc, f"line {line.value}: {msg.value.decode()}")
+        e.line = line.value
+        raise e
+    _check_noctx(rc, "parse_qasm2_subset")
     return Circuit(n.value, _take(g, ng.value, GATE_DTYPE), _take(mk, nmk.value, np.uint32))
 
 
@@ -380,6 +397,14 @@ class Program:
         ms = (C.c_float * 3)()
         self.ctx.check(lib().sk_program_run_profiled(self._h, t._h, seed, ms))
         return {"layer_ms": float(ms[0]), "transpose_ms": float(ms[1]), "measure_ms": float(ms[2])}
+
+    def run_shots(self, t: Tableau, shots: int, seed: int, records: bool = False):
+        """SPEC:330-338.  -> (ones[nm] u32, records[shots, nm] u8 or None); shot s uses seed ^ s."""
+        nm = self.num_measurements
+        ones = np.zeros(max(nm, 1), np.uint32)
+        rec = np.zeros((shots, max(nm, 1)), np.uint8) if records else None
+        self.ctx.check(lib().sk_program_run_shots(self._h, t._h, shots, seed, _ptr(ones), _ptr(rec)))
+        return ones[:nm], (rec[:, :nm] if records else None)
 
     def read_record(self):
         nm = self.num_measurements

@@ -200,6 +200,128 @@ extern "C" int32_t sk_circuit_parse_native(const char* text, size_t len, uint64_
     return (*gates_out && *marks_out) ? SK_OK : SK_ECUDA;
 }
 
+// SPEC:252-260 parse_qasm2_subset: OPENQASM 2.0 header, one qreg, optional cregs, gates {h,s,sdg,x,y,z,cx,cz,swap,t,tdg},
+// `measure q[i] -> c[j];` -> M, `barrier` -> chunk mark; a bare register name applies the statement to every qubit.
+// Unsupported constructs (second qreg, parameterised / unknown gates, `if`, `gate`, `reset`, `opaque`) -> SK_EUNSUPPORTED with
+// the construct and its line in err_msg; malformed text -> SK_EPARSE.
+extern "C" int32_t sk_circuit_parse_qasm2(const char* text, size_t len, uint64_t* n_out, sk_gate** gates_out,
+                                          size_t* ngates_out, uint32_t** marks_out, size_t* nmarks_out,
+                                          size_t* err_line, char* err_msg, size_t err_cap) {
+    if (!text || !n_out || !gates_out || !ngates_out || !marks_out || !nmarks_out) return SK_EARG;
+    auto fail = [&](int32_t code, size_t line, const std::string& what) {
+        if (err_line) *err_line = line;
+        if (err_msg && err_cap) { std::snprintf(err_msg, err_cap, "%s", what.c_str()); }
+        return code;
+    };
+    static const struct { const char* name; uint8_t kind; int arity; } table[] = {
+        {"h", SK_H, 1}, {"s", SK_S, 1}, {"sdg", SK_SDG, 1}, {"x", SK_X, 1}, {"y", SK_Y, 1}, {"z", SK_Z, 1},
+        {"cx", SK_CX, 2}, {"CX", SK_CX, 2}, {"cz", SK_CZ, 2}, {"swap", SK_SWAP, 2}, {"t", SK_T, 1}, {"tdg", SK_TDG, 1}};
+    std::vector<sk_gate> g; std::vector<uint32_t> marks;
+    std::string qname; uint64_t n = 0; bool have_q = false;
+    std::vector<std::string> cregs;
+    // strip // comments, then split into ';'-terminated statements remembering the line each one starts on
+    std::string src(text, len);
+    for (size_t i = 0; i + 1 < src.size(); ++i)
+        if (src[i] == '/' && src[i + 1] == '/') { while (i < src.size() && src[i] != '\n') src[i++] = ' '; }
+    size_t line = 1, pos = 0;
+    auto is_id = [](char c) { return std::isalnum((unsigned char)c) || c == '_'; };
+    // operand "name" or "name[idx]" -> (name, idx or -1)
+    auto operand = [&](std::string t, std::string* name, long long* idx) {
+        size_t a = 0; while (a < t.size() && std::isspace((unsigned char)t[a])) ++a;
+        size_t b = t.size(); while (b > a && std::isspace((unsigned char)t[b - 1])) --b;
+        t = t.substr(a, b - a);
+        size_t lb = t.find('[');
+        if (lb == std::string::npos) { *name = t; *idx = -1; for (char c : t) if (!is_id(c)) return false; return !t.empty(); }
+        if (t.back() != ']') return false;
+        *name = t.substr(0, lb);
+        for (char c : *name) if (!is_id(c)) return false;
+        std::string num = t.substr(lb + 1, t.size() - lb - 2);
+        if (name->empty() || num.empty() || num.size() > 12) return false;
+        long long v = 0; for (char c : num) { if (c < '0' || c > '9') return false; v = v * 10 + (c - '0'); }
+        *idx = v; return true;
+    };
+    while (pos < src.size()) {
+        while (pos < src.size() && std::isspace((unsigned char)src[pos])) { if (src[pos] == '\n') ++line; ++pos; }
+        if (pos >= src.size()) break;
+        const size_t sline = line;
+        size_t end = pos;
+        while (end < src.size() && src[end] != ';') { if (src[end] == '\n') ++line; if (src[end] == '{') break; ++end; }
+        std::string st = src.substr(pos, end - pos);
+        if (end < src.size() && src[end] == '{') return fail(SK_EUNSUPPORTED, sline, "unsupported construct: block statement '" + st.substr(0, st.find_first_of(" \t\n")) + "' (line " + std::to_string(sline) + ")");
+        if (end >= src.size()) return fail(SK_EPARSE, sline, "statement is not terminated by ';'");
+        pos = end + 1;
+        for (char& c : st) if (c == '\n' || c == '\t' || c == '\r') c = ' ';
+        size_t k = 0; while (k < st.size() && (is_id(st[k]) || st[k] == '.')) ++k;
+        const std::string head = st.substr(0, k);
+        std::string rest = st.substr(k);
+        if (head == "OPENQASM") { if (rest.find("2.0") == std::string::npos) return fail(SK_EUNSUPPORTED, sline, "unsupported construct: OPENQASM version" + rest + " (line " + std::to_string(sline) + ")"); continue; }
+        if (head == "include") continue;
+        if (head == "qreg" || head == "creg") {
+            std::string name; long long sz = -1;
+            if (!operand(rest, &name, &sz) || sz <= 0) return fail(SK_EPARSE, sline, "expected '" + head + " name[size]'");
+            if (head == "qreg") {
+                if (have_q) return fail(SK_EUNSUPPORTED, sline, "unsupported construct: multiple qregs ('" + name + "', line " + std::to_string(sline) + ")");
+                have_q = true; qname = name; n = uint64_t(sz);
+            } else cregs.push_back(name);
+            continue;
+        }
+        if (head == "if" || head == "gate" || head == "opaque" || head == "reset" || head == "U" || head == "u1" || head == "u2" || head == "u3")
+            return fail(SK_EUNSUPPORTED, sline, "unsupported construct: '" + head + "' (line " + std::to_string(sline) + ")");
+        if (!rest.empty() && rest.find('(') != std::string::npos && head != "measure")
+            return fail(SK_EUNSUPPORTED, sline, "unsupported construct: parameterised gate '" + head + "' (line " + std::to_string(sline) + ")");
+        if (!have_q) return fail(SK_EPARSE, sline, "statement before the qreg declaration");
+        auto qubit = [&](const std::string& t, long long* idx) -> int32_t {
+            std::string name;
+            if (!operand(t, &name, idx)) return SK_EPARSE;
+            if (name != qname) return SK_EPARSE;
+            if (*idx >= (long long)n) return SK_EDIM;
+            return SK_OK;
+        };
+        if (head == "barrier") {
+            if (!g.empty() && (marks.empty() || marks.back() != g.size())) marks.push_back(uint32_t(g.size()));
+            continue;
+        }
+        if (head == "measure") {
+            size_t arrow = rest.find("->");
+            if (arrow == std::string::npos) return fail(SK_EPARSE, sline, "expected 'measure q[i] -> c[j]'");
+            long long qi = -1, ci = -1; std::string cname;
+            int32_t rc = qubit(rest.substr(0, arrow), &qi);
+            if (rc == SK_EDIM) return fail(SK_EPARSE, sline, "qubit index out of range in 'measure'");
+            if (rc || !operand(rest.substr(arrow + 2), &cname, &ci)) return fail(SK_EPARSE, sline, "expected 'measure q[i] -> c[j]'");
+            bool known = false; for (const std::string& c : cregs) known |= (c == cname);
+            if (!known) return fail(SK_EPARSE, sline, "measure into undeclared creg '" + cname + "'");
+            if (qi < 0) { for (uint64_t q = 0; q < n; ++q) g.push_back(mk(SK_M, uint32_t(q), 0)); }
+            else g.push_back(mk(SK_M, uint32_t(qi), 0));
+            continue;
+        }
+        int found = -1;
+        for (int t = 0; t < 12; ++t) if (head == table[t].name) found = t;
+        if (found < 0) return fail(SK_EUNSUPPORTED, sline, "unsupported construct: gate '" + head + "' (line " + std::to_string(sline) + ")");
+        std::vector<std::string> ops;
+        { size_t a = 0; while (true) { size_t c = rest.find(',', a); ops.push_back(rest.substr(a, c == std::string::npos ? std::string::npos : c - a)); if (c == std::string::npos) break; a = c + 1; } }
+        if (int(ops.size()) != table[found].arity) return fail(SK_EPARSE, sline, "'" + head + "' expects " + std::to_string(table[found].arity) + " operand(s)");
+        long long q[2] = {0, 0};
+        for (int t = 0; t < table[found].arity; ++t) {
+            int32_t rc = qubit(ops[t], &q[t]);
+            if (rc == SK_EDIM) return fail(SK_EPARSE, sline, "qubit index out of range for " + std::to_string(n) + " qubits");
+            if (rc) return fail(SK_EPARSE, sline, "bad operand '" + ops[t] + "'");
+        }
+        if (table[found].arity == 1) {
+            if (q[0] < 0) { for (uint64_t v = 0; v < n; ++v) g.push_back(mk(table[found].kind, uint32_t(v), 0)); }
+            else g.push_back(mk(table[found].kind, uint32_t(q[0]), 0));
+        } else {
+            if (q[0] < 0 || q[1] < 0) return fail(SK_EUNSUPPORTED, sline, "unsupported construct: register-wide two-qubit gate (line " + std::to_string(sline) + ")");
+            if (q[0] == q[1]) return fail(SK_EPARSE, sline, "two-qubit gate on duplicate qubit");
+            g.push_back(mk(table[found].kind, uint32_t(q[0]), uint32_t(q[1])));
+        }
+    }
+    if (!have_q) return fail(SK_EPARSE, line, "missing qreg declaration");
+    while (!marks.empty() && marks.back() >= g.size()) marks.pop_back();
+    *n_out = n; *gates_out = dup(g); *ngates_out = g.size(); *marks_out = dup(marks); *nmarks_out = marks.size();
+    if (err_line) *err_line = 0;
+    return (*gates_out && *marks_out) ? SK_OK : SK_ECUDA;
+}
+
 // SPEC:262-270 validate_chunks.
 extern "C" int32_t sk_circuit_validate_chunks(uint64_t n, const sk_gate* gates, size_t ngates,
                                               const uint32_t* marks, size_t nmarks,

@@ -881,6 +881,38 @@ extern "C" int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_
     return program_run_impl(p, t, seed, class_ms);
 }
 
+// SPEC:330-338 run_shots: per-site counts of outcome 1 over `shots` runs with seeds seed ^ shot (device-side accumulation;
+// nothing is synchronised between shots).
+__global__ void k_accumulate_ones(const uint8_t* __restrict__ out, u32* __restrict__ counts, size_t nm) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nm && out[i]) counts[i] += 1u;
+}
+extern "C" int32_t sk_program_run_shots(sk_program* p, sk_tableau* t, uint64_t shots, uint64_t seed, uint32_t* ones, uint8_t* records) {
+    if (!p || !t || !ones) return SK_EARG;
+    sk_ctx* c = p->ctx;
+    if (shots == 0) SK_FAIL(c, SK_EARG, "run_shots: shots must be >= 1 (SPEC:332)");
+    const size_t nm = p->nmeas;
+    u32* d_counts = nullptr;
+    if (nm) { SK_CUDA(c, dmalloc(c, &d_counts, nm * 4)); SK_CUDA(c, cudaMemsetAsync(d_counts, 0, nm * 4, c->stream)); }
+    const int keep = c->no_graph;
+    c->no_graph = 1;                       // the seed changes every shot: plain launches instead of re-capturing a graph per shot
+    int32_t rc = SK_OK;
+    for (uint64_t s = 0; s < shots && !rc; ++s) {
+        rc = tableau_identity(t);
+        if (!rc) rc = program_run_impl(p, t, seed ^ s, nullptr);
+        if (!rc && nm) {
+            k_accumulate_ones<<<(unsigned)((nm + 255) / 256), 256, 0, c->stream>>>(p->d_out, d_counts, nm);
+            c->cnt.kernel_launches++;
+            if (records && cudaMemcpyAsync(records + s * nm, p->d_out, nm, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { c->err = "run_shots: record copy failed"; rc = SK_ECUDA; }
+        }
+    }
+    c->no_graph = keep;
+    if (!rc && nm && cudaMemcpyAsync(ones, d_counts, nm * 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { c->err = "run_shots: count copy failed"; rc = SK_ECUDA; }
+    const int32_t rc2 = check_ws(c);       // synchronises
+    dfree(c, d_counts);
+    return rc ? rc : rc2;
+}
+
 extern "C" int32_t sk_program_read_record(sk_program* p, uint8_t* outcomes, uint8_t* deterministic) {
     if (!p) return SK_EARG;
     sk_ctx* c = p->ctx;

@@ -41,6 +41,10 @@ static void cpu_checks() {
     CHECK(parse_native("qubits 2\nh 0\nchunk\nh 1").chunk_marks == std::vector<uint32_t>{1});
     CHECK(parse_native(emit_native(bell)).gates == bell.gates);
     CHECK(validate_chunks(parse_native("qubits 2\nh 0\ncx 0 1")).size() == 1);
+    // parse_qasm2_subset
+    CHECK(parse_qasm2_subset("OPENQASM 2.0;\ninclude \"qelib1.inc\";\nqreg q[2];\ncreg c[2];\nh q[0];\ncx q[0],q[1];\nmeasure q[0] -> c[0];\nmeasure q[1] -> c[1];\n").gates == bell.gates);
+    CHECK(throws<UnsupportedError>([] { parse_qasm2_subset("OPENQASM 2.0;\nqreg q[1];\nrz(0.1) q[0];\n"); }));
+    { Circuit c = parse_qasm2_subset("OPENQASM 2.0;\nqreg q[4];\nt q[2];\n"); CHECK(c.n == 4 && c.gates.size() == 1 && c.gates[0].kind == GateKind::T && c.gates[0].q0 == 2); }
     // qec_gen
     CHECK(surface_code_circuit(3, 1).n == 17 && surface_code_circuit(3, 2).num_measurements() == 16);
     CHECK(throws<Error>([] { surface_code_circuit(2, 1); }) && throws<Error>([] { random_layered_circuit(7, 1); }));
@@ -69,6 +73,13 @@ static void gpu_checks() {
     CHECK(a.record.size() == b.record.size() && a.tableau.rows() == b.tableau.rows() && !b.chunk_fallback);
     for (size_t i = 0; i < a.record.size(); ++i) CHECK(a.record[i].outcome == b.record[i].outcome && a.record[i].deterministic == b.record[i].deterministic);
     CHECK(throws<UnsupportedError>([] { sim(parse_native("qubits 1\nt 0"), EngineConfig{}); }));
+    // run_shots
+    { ShotHistogram h = run_shots(parse_native("qubits 3\nh 0\ncx 0 1\ncx 1 2\nm 0\nm 1\nm 2"), 400, EngineConfig{1, 11, false}, true);
+      bool ghz = h.ones[0] == h.ones[1] && h.ones[1] == h.ones[2] && h.ones[0] > 120 && h.ones[0] < 280;
+      for (const auto& r : h.records) ghz = ghz && r[0] == r[1] && r[1] == r[2];
+      CHECK(ghz);
+      ShotHistogram z = run_shots(parse_native("qubits 1\nm 0"), 50, EngineConfig{1, 3, false});
+      CHECK(z.ones.size() == 1 && z.ones[0] == 0); }
     // pauli_core batch op on the device
     std::vector<PauliString> rows = {PauliString::parse("ZZ"), PauliString::parse("ZI")};
     BitVec cv = commutation_vector(PauliString::parse("XX"), rows);

@@ -295,3 +295,28 @@ def test_dense_tableau_falls_back_to_column_form(sk, orc):
         assert dc[k] == oc[k], k
     assert dc["k_rand"] > 1984 * 10          # dense indeed: thousands of rows multiplied per random measurement
     t.close(); c2.close()
+
+
+def test_run_shots_histogram_and_per_shot_records(sk, ctx, orc):
+    """SPEC:330-338 run_shots: seeds seed ^ shot; |+> is 50/50 within 3 sigma, |0> all zero, GHZ-3 only 000 / 111;
+    every shot's record equals the oracle run with that seed."""
+    shots = 2000
+    circ = sk.Circuit(5, [(H, 0, 0), (M, 0, 0), (M, 1, 0), (H, 2, 0), (CX, 2, 3), (CX, 3, 4), (M, 2, 0), (M, 3, 0), (M, 4, 0)])
+    prog = sk.Program(ctx, circ); t = sk.Tableau(ctx, circ.n)
+    ones, rec = prog.run_shots(t, shots, SEED, records=True)
+    assert abs(ones[0] / shots - 0.5) < 0.034 and ones[1] == 0
+    assert (rec[:, 2] == rec[:, 3]).all() and (rec[:, 3] == rec[:, 4]).all() and 0 < ones[2] < shots
+    assert (ones == rec.sum(axis=0)).all()
+    for s in (0, 1, 7, 1999):
+        o = orc.Tableau(circ.n)
+        oo, _, rc = o.sim(circ.gates, SEED ^ s)
+        assert rc == 0 and (rec[s] == oo).all()
+    sc = sk.surface_code_circuit(5, 5, True)
+    prog2 = sk.Program(ctx, sc); t2 = sk.Tableau(ctx, sc.n)
+    ones2, rec2 = prog2.run_shots(t2, 16, 3, records=True)
+    for s in range(16):
+        o = orc.Tableau(sc.n)
+        oo, _, rc = o.sim(sc.gates, 3 ^ s)
+        assert rc == 0 and (rec2[s] == oo).all()
+    assert (ones2 == rec2.sum(axis=0)).all()
+    prog.close(); prog2.close(); t.close(); t2.close()

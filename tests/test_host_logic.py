@@ -102,3 +102,28 @@ def test_validate_chunks(sk):
     assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\nh 1")) == []
     assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\ncx 0 1")) == [(0, 1, "collision")]
     assert sk.validate_chunks(sk.parse_native("qubits 1\nm 0")) == [(0, 0, "measurement")]
+
+
+def test_parse_qasm2_subset(sk):
+    bell = sk.parse_native("qubits 2\nh 0\ncx 0 1\nm 0\nm 1")
+    q = sk.parse_qasm2_subset('OPENQASM 2.0;\ninclude "qelib1.inc";\nqreg q[2];\ncreg c[2];\n// Bell pair\nh q[0];\ncx q[0],q[1];\nmeasure q[0] -> c[0];\nmeasure q[1] -> c[1];\n')
+    assert q.n == 2 and (q.gates == bell.gates).all() and len(q.chunk_marks) == 0
+    with pytest.raises(sk.UnsupportedError) as e:
+        sk.parse_qasm2_subset("OPENQASM 2.0;\nqreg q[1];\nrz(0.1) q[0];\n")
+    assert e.value.line == 3 and "rz" in str(e.value)
+    c = sk.parse_qasm2_subset("OPENQASM 2.0;\nqreg q[4];\nt q[2];\n")
+    assert c.n == 4 and len(c.gates) == 1 and int(c.gates[0]["kind"]) == sk.T and int(c.gates[0]["q0"]) == 2
+    # barrier -> chunk mark; register-wide statements; every supported mnemonic
+    c = sk.parse_qasm2_subset("OPENQASM 2.0; qreg r[3]; creg m[3]; h r; barrier r; s r[0]; sdg r[1]; x r[2]; y r[0]; z r[1];\n"
+                              "cz r[0],r[1]; swap r[1],r[2]; tdg r[0]; barrier r[0],r[1]; measure r -> m;")
+    assert [int(k) for k in c.gates["kind"]] == [sk.H] * 3 + [sk.S, sk.SDG, sk.X, sk.Y, sk.Z, sk.CZ, sk.SWAP, sk.TDG] + [sk.M] * 3
+    assert list(c.chunk_marks) == [3, 11]
+    for bad, exc in (("OPENQASM 2.0; qreg a[2]; qreg b[2];", sk.UnsupportedError), ("OPENQASM 2.0; qreg q[2]; creg c[2]; if (c==1) x q[0];", sk.UnsupportedError),
+                     ("OPENQASM 2.0; qreg q[2]; gate foo a { h a; }", sk.UnsupportedError), ("OPENQASM 2.0; qreg q[2]; ccx q[0],q[1],q[0];", sk.UnsupportedError),
+                     ("OPENQASM 2.0; qreg q[2]; h q[2];", sk.ParseError), ("OPENQASM 2.0; qreg q[2]; cx q[0],q[0];", sk.ParseError),
+                     ("OPENQASM 2.0; qreg q[2]; h q[0]", sk.ParseError), ("OPENQASM 2.0; h q[0];", sk.ParseError),
+                     ("OPENQASM 3.0; qreg q[2];", sk.UnsupportedError), ("OPENQASM 2.0; qreg q[2]; measure q[0] -> c[0];", sk.ParseError)):
+        with pytest.raises(exc):
+            sk.parse_qasm2_subset(bad)
+    # the parsed circuit round-trips through the native format
+    assert (sk.parse_native(c.emit_native()).gates == c.gates).all()
