@@ -965,47 +965,80 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     for (unsigned k = 1; k < nthreads; ++k) workers.emplace_back(work);
     SegScratch mine;
     size_t uploaded = 0, nbatches = 0;          // segments [0, uploaded) are on the device
-    for (size_t si = 0; si < segs.size() && !rc; ++si) {
-        Seg& sg = segs[si];
-        while (!sg.done.load(std::memory_order_acquire)) {
+    auto wait_done = [&](size_t si) {           // helps compiling while it waits
+        while (!segs[si].done.load(std::memory_order_acquire)) {
             if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine, tctas); }
             else std::this_thread::yield();
         }
-        const size_t cnt = sg.hi - sg.lo;
-        if (si == 0) ts_first = since();
-        if (si >= uploaded) {
-            // one copy per array for every segment the workers have finished by now (they run ahead while the device is busy
-            // with a measurement block): the ordered gates and the measured qubits are contiguous across segments
-            size_t e_seg = si + 1;
-            while (e_seg < segs.size() && segs[e_seg].done.load(std::memory_order_acquire)) ++e_seg;
-            size_t g_lo = ~size_t(0), g_hi = 0, m_lo = ~size_t(0), m_hi = 0, b_lo = ~size_t(0), b_hi = 0;
-            for (size_t k = si; k < e_seg; ++k) {
-                const Seg& q = segs[k]; const size_t qc = q.hi - q.lo;
-                if (q.meas) { m_lo = std::min(m_lo, q.out); m_hi = std::max(m_hi, q.out + qc); }
-                else {
-                    g_lo = std::min(g_lo, q.out); g_hi = std::max(g_hi, q.out + qc);
-                    if (!q.boff.empty()) {
-                        std::memcpy(h_boff + q.bslot, q.boff.data(), q.boff.size() * 4);
-                        b_lo = std::min(b_lo, q.bslot); b_hi = std::max(b_hi, q.bslot + q.boff.size());
-                    }
+    };
+    // one copy per array for every segment the workers have finished by now (they run ahead while the device is busy
+    // with a measurement block): the ordered gates and the measured qubits are contiguous across segments
+    auto upload_from = [&](size_t si) -> int32_t {
+        size_t e_seg = si + 1;
+        while (e_seg < segs.size() && segs[e_seg].done.load(std::memory_order_acquire)) ++e_seg;
+        size_t g_lo = ~size_t(0), g_hi = 0, m_lo = ~size_t(0), m_hi = 0, b_lo = ~size_t(0), b_hi = 0;
+        for (size_t k = si; k < e_seg; ++k) {
+            const Seg& q = segs[k]; const size_t qc = q.hi - q.lo;
+            if (q.meas) { m_lo = std::min(m_lo, q.out); m_hi = std::max(m_hi, q.out + qc); }
+            else {
+                g_lo = std::min(g_lo, q.out); g_hi = std::max(g_hi, q.out + qc);
+                if (!q.boff.empty()) {
+                    std::memcpy(h_boff + q.bslot, q.boff.data(), q.boff.size() * 4);
+                    b_lo = std::min(b_lo, q.bslot); b_hi = std::max(b_hi, q.bslot + q.boff.size());
                 }
             }
-            if (!e && m_hi > m_lo) e = cudaMemcpyAsync(p->d_mq + m_lo, h_mq + m_lo, (m_hi - m_lo) * 4, cudaMemcpyHostToDevice, c->stream);
-            if (!e && g_hi > g_lo) e = cudaMemcpyAsync(p->d_gates + g_lo, h_gates + g_lo, (g_hi - g_lo) * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
-            if (!e && b_hi > b_lo) e = cudaMemcpyAsync(p->d_boff + b_lo, h_boff + b_lo, (b_hi - b_lo) * 4, cudaMemcpyHostToDevice, c->stream);
-            if (e) { c->err = cudaGetErrorString(e); rc = SK_ECUDA; break; }
-            uploaded = e_seg; ++nbatches;
         }
-        if (sg.meas) {
-            rc = launch_measure(t, p->d_mq + sg.out, int(cnt), seed, sg.out, p->d_out + sg.out, p->d_det + sg.out);
-        } else {
-            size_t base = sg.out, bo = 0;
-            for (size_t k = 0; k < sg.sizes.size(); ++k) {
-                const uint32_t nb = sg.gblocks[k];
-                launch_layer(t, p->d_gates + base, int(sg.sizes[k]), nb ? p->d_boff + sg.bslot + bo : nullptr, int(nb), int(sg.glayers[k]));
-                if (nb) bo += nb + 1;
-                base += sg.sizes[k];
-            }
+        if (!e && m_hi > m_lo) e = cudaMemcpyAsync(p->d_mq + m_lo, h_mq + m_lo, (m_hi - m_lo) * 4, cudaMemcpyHostToDevice, c->stream);
+        if (!e && g_hi > g_lo) e = cudaMemcpyAsync(p->d_gates + g_lo, h_gates + g_lo, (g_hi - g_lo) * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
+        if (!e && b_hi > b_lo) e = cudaMemcpyAsync(p->d_boff + b_lo, h_boff + b_lo, (b_hi - b_lo) * 4, cudaMemcpyHostToDevice, c->stream);
+        if (e) { c->err = cudaGetErrorString(e); return SK_ECUDA; }
+        uploaded = e_seg; ++nbatches;
+        return SK_OK;
+    };
+    auto launch_seg = [&](size_t si) -> int32_t {
+        const Seg& sg = segs[si];
+        if (sg.meas) return launch_measure(t, p->d_mq + sg.out, int(sg.hi - sg.lo), seed, sg.out, p->d_out + sg.out, p->d_det + sg.out);
+        size_t base = sg.out, bo = 0;
+        for (size_t k = 0; k < sg.sizes.size(); ++k) {
+            const uint32_t nb = sg.gblocks[k];
+            launch_layer(t, p->d_gates + base, int(sg.sizes[k]), nb ? p->d_boff + sg.bslot + bo : nullptr, int(nb), int(sg.glayers[k]));
+            if (nb) bo += nb + 1;
+            base += sg.sizes[k];
+        }
+        return SK_OK;
+    };
+    // Everything behind the first measurement block is launched as ONE CUDA graph: while the device works on that block
+    // (panel mode: milliseconds at d=71) the host finishes compiling, uploads the rest in one batch, captures and
+    // instantiates the remaining launches -- graph replay has none of the gaps of ~420 separate stream launches.
+    size_t first_meas = segs.size();
+    for (size_t si = 0; si < segs.size(); ++si) if (segs[si].meas) { first_meas = si; break; }
+    const size_t graph_from = (!c->no_graph && first_meas + 33 <= segs.size()) ? first_meas + 1 : segs.size();   // short programs: plain launches (instantiation would cost more than the gaps)
+    cudaGraphExec_t gexec = nullptr;
+    for (size_t si = 0; si < graph_from && !rc; ++si) {
+        wait_done(si);
+        if (si == 0) ts_first = since();
+        if (si >= uploaded) rc = upload_from(si);
+        if (!rc) rc = launch_seg(si);
+    }
+    if (!rc && graph_from < segs.size()) {
+        for (size_t si = graph_from; si < segs.size(); ++si) wait_done(si);
+        while (uploaded < segs.size() && !rc) rc = upload_from(std::max(uploaded, graph_from));   // all done: one batch up to the end
+        const bool r_in = t->r_valid, d_in = t->r_destab_stale;
+        const sk_counters before = c->cnt;
+        cudaGraph_t graph = nullptr;
+        bool ok = !rc && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            int32_t rcc = SK_OK;
+            for (size_t si = graph_from; si < segs.size() && !rcc; ++si) rcc = launch_seg(si);
+            ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && !rcc && graph;
+            if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+            if (ok) ok = cudaGraphLaunch(gexec, c->stream) == cudaSuccess;
+        }
+        if (!rc && !ok) {                    // capture is not possible here: plain stream launches
+            cudaGetLastError();
+            t->r_valid = r_in; t->r_destab_stale = d_in; c->cnt = before;
+            for (size_t si = graph_from; si < segs.size() && !rc; ++si) rc = launch_seg(si);
         }
     }
     ts_enq = since();
@@ -1022,6 +1055,7 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
         if (dbg) fprintf(stderr, "sk_sim host ms: validate %.2f scan %.2f alloc+tableau %.2f first segment ready %.2f all enqueued %.2f workers joined %.2f histogram %.2f record read (device done) %.2f | %u threads, %zu segments in %zu uploads\n",
                          ts_val, ts_scan, ts_alloc, ts_first, ts_enq, ts_join, ts_hist, since(), nthreads, segs.size(), nbatches);
     } else cudaStreamSynchronize(c->stream);
+    if (gexec) cudaGraphExecDestroy(gexec);          // the stream is idle here (record read / synchronised)
     sk_program_destroy(p);
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out_t = t;
