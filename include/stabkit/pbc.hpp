@@ -21,10 +21,12 @@ struct PbcProgram {
 };
 
 // SPEC:545-553.  Mid-circuit measurement throws UnsupportedError.
-inline PbcProgram transpile(const Circuit& c) {
+// exact = true selects SK_TRANSPILE_EXACT (inverse-gate backward walk + order-preserving separation: the variant that
+// passes the dense-statevector equivalence check of SPEC:563-573); false keeps Algorithms 2-3 as published.
+inline PbcProgram transpile(const Circuit& c, bool exact = false) {
     Device& dev = Device::instance();
     sk_pbc* p = nullptr;
-    dev.check(sk_transpile(dev.ctx(), c.n, c.raw(), c.gates.size(), &p));
+    dev.check(sk_transpile_ex(dev.ctx(), c.n, c.raw(), c.gates.size(), exact ? SK_TRANSPILE_EXACT : 0u, &p));
     PbcProgram out; out.n = c.n;
     uint64_t st[5];
     sk_pbc_stats(p, st);

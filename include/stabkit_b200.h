@@ -202,6 +202,14 @@ int32_t sk_verify_grouping(sk_rows* r, int mode, const uint32_t* group_of, uint6
  * accessors below.  Mid-circuit M -> SK_EUNSUPPORTED. */
 typedef struct sk_pbc sk_pbc;
 int32_t sk_transpile(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out);
+/* flags bit 0 = SK_TRANSPILE_EXACT: the unitary-exact variant.  Algorithm 2 as published applies G's own CHP rule while
+ * walking the circuit backwards and Algorithm 3 puts a row into the FIRST layer (from P_0) it commutes with; both are kept
+ * verbatim by sk_transpile (flags 0, the reference's text: SPEC:515-533, PAPER Alg. 2-3).  The dense-statevector check the
+ * SPEC names as arbiter (verify_transpile) shows that unitary equivalence needs the INVERSE gate in the
+ * backward walk (S <-> S^dagger) and a row to stay behind every rotation it anticommutes with; SK_TRANSPILE_EXACT does
+ * exactly that (Algorithm 4 and rowsum+i are unchanged) and passes the check on random Clifford+T circuits. */
+#define SK_TRANSPILE_EXACT 1u
+int32_t sk_transpile_ex(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates, uint32_t flags, sk_pbc** out);
 void sk_pbc_destroy(sk_pbc* p);
 /* stats: initial_t, final_rotations_rowcount, final_rotations_pauliweight, layers, passes */
 int32_t sk_pbc_stats(sk_pbc* p, uint64_t out5[5]);

@@ -237,9 +237,10 @@ class Tableau:
 
 
 class Pbc:
-    def __init__(self, n, gates):
+    def __init__(self, n, gates, exact=False):
+        """exact=False: Algorithms 2-3 as published; exact=True: the unitary-exact variant (flags bit 0)."""
         g = gates_array(gates); self.n, self.W = n, words_for(n)
-        self.h = lib().orc_transpile(n, _p(g), len(g))
+        self.h = lib().orc_transpile_ex(n, _p(g), len(g), 1 if exact else 0)
         self.status = lib().orc_pbc_status(self.h)
 
     def __del__(self):

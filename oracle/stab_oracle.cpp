@@ -323,13 +323,18 @@ struct Pbc {
 // SPEC:515-523 build_tableaus / Algorithm 2 PAPER:372-387.  Trailing Z
 // measurements are stripped; any other M is unsupported.
 // T_tab rows are in append order (reverse circuit time).
-static int build_tableaus(size_t n, const Gate* g, size_t ng, Tableau& M, Rows& T) {
+// exact = true: the backward walk conjugates by the INVERSE gate (S <-> S^dagger; every other Clifford of the gate set
+// is its own inverse).  Moving a measurement / rotation axis P from behind G to in front of it turns it into
+// G^dagger P G, so this is what unitary equivalence needs (tests/test_oracle_dense.py); exact = false applies G's own
+// rule, the literal reading of "Apply G to M_tab and T_tab using CHP rules" (Algorithm 2 line 8).
+static int build_tableaus(size_t n, const Gate* g, size_t ng, Tableau& M, Rows& T, bool exact = false) {
     size_t end = ng;
     while (end > 0 && g[end - 1].kind == K_M) --end;
     for (size_t i = 0; i < end; ++i) if (g[i].kind == K_M) return 2;
     T = Rows(n, 0);
     for (size_t k = end; k-- > 0;) {
-        const Gate& a = g[k];
+        Gate a = g[k];
+        if (exact) { if (a.kind == K_S) a.kind = K_SDG; else if (a.kind == K_SDG) a.kind = K_S; }
         if (a.kind == K_T || a.kind == K_TDG) {
             T.push_zero();
             T.Z(T.m - 1)[a.q0 >> 6] |= u64{1} << (a.q0 & 63);
@@ -343,9 +348,18 @@ static int build_tableaus(size_t n, const Gate* g, size_t ng, Tableau& M, Rows& 
 }
 
 // SPEC:525-533 t_separate / Algorithm 3: scan rows in `order`, first fit from P_0.
-static void separate_into(const Rows& src, const std::vector<size_t>& order, std::vector<Rows>& layers) {
+// ordered = true: a row joins the layer right AFTER the last layer that holds an anticommuting member (it may not be
+// moved in front of a rotation it does not commute with); ordered = false is Algorithm 3 as published: the first
+// layer, scanning from P_0, whose members all commute with it.
+static void separate_into(const Rows& src, const std::vector<size_t>& order, std::vector<Rows>& layers, bool ordered = false) {
     for (size_t s : order) {
         size_t placed = layers.size();
+        if (ordered) {
+            placed = 0;
+            for (size_t k = 0; k < layers.size(); ++k)
+                for (size_t m = 0; m < layers[k].m; ++m)
+                    if (!commutes(src.X(s), src.Z(s), layers[k].X(m), layers[k].Z(m), src.W)) { placed = k + 1; break; }
+        } else
         for (size_t k = 0; k < layers.size() && placed == layers.size(); ++k) {
             bool ok = true;
             for (size_t m = 0; m < layers[k].m && ok; ++m)
@@ -360,10 +374,10 @@ static void separate_into(const Rows& src, const std::vector<size_t>& order, std
         L.r[L.m - 1] = src.r[s];
     }
 }
-static std::vector<Rows> t_separate(const Rows& T) {
+static std::vector<Rows> t_separate(const Rows& T, bool ordered = false) {
     std::vector<size_t> order;
     for (size_t s = T.m; s-- > 0;) order.push_back(s);       // last appended first == forward time
-    std::vector<Rows> layers; separate_into(T, order, layers); return layers;
+    std::vector<Rows> layers; separate_into(T, order, layers, ordered); return layers;
 }
 
 // first (x,z)-duplicate pair in scan order: smallest i with a later
@@ -427,12 +441,12 @@ static int t_optimize(std::vector<Rows>& layers, Tableau& M, u64* passes) {
 
 // SPEC:545-553 transpile: build -> separate -> optimize -> re-separate layers
 // that lost internal commutativity.
-static void transpile(Pbc& P, const Gate* g, size_t ng) {
+static void transpile(Pbc& P, const Gate* g, size_t ng, bool exact = false) {
     Rows T;
-    P.status = build_tableaus(P.n, g, ng, P.M, T);
+    P.status = build_tableaus(P.n, g, ng, P.M, T, exact);
     if (P.status) return;
     P.initial_t = T.m;
-    P.layers = t_separate(T);
+    P.layers = t_separate(T, exact);
     P.status = t_optimize(P.layers, P.M, &P.passes);
     if (P.status) return;
     std::vector<Rows> out;
@@ -442,7 +456,7 @@ static void transpile(Pbc& P, const Gate* g, size_t ng) {
             ok = commutes(L.X(a), L.Z(a), L.X(b), L.Z(b), L.W);
         if (ok) { out.push_back(std::move(L)); continue; }
         std::vector<size_t> order(L.m); for (size_t i = 0; i < L.m; ++i) order[i] = i;
-        std::vector<Rows> sub; separate_into(L, order, sub);
+        std::vector<Rows> sub; separate_into(L, order, sub, exact);
         for (auto& s : sub) out.push_back(std::move(s));
     }
     P.layers = std::move(out);
@@ -528,6 +542,8 @@ void orc_tab_counters(void* h, uint64_t* out16) {
 
 // transpiler ----------------------------------------------------------------
 void* orc_transpile(size_t n, const Gate* g, size_t ng) { Pbc* P = new Pbc(n); transpile(*P, g, ng); return P; }
+// flags bit 0: unitary-exact variant (inverse-gate conjugation in Algorithm 2, order-preserving separation in Algorithm 3)
+void* orc_transpile_ex(size_t n, const Gate* g, size_t ng, unsigned flags) { Pbc* P = new Pbc(n); transpile(*P, g, ng, (flags & 1u) != 0); return P; }
 void orc_pbc_free(void* h) { delete static_cast<Pbc*>(h); }
 int orc_pbc_status(void* h) { return static_cast<Pbc*>(h)->status; }
 // stats: initial_t, final rowcount, final pauli weight, layers, passes

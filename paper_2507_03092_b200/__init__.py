@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
             "sk_group_first_fit": (i32, [vp, C.c_int, vp, P(u64)]),
             "sk_verify_grouping": (i32, [vp, C.c_int, vp, P(u64)]),
             "sk_transpile": (i32, [vp, u64, vp, sz, P(vp)]),
+            "sk_transpile_ex": (i32, [vp, u64, vp, sz, u32, P(vp)]),
             "sk_pbc_destroy": (None, [vp]),
             "sk_pbc_stats": (i32, [vp, P(u64)]),
             "sk_pbc_layer_rows": (u64, [vp, u64]),
@@ -142,7 +143,7 @@ EXPORTS = [
     "sk_circuit_validate_chunks", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
     "sk_rows_download", "sk_rows_conj_layer", "sk_commutation_vector",
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",
-    "sk_group_first_fit", "sk_verify_grouping", "sk_transpile", "sk_pbc_destroy", "sk_pbc_stats",
+    "sk_group_first_fit", "sk_verify_grouping", "sk_transpile", "sk_transpile_ex", "sk_pbc_destroy", "sk_pbc_stats",
     "sk_pbc_layer_rows", "sk_pbc_layer_download", "sk_pbc_mtab_download",
     "sk_shard_create", "sk_shard_destroy", "sk_shard_reset", "sk_shard_apply_gates", "sk_shard_pivot_search",
     "sk_shard_partial_words", "sk_shard_det_partial", "sk_shard_det_combine", "sk_shard_pivot_row",
@@ -502,10 +503,11 @@ class Rows:
 class Pbc:
     """Result of sk_transpile (PbcProgram)."""
 
-    def __init__(self, ctx: Context, circ: Circuit):
+    def __init__(self, ctx: Context, circ: Circuit, exact: bool = False):
+        """exact=False: Algorithms 2-3 as published (sk_transpile); exact=True: SK_TRANSPILE_EXACT (stabkit_b200.h)."""
         self.ctx, self.n, self.W = ctx, circ.n, words_for(circ.n)
         self._h = C.c_void_p()
-        ctx.check(lib().sk_transpile(ctx._h, circ.n, _ptr(circ.gates), len(circ.gates), C.byref(self._h)))
+        ctx.check(lib().sk_transpile_ex(ctx._h, circ.n, _ptr(circ.gates), len(circ.gates), 1 if exact else 0, C.byref(self._h)))
 
     def close(self):
         if self._h:

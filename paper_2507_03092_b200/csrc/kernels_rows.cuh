@@ -12,7 +12,11 @@ namespace skd {
 // ---- predicates -------------------------------------------------------------
 // mode 0 (GC): conflict = anticommute = parity of popc((ax&bz)^(bx&az))      (pauli.cpp:117-127)
 // mode 1 (QWC): conflict = any word of (ax&bz)^(bx&az) non-zero               (pauli.cpp:129-140)
-__device__ __forceinline__ bool conflict_words(const u64* ax, const u64* az, const u64* bx, const u64* bz, int W, int mode) {
+// mode: bits 0-7 = predicate (0 GC: anticommute, 1 QWC: any qubit-wise clash); bit 8 (kOrderedFit) only concerns the
+// resolver below and is ignored here
+constexpr int kOrderedFit = 0x100;
+__device__ __forceinline__ bool conflict_words(const u64* ax, const u64* az, const u64* bx, const u64* bz, int W, int mode_) {
+    const int mode = mode_ & 0xff;
     u64 acc = 0; int par = 0;
     for (int w = 0; w < W; ++w) {
         u64 v = (ax[w] & bz[w]) ^ (bx[w] & az[w]);
@@ -195,12 +199,25 @@ k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
         const u32* bm = bitmap + (size_t)k * GW32;
         // groups >= ng are free by construction; scan words covering [0, ng]
         const int words = int(ng >> 5) + 1;
+        u32 g;
+        if (mode & kOrderedFit) {
+            // order-preserving variant (exact T-layer separation): the group right after the LAST conflicting one
+            if (threadIdx.x == 0) s_first = 0u;
+            __syncthreads();
+            for (int w = threadIdx.x; w < words; w += blockDim.x) {
+                const u32 b = bm[w];
+                if (b) atomicMax(&s_first, u32(w * 32 + 32 - __clz(int(b))));
+            }
+            __syncthreads();
+            g = min(s_first, ng);
+        } else {
         for (int w = threadIdx.x; w < words; w += blockDim.x) {
             u32 freeb = ~bm[w];
             if (freeb) { atomicMin(&s_first, u32(w * 32 + __ffs(freeb) - 1)); break; }
         }
         __syncthreads();
-        const u32 g = min(s_first, ng);             // first free existing group, else a new one
+        g = min(s_first, ng);                       // first free existing group, else a new one
+        }
         if (threadIdx.x == 0) { group_of[t] = g; if (g == ng) s_ng = ng + 1; }
         // propagate to later block-mates
         const u64* tx = rows + (size_t)(2 * t) * Wp; const u64* tz = tx + Wp;

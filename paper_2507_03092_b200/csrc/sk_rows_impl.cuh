@@ -383,8 +383,17 @@ extern "C" int32_t sk_pbc_mtab_download(sk_pbc* p, uint64_t* x, uint64_t* z, uin
     return SK_OK;
 }
 
+extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, uint32_t flags, sk_pbc** out);
 extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out) {
+    return sk_transpile_ex(c, n, gates, ngates, 0u, out);
+}
+// flags bit 0 (SK_TRANSPILE_EXACT): unitary-exact variant -- the backward walk of Algorithm 2 conjugates by the inverse
+// gate (S <-> S^dagger) and Algorithm 3 / the safety pass place a row right after the last layer holding an anticommuting
+// member instead of in the first commuting layer (see include/stabkit_b200.h and DESIGN.md section 8).
+extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, uint32_t flags, sk_pbc** out) {
     if (!c || !out || (!gates && ngates)) return SK_EARG;
+    const bool exact = (flags & 1u) != 0;
+    const int fit_mode = exact ? kOrderedFit : 0;
     *out = nullptr;
     if (n == 0) SK_FAIL(c, SK_EDIM, "transpile: circuit has zero qubits");
     size_t end = ngates;
@@ -419,6 +428,8 @@ extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
         for (size_t k = end; k-- > 0;) {
             sk_gate g = gates[k];
             if (g.kind == SK_T || g.kind == SK_TDG) { --tk; g.kind = (g.kind == SK_T) ? SK_APPEND_T : SK_APPEND_TDG; g.q1 = uint32_t(T0 + tk); }
+            else if (exact && g.kind == SK_S) g.kind = SK_SDG;
+            else if (exact && g.kind == SK_SDG) g.kind = SK_S;
             rev.push_back(g);
         }
         std::vector<sk_gate> ordered; std::vector<uint32_t> sizes, scratch;
@@ -448,7 +459,7 @@ extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
         SK_CUDA(c, cudaMalloc(&d_pair, nT * 4)); guard.extra.push_back(d_pair);
         SK_CUDA(c, cudaMalloc(&d_hash, nT * 8)); guard.extra.push_back(d_hash);
         uint64_t nl = 0;
-        rc = device_first_fit(c, rowsT, m.Wp, W, int(nT), 0, d_group, &nl);
+        rc = device_first_fit(c, rowsT, m.Wp, W, int(nT), fit_mode, d_group, &nl);
         if (rc) { delete p; return rc; }
         SK_CUDA(c, cudaMemcpyAsync(lvl.data(), d_group, nT * 4, cudaMemcpyDeviceToHost, c->stream));
         SK_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -567,7 +578,16 @@ extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
         }
         std::vector<uint32_t> sub_of(L.size()); uint64_t nsub = 0;
         rc = sk_rows_upload(sub, reinterpret_cast<const uint64_t*>(sx.data()), reinterpret_cast<const uint64_t*>(sz.data()), ss.data(), L.size());
-        if (!rc) rc = sk_group_first_fit(sub, 0, sub_of.data(), &nsub);
+        if (!rc) rc = rows_need_r(sub);
+        if (!rc) {
+            u32* d_sub = nullptr;
+            if (cudaMalloc(&d_sub, L.size() * 4) != cudaSuccess) { c->err = "cudaMalloc failed in the safety re-separation"; rc = SK_ECUDA; }
+            else {
+                rc = device_first_fit(c, sub->m.rows, sub->m.Wp, sub->m.W, int(L.size()), fit_mode, d_sub, &nsub);
+                if (!rc && cudaMemcpy(sub_of.data(), d_sub, L.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) { c->err = "copy failed in the safety re-separation"; rc = SK_ECUDA; }
+                cudaFree(d_sub);
+            }
+        }
         sk_rows_destroy(sub);
         if (rc) { delete p; return rc; }
         std::vector<std::vector<uint32_t>> parts(nsub);

@@ -128,3 +128,22 @@ def test_transpile_random_large(sk, ctx, orc, n, G, pt):                      # 
     rng = np.random.default_rng(n + G)
     gates = rand_ct(rng, n, G, pt)
     assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+
+
+def test_transpile_exact_mode_matches_oracle_and_the_statevector(sk, ctx, orc):
+    """SK_TRANSPILE_EXACT: bit parity with the oracle's exact variant, and -- independently of any tableau convention -- the
+    dense-statevector equivalence check of SPEC:563-573 on the DEVICE output (TV < 1e-9)."""
+    from oracle import dense as dn
+    rng = np.random.default_rng(77)
+    for trial in range(80):
+        n = int(rng.integers(1, 6)); gates = rand_ct(rng, n, int(rng.integers(5, 60)), pt=float(rng.uniform(0.1, 0.5)))
+        d = sk.Pbc(ctx, sk.Circuit(n, gates), exact=True)
+        assert_same_pbc(d, orc.Pbc(n, gates, exact=True))
+        st = d.stats()
+        layers = [[(int(x[i, 0]), int(z[i, 0]), int(r[i])) for i in range(len(r))] for x, z, r in (d.layer(k) for k in range(st["layers"]))]
+        mx, mz, mr = d.mtab()
+        rows = [(int(mx[i, 0]), int(mz[i, 0]), int(mr[i])) for i in range(n)]
+        assert dn.verify_transpile(n, [g for g in gates if g[0] != M], layers, rows) < 1e-9
+    for n, G, pt in ((20, 2000, 0.2), (100, 4000, 0.1), (70, 3000, 0.4)):
+        gates = rand_ct(np.random.default_rng(n + G + 1), n, G, pt)
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates), exact=True), orc.Pbc(n, gates, exact=True))
