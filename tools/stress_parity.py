@@ -9,7 +9,7 @@ H, S, SDG, X, Y, Z, CX, CZ, SWAP, M = range(10)
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(time.time()) & 0xffff)
 t_end = time.time() + budget
-runs = fails = 0
+runs = fails = sruns = 0
 while time.time() < t_end:
     os.environ["SK_PANEL"] = str(int(rng.choice([1, 3, 8, 17, 64, 64, 64])))
     os.environ["SK_ROW_CAP"] = str(int(rng.choice([0, 0, 0, 10, 40, 150])))
@@ -42,6 +42,17 @@ while time.time() < t_end:
             fails += 1
             print("MISMATCH n", n, "gates", len(gates), "env", {k: os.environ[k] for k in ("SK_PANEL", "SK_ROW_CAP", "SK_NO_FOLD", "SK_PANEL_COLUMNS", "SK_NO_GRAPH")}, flush=True)
         t.close()
+        if rng.random() < 0.15 and len(gates) < 1500:        # the same circuit on a row-sharded tableau (1..8 shards on this GPU)
+            from paper_2507_03092_b200.sharded import ShardedTableau
+            L = int(rng.choice([1, 2, 3, 5, 8]))
+            st = ShardedTableau.create_cuda(n, local_shards=L, device_index=0)
+            so, sd = st.sim(circ, seed)
+            sx, sz, sr = st.gather_tableau()
+            st.close()
+            sruns += 1
+            if not ((so == oo).all() and (sd == od).all() and (sx == ox).all() and (sz == oz).all() and (sr == orr).all()):
+                fails += 1
+                print("SHARDED MISMATCH n", n, "gates", len(gates), "shards", L, flush=True)
     ctx.close()
-print(f"stress: {runs} circuits, {fails} mismatches")
+print(f"stress: {runs} circuits ({sruns} also row-sharded), {fails} mismatches")
 sys.exit(1 if fails else 0)
