@@ -49,6 +49,16 @@ static void cpu_checks() {
     CHECK(surface_code_circuit(3, 1).n == 17 && surface_code_circuit(3, 2).num_measurements() == 16);
     CHECK(throws<Error>([] { surface_code_circuit(2, 1); }) && throws<Error>([] { random_layered_circuit(7, 1); }));
     CHECK(random_layered_circuit(8, 1).gates.size() == 27);
+    // emit_pbc / parse_pbc
+    { PbcProgram e; e.n = 2; e.measurement_rows = {PauliString::parse("ZI"), PauliString::parse("IZ")};
+      CHECK(emit_pbc(e) == "PBC v1\nqubits 2\nt_initial 0\nt_final 0\nmeasure:\n+ZI\n+IZ\n");
+      PbcProgram q; q.n = 3; q.stats.initial_t = 5; q.stats.final_rotations_rowcount = 3;
+      q.layers = {{PauliString::parse("XIZ"), PauliString::parse("-ZZI")}, {PauliString::parse("-YII")}};
+      q.measurement_rows = {PauliString::parse("XXI"), PauliString::parse("-IZZ"), PauliString::parse("IIY")};
+      PbcProgram r = parse_pbc(emit_pbc(q));
+      CHECK(r.n == 3 && r.layers == q.layers && r.measurement_rows == q.measurement_rows && r.stats.initial_t == 5 && r.stats.final_rotations_rowcount == 3 && r.stats.layers == 2 && r.stats.final_rotations_pauliweight == 5);
+      CHECK(emit_pbc(r) == emit_pbc(q));
+      CHECK(throws<ParseError>([] { parse_pbc("PBC v2\nqubits 1\nmeasure:\n+Z\n"); }) && throws<ParseError>([] { parse_pbc("PBC v1\nqubits 2\nmeasure:\n+Z\n"); })); }
 }
 
 static void gpu_checks() {
