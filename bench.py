@@ -273,7 +273,7 @@ def main():
     e2e_s = skdist.max_over_ranks(sum(e2e_times) / len(e2e_times))
 
     if rank == 0:
-        from oracle.oracle_py import algorithmic_bytes     # formula only; no oracle compute here
+        algorithmic_bytes = sk.algorithmic_bytes           # SURVEY 8d formula over the device's own counters
         per_step = {k: cnt[k] / args.steps for k in ("n_rand", "n_det", "k_rand", "k_det")}
         per_step["gate_hist"] = [v / args.steps for v in cnt["gate_hist"]]
         layers_per_step = cnt["layers"] / args.steps

@@ -155,6 +155,22 @@ def words_for(n: int) -> int:
     return (n + 63) // 64
 
 
+def algorithmic_bytes(n: int, counters: dict, fused_layers: float | None = None) -> float:
+    """layout-independent byte count of a CHP run on the bit-packed tableau, from the device's
+    counters (Context.counters(): gate histogram, n_rand / n_det, k_rand / k_det).  R = 2n rows; one column = R/8 bytes;
+    W = ceil(n/64) words per half row.  Used by bench.py for the roofline line."""
+    R = 2 * n; col = R / 8.0; W = words_for(n)
+    h = counters["gate_hist"]
+    # fused-layer form: columns read + written per gate; the sign column is charged once per layer
+    per_gate = {H: 4, S: 3, SDG: 3, X: 1, Y: 2, Z: 1, CX: 6, CZ: 6, SWAP: 8}
+    b = sum(h[k] * c for k, c in per_gate.items()) * col
+    if fused_layers:
+        b += fused_layers * 2 * col
+    b += counters["n_rand"] * (col + 16 * W + 32 * W) + counters["k_rand"] * 32 * W
+    b += counters["n_det"] * col + counters["k_det"] * 16 * W
+    return b
+
+
 def gates_array(gates) -> np.ndarray:
     """[(kind, q0[, q1]), ...] or an existing GATE_DTYPE array -> contiguous GATE_DTYPE array."""
     if isinstance(gates, np.ndarray) and gates.dtype == GATE_DTYPE:

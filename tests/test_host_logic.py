@@ -127,3 +127,11 @@ def test_parse_qasm2_subset(sk):
             sk.parse_qasm2_subset(bad)
     # the parsed circuit round-trips through the native format
     assert (sk.parse_native(c.emit_native()).gates == c.gates).all()
+
+
+def test_algorithmic_bytes_formula_matches_the_oracles_copy(sk, orc):
+    """bench.py's roofline numerator lives in the product package; the oracle keeps its own copy."""
+    cnt = {"gate_hist": [7, 3, 2, 5, 1, 4, 11, 6, 2, 9, 0, 0], "n_rand": 13, "n_det": 29, "k_rand": 101, "k_det": 57}
+    for n in (17, 1249, 10081):
+        assert sk.algorithmic_bytes(n, cnt, fused_layers=5) == orc.algorithmic_bytes(n, cnt, fused_layers=5)
+        assert sk.algorithmic_bytes(n, cnt) == orc.algorithmic_bytes(n, cnt)
