@@ -173,20 +173,48 @@ k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
             const u32 bits = __reduce_or_sync(0xffffffffu, c ? gbit : 0u);
             if ((threadIdx.x & 31) == 0 && bits) {
                 u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + w_first;
-                if ((__ldcg(word) & bits) != bits) atomicOr(word, bits);
+                atomicOr(word, bits);                 // fire-and-forget reduction: no L2 round trip on the warp's path
             }
         } else if (c) {
             u32* word = bitmap + (size_t)(tb + k - t0) * GW32 + widx;
-            if (!(__ldcg(word) & gbit)) atomicOr(word, gbit);
+            atomicOr(word, gbit);
         }
     }
+}
+
+// First free group of every block term with respect to the groups that existed BEFORE the block (one CTA per bitmap row,
+// all rows in parallel): the sequential resolver below starts its scan there instead of at word 0 -- bits only get added
+// by the block-mates, so everything in front of that position stays occupied.
+__global__ void __launch_bounds__(256)
+k_first_free(const u32* __restrict__ bitmap, int GW32, const u32* __restrict__ ngroups, u32* __restrict__ first_free) {
+    __shared__ u32 s_best;
+    const u32* bm = bitmap + (size_t)blockIdx.x * GW32;
+    const int words = int(*ngroups >> 5) + 1;
+    if (threadIdx.x == 0) s_best = 0xffffffffu;
+    __syncthreads();
+    for (int w0 = 0; w0 < words; w0 += 4 * blockDim.x) {
+        u32 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { const int w = w0 + u * int(blockDim.x) + int(threadIdx.x); v[u] = (w < words) ? __ldcg(bm + w) : 0xffffffffu; }
+        u32 best = 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u32 freeb = ~v[u];
+            if (freeb && best == 0xffffffffu) best = u32((w0 + u * int(blockDim.x) + int(threadIdx.x)) * 32 + __ffs(int(freeb)) - 1);
+        }
+        if (best != 0xffffffffu) atomicMin(&s_best, best);
+        if (__syncthreads_or(best != 0xffffffffu)) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) first_free[blockIdx.x] = s_best;
 }
 
 // First-fit resolver for one block (single CTA, sequential over the block's terms):
 // term t takes the first group whose bit is clear; later block-mates that conflict with t get that bit set.
 __global__ void __launch_bounds__(1024)
 k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode,
-                  u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io) {
+                  u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io,
+                  const u32* __restrict__ first_free) {
     __shared__ u32 s_first;
     __shared__ u32 s_ng;
     if (threadIdx.x == 0) s_ng = *ngroups_io;
@@ -205,15 +233,28 @@ k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
             if (threadIdx.x == 0) s_first = 0u;
             __syncthreads();
             for (int w = threadIdx.x; w < words; w += blockDim.x) {
-                const u32 b = bm[w];
+                const u32 b = __ldcg(bm + w);
                 if (b) atomicMax(&s_first, u32(w * 32 + 32 - __clz(int(b))));
             }
             __syncthreads();
             g = min(s_first, ng);
         } else {
-        for (int w = threadIdx.x; w < words; w += blockDim.x) {
-            u32 freeb = ~bm[w];
-            if (freeb) { atomicMin(&s_first, u32(w * 32 + __ffs(freeb) - 1)); break; }
+        {
+            // 8 independent loads per thread and round (the words of a thread ascend, so its first hit is its minimum): the
+            // scan of a long row costs words / (8 * 1024) L2 round trips instead of words / 1024
+            u32 best = 0xffffffffu;
+            const int wstart = min(words - 1, int(first_free[k] >> 5));      // nothing is free in front of it
+            for (int w0 = wstart + int(threadIdx.x); w0 < words && best == 0xffffffffu; w0 += 8 * blockDim.x) {
+                u32 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { const int w = w0 + u * int(blockDim.x); v[u] = (w < words) ? __ldcg(bm + w) : 0xffffffffu; }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const u32 freeb = ~v[u];
+                    if (freeb && best == 0xffffffffu) best = u32((w0 + u * int(blockDim.x)) * 32 + __ffs(int(freeb)) - 1);
+                }
+            }
+            if (best != 0xffffffffu) atomicMin(&s_first, best);
         }
         __syncthreads();
         g = min(s_first, ng);                       // first free existing group, else a new one
@@ -223,7 +264,8 @@ k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
         const u64* tx = rows + (size_t)(2 * t) * Wp; const u64* tz = tx + Wp;
         for (int k2 = k + 1 + threadIdx.x; k2 < B; k2 += blockDim.x) {
             const u64* ox = rows + (size_t)(2 * (t0 + k2)) * Wp; const u64* oz = ox + Wp;
-            if (conflict_words(ox, oz, tx, tz, W, mode)) bitmap[(size_t)k2 * GW32 + (g >> 5)] |= 1u << (g & 31);
+            // fire-and-forget reduction (no load on this thread's path); the scan above reads with ld.cg after the barrier
+            if (conflict_words(ox, oz, tx, tz, W, mode)) atomicOr(bitmap + (size_t)k2 * GW32 + (g >> 5), 1u << (g & 31));
         }
         __syncthreads();
     }

@@ -53,9 +53,10 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     if (count == 0) return SK_OK;
     const int B = std::min(count, 1024);
     const int GW32 = count / 32 + 2;
-    u32* d_bitmap = nullptr; u32* d_ng = nullptr;
+    u32* d_bitmap = nullptr; u32* d_ng = nullptr; u32* d_ff = nullptr;
     SK_CUDA(c, cudaMalloc(&d_bitmap, (size_t)B * GW32 * 4));
-    SK_CUDA(c, cudaMalloc(&d_ng, 4));
+    SK_CUDA(c, cudaMalloc(&d_ng, 4 + (size_t)B * 4));
+    d_ff = d_ng + 1;
     SK_CUDA(c, cudaMemsetAsync(d_ng, 0, 4, c->stream));
     const int Bt = std::max(1, std::min(B, (40 * 1024) / (2 * W * 8)));     // block terms staged per CTA (<= 40 KB smem)
     const size_t smem = (size_t)Bt * 2 * W * 8;
@@ -68,8 +69,9 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
             k_conflict_bitmap<<<grid, 256, smem, c->stream>>>(d_rows, Wp, W, t0, b, Bt, d_group, mode, d_bitmap, GW32);
             c->cnt.kernel_launches++;
         }
-        k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng);
-        c->cnt.kernel_launches++;
+        k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_ff);
+        k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+        c->cnt.kernel_launches += 2;
     }
     SK_CUDA(c, cudaGetLastError());
     u32 ng = 0;
