@@ -182,6 +182,93 @@ k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
     }
 }
 
+// ---- K5, group-major form (rows of at most 128 qubits: W <= 2) ------------------------------------------------------
+// The terms placed so far are kept grouped (CSR: off[g] .. off[g+1] into gterms, 4 words x0 x1 z0 z1 per term), rebuilt
+// per block by a counting sort.  The conflict kernel then runs ONE THREAD PER GROUP: a block term conflicts with the
+// group as soon as one member conflicts, the first four members sit in registers, and 32 consecutive groups are exactly
+// one bitmap word -> a warp ballot and one plain store per (block term, word): no atomics, and for GC ~10x fewer
+// predicate evaluations than the term x term matrix (a random group is rejected after ~2 members).
+__global__ void k_csr_count(const u32* __restrict__ group_of, int m0, int m1, u32* __restrict__ cnt) {
+    const int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < m1) atomicAdd(cnt + group_of[m], 1u);
+}
+// exclusive scan of cnt[0, ng) by one CTA (a thread owns a contiguous chunk); off[ng] = total
+__global__ void __launch_bounds__(1024)
+k_csr_scan(const u32* __restrict__ cnt, const u32* __restrict__ ngroups, u32* __restrict__ off) {
+    __shared__ u32 s_sum[1024];
+    const int ng = int(*ngroups), chunk = (ng + 1023) / 1024;
+    const int lo = min(ng, int(threadIdx.x) * chunk), hi = min(ng, lo + chunk);
+    u32 sum = 0;
+    for (int i = lo; i < hi; ++i) sum += cnt[i];
+    s_sum[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const u32 v = (int(threadIdx.x) >= o) ? s_sum[threadIdx.x - o] : 0u;
+        __syncthreads();
+        s_sum[threadIdx.x] += v;
+        __syncthreads();
+    }
+    u32 run = s_sum[threadIdx.x] - sum;
+    for (int i = lo; i < hi; ++i) { off[i] = run; run += cnt[i]; }
+    if (threadIdx.x == 1023) off[ng] = s_sum[1023];
+}
+__global__ void k_csr_fill(const u64* __restrict__ rows, int Wp, int W, const u32* __restrict__ group_of, int t0,
+                           const u32* __restrict__ off, u32* __restrict__ fillc, u64* __restrict__ gterms) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= t0) return;
+    const u32 g = group_of[m];
+    const u32 pos = off[g] + atomicAdd(fillc + g, 1u);
+    const u64* x = rows + (size_t)(2 * m) * Wp; const u64* z = x + Wp;
+    u64* o = gterms + (size_t)pos * 4;
+    o[0] = x[0]; o[1] = W > 1 ? x[1] : 0ull; o[2] = z[0]; o[3] = W > 1 ? z[1] : 0ull;
+}
+__device__ __forceinline__ bool conflict4(u64 ax0, u64 ax1, u64 az0, u64 az1, u64 bx0, u64 bx1, u64 bz0, u64 bz1, int mode) {
+    const u64 v0 = (ax0 & bz0) ^ (bx0 & az0), v1 = (ax1 & bz1) ^ (bx1 & az1);
+    return mode == 0 ? (((__popcll(v0) + __popcll(v1)) & 1) != 0) : ((v0 | v1) != 0ull);
+}
+__global__ void __launch_bounds__(256)
+k_conflict_groups(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int Bt, const u32* __restrict__ ngroups,
+                  const u32* __restrict__ off, const u64* __restrict__ gterms, int mode_, u32* __restrict__ bitmap, int GW32) {
+    extern __shared__ u64 s_blk[];          // [Bt][4]: x0 x1 z0 z1 of each staged block term
+    const int mode = mode_ & 0xff;
+    const u32 ng = *ngroups;
+    if (blockIdx.x * blockDim.x >= ng) return;                 // the grid is sized for the worst case (one group per term)
+    const int tb = t0 + blockIdx.y * Bt;
+    for (int i = threadIdx.x; i < Bt * 4; i += blockDim.x) {
+        const int k = i >> 2, w = i & 3, t = tb + k;
+        s_blk[i] = (t < t0 + B && (w & 1) < W) ? rows[(size_t)(2 * t + (w >> 1)) * Wp + (w & 1)] : 0ull;
+    }
+    __syncthreads();
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = g < ng;
+    const u32 start = live ? off[g] : 0u, cnt = live ? off[g + 1] - start : 0u;
+    // first four members in registers; an all-zero (absent) member conflicts with nothing
+    u64 m0[4] = {0, 0, 0, 0}, m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0}, m3[4] = {0, 0, 0, 0};
+    if (cnt > 0) { const u64* p = gterms + (size_t)start * 4; m0[0] = p[0]; m0[1] = p[1]; m0[2] = p[2]; m0[3] = p[3]; }
+    if (cnt > 1) { const u64* p = gterms + (size_t)(start + 1) * 4; m1[0] = p[0]; m1[1] = p[1]; m1[2] = p[2]; m1[3] = p[3]; }
+    if (cnt > 2) { const u64* p = gterms + (size_t)(start + 2) * 4; m2[0] = p[0]; m2[1] = p[1]; m2[2] = p[2]; m2[3] = p[3]; }
+    if (cnt > 3) { const u64* p = gterms + (size_t)(start + 3) * 4; m3[0] = p[0]; m3[1] = p[1]; m3[2] = p[2]; m3[3] = p[3]; }
+    const bool singles = __all_sync(0xffffffffu, cnt <= 1u);   // QWC on random strings: every group is a single term
+    const int kend = min(Bt, t0 + B - tb);
+    for (int k = 0; k < kend; ++k) {
+        const u64 bx0 = s_blk[4 * k], bx1 = s_blk[4 * k + 1], bz0 = s_blk[4 * k + 2], bz1 = s_blk[4 * k + 3];
+        bool c = conflict4(m0[0], m0[1], m0[2], m0[3], bx0, bx1, bz0, bz1, mode);
+        if (!singles) {
+            c |= conflict4(m1[0], m1[1], m1[2], m1[3], bx0, bx1, bz0, bz1, mode);
+            c |= conflict4(m2[0], m2[1], m2[2], m2[3], bx0, bx1, bz0, bz1, mode);
+            c |= conflict4(m3[0], m3[1], m3[2], m3[3], bx0, bx1, bz0, bz1, mode);
+            if (!c && cnt > 4u) {
+                for (u32 j = 4; j < cnt && !c; ++j) {
+                    const u64* p = gterms + (size_t)(start + j) * 4;
+                    c = conflict4(p[0], p[1], p[2], p[3], bx0, bx1, bz0, bz1, mode);
+                }
+            }
+        }
+        const u32 bits = __ballot_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0) bitmap[(size_t)(tb + k - t0) * GW32 + (g >> 5)] = bits;
+    }
+}
+
 // First free group of every block term with respect to the groups that existed BEFORE the block (one CTA per bitmap row,
 // all rows in parallel): the sequential resolver below starts its scan there instead of at word 0 -- bits only get added
 // by the block-mates, so everything in front of that position stays occupied.

@@ -61,10 +61,29 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     const int Bt = std::max(1, std::min(B, (40 * 1024) / (2 * W * 8)));     // block terms staged per CTA (<= 40 KB smem)
     const size_t smem = (size_t)Bt * 2 * W * 8;
     if (smem > 48 * 1024) { cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_EDIM, "rows too wide for the conflict kernel (W=%d)", W); }
+    // group-major path (W <= 2, i.e. up to 128 qubits -- BASELINE config 4): CSR of the placed terms, thread per group
+    static const bool csr_off = getenv("SK_GROUP_CSR") && atoi(getenv("SK_GROUP_CSR")) == 0;
+    const bool csr = W <= 2 && !csr_off && count > B;
+    u32* d_cnt = nullptr; u32* d_off = nullptr; u32* d_fillc = nullptr; u64* d_gterms = nullptr;
+    if (csr) {
+        cudaError_t e1 = cudaMalloc(&d_cnt, ((size_t)count + 2) * 4), e2 = cudaMalloc(&d_off, ((size_t)count + 2) * 4);
+        cudaError_t e3 = cudaMalloc(&d_fillc, ((size_t)count + 2) * 4), e4 = cudaMalloc(&d_gterms, (size_t)count * 32);
+        if (e1 || e2 || e3 || e4) { cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_fillc); cudaFree(d_gterms); cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the grouped term store"); }
+        SK_CUDA(c, cudaMemsetAsync(d_cnt, 0, ((size_t)count + 2) * 4, c->stream));
+    }
+    const int Btg = std::min(B, 1024);                                          // 32 B per staged term: 32 KB
     for (int t0 = 0; t0 < count; t0 += B) {
         const int b = std::min(B, count - t0);
         SK_CUDA(c, cudaMemsetAsync(d_bitmap, 0, (size_t)b * GW32 * 4, c->stream));
-        if (t0 > 0) {
+        if (t0 > 0 && csr) {
+            k_csr_count<<<(B + 255) / 256, 256, 0, c->stream>>>(d_group, t0 - B, t0, d_cnt);      // the previous block's terms
+            k_csr_scan<<<1, 1024, 0, c->stream>>>(d_cnt, d_ng, d_off);
+            SK_CUDA(c, cudaMemsetAsync(d_fillc, 0, ((size_t)t0 + 1) * 4, c->stream));
+            k_csr_fill<<<(t0 + 255) / 256, 256, 0, c->stream>>>(d_rows, Wp, W, d_group, t0, d_off, d_fillc, d_gterms);
+            dim3 grid((t0 + 255) / 256, (b + Btg - 1) / Btg);
+            k_conflict_groups<<<grid, 256, (size_t)Btg * 32, c->stream>>>(d_rows, Wp, W, t0, b, Btg, d_ng, d_off, d_gterms, mode, d_bitmap, GW32);
+            c->cnt.kernel_launches += 4;
+        } else if (t0 > 0) {
             dim3 grid((t0 + 255) / 256, (b + Bt - 1) / Bt);
             k_conflict_bitmap<<<grid, 256, smem, c->stream>>>(d_rows, Wp, W, t0, b, Bt, d_group, mode, d_bitmap, GW32);
             c->cnt.kernel_launches++;
@@ -77,7 +96,7 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     u32 ng = 0;
     SK_CUDA(c, cudaMemcpyAsync(&ng, d_ng, 4, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(d_bitmap); cudaFree(d_ng);
+    cudaFree(d_bitmap); cudaFree(d_ng); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_fillc); cudaFree(d_gterms);
     *ngroups = ng;
     return SK_OK;
 }

