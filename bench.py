@@ -95,7 +95,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "sampled": where}
 
 
-def cpu_reference(steps: int, warmup: int, rounds_sample: int = 6):
+def cpu_reference(steps: int, warmup: int, rounds_sample: int = 12):
     """The reference algorithm on the host cores: oracle port (kind 'port'), all host threads.  Bounded sample: the
     d=71 circuit cut to `rounds_sample` rounds and to half of that (both with the final data-qubit M); the difference gives
     the cost of a steady-state round, the rest (round 1 with its random X checks + the final block) is counted once."""
