@@ -188,16 +188,21 @@ k_conflict_bitmap(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
 // group as soon as one member conflicts, the first four members sit in registers, and 32 consecutive groups are exactly
 // one bitmap word -> a warp ballot and one plain store per (block term, word): no atomics, and for GC ~10x fewer
 // predicate evaluations than the term x term matrix (a random group is rejected after ~2 members).
-__global__ void k_csr_count(const u32* __restrict__ group_of, int m0, int m1, u32* __restrict__ cnt) {
+// gmin = smallest group that received a term: the offsets of all groups in front of it do not change
+__global__ void k_csr_count(const u32* __restrict__ group_of, int m0, int m1, u32* __restrict__ cnt, u32* __restrict__ gmin) {
     const int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (m < m1) atomicAdd(cnt + group_of[m], 1u);
+    if (m < m1) { const u32 g = group_of[m]; atomicAdd(cnt + g, 1u); atomicMin(gmin, g); }
 }
 // exclusive scan of cnt[0, ng) by one CTA (a thread owns a contiguous chunk); off[ng] = total
 __global__ void __launch_bounds__(1024)
-k_csr_scan(const u32* __restrict__ cnt, const u32* __restrict__ ngroups, u32* __restrict__ off) {
+k_csr_scan(const u32* __restrict__ cnt, const u32* __restrict__ ngroups, u32* __restrict__ off, const u32* __restrict__ gmin) {
     __shared__ u32 s_sum[1024];
-    const int ng = int(*ngroups), chunk = (ng + 1023) / 1024;
-    const int lo = min(ng, int(threadIdx.x) * chunk), hi = min(ng, lo + chunk);
+    const int ng = int(*ngroups);
+    const int g0 = int(min(*gmin, (u32)ng));                   // groups [0, g0) keep their offsets (off[g0] is still valid)
+    const u32 base = g0 > 0 ? off[g0] : 0u;
+    const int chunk = (ng - g0 + 1023) / 1024;
+    const int lo = min(ng, g0 + int(threadIdx.x) * chunk), hi = min(ng, lo + chunk);
+    __syncthreads();                                            // everybody has read off[g0] before it is rewritten
     u32 sum = 0;
     for (int i = lo; i < hi; ++i) sum += cnt[i];
     s_sum[threadIdx.x] = sum;
@@ -208,9 +213,9 @@ k_csr_scan(const u32* __restrict__ cnt, const u32* __restrict__ ngroups, u32* __
         s_sum[threadIdx.x] += v;
         __syncthreads();
     }
-    u32 run = s_sum[threadIdx.x] - sum;
+    u32 run = base + s_sum[threadIdx.x] - sum;
     for (int i = lo; i < hi; ++i) { off[i] = run; run += cnt[i]; }
-    if (threadIdx.x == 1023) off[ng] = s_sum[1023];
+    if (threadIdx.x == 1023) off[ng] = base + s_sum[1023];
 }
 __global__ void k_csr_fill(const u64* __restrict__ rows, int Wp, int W, const u32* __restrict__ group_of, int t0,
                            const u32* __restrict__ off, u32* __restrict__ fillc, u64* __restrict__ gterms) {
@@ -357,6 +362,81 @@ k_first_fit_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
         __syncthreads();
     }
     if (threadIdx.x == 0) *ngroups_io = s_ng;
+}
+
+// First-fit resolver, thread-per-term form (plain first fit only; the order-preserving variant keeps the kernel above).
+// Thread k owns block term t0+k and its running candidate `cand` = first group that is free for it given the groups
+// that existed before the block (k_first_free) and the groups taken so far by conflicting block-mates.  Per term ONE
+// broadcast (the term that is being placed publishes its group) and one predicate evaluation per later thread; a
+// candidate only has to move when a conflicting block-mate takes exactly that group -- then the next free bit of that
+// thread's bitmap row is searched by the whole CTA (rare for GC; for QWC on random strings the next candidate is always
+// the next new group and no memory is touched).  Row k of the bitmap is only ever modified by thread k (fire-and-forget
+// reductions), and only read by others after a barrier.
+__global__ void __launch_bounds__(1024)
+k_first_fit_threads(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode,
+                    u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io,
+                    const u32* __restrict__ first_free) {
+    __shared__ u32 s_g, s_ngprev, s_ng, s_who, s_best, s_from;
+    const int tid = threadIdx.x;
+    const bool mine = tid < B;
+    const u64* mx = rows + (size_t)(2 * (t0 + (mine ? tid : 0))) * Wp; const u64* mz = mx + Wp;
+    u32* myrow = bitmap + (size_t)(mine ? tid : 0) * GW32;
+    u32 cand = mine ? first_free[tid] : 0xffffffffu;
+    u32 from = 0;                                              // where a handed-over search continues (bit index, word aligned)
+    if (tid == 0) s_ng = *ngroups_io;
+    __syncthreads();
+    for (int k = 0; k < B; ++k) {
+        if (tid == k) {
+            const u32 ng = s_ng, g = min(cand, ng);
+            group_of[t0 + k] = g; s_g = g; s_ngprev = ng;
+            if (g == ng) s_ng = ng + 1;
+            s_who = 0xffffffffu;
+        }
+        __syncthreads();
+        const u32 g = s_g, ng = s_ng;
+        bool need = false;
+        if (mine && tid > k) {
+            const u64* tx = rows + (size_t)(2 * (t0 + k)) * Wp; const u64* tz = tx + Wp;
+            if (conflict_words(mx, mz, tx, tz, W, mode)) {
+                // cand <= group count before this placement, so cand is my effective candidate.  A group below it is occupied
+                // for me already; one above it has to be remembered for later searches; the candidate itself has to move.
+                if (g > cand) atomicOr(myrow + (g >> 5), 1u << (g & 31));
+                else if (g == cand) {
+                    u32 c = g + 1;
+                    for (int steps = 0; c < ng; ++steps) {             // own row: pre-block bits + my own reductions
+                        if (steps == 16) { need = true; from = c; break; }
+                        const u32 w = c >> 5;
+                        u32 freeb = ~__ldcg(myrow + w);
+                        if (c & 31u) freeb &= ~((1u << (c & 31u)) - 1u);
+                        if (freeb) { c = w * 32 + u32(__ffs(int(freeb)) - 1); break; }
+                        c = (w + 1) * 32;
+                    }
+                    if (!need) cand = min(c, ng);                      // everything from ng on is a new group: free by construction
+                    else atomicMin(&s_who, (u32)tid);
+                }
+            }
+        }
+        // rare: a search longer than 16 words is finished by the whole CTA, one row at a time
+        while (__syncthreads_or(need)) {
+            const u32 who = s_who;
+            if ((u32)tid == who) s_from = from;
+            if (tid == 0) s_best = 0xffffffffu;
+            __syncthreads();
+            const u32* bm = bitmap + (size_t)who * GW32;
+            const int w_lo = int(s_from >> 5), w_hi = int(ng >> 5);          // bits >= ng are free
+            u32 best = 0xffffffffu;
+            for (int w = w_lo + tid; w <= w_hi && best == 0xffffffffu; w += blockDim.x) {
+                const u32 freeb = ~__ldcg(bm + w);
+                if (freeb) best = u32(w * 32 + __ffs(int(freeb)) - 1);
+            }
+            if (best != 0xffffffffu) atomicMin(&s_best, best);
+            __syncthreads();
+            if ((u32)tid == who) { cand = min(s_best, ng); need = false; s_who = 0xffffffffu; }
+            __syncthreads();
+            if (need) atomicMin(&s_who, (u32)tid);
+        }
+    }
+    if (tid == 0) *ngroups_io = s_ng;
 }
 
 // verify_grouping: number of intra-group pairs violating the predicate.

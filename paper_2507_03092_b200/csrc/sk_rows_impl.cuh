@@ -64,20 +64,23 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     // group-major path (W <= 2, i.e. up to 128 qubits -- BASELINE config 4): CSR of the placed terms, thread per group
     static const bool csr_off = getenv("SK_GROUP_CSR") && atoi(getenv("SK_GROUP_CSR")) == 0;
     const bool csr = W <= 2 && !csr_off && count > B;
-    u32* d_cnt = nullptr; u32* d_off = nullptr; u32* d_fillc = nullptr; u64* d_gterms = nullptr;
+    static const bool legacy_resolver = getenv("SK_GROUP_RESOLVER") && atoi(getenv("SK_GROUP_RESOLVER")) == 0;   // A/B switch: the sequential-scan resolver
+    u32* d_cnt = nullptr; u32* d_off = nullptr; u32* d_fillc = nullptr; u64* d_gterms = nullptr; u32* d_gmin = nullptr;
     if (csr) {
-        cudaError_t e1 = cudaMalloc(&d_cnt, ((size_t)count + 2) * 4), e2 = cudaMalloc(&d_off, ((size_t)count + 2) * 4);
+        cudaError_t e1 = cudaMalloc(&d_cnt, ((size_t)count + 4) * 4), e2 = cudaMalloc(&d_off, ((size_t)count + 2) * 4);
         cudaError_t e3 = cudaMalloc(&d_fillc, ((size_t)count + 2) * 4), e4 = cudaMalloc(&d_gterms, (size_t)count * 32);
         if (e1 || e2 || e3 || e4) { cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_fillc); cudaFree(d_gterms); cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the grouped term store"); }
-        SK_CUDA(c, cudaMemsetAsync(d_cnt, 0, ((size_t)count + 2) * 4, c->stream));
+        SK_CUDA(c, cudaMemsetAsync(d_cnt, 0, ((size_t)count + 4) * 4, c->stream));
+        d_gmin = d_cnt + count + 3;
     }
-    const int Btg = std::min(B, 1024);                                          // 32 B per staged term: 32 KB
+    const int Btg = std::min(B, 128);                                           // block terms per CTA: 8 CTAs per 256 groups keep the SMs busy while groups are few (GC)
     for (int t0 = 0; t0 < count; t0 += B) {
         const int b = std::min(B, count - t0);
         SK_CUDA(c, cudaMemsetAsync(d_bitmap, 0, (size_t)b * GW32 * 4, c->stream));
         if (t0 > 0 && csr) {
-            k_csr_count<<<(B + 255) / 256, 256, 0, c->stream>>>(d_group, t0 - B, t0, d_cnt);      // the previous block's terms
-            k_csr_scan<<<1, 1024, 0, c->stream>>>(d_cnt, d_ng, d_off);
+            SK_CUDA(c, cudaMemsetAsync(d_gmin, 0xff, 4, c->stream));
+            k_csr_count<<<(B + 255) / 256, 256, 0, c->stream>>>(d_group, t0 - B, t0, d_cnt, d_gmin);      // the previous block's terms
+            k_csr_scan<<<1, 1024, 0, c->stream>>>(d_cnt, d_ng, d_off, d_gmin);
             SK_CUDA(c, cudaMemsetAsync(d_fillc, 0, ((size_t)t0 + 1) * 4, c->stream));
             k_csr_fill<<<(t0 + 255) / 256, 256, 0, c->stream>>>(d_rows, Wp, W, d_group, t0, d_off, d_fillc, d_gterms);
             dim3 grid((t0 + 255) / 256, (b + Btg - 1) / Btg);
@@ -89,7 +92,8 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
             c->cnt.kernel_launches++;
         }
         k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_ff);
-        k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+        if ((mode & kOrderedFit) || legacy_resolver) k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+        else k_first_fit_threads<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
         c->cnt.kernel_launches += 2;
     }
     SK_CUDA(c, cudaGetLastError());

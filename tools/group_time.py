@@ -9,7 +9,7 @@ rng = np.random.default_rng(20250703)
 x = rng.integers(0, 2**64, (N, 2), dtype=np.uint64); z = rng.integers(0, 2**64, (N, 2), dtype=np.uint64); r = np.zeros(N, np.uint8)
 ctx = sk.Context(0)
 rows = sk.Rows(ctx, 128, x, z, r)
-for rep in range(2):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     ctx.sync(); t0 = time.perf_counter()
     g, ng = rows.group_first_fit(mode)
     ctx.sync(); dt = time.perf_counter() - t0
