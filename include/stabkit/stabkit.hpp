@@ -9,4 +9,5 @@
 #include "stabkit/pauli.hpp"
 #include "stabkit/pbc.hpp"
 #include "stabkit/rng.hpp"
+#include "stabkit/sharded.hpp"
 #include "stabkit/tableau.hpp"

@@ -252,6 +252,11 @@ int32_t sk_shard_random_update(sk_shard* s, uint32_t q, uint64_t p, const uint64
 int32_t sk_shard_download(sk_shard* s, uint64_t* x, uint64_t* z, uint8_t* sign);
 /* rowsums performed: out2[0] random branch, out2[1] deterministic branch. Synchronises. */
 int32_t sk_shard_counters(sk_shard* s, uint64_t out2[2]);
+/* Plain device buffers for the exchange, so that a host binding needs no CUDA headers of its own.
+ * sk_dev_copy kind: 0 host->device, 1 device->host (both synchronise), 2 device->device (stream ordered). */
+int32_t sk_dev_alloc(sk_ctx* ctx, size_t bytes, void** out);
+void sk_dev_free(sk_ctx* ctx, void* p);
+int32_t sk_dev_copy(sk_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
 
 #ifdef __cplusplus
 }

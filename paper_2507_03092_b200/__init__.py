@@ -125,6 +125,9 @@ def lib() -> C.CDLL:
             "sk_shard_random_update": (i32, [vp, u32, u64, vp, C.c_uint8]),
             "sk_shard_download": (i32, [vp, vp, vp, vp]),
             "sk_shard_counters": (i32, [vp, P(u64)]),
+            "sk_dev_alloc": (i32, [vp, sz, P(vp)]),
+            "sk_dev_free": (None, [vp, vp]),
+            "sk_dev_copy": (i32, [vp, vp, vp, sz, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)      # AttributeError here == header/library mismatch: fail loudly
@@ -147,7 +150,7 @@ EXPORTS = [
     "sk_pbc_layer_rows", "sk_pbc_layer_download", "sk_pbc_mtab_download",
     "sk_shard_create", "sk_shard_destroy", "sk_shard_reset", "sk_shard_apply_gates", "sk_shard_pivot_search",
     "sk_shard_partial_words", "sk_shard_det_partial", "sk_shard_det_combine", "sk_shard_pivot_row",
-    "sk_shard_random_update", "sk_shard_download", "sk_shard_counters",
+    "sk_shard_random_update", "sk_shard_download", "sk_shard_counters", "sk_dev_alloc", "sk_dev_free", "sk_dev_copy",
 ]
 
 

@@ -213,3 +213,22 @@ extern "C" int32_t sk_shard_counters(sk_shard* s, uint64_t out2[2]) {
     SK_CUDA(c, cudaMemcpyAsync(out2, s->d_cnt, 16, cudaMemcpyDeviceToHost, c->stream));
     return check_ws(c);
 }
+
+// ---- plain device buffers for the exchange (so that a host binding needs no CUDA headers of its own) ----------------
+extern "C" int32_t sk_dev_alloc(sk_ctx* c, size_t bytes, void** out) {
+    if (!c || !out) return SK_EARG;
+    *out = nullptr;
+    SK_CUDA(c, cudaSetDevice(c->device));
+    SK_CUDA(c, cudaMalloc(out, bytes ? bytes : 16));
+    return SK_OK;
+}
+extern "C" void sk_dev_free(sk_ctx* c, void* p) { if (c && p) { cudaSetDevice(c->device); cudaStreamSynchronize(c->stream); cudaFree(p); } }
+// kind: 0 host->device, 1 device->host (synchronises), 2 device->device; ordered on the context's stream
+extern "C" int32_t sk_dev_copy(sk_ctx* c, void* dst, const void* src, size_t bytes, int kind) {
+    if (!c || (!dst && bytes) || (!src && bytes) || kind < 0 || kind > 2) return SK_EARG;
+    if (bytes == 0) return SK_OK;
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    SK_CUDA(c, cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+    if (kind != 2) SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}

@@ -90,6 +90,20 @@ static void gpu_checks() {
       CHECK(ghz);
       ShotHistogram z = run_shots(parse_native("qubits 1\nm 0"), 50, EngineConfig{1, 3, false});
       CHECK(z.ones.size() == 1 && z.ones[0] == 0); }
+    // row-sharded tableau: 3 shards in this process, same record and rows as sim()
+    { Circuit c5 = surface_code_circuit(5, 3, true);
+      SimResult ref = sim(c5, EngineConfig{1, 20250703, false});
+      ShardedTableau st(c5.n, 3);
+      MeasurementRecord rec = st.sim(c5, 20250703);
+      bool same = rec.size() == ref.record.size();
+      for (size_t i = 0; same && i < rec.size(); ++i)
+          same = rec[i].gate_index == ref.record[i].gate_index && rec[i].outcome == ref.record[i].outcome && rec[i].deterministic == ref.record[i].deterministic;
+      CHECK(same);
+      auto all = ref.tableau.rows(); auto mine = st.local_rows();
+      bool rows_same = mine.size() == all.size();
+      for (const auto& [idx, row] : mine) rows_same = rows_same && row == all[idx];
+      CHECK(rows_same);
+      CHECK(ShardedTableau::slot_range(10081, 1, 2) == (std::pair<uint64_t, uint64_t>{5056, 10081})); }
     // pauli_core batch op on the device
     std::vector<PauliString> rows = {PauliString::parse("ZZ"), PauliString::parse("ZI")};
     BitVec cv = commutation_vector(PauliString::parse("XX"), rows);
