@@ -116,22 +116,27 @@ __global__ void __launch_bounds__(256)
 k_shard_fix(DMat m, int NS, int pb, u32 q, const u64* __restrict__ prow, int outcome) {
     const int Wp = int(m.Wp), W = int(m.W), RW = int(m.RW), db = NS + pb;
     const u64 pbit = 1ull << (pb & 63), dbit = 1ull << (db & 63);
+    // bit flips in the C form are fire-and-forget reductions (no load on the thread's path); a column is only touched by
+    // the thread that owns its 64-qubit word, and one thread's atomics to one address keep program order
     for (int w = threadIdx.x; w < W; w += blockDim.x) {
         u64* dx = m.rows + (size_t)(2 * db) * Wp + w; u64* dz = dx + Wp;
         const u64 nx = prow[w], nz = prow[Wp + w];
         u64 tx = *dx ^ nx, tz = *dz ^ nz;                       // C form, bit db: toggle where the old row differs from the new one
-        while (tx) { const int b = __ffsll((long long)tx) - 1; tx &= tx - 1; m.cols[(size_t)(2 * (64 * w + b)) * RW + (db >> 6)] ^= dbit; }
-        while (tz) { const int b = __ffsll((long long)tz) - 1; tz &= tz - 1; m.cols[(size_t)(2 * (64 * w + b) + 1) * RW + (db >> 6)] ^= dbit; }
+        while (tx) { const int b = __ffsll((long long)tx) - 1; tx &= tx - 1; atomicXor(m.cols + (size_t)(2 * (64 * w + b)) * RW + (db >> 6), dbit); }
+        while (tz) { const int b = __ffsll((long long)tz) - 1; tz &= tz - 1; atomicXor(m.cols + (size_t)(2 * (64 * w + b) + 1) * RW + (db >> 6), dbit); }
         u64 cx = nx, cz = nz;                                   // C form, bit pb: the row still equals the pivot row -> clear it
-        while (cx) { const int b = __ffsll((long long)cx) - 1; cx &= cx - 1; m.cols[(size_t)(2 * (64 * w + b)) * RW + (pb >> 6)] ^= pbit; }
-        while (cz) { const int b = __ffsll((long long)cz) - 1; cz &= cz - 1; m.cols[(size_t)(2 * (64 * w + b) + 1) * RW + (pb >> 6)] ^= pbit; }
+        while (cx) { const int b = __ffsll((long long)cx) - 1; cx &= cx - 1; atomicXor(m.cols + (size_t)(2 * (64 * w + b)) * RW + (pb >> 6), pbit); }
+        while (cz) { const int b = __ffsll((long long)cz) - 1; cz &= cz - 1; atomicXor(m.cols + (size_t)(2 * (64 * w + b) + 1) * RW + (pb >> 6), pbit); }
         *dx = nx; *dz = nz;
-        m.rows[(size_t)(2 * pb) * Wp + w] = 0; m.rows[(size_t)(2 * pb + 1) * Wp + w] = 0;
+        m.rows[(size_t)(2 * pb) * Wp + w] = 0;
+        u64 zrow = 0;
+        if (w == int(q >> 6)) {                                 // stabilizer p := Z_q (after this thread's own clearing of that column)
+            zrow = 1ull << (q & 63);
+            atomicOr(m.cols + (size_t)(2 * q + 1) * RW + (pb >> 6), pbit);
+        }
+        m.rows[(size_t)(2 * pb + 1) * Wp + w] = zrow;
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
-        m.rows[(size_t)(2 * pb + 1) * Wp + (q >> 6)] = 1ull << (q & 63);
-        m.cols[(size_t)(2 * q + 1) * RW + (pb >> 6)] |= pbit;
         u64 s = m.sgn[db >> 6]; s = (s & ~dbit) | ((prow[2 * Wp] & 1ull) ? dbit : 0ull); m.sgn[db >> 6] = s;
         s = m.sgn[pb >> 6]; s = (s & ~pbit) | (outcome ? pbit : 0ull); m.sgn[pb >> 6] = s;
     }
