@@ -936,11 +936,14 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     const auto tp0 = std::chrono::steady_clock::now();
     auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count(); };
     double ts_val = 0, ts_scan = 0, ts_alloc = 0, ts_first = 0, ts_enq = 0, ts_join = 0;
-    int32_t rc = validate_circuit(c, n, gates, ngates, nthreads);
-    if (rc) return rc;
-    ts_val = since();
+    // validation runs beside the segment scan and the allocations (neither looks at qubit indices); nothing is compiled or
+    // launched before it has passed
+    int32_t vrc = SK_OK;
+    std::thread vthread([&] { vrc = validate_circuit(c, n, gates, ngates, std::max(1u, nthreads / 2)); ts_val = since(); });
+    struct Joiner { std::thread& t; ~Joiner() { if (t.joinable()) t.join(); } } vjoin{vthread};
+    int32_t rc = SK_OK;
     size_t ng = 0, nm = 0;
-    std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm, nthreads);
+    std::vector<Seg> segs = scan_segments(gates, ngates, ng, nm, std::max(1u, nthreads / 2));
     ts_scan = since();
     const size_t nboff = 2 * ng + 2 * segs.size() + 2;       // chunk tables: a run of k gates needs at most 2k + 2 entries
     rc = reserve_pinned(c, ng * sizeof(sk_gate) + nm * 4 + nboff * 4 + 64);
@@ -955,6 +958,8 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     if (ng) { e = dmalloc(c, &p->d_gates, ng * sizeof(sk_gate)); if (!e) e = dmalloc(c, &p->d_boff, nboff * 4); }
     if (!e && nm) { e = dmalloc(c, &p->d_mq, nm * 4); if (!e) e = dmalloc(c, &p->d_out, nm); if (!e) e = dmalloc(c, &p->d_det, nm); }
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
+    vthread.join();                                            // (validate_circuit may have written c->err: join before any other error path)
+    if (vrc) { sk_program_destroy(p); return vrc; }
     sk_tableau* t = nullptr;
     rc = sk_tableau_create(c, n, &t);
     if (rc) { sk_program_destroy(p); return rc; }
