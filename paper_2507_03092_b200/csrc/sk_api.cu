@@ -1018,7 +1018,7 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     size_t first_meas = segs.size();
     for (size_t si = 0; si < segs.size(); ++si) if (segs[si].meas) { first_meas = si; break; }
     const size_t graph_from = (!c->no_graph && first_meas + 33 <= segs.size()) ? first_meas + 1 : segs.size();   // short programs: plain launches (instantiation would cost more than the gaps)
-    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec = nullptr; cudaStream_t side_stream = nullptr;
     for (size_t si = 0; si < graph_from && !rc; ++si) {
         wait_done(si);
         if (si == 0) ts_first = since();
@@ -1038,6 +1038,17 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && !rcc && graph;
             if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
             if (graph) cudaGraphDestroy(graph);
+            if (ok) {
+                // the executable graph is moved to the device on a side stream while the first block is still running, so
+                // that the launch below does not pay for it
+                cudaStream_t side = nullptr; cudaEvent_t up = nullptr;
+                if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess && cudaEventCreateWithFlags(&up, cudaEventDisableTiming) == cudaSuccess
+                    && cudaGraphUpload(gexec, side) == cudaSuccess && cudaEventRecord(up, side) == cudaSuccess)
+                    cudaStreamWaitEvent(c->stream, up, 0);
+                else cudaGetLastError();
+                if (up) cudaEventDestroy(up);
+                if (side) { side_stream = side; }
+            }
             if (ok) ok = cudaGraphLaunch(gexec, c->stream) == cudaSuccess;
         }
         if (!rc && !ok) {                    // capture is not possible here: plain stream launches
@@ -1061,6 +1072,7 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
                          ts_val, ts_scan, ts_alloc, ts_first, ts_enq, ts_join, ts_hist, since(), nthreads, segs.size(), nbatches);
     } else cudaStreamSynchronize(c->stream);
     if (gexec) cudaGraphExecDestroy(gexec);          // the stream is idle here (record read / synchronised)
+    if (side_stream) cudaStreamDestroy(side_stream);
     sk_program_destroy(p);
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out_t = t;
