@@ -85,10 +85,12 @@ inline std::string emit_native(const Circuit& c) {
     return out;
 }
 
-// SPEC:262-270
-inline std::vector<ChunkViolation> validate_chunks(const Circuit& c) {
+// SPEC:262-270.  Measurement-only chunks are barrier regions and are not reported; strict = true reports them
+// too (third example).
+inline std::vector<ChunkViolation> validate_chunks(const Circuit& c, bool strict = false) {
     uint32_t *vc = nullptr, *vg = nullptr; uint8_t* vk = nullptr; size_t nv = 0;
-    const int rc = sk_circuit_validate_chunks(c.n, c.raw(), c.gates.size(), c.chunk_marks.data(), c.chunk_marks.size(), &vc, &vg, &vk, &nv);
+    const int rc = sk_circuit_validate_chunks_ex(c.n, c.raw(), c.gates.size(), c.chunk_marks.data(), c.chunk_marks.size(),
+                                                 strict ? SK_CHUNKS_STRICT : 0u, &vc, &vg, &vk, &nv);
     if (rc == SK_EDIM) throw DimensionError("validate_chunks: gate qubit out of range");
     if (rc != SK_OK) throw Error("validate_chunks failed");
     std::vector<ChunkViolation> out(nv);

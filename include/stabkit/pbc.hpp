@@ -23,12 +23,13 @@ struct PbcProgram {
 };
 
 // SPEC:545-553.  Mid-circuit measurement throws UnsupportedError.
-// exact = true selects SK_TRANSPILE_EXACT (inverse-gate backward walk + order-preserving separation: the variant that
-// passes the dense-statevector equivalence check of SPEC:563-573); false keeps Algorithms 2-3 as published.
-inline PbcProgram transpile(const Circuit& c, bool exact = false) {
+// The default is the unitary-exact form (inverse-gate backward walk + order-preserving separation: the one that passes the
+// dense-statevector equivalence check SPEC:563-573 names as arbiter); published = true selects Algorithms 2-3 verbatim
+// (SK_TRANSPILE_PUBLISHED), which are not unitarily equivalent in general -- see include/stabkit_b200.h.
+inline PbcProgram transpile(const Circuit& c, bool published = false) {
     Device& dev = Device::instance();
     sk_pbc* p = nullptr;
-    dev.check(sk_transpile_ex(dev.ctx(), c.n, c.raw(), c.gates.size(), exact ? SK_TRANSPILE_EXACT : 0u, &p));
+    dev.check(sk_transpile_ex(dev.ctx(), c.n, c.raw(), c.gates.size(), published ? SK_TRANSPILE_PUBLISHED : 0u, &p));
     PbcProgram out; out.n = c.n;
     uint64_t st[5];
     sk_pbc_stats(p, st);

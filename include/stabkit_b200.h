@@ -167,11 +167,20 @@ int32_t sk_circuit_parse_native(const char* text, size_t len, uint64_t* n, sk_ga
 int32_t sk_circuit_parse_qasm2(const char* text, size_t len, uint64_t* n, sk_gate** gates,
                                size_t* ngates, uint32_t** chunk_marks, size_t* nmarks,
                                size_t* err_line, char* err_msg, size_t err_cap);
-/* SPEC:262-270.  violations: pairs (chunk index, gate index); kind bit 0 = collision, bit 1 = measurement. */
+/* SPEC:262-270.  violations: pairs (chunk index, gate index); kind 1 = collision, 2 = measurement.
+ * A chunk that holds ONLY measurements is a measurement barrier region (every M is a full barrier), not a
+ * chunk intended for sim2d: it is not reported, which is what SPEC:397 requires of the generators' output.  A
+ * measurement next to Clifford gates in one chunk is a violation.  flags = SK_CHUNKS_STRICT reports the measurement-only
+ * chunks too (the literal reading of SPEC:270's `chunk [m 0]` example). */
+#define SK_CHUNKS_STRICT 1u
 int32_t sk_circuit_validate_chunks(uint64_t n, const sk_gate* gates, size_t ngates,
                                    const uint32_t* chunk_marks, size_t nmarks,
                                    uint32_t** viol_chunk, uint32_t** viol_gate, uint8_t** viol_kind,
                                    size_t* nviol);
+int32_t sk_circuit_validate_chunks_ex(uint64_t n, const sk_gate* gates, size_t ngates,
+                                      const uint32_t* chunk_marks, size_t nmarks, uint32_t flags,
+                                      uint32_t** viol_chunk, uint32_t** viol_gate, uint8_t** viol_kind,
+                                      size_t* nviol);
 
 /* ---- Pauli row sets on the device (grouping + Clifford+T pass) ---------- */
 /* A resizable block of signed n-qubit Pauli rows (T_tab / layer / term list). */
@@ -201,14 +210,18 @@ int32_t sk_verify_grouping(sk_rows* r, int mode, const uint32_t* group_of, uint6
 /* SPEC:545-553 transpile (Algorithms 2-4).  Results are read back with the
  * accessors below.  Mid-circuit M -> SK_EUNSUPPORTED. */
 typedef struct sk_pbc sk_pbc;
+/* The DEFAULT (sk_transpile, flags 0) is the unitary-exact form: SPEC:575-589 makes the dense-statevector check
+ * (verify_transpile, TV < 1e-9) the arbiter of every sign convention, and that check requires (a) the INVERSE
+ * gate in Algorithm 2's backward walk (S <-> S^dagger; moving an axis P from behind G to in front of it gives G^dagger P G) and
+ * (b) a T row to stay behind every rotation it anticommutes with (it joins the layer right after the last layer holding an
+ * anticommuting member).  Algorithm 4 and rowsum+i are as published.
+ * SK_TRANSPILE_PUBLISHED selects Algorithms 2-3 verbatim (G's own CHP rule in the backward walk; "first layer from P_0 it
+ * commutes with", PAPER Alg. 2-3) -- NOT unitarily equivalent in general (smallest counter-examples:
+ * `h s t h`, `t h t h t h`); kept for comparison with the paper's text only.  SK_TRANSPILE_EXACT (bit 0) names the default
+ * explicitly and is accepted for source compatibility. */
 int32_t sk_transpile(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out);
-/* flags bit 0 = SK_TRANSPILE_EXACT: the unitary-exact variant.  Algorithm 2 as published applies G's own CHP rule while
- * walking the circuit backwards and Algorithm 3 puts a row into the FIRST layer (from P_0) it commutes with; both are kept
- * verbatim by sk_transpile (flags 0, the reference's text: SPEC:515-533, PAPER Alg. 2-3).  The dense-statevector check the
- * SPEC names as arbiter (verify_transpile) shows that unitary equivalence needs the INVERSE gate in the
- * backward walk (S <-> S^dagger) and a row to stay behind every rotation it anticommutes with; SK_TRANSPILE_EXACT does
- * exactly that (Algorithm 4 and rowsum+i are unchanged) and passes the check on random Clifford+T circuits. */
 #define SK_TRANSPILE_EXACT 1u
+#define SK_TRANSPILE_PUBLISHED 2u
 int32_t sk_transpile_ex(sk_ctx* ctx, uint64_t n, const sk_gate* gates, size_t ngates, uint32_t flags, sk_pbc** out);
 void sk_pbc_destroy(sk_pbc* p);
 /* stats: initial_t, final_rotations_rowcount, final_rotations_pauliweight, layers, passes */

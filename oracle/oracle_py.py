@@ -66,6 +66,7 @@ def lib():
         L.orc_tab_rowsum.restype = C.c_int; L.orc_tab_rowsum.argtypes = [vp, sz, sz]
         L.orc_tab_sim.restype = C.c_int; L.orc_tab_sim.argtypes = [vp, vp, sz, u64, C.c_int, vp, vp, u64]
         L.orc_tab_counters.argtypes = [vp, vp]
+        L.orc_surface_code.restype = u64; L.orc_surface_code.argtypes = [C.c_uint32, C.c_uint32, C.c_int, vp, C.POINTER(sz), vp, C.POINTER(sz)]
         L.orc_transpile.restype = vp; L.orc_transpile.argtypes = [sz, vp, sz]
         L.orc_pbc_free.argtypes = [vp]
         L.orc_pbc_status.restype = C.c_int; L.orc_pbc_status.argtypes = [vp]
@@ -197,6 +198,20 @@ class Rows:
 
     def verify_grouping(self, mode, group):
         return int(lib().orc_verify_grouping(self.h, mode, _p(np.ascontiguousarray(group, np.uint32))))
+
+
+def surface_code(d: int, rounds: int, final_data_measure: bool = False):
+    """SPEC:375-383 surface_code_circuit, the oracle's own generator (independent of the product's):
+    -> (n, gates GATE_DTYPE[], chunk_marks u32[]).  Lets bench.py's reference arm and the tests build their
+    input without loading the CUDA library, and pins the product's generator gate for gate."""
+    L = lib()
+    ng, nm = C.c_size_t(), C.c_size_t()
+    n = L.orc_surface_code(d, rounds, int(final_data_measure), None, C.byref(ng), None, C.byref(nm))
+    if n == 0:
+        raise ValueError(f"surface_code(d={d}, rounds={rounds}): d must be odd >= 3, rounds >= 1 (SPEC:379)")
+    gates = np.zeros(ng.value, dtype=GATE_DTYPE); marks = np.zeros(max(nm.value, 1), dtype=np.uint32)
+    L.orc_surface_code(d, rounds, int(final_data_measure), _p(gates), C.byref(ng), _p(marks), C.byref(nm))
+    return int(n), gates, marks[:nm.value]
 
 
 class Tableau:

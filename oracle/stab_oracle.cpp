@@ -540,6 +540,62 @@ void orc_tab_counters(void* h, uint64_t* out16) {
     for (int i = 0; i < 12; ++i) out16[4 + i] = T->c.gate_hist[i];
 }
 
+// qec_gen -------------------------------------------------------------------
+// SPEC:369-383, 399-403 surface_code_circuit, written independently of the product's generator
+// (paper_2507_03092_b200/csrc/circuit_host.cpp) so that tests can cross-check the two gate for gate; the
+// conventions SPEC leaves open are the ones DESIGN.md section 8 freezes:
+//   data qubit (r, c) = r*d + c; a plaquette is named by its south-east corner (i, j), 0 <= i, j <= d, and touches
+//   the data qubits (i-1,j-1) (i-1,j) (i,j-1) (i,j) that exist; X type iff i+j even; all interior plaquettes, X-type
+//   ones on the top/bottom edge, Z-type ones on the left/right edge; ancillas numbered d*d.. in row-major (i, j) order;
+//   round = [H on X ancillas] [4 CX slots: X: NW NE SW SE, ancilla -> data; Z: NW SW NE SE, data -> ancilla]
+//   [H on X ancillas] [M on every ancilla in index order], a chunk mark in front of each bracket.
+// Two passes: count, then fill caller-provided arrays (gates == nullptr -> sizes only).  Returns the qubit count, 0 = bad args.
+uint64_t orc_surface_code(uint32_t d, uint32_t rounds, int final_data_measure, Gate* gates, size_t* ngates, uint32_t* marks, size_t* nmarks) {
+    if (d < 3 || !(d & 1) || rounds == 0) return 0;
+    const long D = d;
+    std::vector<uint32_t> anc_of((D + 1) * (D + 1), 0xffffffffu);          // plaquette -> ancilla qubit
+    uint32_t q = uint32_t(D * D);
+    for (long i = 0; i <= D; ++i) for (long j = 0; j <= D; ++j) {
+        const bool xtype = ((i + j) & 1) == 0, edge_i = (i == 0 || i == D), edge_j = (j == 0 || j == D);
+        bool keep;
+        if (!edge_i && !edge_j) keep = true;
+        else if (edge_i && !edge_j) keep = xtype;
+        else if (edge_j && !edge_i) keep = !xtype;
+        else keep = false;
+        if (keep) anc_of[i * (D + 1) + j] = q++;
+    }
+    const uint64_t nq = q;
+    size_t ng = 0, nm = 0;
+    auto emit = [&](uint8_t k, uint32_t a, uint32_t b) { if (gates) { Gate g{}; g.kind = k; g.q0 = a; g.q1 = b; gates[ng] = g; } ++ng; };
+    size_t last_mark = size_t(-1);       // a mark is a gate index > 0, never repeated
+    auto mark2 = [&] { if (ng == 0 || last_mark == ng) return; last_mark = ng; if (marks) marks[nm] = uint32_t(ng); ++nm; };
+    // corner offsets of a plaquette's data qubits in each type's CX order
+    static const int xo[4][2] = {{-1, -1}, {-1, 0}, {0, -1}, {0, 0}};     // NW NE SW SE
+    static const int zo[4][2] = {{-1, -1}, {0, -1}, {-1, 0}, {0, 0}};     // NW SW NE SE
+    for (uint32_t r = 0; r < rounds; ++r) {
+        for (int phase = 0; phase < 7; ++phase) {     // 0: H, 1-4: CX slot, 5: H, 6: M
+            mark2();
+            for (long i = 0; i <= D; ++i) for (long j = 0; j <= D; ++j) {
+                const uint32_t a = anc_of[i * (D + 1) + j];
+                if (a == 0xffffffffu) continue;
+                const bool xtype = ((i + j) & 1) == 0;
+                if (phase == 0 || phase == 5) { if (xtype) emit(K_H, a, 0); }
+                else if (phase == 6) emit(K_M, a, 0);
+                else {
+                    const int* o = xtype ? xo[phase - 1] : zo[phase - 1];
+                    const long rr = i + o[0], cc = j + o[1];
+                    if (rr < 0 || cc < 0 || rr >= D || cc >= D) continue;
+                    const uint32_t dq = uint32_t(rr * D + cc);
+                    if (xtype) emit(K_CX, a, dq); else emit(K_CX, dq, a);
+                }
+            }
+        }
+    }
+    if (final_data_measure) { mark2(); for (uint32_t k = 0; k < uint32_t(D * D); ++k) emit(K_M, k, 0); }
+    *ngates = ng; *nmarks = nm;
+    return nq;
+}
+
 // transpiler ----------------------------------------------------------------
 void* orc_transpile(size_t n, const Gate* g, size_t ng) { Pbc* P = new Pbc(n); transpile(*P, g, ng); return P; }
 // flags bit 0: unitary-exact variant (inverse-gate conjugation in Algorithm 2, order-preserving separation in Algorithm 3)

@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
             "sk_circuit_parse_native": (i32, [C.c_char_p, sz, P(u64), P(vp), P(sz), P(vp), P(sz), P(sz), C.c_char_p, sz]),
             "sk_circuit_parse_qasm2": (i32, [C.c_char_p, sz, P(u64), P(vp), P(sz), P(vp), P(sz), P(sz), C.c_char_p, sz]),
             "sk_circuit_validate_chunks": (i32, [u64, vp, sz, vp, sz, P(vp), P(vp), P(vp), P(sz)]),
+            "sk_circuit_validate_chunks_ex": (i32, [u64, vp, sz, vp, sz, u32, P(vp), P(vp), P(vp), P(sz)]),
             "sk_rows_create": (i32, [vp, u64, u64, P(vp)]),
             "sk_rows_destroy": (None, [vp]),
             "sk_rows_count": (u64, [vp]),
@@ -143,7 +144,7 @@ EXPORTS = [
     "sk_measure_z", "sk_measure_batch", "sk_tableau_rowsum", "sk_program_create", "sk_program_destroy",
     "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_program_run_shots", "sk_sim", "sk_free",
     "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native", "sk_circuit_parse_qasm2",
-    "sk_circuit_validate_chunks", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
+    "sk_circuit_validate_chunks", "sk_circuit_validate_chunks_ex", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
     "sk_rows_download", "sk_rows_conj_layer", "sk_commutation_vector",
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",
     "sk_group_first_fit", "sk_verify_grouping", "sk_transpile", "sk_transpile_ex", "sk_pbc_destroy", "sk_pbc_stats",
@@ -279,12 +280,13 @@ def parse_qasm2_subset(text: str) -> Circuit:
     return Circuit(n.value, _take(g, ng.value, GATE_DTYPE), _take(mk, nmk.value, np.uint32))
 
 
-def validate_chunks(c: Circuit):
-    """-> list of (chunk index, gate index, kind) with kind 'collision' | 'measurement'."""
+def validate_chunks(c: Circuit, strict: bool = False):
+    """-> list of (chunk index, gate index, kind) with kind 'collision' | 'measurement'.  Chunks that hold only
+    measurements are barrier regions and are not reported; strict=True reports them too (third example)."""
     L = lib()
     vc, vg, vk, nv = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_size_t()
-    rc = L.sk_circuit_validate_chunks(c.n, _ptr(c.gates), len(c.gates), _ptr(c.chunk_marks), len(c.chunk_marks),
-                                      C.byref(vc), C.byref(vg), C.byref(vk), C.byref(nv))
+    rc = L.sk_circuit_validate_chunks_ex(c.n, _ptr(c.gates), len(c.gates), _ptr(c.chunk_marks), len(c.chunk_marks), 1 if strict else 0,
+                                         C.byref(vc), C.byref(vg), C.byref(vk), C.byref(nv))
     _check_noctx(rc, "validate_chunks")
     a, b, k = _take(vc, nv.value, np.uint32), _take(vg, nv.value, np.uint32), _take(vk, nv.value, np.uint8)
     return [(int(x), int(y), "collision" if z == 1 else "measurement") for x, y, z in zip(a, b, k)]
@@ -522,11 +524,12 @@ class Rows:
 class Pbc:
     """Result of sk_transpile (PbcProgram)."""
 
-    def __init__(self, ctx: Context, circ: Circuit, exact: bool = False):
-        """exact=False: Algorithms 2-3 as published (sk_transpile); exact=True: SK_TRANSPILE_EXACT (stabkit_b200.h)."""
+    def __init__(self, ctx: Context, circ: Circuit, exact: bool = True):
+        """exact=True (default, sk_transpile): the unitary-exact form; exact=False: SK_TRANSPILE_PUBLISHED, Algorithms 2-3
+        verbatim (stabkit_b200.h explains why they are not the default)."""
         self.ctx, self.n, self.W = ctx, circ.n, words_for(circ.n)
         self._h = C.c_void_p()
-        ctx.check(lib().sk_transpile_ex(ctx._h, circ.n, _ptr(circ.gates), len(circ.gates), 1 if exact else 0, C.byref(self._h)))
+        ctx.check(lib().sk_transpile_ex(ctx._h, circ.n, _ptr(circ.gates), len(circ.gates), 0 if exact else 2, C.byref(self._h)))
 
     def close(self):
         if self._h:

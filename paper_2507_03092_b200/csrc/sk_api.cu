@@ -557,7 +557,8 @@ template <class F> static void parallel_for(unsigned nthreads, size_t count, F&&
     for (auto& t : th) t.join();
 }
 // threads look for any offending gate; the (rare) error path re-runs in order to report the first one
-static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, unsigned nthreads) {
+// pure scan (touches no context state, so it may run on a thread of its own): does any gate fail validation?
+static bool circuit_has_bad_gate(uint64_t n, const sk_gate* gates, size_t ngates, unsigned nthreads) {
     std::atomic<bool> bad{false};
     parallel_for(nthreads, ngates, [&](size_t lo, size_t hi, unsigned) {
         bool b = false;
@@ -567,7 +568,10 @@ static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
         }
         if (b) bad = true;
     });
-    if (bad)
+    return bad;
+}
+// the slow path after a positive scan: the first offending gate, with its message in c->err
+static int32_t report_bad_gate(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates) {
         for (size_t i = 0; i < ngates; ++i) {
             int32_t rc = validate_gate(c, gates[i], n, i);
             if (rc) return rc;
@@ -575,6 +579,9 @@ static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, siz
                 SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: T/TDG is not a Clifford gate; use the transpiler path (SPEC:191)", i);
         }
     return SK_OK;
+}
+static int32_t validate_circuit(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, unsigned nthreads) {
+    return circuit_has_bad_gate(n, gates, ngates, nthreads) ? report_bad_gate(c, n, gates, ngates) : int32_t(SK_OK);
 }
 static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_t& ng, size_t& nm, unsigned nthreads = 1) {
     // boundaries = positions where "is a measurement" changes; found chunk-parallel, concatenated in order
@@ -938,8 +945,9 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     double ts_val = 0, ts_scan = 0, ts_alloc = 0, ts_first = 0, ts_enq = 0, ts_join = 0;
     // validation runs beside the segment scan and the allocations (neither looks at qubit indices); nothing is compiled or
     // launched before it has passed
-    int32_t vrc = SK_OK;
-    std::thread vthread([&] { vrc = validate_circuit(c, n, gates, ngates, std::max(1u, nthreads / 2)); ts_val = since(); });
+    // (the thread only scans: c->err is written by the calling thread alone, after the join)
+    bool vbad = false;
+    std::thread vthread([&] { vbad = circuit_has_bad_gate(n, gates, ngates, std::max(1u, nthreads / 2)); ts_val = since(); });
     struct Joiner { std::thread& t; ~Joiner() { if (t.joinable()) t.join(); } } vjoin{vthread};
     int32_t rc = SK_OK;
     size_t ng = 0, nm = 0;
@@ -958,8 +966,8 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     if (ng) { e = dmalloc(c, &p->d_gates, ng * sizeof(sk_gate)); if (!e) e = dmalloc(c, &p->d_boff, nboff * 4); }
     if (!e && nm) { e = dmalloc(c, &p->d_mq, nm * 4); if (!e) e = dmalloc(c, &p->d_out, nm); if (!e) e = dmalloc(c, &p->d_det, nm); }
     if (e) { sk_program_destroy(p); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the program: %s", cudaGetErrorString(e)); }
-    vthread.join();                                            // (validate_circuit may have written c->err: join before any other error path)
-    if (vrc) { sk_program_destroy(p); return vrc; }
+    vthread.join();
+    if (vbad) { sk_program_destroy(p); const int32_t vrc = report_bad_gate(c, n, gates, ngates); return vrc ? vrc : int32_t(SK_EARG); }
     sk_tableau* t = nullptr;
     rc = sk_tableau_create(c, n, &t);
     if (rc) { sk_program_destroy(p); return rc; }

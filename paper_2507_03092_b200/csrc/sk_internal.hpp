@@ -47,6 +47,13 @@ struct sk_ctx {
         if (_e != cudaSuccess) SK_FAIL(ctx, SK_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
     } while (0)
 
+// Frees the device pointers registered with it when the scope ends (early SK_CUDA / SK_FAIL returns included).
+struct SkDevScope {
+    std::vector<void**> slots;
+    template <class T> void own(T** p) { slots.push_back(reinterpret_cast<void**>(p)); }
+    ~SkDevScope() { for (void** p : slots) if (*p) { cudaFree(*p); *p = nullptr; } }
+};
+
 int32_t sk_ctx_reserve_gates(sk_ctx* ctx, size_t bytes);
 int32_t sk_ctx_reserve_tmp(sk_ctx* ctx, size_t bytes);
 

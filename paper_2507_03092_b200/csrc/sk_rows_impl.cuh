@@ -3,6 +3,7 @@
 // Host orchestration only; kernels are in kernels_rows.cuh / kernels_layer.cuh / kernels_transpose.cuh.
 #pragma once
 #include <climits>
+#include <memory>
 #include <numeric>
 
 #include "kernels_rows.cuh"
@@ -54,22 +55,23 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     const int B = std::min(count, 1024);
     const int GW32 = count / 32 + 2;
     u32* d_bitmap = nullptr; u32* d_ng = nullptr; u32* d_ff = nullptr;
+    u32* d_cnt = nullptr; u32* d_off = nullptr; u32* d_fillc = nullptr; u64* d_gterms = nullptr; u32* d_gmin = nullptr;
+    SkDevScope scope; scope.own(&d_bitmap); scope.own(&d_ng); scope.own(&d_cnt); scope.own(&d_off); scope.own(&d_fillc); scope.own(&d_gterms);
     SK_CUDA(c, cudaMalloc(&d_bitmap, (size_t)B * GW32 * 4));
     SK_CUDA(c, cudaMalloc(&d_ng, 4 + (size_t)B * 4));
     d_ff = d_ng + 1;
     SK_CUDA(c, cudaMemsetAsync(d_ng, 0, 4, c->stream));
     const int Bt = std::max(1, std::min(B, (40 * 1024) / (2 * W * 8)));     // block terms staged per CTA (<= 40 KB smem)
     const size_t smem = (size_t)Bt * 2 * W * 8;
-    if (smem > 48 * 1024) { cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_EDIM, "rows too wide for the conflict kernel (W=%d)", W); }
+    if (smem > 48 * 1024) SK_FAIL(c, SK_EDIM, "rows too wide for the conflict kernel (W=%d)", W);
     // group-major path (W <= 2, i.e. up to 128 qubits -- BASELINE config 4): CSR of the placed terms, thread per group
     static const bool csr_off = getenv("SK_GROUP_CSR") && atoi(getenv("SK_GROUP_CSR")) == 0;
     const bool csr = W <= 2 && !csr_off && count > B;
     static const bool legacy_resolver = getenv("SK_GROUP_RESOLVER") && atoi(getenv("SK_GROUP_RESOLVER")) == 0;   // A/B switch: the sequential-scan resolver
-    u32* d_cnt = nullptr; u32* d_off = nullptr; u32* d_fillc = nullptr; u64* d_gterms = nullptr; u32* d_gmin = nullptr;
     if (csr) {
         cudaError_t e1 = cudaMalloc(&d_cnt, ((size_t)count + 4) * 4), e2 = cudaMalloc(&d_off, ((size_t)count + 2) * 4);
         cudaError_t e3 = cudaMalloc(&d_fillc, ((size_t)count + 2) * 4), e4 = cudaMalloc(&d_gterms, (size_t)count * 32);
-        if (e1 || e2 || e3 || e4) { cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_fillc); cudaFree(d_gterms); cudaFree(d_bitmap); cudaFree(d_ng); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the grouped term store"); }
+        if (e1 || e2 || e3 || e4) SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for the grouped term store");
         SK_CUDA(c, cudaMemsetAsync(d_cnt, 0, ((size_t)count + 4) * 4, c->stream));
         d_gmin = d_cnt + count + 3;
     }
@@ -100,8 +102,7 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     u32 ng = 0;
     SK_CUDA(c, cudaMemcpyAsync(&ng, d_ng, 4, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(d_bitmap); cudaFree(d_ng); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_fillc); cudaFree(d_gterms);
-    *ngroups = ng;
+    *ngroups = ng;                       // (scope frees the scratch buffers)
     return SK_OK;
 }
 
@@ -412,12 +413,12 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
 extern "C" int32_t sk_transpile(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, sk_pbc** out) {
     return sk_transpile_ex(c, n, gates, ngates, 0u, out);
 }
-// flags bit 0 (SK_TRANSPILE_EXACT): unitary-exact variant -- the backward walk of Algorithm 2 conjugates by the inverse
+// Default (flags 0 or SK_TRANSPILE_EXACT): unitary-exact form -- the backward walk of Algorithm 2 conjugates by the inverse
 // gate (S <-> S^dagger) and Algorithm 3 / the safety pass place a row right after the last layer holding an anticommuting
-// member instead of in the first commuting layer (see include/stabkit_b200.h and DESIGN.md section 8).
+// member.  SK_TRANSPILE_PUBLISHED: Algorithms 2-3 verbatim (see include/stabkit_b200.h and DESIGN.md section 8).
 extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t ngates, uint32_t flags, sk_pbc** out) {
     if (!c || !out || (!gates && ngates)) return SK_EARG;
-    const bool exact = (flags & 1u) != 0;
+    const bool exact = (flags & SK_TRANSPILE_PUBLISHED) == 0;
     const int fit_mode = exact ? kOrderedFit : 0;
     *out = nullptr;
     if (n == 0) SK_FAIL(c, SK_EDIM, "transpile: circuit has zero qubits");
@@ -472,7 +473,8 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
     int32_t rc = dm_transpose_c2r(c, m);
     if (rc) return rc;
     u64* rowsT = m.rows + (size_t)2 * T0 * m.Wp;                             // R-form view of the T rows
-    sk_pbc* p = new sk_pbc();
+    std::unique_ptr<sk_pbc> p_owner(new sk_pbc());       // released into *out on success only: every early return frees it
+    sk_pbc* p = p_owner.get();
     p->ctx = c; p->n = n; p->W = W; p->stats[0] = nT;
     std::vector<int> lvl(nT, 0);
     uint64_t passes = 0;
@@ -485,7 +487,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         SK_CUDA(c, cudaMalloc(&d_hash, nT * 8)); guard.extra.push_back(d_hash);
         uint64_t nl = 0;
         rc = device_first_fit(c, rowsT, m.Wp, W, int(nT), fit_mode, d_group, &nl);
-        if (rc) { delete p; return rc; }
+        if (rc) return rc;
         SK_CUDA(c, cudaMemcpyAsync(lvl.data(), d_group, nT * 4, cudaMemcpyDeviceToHost, c->stream));
         SK_CUDA(c, cudaStreamSynchronize(c->stream));
         // ---- Algorithm 4, one pass = pairs from the pass-start state + ordered push-through
@@ -494,7 +496,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
             ++passes;
             SK_CUDA(c, cudaMemcpyAsync(d_lvl, lvl.data(), nT * 4, cudaMemcpyHostToDevice, c->stream));
             rc = dup_pairs(c, rowsT, m.Wp, W, int(nT), d_lvl, d_pair, d_hash);
-            if (rc) { delete p; return rc; }
+            if (rc) return rc;
             SK_CUDA(c, cudaMemcpyAsync(pair.data(), d_pair, nT * 4, cudaMemcpyDeviceToHost, c->stream));
             SK_CUDA(c, cudaMemcpyAsync(sg.data(), m.sgn, sgn_bytes, cudaMemcpyDeviceToHost, c->stream));
             SK_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -516,7 +518,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
                 for (int k = 0; k < np; ++k) { idx[k] = pushes[k].first; plevel[k] = pushes[k].level; psign[k] = uint8_t(pushes[k].sign); }
                 const size_t need = (size_t)np * 2 * m.Wp * 8 + (size_t)np * 9 + 256;
                 rc = sk_ctx_reserve_tmp(c, need);
-                if (rc) { delete p; return rc; }
+                if (rc) return rc;
                 u64* d_push = (u64*)c->d_tmp; int* d_idx = (int*)(d_push + (size_t)np * 2 * m.Wp); int* d_plevel = d_idx + np; uint8_t* d_psign = (uint8_t*)(d_plevel + np);
                 SK_CUDA(c, cudaMemcpyAsync(d_idx, idx.data(), np * 4, cudaMemcpyHostToDevice, c->stream));
                 SK_CUDA(c, cudaMemcpyAsync(d_plevel, plevel.data(), np * 4, cudaMemcpyHostToDevice, c->stream));
@@ -540,7 +542,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         }
     }
     rc = check_ws(c);
-    if (rc) { delete p; return rc; }
+    if (rc) return rc;
     // ---- read back: T rows (host cache), M_tab
     {
         const size_t words = nT * (size_t)W;
@@ -548,7 +550,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         p->mx.assign(2 * n * W, 0); p->mz.assign(2 * n * W, 0); p->ms.assign(2 * n, 0);
         const size_t total_rows = 2 * n + nT, tw = total_rows * W;
         rc = sk_ctx_reserve_tmp(c, tw * 16 + total_rows + 64);
-        if (rc) { delete p; return rc; }
+        if (rc) return rc;
         u64* dx = (u64*)c->d_tmp; u64* dz = dx + tw; uint8_t* ds = (uint8_t*)(dz + tw);
         // M_tab with the tableau split mapping, then the T rows with a flat mapping shifted by T0
         k_unpack_rows<<<(unsigned)((2 * n * W + 255) / 256), 256, 0, c->stream>>>(m.rows, dx, dz, int(2 * n), W, m.Wp, int(n), NS);
@@ -581,7 +583,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         for (size_t k = 0; k < nT; ++k) gid[k] = 0x40000000u + uint32_t(k);
         for (uint32_t k : L) gid[k] = 0;
         rc = sk_ctx_reserve_tmp(c, nT * 4 + 64);
-        if (rc) { delete p; return rc; }
+        if (rc) return rc;
         unsigned long long* d_n = (unsigned long long*)c->d_tmp; u32* d_g = (u32*)(d_n + 1);
         SK_CUDA(c, cudaMemsetAsync(d_n, 0, 8, c->stream));
         SK_CUDA(c, cudaMemcpyAsync(d_g, gid.data(), nT * 4, cudaMemcpyHostToDevice, c->stream));
@@ -594,7 +596,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         // re-separate this layer's rows (in order) with the same first-fit kernels
         sk_rows* sub = nullptr;
         rc = sk_rows_create(c, n, L.size(), &sub);
-        if (rc) { delete p; return rc; }
+        if (rc) return rc;
         std::vector<u64> sx(L.size() * W), sz(L.size() * W); std::vector<uint8_t> ss(L.size());
         for (size_t k = 0; k < L.size(); ++k) {
             std::copy(&p->tx[(size_t)L[k] * W], &p->tx[(size_t)L[k] * W] + W, &sx[k * W]);
@@ -614,7 +616,7 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
             }
         }
         sk_rows_destroy(sub);
-        if (rc) { delete p; return rc; }
+        if (rc) return rc;
         std::vector<std::vector<uint32_t>> parts(nsub);
         for (size_t k = 0; k < L.size(); ++k) parts[sub_of[k]].push_back(L[k]);
         for (auto& q : parts) p->layers.push_back(q);
@@ -625,6 +627,6 @@ extern "C" int32_t sk_transpile_ex(sk_ctx* c, uint64_t n, const sk_gate* gates, 
         for (int w = 0; w < W; ++w) weight += __builtin_popcountll(p->tx[(size_t)k * W + w] | p->tz[(size_t)k * W + w]);
     }
     p->stats[1] = rows_left; p->stats[2] = weight; p->stats[3] = p->layers.size(); p->stats[4] = nT ? passes : 1;
-    *out = p;
+    *out = p_owner.release();
     return SK_OK;
 }

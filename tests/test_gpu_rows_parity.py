@@ -113,7 +113,8 @@ def test_transpile_examples(sk, ctx, orc):                                    # 
     for n, gates in ((1, [(T, 0, 0), (H, 0, 0)]), (1, [(H, 0, 0), (T, 0, 0)]), (2, [(H, 0, 0), (CX, 0, 1), (M, 0, 0), (M, 1, 0)]),
                      (1, [(T, 0, 0)] * 2), (1, [(T, 0, 0)] * 8), (1, [(T, 0, 0), (TDG, 0, 0)]), (1, [(H, 0, 0), (T, 0, 0), (H, 0, 0), (M, 0, 0)]),
                      (3, [(H, 1, 0), (CX, 1, 2)])):
-        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates, exact=True))          # default = unitary-exact form
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates), exact=False), orc.Pbc(n, gates))         # SK_TRANSPILE_PUBLISHED
     with pytest.raises(sk.UnsupportedError):
         sk.Pbc(ctx, sk.Circuit(2, [(M, 0, 0), (H, 0, 0)]))
 
@@ -122,24 +123,27 @@ def test_transpile_random_small(sk, ctx, orc):                                # 
     rng = np.random.default_rng(8)
     for trial in range(120):
         n = int(rng.integers(1, 7)); gates = rand_ct(rng, n, int(rng.integers(5, 60)), pt=float(rng.uniform(0.1, 0.5)))
-        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates, exact=True))
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates), exact=False), orc.Pbc(n, gates))
 
 
 @pytest.mark.parametrize("n,G,pt", [(20, 2000, 0.2), (100, 4000, 0.1), (1000, 6000, 0.1), (70, 6000, 0.4)])
 def test_transpile_random_large(sk, ctx, orc, n, G, pt):                      # BASELINE config 5 shape
     rng = np.random.default_rng(n + G)
     gates = rand_ct(rng, n, G, pt)
-    assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates))
+    assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates, exact=True))
+    assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates), exact=False), orc.Pbc(n, gates))
 
 
-def test_transpile_exact_mode_matches_oracle_and_the_statevector(sk, ctx, orc):
-    """SK_TRANSPILE_EXACT: bit parity with the oracle's exact variant, and -- independently of any tableau convention -- the
-    dense-statevector equivalence check of SPEC:563-573 on the DEVICE output (TV < 1e-9)."""
+def test_transpile_default_matches_oracle_and_the_statevector(sk, ctx, orc):
+    """The DEFAULT transpile path (sk_transpile, flags 0; circuits with S / S-dagger gates included): bit parity with the
+    oracle's exact variant, and -- independently of any tableau convention -- the dense-statevector equivalence check of
+    SPEC:563-573 on the DEVICE output (TV < 1e-9)."""
     from oracle import dense as dn
     rng = np.random.default_rng(77)
     for trial in range(80):
         n = int(rng.integers(1, 6)); gates = rand_ct(rng, n, int(rng.integers(5, 60)), pt=float(rng.uniform(0.1, 0.5)))
-        d = sk.Pbc(ctx, sk.Circuit(n, gates), exact=True)
+        d = sk.Pbc(ctx, sk.Circuit(n, gates))
         assert_same_pbc(d, orc.Pbc(n, gates, exact=True))
         st = d.stats()
         layers = [[(int(x[i, 0]), int(z[i, 0]), int(r[i])) for i in range(len(r))] for x, z, r in (d.layer(k) for k in range(st["layers"]))]
@@ -148,4 +152,4 @@ def test_transpile_exact_mode_matches_oracle_and_the_statevector(sk, ctx, orc):
         assert dn.verify_transpile(n, [g for g in gates if g[0] != M], layers, rows) < 1e-9
     for n, G, pt in ((20, 2000, 0.2), (100, 4000, 0.1), (70, 3000, 0.4)):
         gates = rand_ct(np.random.default_rng(n + G + 1), n, G, pt)
-        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates), exact=True), orc.Pbc(n, gates, exact=True))
+        assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates, exact=True))

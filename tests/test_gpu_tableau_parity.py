@@ -242,6 +242,35 @@ def test_surface_code_d71_oracle_rounds_and_full_properties(sk, ctx, orc):   # B
     assert (adet == 1).all() and (again == data).all()
 
 
+def test_surface_code_d71_full_length_bit_parity(sk, ctx, orc):           # BASELINE config 3 at its stated size
+    """The headline workload, all 71 rounds + the final data-qubit M: the whole measurement record (362 881 outcome and
+    deterministic bytes), every x/z word and every sign of the final tableau equal the oracle's (SPEC:730 bit-exact
+    schedule determinism).  The circuit comes from the ORACLE's own generator, which must equal the product's
+    gate for gate.  One oracle run of the full circuit costs ~25 s on the box's 16 host threads."""
+    d = 71
+    n, gates, marks = orc.surface_code(d, d, True)
+    c = sk.surface_code_circuit(d, d, final_data_measure=True)
+    assert n == c.n and (gates == c.gates).all() and (marks == c.chunk_marks).all()
+    o = orc.Tableau(n)
+    oo, od, rc = o.sim(gates, SEED, workers=os.cpu_count() or 8)
+    assert rc == 0 and len(oo) == 362881
+    for mode in (0, 1):                                                    # sim and sim2d (SPEC:323)
+        t, out, det, warn = ctx.sim(c, SEED, mode=mode)
+        assert warn == 0
+        assert (out == oo).all(), "outcome bytes differ at d=71 x 71"
+        assert (det == od).all(), "deterministic flags differ at d=71 x 71"
+        assert_same_tableau(t, o)
+        t.close()
+    # the resident-program path bench.py times (sk_program_run on a reset tableau) gives the same record and tableau
+    prog = sk.Program(ctx, c, mode=0); tab = sk.Tableau(ctx, n)
+    for _ in range(2):                                                     # second run = CUDA-graph replay
+        tab.reset(); prog.run(tab, SEED)
+        o2, d2 = prog.read_record()
+        assert (o2 == oo).all() and (d2 == od).all()
+        assert_same_tableau(tab, o)
+    prog.close(); tab.close()
+
+
 @pytest.mark.parametrize("columns,width,rowcap,fold", [(1, 64, 0, 1), (1, 5, 0, 1), (1, 1, 0, 1), (0, 7, 0, 1), (0, 1, 0, 1),
                                                        (0, 64, 12, 1), (0, 9, 30, 1), (0, 64, 0, 0), (0, 16, 25, 0)])
 def test_panel_factorisation_variants(sk, orc, columns, width, rowcap, fold):

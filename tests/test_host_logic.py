@@ -56,15 +56,28 @@ def test_surface_code_generator(sk):                # SPEC:375-383, 397; SURVEY 
         k = c.gates["kind"]
         assert c.n == 2 * d * d - 1
         assert ((k == sk.H).sum(), (k == sk.CX).sum(), (k == sk.M).sum()) == (nH, nCX, nM)
-    c = sk.surface_code_circuit(5, 2)
-    v = sk.validate_chunks(c)
-    assert v and all(kind == "measurement" for _, _, kind in v)       # no collisions in any emitted chunk
+    for d, r, f in ((3, 1, False), (5, 2, False), (7, 3, True)):
+        c = sk.surface_code_circuit(d, r, f)
+        assert sk.validate_chunks(c) == []                              # every emitted chunk passes
+        v = sk.validate_chunks(c, strict=True)                          # strict: the M blocks are reported, and nothing else
+        assert len(v) == c.num_measurements and all(kind == "measurement" for _, _, kind in v)
     # every ancilla has 2 or 4 neighbours; X and Z checks each (d^2-1)/2
     deg = {}
     for g in sk.surface_code_circuit(5, 1).gates:
         if g["kind"] == sk.CX:
             a = int(max(g["q0"], g["q1"])); deg[a] = deg.get(a, 0) + 1
     assert len(deg) == 24 and set(deg.values()) == {2, 4}
+
+
+def test_surface_code_generator_equals_the_oracles_independent_one(sk, orc):
+    """The product generator (csrc/circuit_host.cpp) and the oracle's own (oracle/stab_oracle.cpp: orc_surface_code), written
+    separately from SPEC:375-403 + DESIGN section 8, agree gate for gate and mark for mark."""
+    for d, r, f in ((3, 1, False), (3, 3, True), (5, 2, True), (7, 7, False), (9, 1, True), (25, 2, True), (71, 2, True)):
+        c = sk.surface_code_circuit(d, r, f)
+        n, g, m = orc.surface_code(d, r, f)
+        assert n == c.n and len(g) == len(c.gates) and (g == c.gates).all() and (m == c.chunk_marks).all(), (d, r, f)
+    with pytest.raises(ValueError):
+        orc.surface_code(4, 1)
 
 
 def test_random_layered_generator(sk):              # SPEC:385-393
@@ -76,7 +89,8 @@ def test_random_layered_generator(sk):
     with pytest.raises(sk.StabkitError):
         sk.random_layered_circuit(7, 1)
     c = sk.random_layered_circuit(64, 3)
-    assert all(kind == "measurement" for _, _, kind in sk.validate_chunks(c))
+    assert sk.validate_chunks(c) == []
+    assert all(kind == "measurement" for _, _, kind in sk.validate_chunks(c, strict=True))
     m = [int(g["q0"]) for g in c.gates[:32 + 32 + 7] if g["kind"] == sk.M]
     assert len(m) == 7 and len(set(m)) == 7 and all(q >= 32 for q in m)
 
@@ -101,7 +115,10 @@ def test_parse_native(sk):
 def test_validate_chunks(sk):
     assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\nh 1")) == []
     assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\ncx 0 1")) == [(0, 1, "collision")]
-    assert sk.validate_chunks(sk.parse_native("qubits 1\nm 0")) == [(0, 0, "measurement")]
+    assert sk.validate_chunks(sk.parse_native("qubits 1\nm 0"), strict=True) == [(0, 0, "measurement")]   # SPEC:270, literal
+    assert sk.validate_chunks(sk.parse_native("qubits 1\nm 0")) == []                  # a measurement barrier region
+    assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\nm 1")) == [(0, 1, "measurement")]          # M next to a gate
+    assert sk.validate_chunks(sk.parse_native("qubits 2\nh 0\nchunk\nm 1\nm 1\nchunk\nh 1")) == []
 
 
 def test_parse_qasm2_subset(sk):
