@@ -86,6 +86,7 @@ struct MeasWs {
     u64 cprof[16];      // debug: SM cycles per step section, thread 0 [0..7] and thread 96 [8..15]: random {search+bar, gather+bar, update}, det {search+bar, gather+bar, rest}
     u64 ctaphase[160 * 4];   // debug: per-CTA own time (ns) in panel phases G, F, V+D1, A+D2 (excluding barrier waits)
     u64 fprof[8];       // factorise (CTA 0) ns: load, random steps, deterministic steps, tail ; [4] random steps, [5] deterministic steps
+    u64 trace[8 * 3 * 8];   // debug timeline (globaltimer ns): panels 20..27 of a launch x CTA {0, 1, last} x 8 events
 };
 
 constexpr int kMeasThreads = 512;
@@ -126,6 +127,7 @@ struct MeasArgs {
     int row_cap;        // most active rows the row-form factorisation takes (kRowCap; SK_ROW_CAP lowers it for tests)
     int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
+    int seq_rows;       // SK_PANEL_SEQ=1: step-by-step row-form factorisation instead of the level form (A/B and testing aid)
 };
 
 __device__ __forceinline__ u64 gtime() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
@@ -347,6 +349,41 @@ struct PanelSmem {
     u32 dcnt[kPanelMax]; u32 gmin[3]; u64 wbp[2][kRowThreads / 32], wmp[2][kRowThreads / 32]; u32 wcnt[kRowThreads / 32]; u64 psign; u32 podd; u32 pready;
 };
 
+// Common tail of the row-form factorisations: the pivots join the touched-row list, outcomes of the random steps
+// (counter RNG), panel-start signs of the pivot rows, counters, and the panel description for the other CTAs.
+__device__ __forceinline__ void panel_rows_tail(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32* tlist, u64* tM) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    constexpr u32 kInf = 0xffffffffu;
+    u64 randmask = 0;
+    for (int j = 0; j < Bn; ++j) if (ps.piv[j] != kInf) randmask |= 1ull << j;
+    const int nrand = __popcll(randmask);
+    const u32 ntr = ps.nt;
+    if (tid < Bn && ((randmask >> tid) & 1ull)) {
+        ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
+        const u32 at = ntr + (u32)__popcll(randmask & ((1ull << tid) - 1ull));
+        __stcg(tlist + at, ps.piv[tid]); __stcg(tM + at, 0ull);          // the pivot itself: -> +-Z_q
+        atomicOr(a.tbits + (ps.piv[tid] >> 6), 1ull << (ps.piv[tid] & 63));
+    }
+    if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
+        const u32 pl = ps.piv[tid];
+        const u32 bal = __ballot_sync(0xffffffffu, pl != kInf && sign_bit(a.m.sgn, int(pl)));
+        if (lane == 0) ps.full32[tid >> 5] = bal;
+        if (tid < Bn && pl == kInf) atomicAdd(&ps.kdet, ps.dcnt[tid] + (u32)__popcll(ps.dZ[tid]));
+    }
+    __syncthreads();
+    PanelInfo* info = a.info;
+    if (tid < kPanelMax) {
+        info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid]; info->dcnt[tid] = ps.dcnt[tid];
+        info->piv[tid] = ps.piv[tid]; info->outc[tid] = ps.outc[tid];
+    }
+    if (tid == 0) {
+        info->randmask = randmask; info->nt = ntr + (u32)nrand; info->dmode = 1; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        atomicAdd(&a.ws->n_rand, (u64)nrand); atomicAdd(&a.ws->n_det, (u64)(Bn - nrand));
+        atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)ps.kdet);
+        atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
+    }
+}
+
 // F, row form (the common case: <= kRowCap rows have an x in any of the panel's columns).  The active rows
 // live in REGISTERS of kRowThreads/32 warps as (row-bit, panel bits, step mask M); sequential CHP on them is then
 //   pivot  = min row-bit among stabilizer rows with bit j            (scan + REDUX, one smem hop across the warps)
@@ -355,7 +392,7 @@ struct PanelSmem {
 //   deterministic: partners = destabilizer rows with bit j (virtual ones stand for the +-Z rows of earlier steps)
 // which yields the same schedule (pivots, histories, step masks, partner sets) as the column form below.
 template <int KT>       // slots per thread actually used (1, 2 or 4): fewer slots = fewer dependent instructions per step
-__device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
+__device__ __noinline__ void panel_factorise_rows(const MeasArgs& a, PanelSmem& ps, int pos, int Bn, u32 A, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
     const int NS = a.NS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr u32 kInf = 0xffffffffu;
@@ -495,36 +532,282 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
     }
     __syncthreads();
     SK_RPROF(3);
-    randmask = 0;
-    for (int j = 0; j < Bn; ++j) if (ps.piv[j] != kInf) randmask |= 1ull << j;
-    const int nrand = __popcll(randmask);
-    const u32 ntr = ps.nt;
-    if (tid < Bn && ((randmask >> tid) & 1ull)) {
-        ps.outc[tid] = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
-        const u32 at = ntr + (u32)__popcll(randmask & ((1ull << tid) - 1ull));
-        __stcg(tlist + at, ps.piv[tid]); __stcg(tM + at, 0ull);          // the pivot itself: -> +-Z_q
-        atomicOr(a.tbits + (ps.piv[tid] >> 6), 1ull << (ps.piv[tid] & 63));
-    }
-    if (tid < 64) {       // panel-start signs of the pivot rows (A overwrites them)
-        const u32 pl = ps.piv[tid];
-        const u32 bal = __ballot_sync(0xffffffffu, pl != kInf && sign_bit(a.m.sgn, int(pl)));
-        if (lane == 0) ps.full32[tid >> 5] = bal;
-        if (tid < Bn && pl == kInf) atomicAdd(&ps.kdet, ps.dcnt[tid] + (u32)__popcll(ps.dZ[tid]));
+    panel_rows_tail(a, ps, pos, Bn, tlist, tM);
+    SK_RPROF(4);
+#undef SK_RPROF
+}
+
+// F, level form (the default for <= row_cap active rows).  The same symbolic elimination as the row form above, but the
+// steps of a panel are not walked one by one: in every ROUND all steps whose outcome no earlier unfinished step can
+// influence are executed together (a level-set / wavefront schedule of the elimination DAG).  A surface-code panel needs
+// 1-2 rounds instead of 64 dependent steps (d=71: 306 rounds for 10 081 measurements).
+//
+// State: the active rows are joined into PAIRS (stabilizer i, destabilizer n+i) by a shared-memory hash; a pair slot
+// holds the two rows' bits in the panel columns (sb, db), their step masks (Ms, Md) and `born` (step+1 that overwrote the
+// destabilizer with a pivot row: from then on it stands for the +-Z row of that step).  U = unfinished steps.
+// One round:
+//   1  every stabilizer row offers itself as pivot candidate of its unfinished columns (atomicMin: smallest row)
+//      and records what an elimination with it could touch: A_j |= (sb | db) & above(j)   (rows with more than kLevelK
+//      bits do so for their lowest column only and force that column to count as a contributor, which covers the rest);
+//   2  one warp, a lane per column: T_j = bits of the candidate pivot (and of its partner, which step j overwrites) above j,
+//      J_j = the same below j.  A step is HARMLESS if it is ready and T_j = 0 (it changes no unfinished column).
+//      ready(l)  <=>  l not in the union of A_j over the unfinished non-harmless j  (nothing can alter column l before l),
+//                     J_l only holds harmless steps (the pivot row and its partner arrive at step l unchanged; those
+//                     steps only add themselves to the pivot's history), and the candidate is not also the candidate
+//                     of one of them.  Fixpoint over the harmless set (monotone, usually 1-2 sweeps of ballots + REDUX).
+//      The lowest unfinished step is always ready, so every round makes progress.
+//   3  every pair applies all ready steps at once: pivots retire (sb := 0, db := pivot bits above l, born := l+1), hit rows
+//      XOR the pivots' bits and extend their step masks, deterministic steps collect their partners.
+// Ready steps touch pairwise disjoint pivot rows and never flip each other's column bits, so executing them together
+// equals executing them in index order; tools/proto_levels.py checks the rule against sequential elimination.
+constexpr int kLevelK = 4;
+__host__ __device__ inline int level_pair_cap(int NS) { return NS < kRowSlots ? NS : kRowSlots; }
+__host__ __device__ inline int level_hash_size(int NS) { int h = 64; while (h < 2 * level_pair_cap(NS)) h <<= 1; return h; }
+__host__ __device__ inline size_t level_smem_bytes(int NS) { return (size_t)level_pair_cap(NS) * (4 * 8 + 4 + 2) + (size_t)level_hash_size(NS) * (4 + 2) + 64; }
+
+__device__ __forceinline__ u64 bits_above(int l) { return (l < 63) ? ~((2ull << l) - 1ull) : 0ull; }
+__device__ __forceinline__ u64 bits_below(int l) { return (1ull << l) - 1ull; }
+// 64-bit OR into shared memory as two native 32-bit reductions (a 64-bit shared atomic is a CAS spin loop)
+__device__ __forceinline__ void smem_or64(u64* p, u64 v) {
+    u32* q = reinterpret_cast<u32*>(p);
+    if ((u32)v) atomicOr(q, (u32)v);
+    if ((u32)(v >> 32)) atomicOr(q + 1, (u32)(v >> 32));
+}
+__device__ __forceinline__ u64 warp_or64(u64 v) {
+    return (u64)__reduce_or_sync(0xffffffffu, (u32)v) | ((u64)__reduce_or_sync(0xffffffffu, (u32)(v >> 32)) << 32);
+}
+
+struct LevelSmem {
+    u32 piv[kPanelMax], dcnt[kPanelMax], cand[kPanelMax], pslot[kPanelMax]; u64 hist[kPanelMax], dZ[kPanelMax], Aany[kPanelMax], bpA[kPanelMax];
+    u64 ready, forced; u32 npairs, rounds, nt, krand, kdet; u32 wcnt[kMeasThreads / 32]; long long tacc[8];
+};
+// (not inlined: the function gets a register allocation of its own instead of adding to the pressure of the kernel body)
+__device__ __noinline__ void panel_factorise_levels(const MeasArgs& a, int pos, int Bn, u32 A, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
+    const int NS = a.NS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr u32 kInf = 0xffffffffu;
+    constexpr int T = kMeasThreads;
+    extern __shared__ __align__(16) u64 sp[];          // the kernel's dynamic shared memory (free in CTA 0 during F)
+    __shared__ LevelSmem ps;
+    const int Pc = level_pair_cap(NS), HS = level_hash_size(NS);
+    u64* sb = sp; u64* db = sb + Pc; u64* Ms = db + Pc; u64* Md = Ms + Pc;
+    u32* id = reinterpret_cast<u32*>(Md + Pc); u32* hkey = id + Pc;
+    unsigned short* hslot = reinterpret_cast<unsigned short*>(hkey + HS);
+    uint8_t* born = reinterpret_cast<uint8_t*>(hslot + HS); uint8_t* pvd = born + Pc;
+    long long tc = clock64();
+    if (tid < 8) ps.tacc[tid] = 0;
+#define SK_LPROF(k) do { if (a.prof && tid == 0) { const long long _c = clock64(); ps.tacc[k] += _c - tc; tc = _c; } } while (0)
+    // the active rows (issued first: one L2 round trip overlapped with the initialisation)
+    u32 eh[kRowK]; u64 eb[kRowK];
+#pragma unroll
+    for (int k = 0; k < kRowK; ++k) { const u32 i = u32(k) * T + tid; eh[k] = kInf; eb[k] = 0; if (i < A) { eh[k] = __ldcg(a.alist_h + i); eb[k] = ldcg(a.alist_b + i); } }
+    for (int i = tid; i < Pc; i += T) { sb[i] = 0; db[i] = 0; Ms[i] = 0; Md[i] = 0; born[i] = 0; pvd[i] = 0; }
+    for (int i = tid; i < HS; i += T) hkey[i] = 0;
+    if (tid < kPanelMax) { ps.piv[tid] = kInf; ps.hist[tid] = 0; ps.dZ[tid] = 0; ps.dcnt[tid] = 0; ps.cand[tid] = kInf; ps.Aany[tid] = 0; }
+    if (tid == 0) { ps.nt = 0; ps.krand = 0; ps.kdet = 0; ps.npairs = 0; ps.forced = 0; ps.rounds = 0; a.info->dmode = 1; }
+    __syncthreads();
+    // pair join: key = stabilizer index + 1, open addressing
+    u32 epos[kRowK]; bool ewon[kRowK];
+#pragma unroll
+    for (int k = 0; k < kRowK; ++k) {
+        epos[k] = 0; ewon[k] = false;
+        if (eh[k] == kInf) continue;
+        const u32 pid = eh[k] < (u32)NS ? eh[k] : eh[k] - (u32)NS;
+        u32 at = (pid * 2654435761u) >> 7 & u32(HS - 1);
+        for (;;) {
+            const u32 old = atomicCAS(&hkey[at], 0u, pid + 1u);
+            if (old == 0u) { ewon[k] = true; break; }
+            if (old == pid + 1u) break;
+            at = (at + 1u) & u32(HS - 1);
+        }
+        epos[k] = at;
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRowK; ++k) if (ewon[k]) {
+        const u32 slot = atomicAdd(&ps.npairs, 1u);
+        hslot[epos[k]] = (unsigned short)slot; id[slot] = eh[k] < (u32)NS ? eh[k] : eh[k] - (u32)NS;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRowK; ++k) if (eh[k] != kInf) { const u32 slot = hslot[epos[k]]; if (eh[k] < (u32)NS) sb[slot] = eb[k]; else db[slot] = eb[k]; }
+    __syncthreads();
+    const int P = int(ps.npairs);
+    SK_LPROF(0);
+    u64 U = (Bn < 64) ? ((1ull << Bn) - 1ull) : ~0ull;
+    int ntarget = 0;
+    bool isr[2] = {false, false}; u64 sgw[2] = {0, 0}; u32 spid[2] = {0, 0};      // warp 0: this lane's columns that turned out random
+    while (U) {
+        // ---- 1: pivot candidates and reach sets
+        for (int s = tid; s < P; s += T) {
+            const u64 sv = sb[s] & U;
+            if (!sv) continue;
+            const u64 all = sv | (db[s] & U);
+            const u32 key = (id[s] << 11) | u32(s);
+            if (__popcll(sv) > kLevelK) {
+                const int low = __ffsll((long long)sv) - 1;
+                atomicMin(&ps.cand[low], key); smem_or64(&ps.Aany[low], all & bits_above(low)); smem_or64(&ps.forced, 1ull << low);
+            } else {
+                u64 t = sv;
+                while (t) {
+                    const int j = __ffsll((long long)t) - 1; t &= t - 1;
+                    atomicMin(&ps.cand[j], key);
+                    const u64 r = all & bits_above(j);
+                    smem_or64(&ps.Aany[j], r);
+                }
+            }
+        }
+        __syncthreads();
+        SK_LPROF(4);
+        // ---- 2: which steps are ready (warp 0; lane owns columns lane and lane + 32)
+        if (warp == 0) {
+            u64 Tm[2], Jm[2], Am[2], Js[2]; u32 cd[2]; bool inU[2], rnd[2], conf[2], hb[2];
+            const u64 forced = ps.forced;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                inU[h] = (U >> j) & 1ull; cd[h] = ps.cand[j]; rnd[h] = inU[h] && cd[h] != kInf;
+                Tm[h] = 0; Jm[h] = 0; Am[h] = 0; Js[h] = 0; conf[h] = false;
+                if (rnd[h]) {
+                    const u32 slot = cd[h] & 2047u;
+                    const u64 sv = sb[slot] & U, all = sv | (db[slot] & U);
+                    Tm[h] = all & bits_above(j); Jm[h] = all & bits_below(j); Js[h] = sv & bits_below(j); Am[h] = ps.Aany[j];
+                    u64 t = Js[h];
+                    while (t) { const int j2 = __ffsll((long long)t) - 1; t &= t - 1; if (ps.cand[j2] == cd[h]) conf[h] = true; }
+                }
+                hb[h] = inU[h] && (!rnd[h] || (Tm[h] == 0 && !((forced >> j) & 1ull)));
+            }
+            u64 H = (u64)__ballot_sync(0xffffffffu, hb[0]) | ((u64)__ballot_sync(0xffffffffu, hb[1]) << 32);
+            u64 acc = warp_or64(((inU[0] && !hb[0]) ? Am[0] : 0ull) | ((inU[1] && !hb[1]) ? Am[1] : 0ull));
+            u64 ready;
+            bool rd[2];
+            for (;;) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; rd[h] = inU[h] && !((acc >> j) & 1ull) && !conf[h] && (Jm[h] & ~H) == 0; }
+                ready = (u64)__ballot_sync(0xffffffffu, rd[0]) | ((u64)__ballot_sync(0xffffffffu, rd[1]) << 32);
+                const u64 newH = H & ready;
+                if (newH == H) break;
+                const u64 drop = H & ~newH;
+                acc |= warp_or64((((drop >> lane) & 1ull) ? Am[0] : 0ull) | (((drop >> (lane + 32)) & 1ull) ? Am[1] : 0ull));
+                H = newH;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                if (!rd[h]) continue;
+                if (rnd[h]) {
+                    const u32 slot = cd[h] & 2047u;
+                    const u64 hist = Ms[slot] | Js[h];
+                    ps.pslot[j] = slot; ps.bpA[j] = sb[slot] & bits_above(j);
+                    ps.piv[j] = id[slot]; ps.hist[j] = hist;
+                    __stcg(rowM + id[slot], hist);
+                    isr[h] = true; spid[h] = id[slot]; sgw[h] = ldcg(a.m.sgn + (id[slot] >> 6));
+                } else ps.pslot[j] = kInf;
+            }
+            if (lane == 0) { ps.ready = ready; ps.rounds++; }
+        }
+        __syncthreads();
+        SK_LPROF(5);
+        // ---- 3: all ready steps at once
+        const u64 ready = ps.ready;
+        for (int s = tid; s < P; s += T) {
+            const u64 sv = sb[s], dv = db[s];
+            const u64 sh = sv & ready, dh = dv & ready;
+            if (!(sh | dh)) continue;
+            int pl = -1;
+            { u64 t = sh; while (t) { const int l = __ffsll((long long)t) - 1; t &= t - 1; if (ps.pslot[l] == (u32)s) { pl = l; break; } } }
+            const u32 bo = born[s];
+            if (pl >= 0) {
+                // pivot of step pl: the ready steps below pl multiplied this row (they are in its history) and read or
+                // multiplied its old partner, which step pl then overwrites with the pivot row
+                ntarget += __popcll(sh & bits_below(pl));
+                u64 t = dh & bits_below(pl);
+                while (t) {
+                    const int l2 = __ffsll((long long)t) - 1; t &= t - 1;
+                    if (ps.pslot[l2] != kInf) ++ntarget;
+                    else if (bo) smem_or64(&ps.dZ[l2], 1ull << (bo - 1));
+                    else { const u32 at = atomicAdd(&ps.dcnt[l2], 1u); __stcg(a.dpart + (size_t)l2 * kRowSlots + at, id[s]); }
+                }
+                sb[s] = 0; db[s] = sv & bits_above(pl); Ms[s] = ps.hist[pl]; Md[s] = 0; born[s] = uint8_t(pl + 1); pvd[s] = 1;
+            } else {
+                if (sh) {
+                    u64 v = sv, t = sh;
+                    while (t) { const int l = __ffsll((long long)t) - 1; t &= t - 1; v ^= ps.bpA[l]; }
+                    sb[s] = v; Ms[s] |= sh; ntarget += __popcll(sh);
+                }
+                if (dh) {
+                    u64 v = dv, t = dh, md = 0;
+                    while (t) {
+                        const int l = __ffsll((long long)t) - 1; t &= t - 1;
+                        if (ps.pslot[l] != kInf) { v ^= ps.bpA[l]; md |= 1ull << l; ++ntarget; }
+                        else if (bo) smem_or64(&ps.dZ[l], 1ull << (bo - 1));
+                        else { const u32 at = atomicAdd(&ps.dcnt[l], 1u); __stcg(a.dpart + (size_t)l * kRowSlots + at, id[s]); }
+                    }
+                    db[s] = v; Md[s] |= md;
+                }
+            }
+        }
+        U &= ~ready;
+        if (tid < kPanelMax) { ps.cand[tid] = kInf; ps.Aany[tid] = 0; }
+        if (tid == 0) ps.forced = 0;
+        __syncthreads();
+        SK_LPROF(6);
+    }
+    // ---- touched rows: regular rows that were multiplied at least once, and every overwritten destabilizer
+    int cnt = 0;
+    for (int s = tid; s < P; s += T) { cnt += (!pvd[s] && Ms[s]) ? 1 : 0; cnt += (born[s] || Md[s]) ? 1 : 0; }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
+    if (lane == 31) ps.wcnt[warp] = incl;
+    ntarget = warp_sum(ntarget);
+    if (lane == 0 && ntarget) atomicAdd(&ps.krand, (u32)ntarget);
+    if (warp == 0) {      // random steps and the panel-start signs of their pivot rows (loaded when the pivots were fixed)
+        const u64 rm = (u64)__ballot_sync(0xffffffffu, isr[0]) | ((u64)__ballot_sync(0xffffffffu, isr[1]) << 32);
+        const u64 os = (u64)__ballot_sync(0xffffffffu, isr[0] && ((sgw[0] >> (spid[0] & 63)) & 1ull)) | ((u64)__ballot_sync(0xffffffffu, isr[1] && ((sgw[1] >> (spid[1] & 63)) & 1ull)) << 32);
+        if (lane == 0) { ps.ready = rm; ps.forced = os; }
+    }
+    __syncthreads();
+    u32 at = incl - cnt, ntr = 0;
+    for (int t = 0; t < T / 32; ++t) { const u32 c = ps.wcnt[t]; if (t < warp) at += c; ntr += c; }
+    for (int s = tid; s < P; s += T) {
+        const u32 pid = id[s];
+        if (!pvd[s] && Ms[s]) {
+            __stcg(tlist + at, pid); __stcg(tM + at, Ms[s]); atomicOr(a.tbits + (pid >> 6), 1ull << (pid & 63)); __stcg(rowM + pid, Ms[s]); ++at;
+        }
+        if (born[s] || Md[s]) {
+            const u32 row = (u32)NS + pid;
+            __stcg(tlist + at, row); __stcg(tM + at, Md[s]); atomicOr(a.tbits + (row >> 6), 1ull << (row & 63)); ++at;
+        }
+    }
+    const u64 randmask = ps.ready, osign = ps.forced;
+    const int nrand = __popcll(randmask);
     PanelInfo* info = a.info;
     if (tid < kPanelMax) {
+        uint8_t oc = 0;
+        if (tid < Bn) {
+            if ((randmask >> tid) & 1ull) {       // the pivot itself joins the touched rows: -> +-Z_q with the counter RNG bit
+                oc = uint8_t(counter_bit(a.seed, a.ordinal0 + (uint64_t)(pos + tid)));
+                const u32 pt = ntr + (u32)__popcll(randmask & ((1ull << tid) - 1ull));
+                __stcg(tlist + pt, ps.piv[tid]); __stcg(tM + pt, 0ull);
+                atomicOr(a.tbits + (ps.piv[tid] >> 6), 1ull << (ps.piv[tid] & 63));
+            } else atomicAdd(&ps.kdet, ps.dcnt[tid] + (u32)__popcll(ps.dZ[tid]));
+        }
         info->hist[tid] = ps.hist[tid]; info->dZ[tid] = ps.dZ[tid]; info->dcnt[tid] = ps.dcnt[tid];
-        info->piv[tid] = ps.piv[tid]; info->outc[tid] = ps.outc[tid];
+        info->piv[tid] = ps.piv[tid]; info->outc[tid] = oc;
     }
+    if (tid == 64) { info->randmask = randmask; info->nt = ntr + (u32)nrand; info->dmode = 1; info->osign = osign; }
+    SK_LPROF(2);
+    __syncthreads();
     if (tid == 0) {
-        info->randmask = randmask; info->nt = ntr + (u32)nrand; info->dmode = 1; info->osign = (u64)ps.full32[0] | ((u64)ps.full32[1] << 32);
+        st_release(&a.ws->progress, pbase + u32(Bn));         // everything is published at once (cumulative over the barrier)
         atomicAdd(&a.ws->n_rand, (u64)nrand); atomicAdd(&a.ws->n_det, (u64)(Bn - nrand));
         atomicAdd(&a.ws->k_rand, (u64)ps.krand); atomicAdd(&a.ws->k_det, (u64)ps.kdet);
         atomicAdd(&a.ws->waves, 1ull); atomicAdd(&a.ws->panels, 1ull);
     }
-    SK_RPROF(4);
-#undef SK_RPROF
+    SK_LPROF(3);
+    if (a.prof && tid == 0) { a.ws->cprof[10] += ps.rounds; for (int k = 0; k < 7; ++k) atomicAdd(&a.ws->cprof[k], (u64)ps.tacc[k]); }
+#undef SK_LPROF
 }
 
 // F: symbolic factorisation of one panel by CTA 0 (see the file header).
@@ -536,7 +819,7 @@ __device__ __forceinline__ void panel_factorise_rows(const MeasArgs& a, PanelSme
 //   cur_j = (orig_j ^ XOR_{l in S_j} m_l) & ~retired,   S_j = earlier random steps whose pivot row has an x
 // in column j (S_j bit l = pw_l bit j; the virtual word starts as S_j itself), sparse in the word index
 // through nzm.  m_l = column l at step l minus the pivot and its partner = the rows step l multiplies.
-__device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, u32* s_rows, u64* mbar, u32& tma_parity, int pos, int Bn, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
+__device__ __noinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSmem& ps, u32* s_rows, u64* mbar, u32& tma_parity, int pos, int Bn, u64* rowM, u32* tlist, u64* tM, u32 pbase) {
     const int RW = a.m.RW, W = a.m.W, NS = a.NS;
     const int CS = RW + 2, RV = RW + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -790,13 +1073,13 @@ __device__ __forceinline__ void panel_factorise(const MeasArgs& a, u64* sp, Pane
 
 // dynamic smem (u64): max( acc[kMeasWarps][2*Wp] + values scratch, panel [B][RW] + pivmask [W] )
 __global__ void __launch_bounds__(kMeasThreads, 1)
-k_measure_block(MeasArgs a) {
+k_measure_block(const __grid_constant__ MeasArgs a) {
     extern __shared__ __align__(16) u64 smem[];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
     __shared__ int s_wcnt[kMeasWarps];
     __shared__ u64 s_pn[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
-    __shared__ int s_cnt1;
+    __shared__ int s_cnt1, s_fast;
     __shared__ u32 s_targets[kMaxTargets];
     __shared__ PanelSmem ps;
     __shared__ PanelInfo s_info;
@@ -943,9 +1226,12 @@ k_measure_block(MeasArgs a) {
     u64 t_cta = 0;
 #define SK_CSTART() do { if (a.prof && tid == 0) t_cta = gtime(); } while (0)
 #define SK_CPROF(k) do { if (a.prof && tid == 0 && blockIdx.x < 160) ws->ctaphase[blockIdx.x * 4 + k] += gtime() - t_cta; } while (0)
+    int pidx = 0;                       // panel index within this launch
+    const int tsel = (blockIdx.x == 0) ? 0 : (blockIdx.x == 1) ? 1 : (blockIdx.x == gridDim.x - 1) ? 2 : -1;
+#define SK_TRACE(ev) do { if (a.prof && tid == 0 && tsel >= 0 && pidx >= 20 && pidx < 28) ws->trace[((pidx - 20) * 3 + tsel) * 8 + (ev)] = gtime(); } while (0)
     while (pos < a.count) {
         const int Bn = min(B, a.count - pos);
-        SK_CSTART();
+        SK_CSTART(); SK_TRACE(0);
         u64* rowM = a.rowM + (size_t)kpar * rowcap;
         u32* tlist = a.tlist + (size_t)kpar * a.tcap;
         u64* tM = a.tM + (size_t)kpar * a.tcap;
@@ -1004,7 +1290,8 @@ k_measure_block(MeasArgs a) {
             for (int w = tid; w < RW; w += kMeasThreads) a.tbits[w] = 0;
             __syncthreads();
             if (tid == 0) { info->acount = 0; if (a.prof) { ws->cprof[8] += A; if (A > ws->cprof[9]) ws->cprof[9] = A; } }
-            if (A <= (u32)a.row_cap && !a.force_columns) {
+            if (A <= (u32)a.row_cap && !a.force_columns && !a.seq_rows) panel_factorise_levels(a, pos, Bn, A, rowM, tlist, tM, pbase);
+            else if (A <= (u32)a.row_cap && !a.force_columns) {
                 if (A + kPanelMax <= (u32)kRowThreads) panel_factorise_rows<1>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
                 else if (A + kPanelMax <= 2u * kRowThreads) panel_factorise_rows<2>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
                 else panel_factorise_rows<4>(a, ps, pos, Bn, A, rowM, tlist, tM, pbase);
@@ -1016,6 +1303,7 @@ k_measure_block(MeasArgs a) {
             }
         }
         SK_PROF(3); SK_CPROF(1);
+        if (blockIdx.x == 0) SK_TRACE(1);
         // ---- consumers (every CTA but 0, which is busy factorising): V pivot values + D part 1, fed step by step
         const int nC = max(1, G - 1);
         const int cidx = (G == 1) ? 0 : int(blockIdx.x) - 1;
@@ -1023,6 +1311,7 @@ k_measure_block(MeasArgs a) {
         SK_CSTART();
         { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + 1u) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
           if (__syncthreads_or(bad)) return; }
+        SK_TRACE(1);
         const u32 dmode = __ldcg(&info->dmode);         // written before the first publication
         const int wpc = (W + nC - 1) / nC;
         const int wlo = min(W, cidx * wpc), whi = min(W, wlo + wpc);
@@ -1030,6 +1319,56 @@ k_measure_block(MeasArgs a) {
         const int nvw = min(kMeasWarps - 1, (nw + 31) / 32);    // warps busy with V (a thread may own several words)
         u64* vs = smem + (size_t)kMeasWarps * 2 * Wp;           // [Bn][2][wpc] after the accumulators
         if (dmode == 1) {
+            // The level form publishes the whole panel at once: then the description is staged in shared memory and the
+            // pivot rows' words are loaded by the whole CTA, all in flight together (two L2 round trips for the whole phase).
+            if (tid == 0) s_fast = int(ld_acquire(&ws->progress) - pbase) >= Bn ? 1 : 0;
+            __syncthreads();
+            const bool fast = s_fast != 0;
+            if (fast) {
+                for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
+                __syncthreads();
+                {   // stage the panel-start words [wlo, whi) of every pivot row: the whole CTA loads, 4 items in flight per thread
+                    const int nitems = Bn * 2 * nw;
+                    for (int i0 = tid; i0 < nitems; i0 += 4 * kMeasThreads) {
+                        u64 v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + u * kMeasThreads;
+                            v[u] = 0;
+                            if (i < nitems) {
+                                const int k = i / (2 * nw), r = i - k * 2 * nw, half = r / nw, t = r - half * nw;
+                                const u32 pk = s_info.piv[k];
+                                if (pk != 0xffffffffu) v[u] = ldcg(a.m.rows + (size_t)(2 * pk + half) * Wp + wlo + t);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + u * kMeasThreads;
+                            if (i < nitems) { const int k = i / (2 * nw), r = i - k * 2 * nw, half = r / nw, t = r - half * nw; vs[(size_t)(2 * k + half) * wpc + t] = v[u]; }
+                        }
+                    }
+                }
+                __syncthreads();
+                if (warp < nvw) {
+                    const int nvt = 32 * nvw;
+                    for (int t = tid; t < nw; t += nvt) {
+                        const int w = wlo + t;
+                        for (int k = 0; k < Bn; ++k) {
+                            if (s_info.piv[k] == 0xffffffffu) continue;
+                            u64 ax = vs[(size_t)(2 * k) * wpc + t], az = vs[(size_t)(2 * k + 1) * wpc + t], hb = s_info.hist[k];
+                            int e = 0;
+                            while (hb) {
+                                const int l = __ffsll((long long)hb) - 1; hb &= hb - 1;
+                                const u64 bx = vs[(size_t)(2 * l) * wpc + t], bz = vs[(size_t)(2 * l + 1) * wpc + t];
+                                e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
+                            }
+                            vs[(size_t)(2 * k) * wpc + t] = ax; vs[(size_t)(2 * k + 1) * wpc + t] = az;
+                            __stcg(a.pivbuf + (size_t)(2 * k) * Wp + w, ax); __stcg(a.pivbuf + (size_t)(2 * k + 1) * Wp + w, az);
+                            if (e & 3) atomicAdd(&info->eph[kpar][k], (u32)(e & 3));
+                        }
+                    }
+                }
+            } else
             // ---------- streaming: V consumes the published steps in chunks of 8 (two L2 round trips per chunk)
             if (warp < nvw) {
                 const int nvt = 32 * nvw;
@@ -1066,13 +1405,16 @@ k_measure_block(MeasArgs a) {
                 }
             }
             if (nvw) __syncthreads();
+            SK_TRACE(2);
             // ---------- streaming D part 1: step j belongs to consumer nC-1 - j % nC (from the far end: V uses the first ones);
             // the step masks N_j are taken in D part 2, when the factorisation has finished
             for (int j = nC - 1 - cidx; j < Bn; j += nC) {
-                { int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + u32(j + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
-                  if (__syncthreads_or(bad)) return; }
-                if (__ldcg(&info->piv[j]) != 0xffffffffu) continue;
-                const int cnt = int(__ldcg(&info->dcnt[j]));
+                if (!fast) {
+                    int bad = 0; if (tid == 0) { bad = wait_geq(&ws->progress, pbase + u32(j + 1)) ? 0 : 1; if (bad) atomicOr(&ws->err, 0x80000000u); }
+                    if (__syncthreads_or(bad)) return;
+                }
+                if ((fast ? s_info.piv[j] : __ldcg(&info->piv[j])) != 0xffffffffu) continue;
+                const int cnt = int(fast ? s_info.dcnt[j] : __ldcg(&info->dcnt[j]));
                 const u32* gl = a.dpart + (size_t)j * kRowSlots;
                 u64* dx = a.detacc + (size_t)(2 * j) * Wp;
                 if (cnt <= kWarpDirect) {
@@ -1211,9 +1553,9 @@ k_measure_block(MeasArgs a) {
         }   // column form
         SK_CPROF(2);
         }   // consumers
-        SK_PROF(4);
+        SK_PROF(4); SK_TRACE(3);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(7); SK_CSTART();
+        SK_PROF(7); SK_CSTART(); SK_TRACE(4);
         // ---- the finished panel description (one round trip), then the signs of the pivot values
         // (triangular GF(2) recurrence; every CTA solves it itself)
         for (int i = tid; i < int(sizeof(PanelInfo) / 8); i += kMeasThreads) reinterpret_cast<u64*>(&s_info)[i] = ldcg(reinterpret_cast<const u64*>(info) + i);
@@ -1363,6 +1705,7 @@ k_measure_block(MeasArgs a) {
                 }
             }
             // folded gather, untouched rows: a lane per row, rows listed in tbits are skipped (their warps emitted them above)
+            SK_TRACE(5);
             if (do_fold) {
                 // groups are handed out from the far end of the warp index space: the item loop above keeps the first warps busy
                 for (int g = GW - 1 - gwi; g < 2 * RW; g += GW) {
@@ -1399,9 +1742,10 @@ k_measure_block(MeasArgs a) {
                 }
             }
         }
-        SK_PROF(5); SK_CPROF(3);
+        SK_PROF(5); SK_CPROF(3); SK_TRACE(6);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
-        SK_PROF(7);
+        SK_PROF(7); SK_TRACE(7);
+        ++pidx;
         prev_nt = s_info.nt;
         have_list = do_fold;
         kpar ^= 1;

@@ -41,6 +41,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (const char* e = getenv("SK_NO_FOLD")) c->no_fold = atoi(e);
     if (const char* e = getenv("SK_ROW_CAP")) c->row_cap = atoi(e);
     if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
+    if (const char* e = getenv("SK_PANEL_SEQ")) c->seq_rows = atoi(e);
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
@@ -201,7 +202,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         const int wpc = (t->W + ncons - 1) / ncons;
         while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
         t->B = B;
-        t->meas_smem = std::max<size_t>(std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8, 2 * 512 * 9 * 4);   // >= the in-kernel transpose tiles
+        t->meas_smem = std::max<size_t>(std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8, std::max<size_t>(2 * 512 * 9 * 4, level_smem_bytes(t->NS)));   // >= the in-kernel transpose tiles
     }
     cudaError_t e1 = dmalloc(c, &t->m.cols, t->cols_bytes);
     cudaError_t e2 = dmalloc(c, &t->m.rows, t->rows_bytes);
@@ -416,7 +417,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
     a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.tbits = t->d_tbits; a.tcap = t->tcap; a.fold = c->no_fold ? 0 : 1; a.row_cap = c->row_cap > 0 ? std::min(c->row_cap, kRowCap) : kRowCap; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
-    a.prof = c->prof; a.force_columns = c->force_columns; a.destab_stale = t->r_destab_stale ? 1 : 0;
+    a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.destab_stale = t->r_destab_stale ? 1 : 0;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -477,7 +478,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     if (!c) return SK_EARG;
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
-    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, (38 + 640) * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, (38 + 640 + 192) * 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -496,6 +497,15 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
             double mx = 0, sum = 0; int arg = 0, cnt = 0;
             for (int b = 0; b < 160; ++b) { double v = h.ctaphase[b * 4 + ph] / 1e3; if (v > 0) { sum += v; ++cnt; } if (v > mx) { mx = v; arg = b; } }
             fprintf(stderr, "panel phase %-5s own time per CTA (us): avg %.0f max %.0f (CTA %d) cta0 %.0f\n", nm[ph], cnt ? sum / cnt : 0.0, mx, arg, h.ctaphase[ph] / 1e3);
+        }
+    }
+    if (getenv("SK_DEBUG_PROF") && h.trace[0]) {
+        fprintf(stderr, "timeline (us from panel 20 start on CTA 0): events start, F/published seen, V, V+D1, bar1 exit, items, fold, bar2 exit\n");
+        const u64 t0 = h.trace[0];
+        for (int pnl = 0; pnl < 8; ++pnl) for (int cs = 0; cs < 3; ++cs) {
+            fprintf(stderr, "  panel %d cta %s:", 20 + pnl, cs == 0 ? "0   " : cs == 1 ? "1   " : "last");
+            for (int ev = 0; ev < 8; ++ev) { const u64 v = h.trace[(pnl * 3 + cs) * 8 + ev]; if (v) fprintf(stderr, " %7.2f", (double)(long long)(v - t0) / 1e3); else fprintf(stderr, "       -"); }
+            fprintf(stderr, "\n");
         }
     }
     if (getenv("SK_DEBUG_PROF")) { fprintf(stderr, "cprof cycles:"); for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", (unsigned long long)h.cprof[k]); fprintf(stderr, "\n"); }

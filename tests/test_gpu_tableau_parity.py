@@ -271,16 +271,19 @@ def test_surface_code_d71_full_length_bit_parity(sk, ctx, orc):           # BASE
     prog.close(); tab.close()
 
 
+@pytest.mark.parametrize("seq", [0, 1])
 @pytest.mark.parametrize("columns,width,rowcap,fold", [(1, 64, 0, 1), (1, 5, 0, 1), (1, 1, 0, 1), (0, 7, 0, 1), (0, 1, 0, 1),
                                                        (0, 64, 12, 1), (0, 9, 30, 1), (0, 64, 0, 0), (0, 16, 25, 0)])
-def test_panel_factorisation_variants(sk, orc, columns, width, rowcap, fold):
-    """Panel mode (kernels_measure.cuh) has two factorisations -- row form in registers and the
+def test_panel_factorisation_variants(sk, orc, columns, width, rowcap, fold, seq):
+    """Panel mode (kernels_measure.cuh) has three factorisations -- the level form (all mutually independent steps of a
+    panel per round; the default), the step-by-step row form in registers (SK_PANEL_SEQ=1) and the
     column form in shared memory (TMA staged) used when too many rows are active -- any panel
     width 1..64, and the gather of the next panel either folded into the apply phase or on its own (a panel
     that outgrows the row form after a folded gather asks for a full one: SK_ROW_CAP makes that happen on
     small inputs).  Every variant must reproduce sequential CHP bit for bit."""
-    old = {k: os.environ.get(k) for k in ("SK_PANEL_COLUMNS", "SK_PANEL", "SK_ROW_CAP", "SK_NO_FOLD")}
-    os.environ["SK_PANEL_COLUMNS"] = str(columns); os.environ["SK_PANEL"] = str(width)
+    if seq and columns: pytest.skip("SK_PANEL_SEQ only selects between the two row-form factorisations")
+    old = {k: os.environ.get(k) for k in ("SK_PANEL_COLUMNS", "SK_PANEL", "SK_ROW_CAP", "SK_NO_FOLD", "SK_PANEL_SEQ")}
+    os.environ["SK_PANEL_COLUMNS"] = str(columns); os.environ["SK_PANEL"] = str(width); os.environ["SK_PANEL_SEQ"] = str(seq)
     os.environ["SK_ROW_CAP"] = str(rowcap); os.environ["SK_NO_FOLD"] = str(1 - fold)      # small caps force the regather path
     try:
         c2 = sk.Context(0)
