@@ -68,6 +68,7 @@ struct PanelInfo {      // global scratch describing the current panel (written 
     u32 pad;
     u32 dcnt[kPanelMax];   // dmode 1: partners per deterministic step
     uint8_t outc[kPanelMax];   // outcome of the random steps (counter RNG)
+    u32 lvcount[2];        // replicated path (kernels_panel.cuh): pairs in the two pair-list buffers
 };
 
 struct MeasWs {
@@ -127,6 +128,7 @@ struct MeasArgs {
     int row_cap;        // most active rows the row-form factorisation takes (kRowCap; SK_ROW_CAP lowers it for tests)
     int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
+    int lv_enable;      // replicated level-form panel path (kernels_panel.cuh); SK_PANEL_REPL=0 disables
     int seq_rows;       // SK_PANEL_SEQ=1: step-by-step row-form factorisation instead of the level form (A/B and testing aid)
 };
 
@@ -1071,6 +1073,10 @@ __device__ __noinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSm
 #undef SK_FPROF
 }
 
+}  // namespace skd
+#include "kernels_panel.cuh"
+namespace skd {
+
 // dynamic smem (u64): max( acc[kMeasWarps][2*Wp] + values scratch, panel [B][RW] + pivmask [W] )
 __global__ void __launch_bounds__(kMeasThreads, 1)
 k_measure_block(const __grid_constant__ MeasArgs a) {
@@ -1215,6 +1221,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         }
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
     }
+    if (a.lv_enable) { pos = panel_levels_loop(a, pos, epoch); if (pos < 0) return; }
     const int B = a.B;
     PanelInfo* info = a.info;
     const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs

@@ -42,6 +42,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (const char* e = getenv("SK_ROW_CAP")) c->row_cap = atoi(e);
     if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
     if (const char* e = getenv("SK_PANEL_SEQ")) c->seq_rows = atoi(e);
+    if (const char* e = getenv("SK_PANEL_REPL")) c->no_repl = atoi(e) == 0;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
     if (stream) { c->stream = (cudaStream_t)stream; c->own_stream = false; }
@@ -112,7 +113,7 @@ struct sk_tableau {
     bool r_destab_stale = false;    // R holds the stabilizer rows only (C -> R was restricted to that half)
     size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
     u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
-    int meas_grid = 0; size_t meas_smem = 0;
+    int meas_grid = 0; size_t meas_smem = 0; bool lv_ok = false;
     u32* d_wpiv = nullptr;
     // panel-mode scratch (kernels_measure.cuh)
     uint64_t uid = 0;               // distinguishes tableaux that reuse a host address (graph cache key)
@@ -203,6 +204,9 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
         while (B > 1 && (acc_words + (size_t)B * 2 * wpc) * 8 > avail) --B;
         t->B = B;
         t->meas_smem = std::max<size_t>(std::max(acc_words + (size_t)B * 2 * wpc, (size_t)B * col_words + aux_words) * 8, std::max<size_t>(2 * 512 * 9 * 4, level_smem_bytes(t->NS)));   // >= the in-kernel transpose tiles
+        const size_t lvb = lv_smem_bytes(t->NS, t->W, t->Wp, t->meas_grid, B);
+        t->lv_ok = lv_supported(t->W) && lvb <= avail;
+        if (t->lv_ok) t->meas_smem = std::max(t->meas_smem, lvb);
     }
     cudaError_t e1 = dmalloc(c, &t->m.cols, t->cols_bytes);
     cudaError_t e2 = dmalloc(c, &t->m.rows, t->rows_bytes);
@@ -219,7 +223,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e11 = dmalloc(c, &t->d_rowM, (size_t)2 * 64 * t->RW * 8);
     if (!e11) e11 = dmalloc(c, &t->d_tbits, (size_t)t->RW * 8);
     cudaError_t e12 = dmalloc(c, &t->d_alist_h, (size_t)64 * t->RW * 4);
-    cudaError_t e13 = dmalloc(c, &t->d_alist_b, (size_t)64 * t->RW * 8);
+    cudaError_t e13 = dmalloc(c, &t->d_alist_b, (size_t)2 * 64 * t->RW * 8);      // two pair-list buffers (kernels_panel.cuh)
     cudaError_t e14 = dmalloc(c, &t->d_dpart, (size_t)kPanelMax * kRowSlots * 4);
     if (!e8) e8 = cudaMemsetAsync(t->d_info, 0, sizeof(PanelInfo), c->stream);
     if (e1 || e2 || e3 || e4 || e5 || e6 || e7 || e8 || e9 || e10 || e11 || e12 || e13 || e14) { sk_tableau_destroy(t); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a %llu-qubit tableau", (unsigned long long)n); }
@@ -417,7 +421,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
     a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.tbits = t->d_tbits; a.tcap = t->tcap; a.fold = c->no_fold ? 0 : 1; a.row_cap = c->row_cap > 0 ? std::min(c->row_cap, kRowCap) : kRowCap; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
-    a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.destab_stale = t->r_destab_stale ? 1 : 0;
+    a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.lv_enable = (t->lv_ok && !c->no_repl && !c->force_columns && !c->seq_rows) ? 1 : 0; a.destab_stale = t->r_destab_stale ? 1 : 0;
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -497,6 +501,7 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
             double mx = 0, sum = 0; int arg = 0, cnt = 0;
             for (int b = 0; b < 160; ++b) { double v = h.ctaphase[b * 4 + ph] / 1e3; if (v > 0) { sum += v; ++cnt; } if (v > mx) { mx = v; arg = b; } }
             fprintf(stderr, "panel phase %-5s own time per CTA (us): avg %.0f max %.0f (CTA %d) cta0 %.0f\n", nm[ph], cnt ? sum / cnt : 0.0, mx, arg, h.ctaphase[ph] / 1e3);
+            if (getenv("SK_DEBUG_CTAS")) { fprintf(stderr, "   per CTA:"); for (int b = 0; b < 148; ++b) fprintf(stderr, " %.0f", h.ctaphase[b * 4 + ph] / 1e3); fprintf(stderr, "\n"); }
         }
     }
     if (getenv("SK_DEBUG_PROF") && h.trace[0]) {
