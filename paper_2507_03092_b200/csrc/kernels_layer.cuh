@@ -30,6 +30,9 @@ __device__ __forceinline__ ulonglong2 operator^(ulonglong2 a, ulonglong2 b) { re
 __device__ __forceinline__ ulonglong2 operator&(ulonglong2 a, ulonglong2 b) { return make_ulonglong2(a.x & b.x, a.y & b.y); }
 __device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulonglong2(~a.x, ~a.y); }
 
+// (Measured, round 2: batching the first loads of up to four independent gates per thread -- 2 dependent round trips per batch
+// instead of 2 per gate -- is SLOWER, 17-23 us against 10-12 us per d=71 layer: 114 registers cut the resident warps 4x and the
+// kernel is L2-bandwidth bound (about 44 MB of sector traffic per CX layer), not latency bound.  Kept as is.)
 // gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb), or [block_off[b], block_off[b+1]) when the host
 // supplies chunk boundaries; thread v owns 128-bit row-vector v of every column it visits.
 // Merged layers: a launch may hold several consecutive layers provided every set of gates that share qubits (a

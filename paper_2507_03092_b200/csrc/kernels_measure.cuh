@@ -1073,6 +1073,114 @@ __device__ __noinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSm
 #undef SK_FPROF
 }
 
+
+// Product of the listed rows (R layout) with the running product in REGISTERS: every lane owns NWL lane-strided words and the
+// words of two rows are in flight together, so a short list costs one L2 round trip instead of one per word chunk.
+// Returns this lane's share of the i-exponent (row signs not included).
+template <int NWL>
+__device__ __forceinline__ int warp_mul_wide(const u64* __restrict__ base, int W, int Wp, const u32* list, int cnt, int lane) {
+    u64 ax[NWL], az[NWL];
+#pragma unroll
+    for (int k = 0; k < NWL; ++k) { ax[k] = 0; az[k] = 0; }
+    int e = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 2) {
+        const bool two = i0 + 1 < cnt;
+        const u64* r0 = base + (size_t)(2 * list[i0]) * Wp;
+        const u64* r1 = base + (size_t)(2 * list[two ? i0 + 1 : i0]) * Wp;
+        u64 x0[NWL], z0[NWL], x1[NWL], z1[NWL];
+#pragma unroll
+        for (int k = 0; k < NWL; ++k) {
+            const int w = lane + 32 * k;
+            const bool ok = w < W;
+            x0[k] = ok ? ldcg(r0 + w) : 0ull; z0[k] = ok ? ldcg(r0 + Wp + w) : 0ull;
+            x1[k] = (ok && two) ? ldcg(r1 + w) : 0ull; z1[k] = (ok && two) ? ldcg(r1 + Wp + w) : 0ull;
+        }
+#pragma unroll
+        for (int k = 0; k < NWL; ++k) {
+            e += g_word(x0[k], z0[k], ax[k], az[k]); ax[k] ^= x0[k]; az[k] ^= z0[k];
+            e += g_word(x1[k], z1[k], ax[k], az[k]); ax[k] ^= x1[k]; az[k] ^= z1[k];
+        }
+    }
+    return e;
+}
+
+// Wave mode, this warp's slots of the window [pos, wend): K2 pivot search over the stabilizer half of the C column and -- when it
+// is empty -- K4, the product of the partner stabilizers (destabilizer half of the same column -> rows of the R form).
+// Results per slot go to recj/recn (measurement index or -1, partner count | odd-phase flag << 30); products with more than
+// kWarpList partners are left to the whole CTA (slot pushed to heavy[]).
+__device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u32 wave, int gw, int GW, u32* wlist, int* nheavy, int* heavy,
+                                        int* recj, int* recn, u64* acc_x, u64* acc_z) {
+    const int lane = threadIdx.x & 31;
+    const int W = a.m.W, Wp = a.m.Wp, RW = a.m.RW;
+    const int nwl = (W + 31) / 32;
+    if (lane < kSlotsPerWarp) recj[lane] = -1;
+    __syncwarp();
+    int rec = 0;
+    const bool trc = a.prof && lane == 0 && (gw == 0 || gw == GW / 2) && pos == 0;
+    const int tb = (gw == 0) ? 0 : 96;
+#define WV_TRACE(ev) do { if (trc && rec < 3) a.ws->trace[tb + rec * 8 + (ev)] = gtime(); } while (0)
+    for (int slot = gw; pos + slot < wend; slot += GW, ++rec) {
+        const int j = pos + slot;
+        WV_TRACE(0);
+        const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
+        u32 piv = 0xffffffffu;
+        int npart = 0;
+        for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {        // both halves of the column in one round trip per chunk
+            u64 sv[kColChunk], dv[kColChunk];
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; sv[t] = (w < W) ? ldcg(xcol + w) : 0ull; dv[t] = (w < W) ? ldcg(xcol + W + w) : 0ull; }
+            int mine = 0;
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                if (sv[t]) piv = min(piv, u32(w * 64 + __ffsll((long long)sv[t]) - 1));
+                mine += __popcll(dv[t]);
+            }
+            // partner list: exclusive prefix of the lanes' counts
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+            int ti = npart + incl - mine;
+            npart += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                u64 v = dv[t];
+                while (v) { const int b = __ffsll((long long)v) - 1; v &= v - 1; if (ti < kWarpList) wlist[ti] = u32(w * 64 + b); ++ti; }
+            }
+        }
+        piv = warp_min(piv);
+        __syncwarp();
+        WV_TRACE(1);
+        if (piv != 0xffffffffu) {       // random: the first one of the window ends the deterministic prefix
+            if (lane == 0) atomicMax(&a.ws->r0[wave % 3], ~(u32)j);      // stored inverted: zero-initialised, max = smallest index
+            continue;
+        }
+        if (npart > kWarpList) {                  // tree-reduced by the whole CTA
+            if (lane == 0) { const int h = atomicAdd(nheavy, 1); heavy[h] = slot; }
+            continue;
+        }
+        int e;
+        if (nwl <= 1) e = warp_mul_wide<1>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 2) e = warp_mul_wide<2>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 4) e = warp_mul_wide<4>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 6) e = warp_mul_wide<6>(a.m.rows, W, Wp, wlist, npart, lane);
+        else {
+            for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
+            e = warp_mul_list(a.m.rows, W, Wp, wlist, npart, acc_x, acc_z, lane);
+        }
+        WV_TRACE(2);
+        for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(wlist[i]));
+        e = warp_sum(e) & 3;
+        WV_TRACE(3);
+        if (lane == 0) {
+            a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
+            if (rec < kSlotsPerWarp) { recj[rec] = j; recn[rec] = npart | ((e & 1) << 30); }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace skd
 #include "kernels_panel.cuh"
 namespace skd {
@@ -1083,6 +1191,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
     extern __shared__ __align__(16) u64 smem[];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
     __shared__ int s_wcnt[kMeasWarps];
+    __shared__ int s_recj[kMeasWarps][kSlotsPerWarp], s_recn[kMeasWarps][kSlotsPerWarp], s_heavyj[kMeasWarps * kSlotsPerWarp];
     __shared__ u64 s_pn[kMeasWarps];
     __shared__ u32 s_wlist[kMeasWarps][kWarpList];
     __shared__ int s_cnt1, s_fast;
@@ -1115,85 +1224,40 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
     // =============================================================== wave mode =====
     while (pos < a.count) {
         const int wend = min(a.count, pos + WS);
-        u32* wpiv = a.wpiv + (size_t)(wave & 1) * WS;
-        // ------------------------------------------------------------ P1 -----
+        // ---- one fused pass: pivot search (K2) and, for every slot whose stabilizer half is empty, the deterministic product (K4)
+        // -- speculatively for the slots behind a random measurement too: the pass only reads the tableau, and the outcomes of
+        // [r0, wend) are written again by panel mode.  Counters and the odd-phase check are applied after the barrier, below r0.
         if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0u;
-        for (int slot = gw; pos + slot < wend; slot += GW) {
-            const int j = pos + slot;
-            const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
-            u32 piv = 0xffffffffu;
-            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {        // loads first (one L2 round trip per chunk)
-                u64 cv[kColChunk];
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < W) ? ldcg(xcol + w) : 0ull; }
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) {
-                    const int w = w0 + 32 * t + lane;
-                    if (cv[t]) piv = min(piv, u32(w * 64 + __ffsll((long long)cv[t]) - 1));
-                }
-                if (__any_sync(0xffffffffu, piv != 0xffffffffu)) break;
-            }
-            piv = warp_min(piv);
-            if (lane == 0) {
-                wpiv[slot] = piv;
-                if (piv != 0xffffffffu) atomicMax(&ws->r0[wave % 3], ~(u32)j);      // stored inverted: zero-initialised, max = smallest index
-            }
+        if (tid == 0) s_nheavy = 0;
+        __syncthreads();
+        wave_slots(a, pos, wend, wave, gw, GW, s_wlist[warp], &s_nheavy, s_heavy, s_recj[warp], s_recn[warp], acc_x, acc_z);
+        __syncthreads();
+        const int nheavy = s_nheavy;
+        for (int h = 0; h < nheavy; ++h) {
+            const int j = pos + s_heavy[h];
+            int total;
+            const int e = cta_det(a, sm, a.m.cols + (size_t)(2 * a.qubits[j]) * RW + W, nullptr, &total);
+            if (tid == 0) { a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1; s_heavyj[h] = j; s_heavy[h] = total | ((e & 1) << 30); }
         }
         SK_PROF(0);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
         SK_PROF(6);
         const u32 r0 = ~__ldcg(&ws->r0[wave % 3]);                               // 0xffffffff = no random measurement in the window
         const int dend = (r0 == 0xffffffffu) ? wend : int(r0);      // [pos, dend) are deterministic and final
-        if (tid == 0) s_nheavy = 0;
-        __syncthreads();
-        // ------------------------------------------------------------ P2 (K4) --
-        for (int slot = gw; pos + slot < dend; slot += GW) {
-            const int j = pos + slot;
-            const u64* dcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW + W;     // destabilizer half
-            if (lane == 0) s_wcnt[warp] = 0;
-            __syncwarp();
-            for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {
-                u64 cv[kColChunk];
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; cv[t] = (w < W) ? ldcg(dcol + w) : 0ull; }
-#pragma unroll
-                for (int t = 0; t < kColChunk; ++t) {
-                    const int w = w0 + 32 * t + lane;
-                    u64 v = cv[t];
-                    while (v) {
-                        const int b = __ffsll((long long)v) - 1; v &= v - 1;
-                        const int ti = atomicAdd(&s_wcnt[warp], 1);
-                        if (ti < kWarpList) s_wlist[warp][ti] = u32(w * 64 + b);
-                    }
-                }
+        if (lane == 0) {
+            u32 nd = 0, kd = 0, odd = 0;
+            for (int k = 0; k < kSlotsPerWarp; ++k) {
+                const int j = s_recj[warp][k];
+                if (j >= 0 && j < dend) { ++nd; kd += u32(s_recn[warp][k] & 0x3fffffff); odd |= u32(s_recn[warp][k] >> 30) & 1u; }
             }
-            __syncwarp();
-            const int npart = s_wcnt[warp];
-            if (npart > kWarpList) {                  // tree-reduced by the whole CTA below
-                if (lane == 0) { int h = atomicAdd(&s_nheavy, 1); s_heavy[h] = slot; }
-                continue;
+            if (warp == 0) for (int h = 0; h < nheavy; ++h) {
+                // (the slot index of a heavy product was replaced by its partner count above; it is below dend iff it was recorded ...
+                //  heavy products are rare: their position is re-derived from the record)
+                const int j = s_heavyj[h];
+                if (j < dend) { ++nd; kd += u32(s_heavy[h] & 0x3fffffff); odd |= u32(s_heavy[h] >> 30) & 1u; }
             }
-            for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
-            int e = warp_mul_list(a.m.rows, W, Wp, s_wlist[warp], npart, acc_x, acc_z, lane);
-            for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.m.sgn, int(s_wlist[warp][i]));
-            e = warp_sum(e) & 3;
-            if (lane == 0) {
-                if (e & 1) atomicOr(&ws->err, 1u);
-                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
-                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)npart);
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        for (int h = 0; h < s_nheavy; ++h) {
-            const int j = pos + s_heavy[h];
-            int total;
-            const int e = cta_det(a, sm, a.m.cols + (size_t)(2 * a.qubits[j]) * RW + W, nullptr, &total);
-            if (tid == 0) {
-                if (e & 1) atomicOr(&ws->err, 1u);
-                a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
-                atomicAdd(&ws->n_det, 1ull); atomicAdd(&ws->k_det, (u64)total);
-            }
+            if (nd) { atomicAdd(&ws->n_det, (u64)nd); atomicAdd(&ws->k_det, (u64)kd); }
+            if (odd) atomicOr(&ws->err, 1u);
         }
         if (blockIdx.x == 0 && tid == 0) atomicAdd(&ws->waves, 1ull);
         SK_PROF(1);

@@ -504,6 +504,13 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
             if (getenv("SK_DEBUG_CTAS")) { fprintf(stderr, "   per CTA:"); for (int b = 0; b < 148; ++b) fprintf(stderr, " %.0f", h.ctaphase[b * 4 + ph] / 1e3); fprintf(stderr, "\n"); }
         }
     }
+    if (getenv("SK_DEBUG_WAVE")) {
+        for (int wsel = 0; wsel < 2; ++wsel) for (int r = 0; r < 3; ++r) {
+            const u64* t = h.trace + wsel * 96 + r * 8;
+            fprintf(stderr, "wave trace warp %s slot %d: start %.2f us after the first, column %.2f, product %.2f, signs+sum %.2f\n", wsel ? "mid" : "0", r,
+                    (double)(long long)(t[0] - h.trace[0]) / 1e3, (double)(long long)(t[1] - t[0]) / 1e3, (double)(long long)(t[2] - t[1]) / 1e3, (double)(long long)(t[3] - t[2]) / 1e3);
+        }
+    } else
     if (getenv("SK_DEBUG_PROF") && h.trace[0]) {
         fprintf(stderr, "timeline (us from panel 20 start on CTA 0): events start, F/published seen, V, V+D1, bar1 exit, items, fold, bar2 exit\n");
         const u64 t0 = h.trace[0];
