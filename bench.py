@@ -9,11 +9,15 @@ One JSON line on stdout (rank 0).  `value` = seconds per full simulation with th
 and tableau already resident in HBM (CUDA events on the library's stream, max over ranks);
 `e2e` = the same simulation through the C-ABI call `sk_sim` with HOST buffers (circuit in pinned
 host memory -> compile -> upload -> simulate -> measurement record back to the host).
-N > 1: every rank simulates the whole circuit (independent shots, seed ^ rank) -- "replicas", the
-layout that is fastest for a 102 MB working set.  `--sharding rows` instead runs ONE simulation whose
-tableau is row-sharded over the N ranks (paper_2507_03092_b200/sharded.py; NCCL allreduce-min /
-broadcast / allgather per measurement window) and reports it as strong scaling; `--local-shards L` puts L
-shards on each GPU (how the protocol is exercised on a single B200).
+N > 1 runs BASELINE config 3 as it is stated -- ONE simulation whose tableau is row-sharded over the N ranks (SURVEY 8e;
+paper_2507_03092_b200/sharded.py; NCCL allreduce-min / broadcast / allgather per measurement window), strong scaling;
+`--sharding replicas` instead lets every rank simulate the whole circuit (independent shots, seed ^ rank: the layout that is
+fastest for a 102 MB working set, weak scaling).  `--local-shards L` puts L shards on each GPU (how the protocol is
+exercised on a single B200).
+
+`--config c4` / `--config c5` time the other two BASELINE workloads on one GPU (one line each, same keys):
+    c4  first-fit commutation grouping of 10^6 random 128-qubit Pauli strings (`--c4-mode gc|qwc`)
+    c5  Clifford+T transpile of a random 1000-qubit, 10^5-gate circuit with 10 % T gates
 """
 from __future__ import annotations
 
@@ -177,6 +181,202 @@ def bench_row_sharded(args, sk, skdist, torch, rank, local_rank, world, workload
     return 0
 
 
+def _load_workloads():
+    """paper_2507_03092_b200/workloads.py without importing the package (the reference arm must not map the CUDA library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("sk_workloads", os.path.join(ROOT, "paper_2507_03092_b200", "workloads.py"))
+    m = importlib.util.module_from_spec(spec); spec.loader.exec_module(m)
+    return m
+
+
+def _golden_c4(N):
+    p = os.path.join(ROOT, "tests", "golden", f"c4_groups_{N}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def _c4_cpu(mode, mname, N_full, N_sample=100_000):
+    """CPU oracle on a bounded sample (N_sample terms), scaled to N_full by the predicate calls the oracle itself needed at
+    N_full (tests/golden/c4_groups_*.json, measured once) or, without that file, by (N_full / N_sample)^2."""
+    import numpy as np
+    from oracle import oracle_py as orc
+    wl = _load_workloads()
+    x, z, _ = wl.c4_terms(N_sample)
+    o = orc.Rows(128, x, z, np.zeros(N_sample, np.uint8))
+    t0 = time.perf_counter(); g, ng, calls = o.group_first_fit(mode); dt = time.perf_counter() - t0
+    gold = _golden_c4(N_full)
+    if gold and mname in gold["modes"]:
+        scale = gold["modes"][mname]["predicate_calls"] / max(1, calls); how = "ratio of the oracle's own predicate calls at the two sizes"
+        full_s = gold["modes"][mname].get("oracle_seconds")
+    else:
+        scale = (N_full / N_sample) ** 2; how = "(N_full / N_sample)^2"; full_s = None
+    return {"value": dt * scale, "unit": "s", "cores": 1, "kind": "port", "extrapolated": True,
+            "sample": f"first-fit {mname} of the first-sorted N={N_sample} terms of the same generator: {dt:.2f} s, {calls} predicate calls, {ng} groups; scaled x{scale:.1f} ({how})"
+                      + (f"; the oracle's one full N={N_full} run took {full_s} s (tools/make_c4_golden.py)" if full_s else "")}
+
+
+def bench_c4(args):
+    """BASELINE config 4: first-fit grouping of N random 128-qubit Pauli strings."""
+    mode = 0 if args.c4_mode == "gc" else 1
+    mname = "GC" if mode == 0 else "QWC"
+    N = args.c4_n
+    metric = f"Pauli commutation grouping time (N={N}, n=128, first fit {mname})"
+    workload = f"{N} random Pauli strings on 128 qubits (SplitMix64 seed {SEED}, SURVEY 8d), sorted by |coeff| descending, first-fit {mname} grouping"
+    if args.impl == "reference":
+        cb = _c4_cpu(mode, mname, N)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+                          "ms_per_step": cb["value"] * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                          "config": {"workload": workload, "seed": SEED, "parallelism": "one host thread"}, "cpu_baseline": cb,
+                          "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}))
+        return 0
+    import hashlib
+    import numpy as np
+    import torch
+    import paper_2507_03092_b200 as sk
+    from paper_2507_03092_b200 import workloads as wl
+    sk.lib()
+    ctx = sk.Context(0)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    x, z, _ = wl.c4_terms(N)
+    xp = torch.from_numpy(x).pin_memory().numpy(); zp = torch.from_numpy(z).pin_memory().numpy(); sp = torch.zeros(N, dtype=torch.uint8).pin_memory().numpy()
+    rows = sk.Rows(ctx, 128, xp, zp, sp)
+    steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
+    sampler = ClockSampler(0); sampler.start()
+    for _ in range(warm):
+        g, ng = rows.group_first_fit(mode)
+    ctx.sync(); ctx.reset_counters()
+    t_region0 = time.time()
+    ms = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream); g, ng = rows.group_first_fit(mode); e1.record(stream); ctx.sync()
+        ms.append(e0.elapsed_time(e1))
+    t_region1 = time.time()
+    clocks = sampler.stop(t_region0, t_region1)
+    cnt = ctx.counters()
+    viol = rows.verify_grouping(mode, g)
+    rows.close()
+    # end to end: host arrays -> device rows -> groups -> group ids back on the host
+    e2e = []
+    for i in range(1 + max(1, min(args.e2e_steps, 3))):
+        t0 = time.perf_counter()
+        r2 = sk.Rows(ctx, 128, xp, zp, sp); g2, ng2 = r2.group_first_fit(mode); ctx.sync()
+        dt = time.perf_counter() - t0
+        r2.close()
+        if i: e2e.append(dt)
+    assert ng2 == ng and (g2 == g).all()
+    ms_step = sum(ms) / len(ms)
+    gold = _golden_c4(N)
+    g32 = np.ascontiguousarray(g, np.uint32)
+    parity = None
+    if gold and mname in gold["modes"]:
+        parity = bool(gold["modes"][mname]["groups"] == ng and hashlib.sha256(g32.tobytes()).hexdigest() == gold["modes"][mname]["sha256"])
+    pred = cnt["pred_evals"] / steps
+    peak = 148 * 16 * 1.965e9 / 4 / 1e9 if mode == 0 else 148 * 64 * 1.965e9 / 20 / 1e9
+    line = {"metric": metric, "value": ms_step * 1e-3, "unit": "s", "n_gpus": 1, "steps": steps, "warmup": warm, "ms_per_step": ms_step, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload, "seed": SEED, "parallelism": "one GPU", "l2": "inputs (32 MB) + group store exceed nothing: L2 resident by design; not flushed",
+                       "timing": "CUDA events on the library stream around sk_group_first_fit (rows resident, group ids copied back), mean of steps"},
+            "e2e": {"value": sum(e2e) / len(e2e), "unit": "s", "h2d_bytes_per_step": int(N * 33), "d2h_bytes_per_step": int(N * 4),
+                    "call": "sk_rows_create + sk_rows_upload (pinned host arrays) + sk_group_first_fit"},
+            "gpu_launches": int(cnt["kernel_launches"]),
+            "roofline": {"bound": "int", "kernel": "k_conflict_groups", "achieved": pred / (ms_step * 1e-3) / 1e9, "peak": peak, "unit": "Gpred/s",
+                         "frac": pred / (ms_step * 1e-3) / 1e9 / peak, "traffic": None,
+                         "predicates_per_step": pred, "pair_equivalents_per_step": N * (N - 1) / 2,
+                         "peak_source": "nominal integer pipe: 148 SMs x 16 POPC/clk x 1.965 GHz / 4 POPC per 128-qubit predicate (GC); 148 x 64 INT32/clk / ~20 ops (QWC) -- no measured INT peak exists; "
+                                        "the whole-run fraction is low because the single-CTA first-fit resolver (sequential in the term index) takes most of the time"},
+            "clocks": clocks, "groups": int(ng), "verify_violations": int(viol), "bit_exact_vs_oracle_golden": parity}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = _c4_cpu(mode, mname, N)
+    print(json.dumps(line))
+    ctx.close()
+    return 0
+
+
+def _c5_alg2_bytes(gates, n, kinds):
+    """Algorithm 2 walks the circuit backwards; a Clifford gate sweeps R = 2n + |T_tab at that point| rows."""
+    import numpy as np
+    H, S, CX, T, TDG = kinds
+    k = gates["kind"]
+    is_t = (k == T) | (k == TDG)
+    t_after = np.cumsum(is_t[::-1])[::-1] - is_t          # T rows already appended when gate i is reached
+    cols = np.where(k == H, 4, np.where(k == S, 3, np.where(k == CX, 6, 0))).astype(np.float64)
+    R = 2.0 * n + t_after
+    return float((cols * R / 8.0).sum())
+
+
+def bench_c5(args):
+    """BASELINE config 5: Clifford+T transpile of a random 1000-qubit circuit, 10 % T gates."""
+    n, G = 1000, 100_000
+    metric = f"Clifford+T transpile time (n={n}, {G} gates, 10% T)"
+    workload = f"random Clifford+T circuit on {n} qubits, {G} gates (SplitMix64 seed 20250704, SURVEY 8d: 5% t, 5% tdg, 30% h, 30% s, 30% cx), exact transpile to T layers + M_tab"
+    wl = _load_workloads()
+    import numpy as np
+    dt12 = np.dtype([("kind", "u1"), ("pad", "u1", (3,)), ("q0", "<u4"), ("q1", "<u4")])
+    kinds = (0, 1, 6, 10, 11)
+    gates = wl.c5_gates(n, G, gate_dtype=dt12, kinds=kinds)
+    if args.impl == "reference" or not args.no_cpu_baseline:
+        from oracle import oracle_py as orc
+        t0 = time.perf_counter(); op = orc.Pbc(n, gates, exact=True); cpu_s = time.perf_counter() - t0
+        ostats = op.stats()
+        cb = {"value": cpu_s, "unit": "s", "cores": 1, "kind": "port", "extrapolated": False,
+              "sample": f"the full workload, measured once ({cpu_s:.2f} s): {ostats}"}
+    if args.impl == "reference":
+        print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+                          "ms_per_step": cb["value"] * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                          "config": {"workload": workload, "seed": 20250704, "parallelism": "one host thread"}, "cpu_baseline": cb,
+                          "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}))
+        return 0
+    import torch
+    import paper_2507_03092_b200 as sk
+    sk.lib()
+    ctx = sk.Context(0)
+    gp = torch.empty(G * 12, dtype=torch.uint8).pin_memory().numpy().view(sk.GATE_DTYPE); gp[:] = gates
+    circ = sk.Circuit(n, gp)
+    steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
+    sampler = ClockSampler(0); sampler.start()
+    for _ in range(warm):
+        sk.Pbc(ctx, circ).close()
+    ctx.sync(); ctx.reset_counters()
+    t_region0 = time.time()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter(); pb = sk.Pbc(ctx, circ); ctx.sync(); ts.append(time.perf_counter() - t0)
+        stats = pb.stats()
+        if _ < steps - 1: pb.close()
+    t_region1 = time.time()
+    clocks = sampler.stop(t_region0, t_region1)
+    cnt = ctx.counters()
+    same = None
+    if not args.no_cpu_baseline:
+        same = stats == ostats
+        for k in range(stats["layers"]):
+            same = same and all((u == v).all() for u, v in zip(pb.layer(k), op.layer(k)))
+        same = bool(same and all((u == v).all() for u, v in zip(pb.mtab(), op.mtab().get())))
+    pb.close()
+    sec = sum(ts) / len(ts)
+    ab = _c5_alg2_bytes(gates, n, kinds)
+    peak, peak_src = peaks()
+    line = {"metric": metric, "value": sec, "unit": "s", "n_gpus": 1, "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload, "seed": 20250704, "parallelism": "one GPU", "l2": "working set ~3 MB: L2 resident by nature; not flushed",
+                       "timing": "wall clock around sk_transpile_ex + sync (the call takes the gate list from pinned host memory: value and e2e are the same call), mean of steps"},
+            "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": int(G * 12), "d2h_bytes_per_step": 40, "call": "sk_transpile_ex(ctx, n, gates, ngates, flags=0) with a pinned host gate list"},
+            "gpu_launches": int(cnt["kernel_launches"]),
+            "roofline": {"bound": "hbm", "kernel": "k_layer (Algorithm 2 backward walk)", "achieved": ab / sec / 1e9, "peak": peak, "unit": "GB/s", "frac": ab / sec / 1e9 / peak,
+                         "traffic": None, "peak_source": peak_src, "algorithmic_bytes": ab,
+                         "note": "Algorithm 2 only (SURVEY 8d: a Clifford gate sweeps 2n + |T_tab| rows); the commutation scans and rowsum+i of Algorithms 3-4 are not counted, so this is a lower bound; "
+                                 "the pass is a chain of ~10^5 small dependent launches on a 3 MB working set: launch bound, not bandwidth bound"},
+            "clocks": clocks, "stats": stats, "bit_exact_vs_oracle": same}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cb
+    print(json.dumps(line))
+    ctx.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -186,9 +386,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", action="store_true", help="cpu_baseline: extrapolate from 6- and 12-round cuts instead of timing the full 71-round run (~25 s on 16 threads)")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--sharding", default="replicas", choices=["replicas", "rows"])
+    ap.add_argument("--sharding", default=None, choices=["replicas", "rows"], help="default: rows when --gpus > 1 (BASELINE config 3), replicas on one GPU")
+    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c5"])
+    ap.add_argument("--c4-mode", default="gc", choices=["gc", "qwc"])
+    ap.add_argument("--c4-n", type=int, default=1_000_000)
     ap.add_argument("--local-shards", type=int, default=1)
     args = ap.parse_args()
+    if args.sharding is None:
+        args.sharding = "rows" if (args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1) else "replicas"
+    if args.config != "c3":
+        if int(os.environ.get("RANK", "0")) != 0:           # single-GPU configs: rank 0 alone works
+            return 0
+        return bench_c4(args) if args.config == "c4" else bench_c5(args)
 
     if args.impl == "reference":
         # Rank 0 alone works; nothing here imports the CUDA package (env_world is read from the environment directly).

@@ -9,7 +9,8 @@
 namespace stabkit {
 
 // SPEC:304-307.  `workers` is kept for API compatibility; the device engine ignores it
-// (row parallelism is the GPU's), `audit` is accepted and ignored.
+// (row parallelism is the GPU's).  `audit` checks the tableau invariants of SPEC:111-116 on the device after the run
+// (sk_tableau_audit: every row pair has the symplectic product the CHP form demands) and throws InvariantError otherwise.
 struct EngineConfig { size_t workers = 1; uint64_t seed = 0; bool audit = false; };
 
 // SPEC:299-302
@@ -26,6 +27,11 @@ inline SimResult run(const Circuit& c, const EngineConfig& cfg, int mode) {
     std::vector<uint8_t> o(nm + 1), det(nm + 1);
     sk_tableau* t = nullptr; uint32_t warn = 0;
     d.check(sk_sim(d.ctx(), c.n, c.raw(), c.gates.size(), c.chunk_marks.data(), c.chunk_marks.size(), mode, cfg.seed, &t, o.data(), det.data(), &warn));
+    if (cfg.audit) {
+        uint64_t bad = 0;
+        const int32_t rc = sk_tableau_audit(t, &bad);
+        if (rc || bad) { sk_tableau_destroy(t); d.check(rc); throw InvariantError("audit: " + std::to_string(bad) + " row pairs violate the tableau invariants (SPEC:111-116)"); }
+    }
     SimResult r{Tableau(c.n, t), {}, (warn & 1u) != 0};
     r.record.reserve(nm);
     size_t k = 0;

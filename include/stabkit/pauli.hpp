@@ -201,4 +201,37 @@ inline BitVec commutation_vector(const PauliString& p, std::span<const PauliStri
     return out;
 }
 
+// A row set that stays on the device: upload once, then any number of commutation_vector calls (Algorithm 3 asks for one per
+// rotation: the free function above re-uploads the rows every time).  append() grows it within the capacity given up front.
+class DeviceRows {
+  public:
+    DeviceRows(size_t n, std::span<const PauliString> rows, size_t capacity = 0) : n_(n) {
+        Device& dev = Device::instance();
+        dev.check(sk_rows_create(dev.ctx(), n, std::max(capacity, rows.size()), &r_));
+        std::vector<uint64_t> x, z; std::vector<uint8_t> s;
+        pack_rows(rows, n, x, z, s);
+        const int rc = rows.empty() ? 0 : sk_rows_upload(r_, x.data(), z.data(), s.data(), rows.size());
+        if (rc) { const std::string msg = sk_last_error(dev.ctx()); sk_rows_destroy(r_); r_ = nullptr; throw_status(rc, msg); }
+    }
+    ~DeviceRows() { if (r_) sk_rows_destroy(r_); }
+    DeviceRows(const DeviceRows&) = delete;
+    DeviceRows& operator=(const DeviceRows&) = delete;
+    size_t size() const { return size_t(sk_rows_count(r_)); }
+    void append(std::span<const PauliString> rows) {
+        std::vector<uint64_t> x, z; std::vector<uint8_t> s;
+        pack_rows(rows, n_, x, z, s);
+        Device::instance().check(sk_rows_append(r_, x.data(), z.data(), s.data(), rows.size()));
+    }
+    // ref: proj/src/pauli.cpp:215-237
+    BitVec commutation_vector(const PauliString& p) const {
+        if (p.num_qubits() != n_) throw DimensionError("commutation_vector: Pauli has length " + std::to_string(p.num_qubits()) + ", rows have " + std::to_string(n_));
+        BitVec out(size());
+        if (size()) Device::instance().check(sk_commutation_vector(r_, p.x_words().data(), p.z_words().data(), out.words.data()));
+        return out;
+    }
+    sk_rows* handle() const { return r_; }
+  private:
+    size_t n_; sk_rows* r_ = nullptr;
+};
+
 }  // namespace stabkit

@@ -73,6 +73,11 @@ typedef struct sk_counters {
     uint64_t transposes;           /* column-major <-> row-major conversions    */
     uint64_t kernel_launches;      /* kernels launched by this library          */
     uint64_t meas_phase_ns[8];     /* measurement kernel, CTA 0 wall ns per phase: inspect, barrier, classify+det, barrier, random, barrier, window */
+    /* "algorithmic bytes, per-kernel times" */
+    uint64_t pred_evals;           /* commutation predicates evaluated by the grouping conflict kernels (config C4 roofline)      */
+    double   algorithmic_bytes;    /* SURVEY 8d byte count of the gates and measurements run since the last reset, for the qubit
+                                      count of the tableau used last (exact when one tableau size was in use)                      */
+    double   class_ms[3];          /* device time of the last sk_program_run_profiled by kernel class: layers, measurement, transposes */
 } sk_counters;
 
 /* ---- context ---------------------------------------------------------- */
@@ -96,6 +101,10 @@ uint64_t sk_tableau_qubits(const sk_tableau* t);
 /* Row-major 2n x W words for x and z, 2n sign bytes. */
 int32_t sk_tableau_upload(sk_tableau* t, const uint64_t* x, const uint64_t* z, const uint8_t* sign);
 int32_t sk_tableau_download(sk_tableau* t, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* EngineConfig.audit, the tableau invariants of SPEC:111-116 checked on the device: every pair of rows has the
+ * symplectic product the CHP form demands (stabilizers commute, destabilizers commute, destabilizer i anticommutes with
+ * stabilizer i and with nothing else).  *violations = number of row pairs (a < b) that break it; 0 for a valid tableau. */
+int32_t sk_tableau_audit(sk_tableau* t, uint64_t* violations);
 
 /* One fused layer of Clifford gates on pairwise-disjoint qubits: every
  * tableau word is read/written once per layer.  Replaces a loop of
@@ -189,6 +198,14 @@ void sk_rows_destroy(sk_rows* r);
 uint64_t sk_rows_count(const sk_rows* r);
 int32_t sk_rows_upload(sk_rows* r, const uint64_t* x, const uint64_t* z, const uint8_t* sign, uint64_t m);
 int32_t sk_rows_download(sk_rows* r, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* Appends m rows behind the current ones (T_tab grows by one row per T gate; PAPER Alg. 2).  SK_EDIM when the
+ * capacity given to sk_rows_create is exceeded. */
+int32_t sk_rows_append(sk_rows* r, const uint64_t* x, const uint64_t* z, const uint8_t* sign, uint64_t m);
+/* ref: proj/src/pauli.cpp:117-140 commutes_with / qubitwise_commutes_with over a tile of the pair matrix: bit (j - j0) of
+ * out_bits[(i - i0) * words + ...] is set iff rows i and j CONFLICT (mode 0: anticommute, mode 1: not qubit-wise commuting),
+ * i in [i0, i0+ni), j in [j0, j0+nj), words = ceil(nj/64) per output row (host buffer).  The grouping driver itself
+ * consumes conflicts on the fly (group-major kernel); the tile is the API for callers that want the matrix. */
+int32_t sk_commute_matrix_tile(sk_rows* r, int mode, uint64_t i0, uint64_t ni, uint64_t j0, uint64_t nj, uint64_t* out_bits);
 /* ref: proj/src/pauli.cpp:146-187 applied to every row (Algorithm 2 inner loop). */
 int32_t sk_rows_conj_layer(sk_rows* r, const sk_gate* gates, size_t ngates);
 /* ref: proj/src/pauli.cpp:215-237 commutation_vector: bit i set iff p anticommutes with row i. */

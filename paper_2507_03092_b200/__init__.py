@@ -43,7 +43,8 @@ _ERR = {SK_EDIM: DimensionError, SK_EUNSUPPORTED: UnsupportedError, SK_EINVARIAN
 class Counters(C.Structure):
     _fields_ = [("n_rand", C.c_uint64), ("n_det", C.c_uint64), ("k_rand", C.c_uint64), ("k_det", C.c_uint64),
                 ("gate_hist", C.c_uint64 * 12), ("layers", C.c_uint64), ("waves", C.c_uint64),
-                ("transposes", C.c_uint64), ("kernel_launches", C.c_uint64), ("meas_phase_ns", C.c_uint64 * 8)]
+                ("transposes", C.c_uint64), ("kernel_launches", C.c_uint64), ("meas_phase_ns", C.c_uint64 * 8),
+                ("pred_evals", C.c_uint64), ("algorithmic_bytes", C.c_double), ("class_ms", C.c_double * 3)]
 
 
 _lib = None
@@ -100,6 +101,9 @@ def lib() -> C.CDLL:
             "sk_rows_count": (u64, [vp]),
             "sk_rows_upload": (i32, [vp, vp, vp, vp, u64]),
             "sk_rows_download": (i32, [vp, vp, vp, vp]),
+            "sk_rows_append": (i32, [vp, vp, vp, vp, u64]),
+            "sk_commute_matrix_tile": (i32, [vp, C.c_int, u64, u64, u64, u64, vp]),
+            "sk_tableau_audit": (i32, [vp, P(u64)]),
             "sk_rows_conj_layer": (i32, [vp, vp, sz]),
             "sk_commutation_vector": (i32, [vp, vp, vp, vp]),
             "sk_rowsum_plus_i_where_anticommuting": (i32, [vp, vp, vp, C.c_uint8, P(u64)]),
@@ -145,7 +149,7 @@ EXPORTS = [
     "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_program_run_shots", "sk_sim", "sk_free",
     "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native", "sk_circuit_parse_qasm2",
     "sk_circuit_validate_chunks", "sk_circuit_validate_chunks_ex", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
-    "sk_rows_download", "sk_rows_conj_layer", "sk_commutation_vector",
+    "sk_rows_download", "sk_rows_append", "sk_commute_matrix_tile", "sk_tableau_audit", "sk_rows_conj_layer", "sk_commutation_vector",
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",
     "sk_group_first_fit", "sk_verify_grouping", "sk_transpile", "sk_transpile_ex", "sk_pbc_destroy", "sk_pbc_stats",
     "sk_pbc_layer_rows", "sk_pbc_layer_download", "sk_pbc_mtab_download",
@@ -328,6 +332,7 @@ class Context:
         d = {k: int(getattr(c, k)) for k in ("n_rand", "n_det", "k_rand", "k_det", "layers", "waves", "transposes", "kernel_launches")}
         d["gate_hist"] = [int(v) for v in c.gate_hist]
         d["meas_phase_ns"] = [int(v) for v in c.meas_phase_ns]
+        d["pred_evals"] = int(c.pred_evals); d["algorithmic_bytes"] = float(c.algorithmic_bytes); d["class_ms"] = [float(v) for v in c.class_ms]
         return d
 
     def reset_counters(self):
@@ -363,6 +368,12 @@ class Tableau:
             self.close()
         except Exception:
             pass
+
+    def audit(self) -> int:
+        """sk_tableau_audit (EngineConfig.audit): row pairs that violate the CHP symplectic form; 0 = valid."""
+        v = C.c_uint64(0)
+        self.ctx.check(lib().sk_tableau_audit(self._h, C.byref(v)))
+        return int(v.value)
 
     def reset(self):
         self.ctx.check(lib().sk_tableau_reset(self._h))
@@ -483,6 +494,20 @@ class Rows:
         if m:
             self.ctx.check(lib().sk_rows_download(self._h, _ptr(x), _ptr(z), _ptr(s)))
         return x, z, s
+
+    def append(self, x, z, sign):
+        """sk_rows_append: m more rows behind the current ones (up to the capacity given at creation)."""
+        x = np.ascontiguousarray(x, np.uint64).reshape(-1, self.W); z = np.ascontiguousarray(z, np.uint64).reshape(-1, self.W)
+        s = np.ascontiguousarray(sign, np.uint8)
+        self.ctx.check(lib().sk_rows_append(self._h, _ptr(x), _ptr(z), _ptr(s), x.shape[0]))
+
+    def commute_tile(self, mode: int, i0: int, ni: int, j0: int, nj: int) -> np.ndarray:
+        """sk_commute_matrix_tile -> bool [ni, nj]: True where rows i0+a and j0+b conflict (mode 0: anticommute, 1: not qubit-wise commuting)."""
+        words = (nj + 63) // 64
+        out = np.zeros((ni, max(words, 1)), np.uint64)
+        self.ctx.check(lib().sk_commute_matrix_tile(self._h, mode, i0, ni, j0, nj, _ptr(out)))
+        bits = np.unpackbits(out.view(np.uint8).reshape(ni, -1), axis=1, bitorder="little")
+        return bits[:, :nj].astype(bool)
 
     def conj_layer(self, gates):
         g = gates_array(gates)

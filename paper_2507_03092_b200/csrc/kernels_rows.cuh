@@ -233,7 +233,8 @@ __device__ __forceinline__ bool conflict4(u64 ax0, u64 ax1, u64 az0, u64 az1, u6
 }
 __global__ void __launch_bounds__(256)
 k_conflict_groups(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int Bt, const u32* __restrict__ ngroups,
-                  const u32* __restrict__ off, const u64* __restrict__ gterms, int mode_, u32* __restrict__ bitmap, int GW32) {
+                  const u32* __restrict__ off, const u64* __restrict__ gterms, int mode_, u32* __restrict__ bitmap, int GW32,
+                  unsigned long long* __restrict__ npred) {
     extern __shared__ u64 s_blk[];          // [Bt][4]: x0 x1 z0 z1 of each staged block term
     const int mode = mode_ & 0xff;
     const u32 ng = *ngroups;
@@ -255,9 +256,11 @@ k_conflict_groups(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
     if (cnt > 3) { const u64* p = gterms + (size_t)(start + 3) * 4; m3[0] = p[0]; m3[1] = p[1]; m3[2] = p[2]; m3[3] = p[3]; }
     const bool singles = __all_sync(0xffffffffu, cnt <= 1u);   // QWC on random strings: every group is a single term
     const int kend = min(Bt, t0 + B - tb);
+    u32 evals = 0;                        // predicates this thread really evaluates (members that exist), for the C4 roofline
     for (int k = 0; k < kend; ++k) {
         const u64 bx0 = s_blk[4 * k], bx1 = s_blk[4 * k + 1], bz0 = s_blk[4 * k + 2], bz1 = s_blk[4 * k + 3];
         bool c = conflict4(m0[0], m0[1], m0[2], m0[3], bx0, bx1, bz0, bz1, mode);
+        evals += min(cnt, 4u);
         if (!singles) {
             c |= conflict4(m1[0], m1[1], m1[2], m1[3], bx0, bx1, bz0, bz1, mode);
             c |= conflict4(m2[0], m2[1], m2[2], m2[3], bx0, bx1, bz0, bz1, mode);
@@ -266,12 +269,65 @@ k_conflict_groups(const u64* __restrict__ rows, int Wp, int W, int t0, int B, in
                 for (u32 j = 4; j < cnt && !c; ++j) {
                     const u64* p = gterms + (size_t)(start + j) * 4;
                     c = conflict4(p[0], p[1], p[2], p[3], bx0, bx1, bz0, bz1, mode);
+                    ++evals;
                 }
             }
         }
         const u32 bits = __ballot_sync(0xffffffffu, c);
         if ((threadIdx.x & 31) == 0) bitmap[(size_t)(tb + k - t0) * GW32 + (g >> 5)] = bits;
     }
+    if (npred) { evals = __reduce_add_sync(0xffffffffu, evals); if ((threadIdx.x & 31) == 0 && evals) atomicAdd(npred, (unsigned long long)evals); }
+}
+
+// K5 tile form (ref: proj/src/pauli.cpp:117-140): one bit per row pair of the tile [i0, i0+ni) x [j0, j0+nj).  A warp owns one
+// output word (row i, 64 consecutive j): lane l evaluates pairs (i, j0 + 64*w + l) and (.., + 32 + l); the row i words are
+// broadcast loads.  out[(i - i0) * words + w].
+__global__ void __launch_bounds__(256)
+k_commute_tile(const u64* __restrict__ rows, int Wp, int W, int mode, int i0, int ni, int j0, int nj, int words, u64* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (item >= (long long)ni * words) return;
+    const int i = i0 + int(item / words), w = int(item % words);
+    const u64* ax = rows + (size_t)(2 * i) * Wp; const u64* az = ax + Wp;
+    u32 bits[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int jj = 64 * w + 32 * h + lane;
+        bool c = false;
+        if (jj < nj) {
+            const u64* bx = rows + (size_t)(2 * (j0 + jj)) * Wp; const u64* bz = bx + Wp;
+            int par = 0; u64 any = 0;
+            for (int k = 0; k < W; ++k) { const u64 v = (ax[k] & bz[k]) ^ (bx[k] & az[k]); par ^= __popcll(v); any |= v; }
+            c = mode == 0 ? (par & 1) : (any != 0);
+        }
+        bits[h] = __ballot_sync(0xffffffffu, c);
+    }
+    if (lane == 0) out[(size_t)(i - i0) * words + w] = (u64)bits[0] | ((u64)bits[1] << 32);
+}
+
+// EngineConfig.audit: symplectic form of a CHP tableau in the R form.  Row-bit a (stabilizer i = bit i,
+// destabilizer i = bit NS + i) against row-bit b > a must anticommute iff b == a + NS.  Same warp-per-word layout as the tile.
+__global__ void __launch_bounds__(256)
+k_audit_tile(const u64* __restrict__ rows, int Wp, int W, int NS, int n, int a0, int na, unsigned long long* __restrict__ violations) {
+    const int lane = threadIdx.x & 31;
+    const int words = (2 * NS + 63) / 64;
+    const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (item >= (long long)na * words) return;
+    const int a = a0 + int(item / words), w = int(item % words);
+    const bool alive = (a < NS) ? (a < n) : (a - NS < n);
+    const u64* ax = rows + (size_t)(2 * a) * Wp; const u64* az = ax + Wp;
+    int bad = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int b = 64 * w + 32 * h + lane;
+        if (!alive || b <= a || b >= 2 * NS || ((b < NS) ? (b >= n) : (b - NS >= n))) continue;
+        const u64* bx = rows + (size_t)(2 * b) * Wp; const u64* bz = bx + Wp;
+        int par = 0;
+        for (int k = 0; k < W; ++k) par ^= __popcll((ax[k] & bz[k]) ^ (bx[k] & az[k]));
+        bad += ((par & 1) != (b == a + NS ? 1 : 0)) ? 1 : 0;
+    }
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicAdd(violations, (unsigned long long)bad);
 }
 
 // First free group of every block term with respect to the groups that existed BEFORE the block (one CTA per bitmap row,

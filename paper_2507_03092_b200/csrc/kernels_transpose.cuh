@@ -107,6 +107,14 @@ __global__ void k_bytes_to_signs(const uint8_t* __restrict__ in, u64* __restrict
     if (in[i]) atomicOr(&sgn[rb >> 6], 1ull << (rb & 63));
 }
 
+// sign bytes of rows [first, first + nrows) of a plain row set (no stabilizer / destabilizer split): set or clear each bit
+__global__ void k_bytes_to_signs_at(const uint8_t* __restrict__ in, u64* __restrict__ sgn, int nrows, int first) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int rb = first + i;
+    if (in[i]) atomicOr(&sgn[rb >> 6], 1ull << (rb & 63)); else atomicAnd(&sgn[rb >> 6], ~(1ull << (rb & 63)));
+}
+
 // host row-major (nrows x W, separate x / z arrays) <-> device R form (stride 2*Wp, row-bit mapped)
 __global__ void k_pack_rows(const u64* __restrict__ hx, const u64* __restrict__ hz, u64* __restrict__ rows,
                             int nrows, int W, int Wp, int split, int NS) {

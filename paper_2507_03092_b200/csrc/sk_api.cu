@@ -10,6 +10,7 @@
 
 #include "kernels_layer.cuh"
 #include "kernels_measure.cuh"
+#include "kernels_rows.cuh"
 #include "kernels_transpose.cuh"
 #include "sk_internal.hpp"
 
@@ -273,6 +274,28 @@ extern "C" int32_t sk_tableau_upload(sk_tableau* t, const uint64_t* x, const uin
     return SK_OK;
 }
 
+extern "C" int32_t sk_tableau_audit(sk_tableau* t, uint64_t* violations) {
+    if (!t || !violations) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    { int32_t rc0 = rows_full(t); if (rc0) return rc0; }
+    unsigned long long* d_v = reinterpret_cast<unsigned long long*>(c->d_err) + 2;
+    SK_CUDA(c, cudaMemsetAsync(d_v, 0, 8, c->stream));
+    const int rowbits = 2 * t->NS, words = (rowbits + 63) / 64;
+    const int step = 4096;                       // row-bits per launch: keeps the grid below 2^31 threads
+    for (int a0 = 0; a0 < rowbits; a0 += step) {
+        const int na = std::min(step, rowbits - a0);
+        const size_t threads = (size_t)na * words * 32;
+        k_audit_tile<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(t->m.rows, t->Wp, t->W, t->NS, int(t->n), a0, na, d_v);
+        c->cnt.kernel_launches++;
+    }
+    SK_CUDA(c, cudaGetLastError());
+    unsigned long long v = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&v, d_v, 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    *violations = v;
+    return SK_OK;
+}
+
 static int32_t check_ws(sk_ctx* c) {
     MeasWs* ws = (MeasWs*)c->d_ws;
     MeasWs h;
@@ -334,6 +357,7 @@ static void launch_layer(sk_tableau* t, const sk_gate* d_gates, int ngates, cons
         k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb, nullptr);
     }
     c->cnt.kernel_launches++; c->cnt.layers += (uint64_t)nlayers;
+    c->last_n = t->n;
     t->r_valid = false;
 }
 
@@ -413,6 +437,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
                               uint8_t* d_out, uint8_t* d_det) {
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
+    c->last_n = t->n;
     if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; }
     // the launch-scoped words (barrier counter, progress counter, wave slots) are zero: the previous launch's last CTA
     // re-zeroed them on its way out (check_ws does it after an error)
@@ -483,6 +508,7 @@ extern "C" int32_t sk_reset_counters(sk_ctx* c) {
     c->cnt = sk_counters{};
     MeasWs* ws = (MeasWs*)c->d_ws;
     SK_CUDA(c, cudaMemsetAsync(&ws->n_rand, 0, (38 + 640 + 192) * 8, c->stream));
+    SK_CUDA(c, cudaMemsetAsync(reinterpret_cast<unsigned long long*>(c->d_err) + 1, 0, 8, c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
@@ -490,8 +516,22 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
     MeasWs h;
     SK_CUDA(c, cudaMemcpyAsync(&h, c->d_ws, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    unsigned long long npred = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&npred, reinterpret_cast<unsigned long long*>(c->d_err) + 1, 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
     *out = c->cnt;
     out->n_rand = h.n_rand; out->n_det = h.n_det; out->k_rand = h.k_rand; out->k_det = h.k_det; out->waves = h.waves;
+    out->pred_evals = c->cnt.pred_evals + npred;
+    {   // columns read or written per gate kind x R/8 bytes, + 2 R/8 per fused layer for the sign column, + the measurement terms
+        const double R = 2.0 * double(c->last_n), col = R / 8.0, W = double((c->last_n + 63) / 64);
+        static const double kCols[12] = {4, 3, 3, 1, 2, 1, 6, 6, 8, 0, 0, 0};      // H S SDG X Y Z CX CZ SWAP M T TDG
+        double b = 0;
+        for (int k = 0; k < 12; ++k) b += kCols[k] * double(c->cnt.gate_hist[k]) * col;
+        b += 2.0 * col * double(c->cnt.layers);
+        b += double(h.n_rand) * (col + 48.0 * W) + double(h.k_rand) * 32.0 * W + double(h.n_det) * col + double(h.k_det) * 16.0 * W;
+        out->algorithmic_bytes = b;
+    }
+    for (int k = 0; k < 3; ++k) out->class_ms[k] = c->class_ms[k];
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "measure kernel CTA0 us: P1 %.0f P2 %.0f | gather %.0f factorise %.0f values+detA %.0f apply+detB %.0f | barriers wave %.0f panel %.0f | panels %llu\n",
                                          h.prof[0] / 1e3, h.prof[1] / 1e3, h.prof[2] / 1e3, h.prof[3] / 1e3, h.prof[4] / 1e3, h.prof[5] / 1e3, h.prof[6] / 1e3, h.prof[7] / 1e3, (unsigned long long)h.panels);
@@ -900,6 +940,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         SK_CUDA(c, cudaStreamSynchronize(c->stream));
         class_ms[0] = class_ms[1] = class_ms[2] = 0.f;
         for (size_t i = 1; i < ev.size(); ++i) { float ms = 0; cudaEventElapsedTime(&ms, ev[i - 1], ev[i]); class_ms[cls[i]] += ms; }
+        for (int k = 0; k < 3; ++k) c->class_ms[k] = class_ms[k];
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
     return SK_OK;

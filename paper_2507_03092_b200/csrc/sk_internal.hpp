@@ -34,6 +34,8 @@ struct sk_ctx {
     void* d_ws = nullptr;                   // skd::MeasWs: barrier, wave slots, device-side counters
     // host-side counters (device-side ones live in MeasWs)
     sk_counters cnt{};
+    uint64_t last_n = 0;                    // qubit count of the tableau used last (for sk_counters.algorithmic_bytes)
+    double class_ms[3] = {0, 0, 0};         // last sk_program_run_profiled: layers, measurement, transposes
     std::vector<uint32_t> q_epoch; uint32_t epoch = 0;   // qubit-collision scratch
 };
 

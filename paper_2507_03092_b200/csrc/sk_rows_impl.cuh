@@ -86,7 +86,8 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
             SK_CUDA(c, cudaMemsetAsync(d_fillc, 0, ((size_t)t0 + 1) * 4, c->stream));
             k_csr_fill<<<(t0 + 255) / 256, 256, 0, c->stream>>>(d_rows, Wp, W, d_group, t0, d_off, d_fillc, d_gterms);
             dim3 grid((t0 + 255) / 256, (b + Btg - 1) / Btg);
-            k_conflict_groups<<<grid, 256, (size_t)Btg * 32, c->stream>>>(d_rows, Wp, W, t0, b, Btg, d_ng, d_off, d_gterms, mode, d_bitmap, GW32);
+            k_conflict_groups<<<grid, 256, (size_t)Btg * 32, c->stream>>>(d_rows, Wp, W, t0, b, Btg, d_ng, d_off, d_gterms, mode, d_bitmap, GW32,
+                                                                         reinterpret_cast<unsigned long long*>(c->d_err) + 1);
             c->cnt.kernel_launches += 4;
         } else if (t0 > 0) {
             dim3 grid((t0 + 255) / 256, (b + Bt - 1) / Bt);
@@ -179,6 +180,50 @@ extern "C" int32_t sk_rows_upload(sk_rows* r, const uint64_t* x, const uint64_t*
         SK_CUDA(c, cudaStreamSynchronize(c->stream));
     }
     r->count = m; r->r_valid = true; r->c_valid = false;
+    return SK_OK;
+}
+extern "C" int32_t sk_rows_append(sk_rows* r, const uint64_t* x, const uint64_t* z, const uint8_t* sign, uint64_t m) {
+    if (!r || (m && (!x || !z || !sign))) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    if (m == 0) return SK_OK;
+    if (r->count + m > r->cap) SK_FAIL(c, SK_EDIM, "rows: appending %llu rows to %llu exceeds the capacity %llu", (unsigned long long)m, (unsigned long long)r->count, (unsigned long long)r->cap);
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    const int W = r->m.W; const size_t words = (size_t)m * W;
+    rc = sk_ctx_reserve_tmp(c, words * 16 + m + 64);
+    if (rc) return rc;
+    u64* dx = (u64*)c->d_tmp; u64* dz = dx + words; uint8_t* ds = (uint8_t*)(dz + words);
+    SK_CUDA(c, cudaMemcpyAsync(dx, x, words * 8, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(dz, z, words * 8, cudaMemcpyHostToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(ds, sign, m, cudaMemcpyHostToDevice, c->stream));
+    // rows [count, count + m) of the R form (all-zero until now); sign bits likewise
+    k_pack_rows<<<(unsigned)((words + 255) / 256), 256, 0, c->stream>>>(dx, dz, r->m.rows + (size_t)2 * r->count * r->m.Wp, int(m), W, r->m.Wp, int(m), 0);
+    k_bytes_to_signs_at<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(ds, r->m.sgn, int(m), int(r->count));
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    r->count += m; r->c_valid = false;
+    return SK_OK;
+}
+extern "C" int32_t sk_commute_matrix_tile(sk_rows* r, int mode, uint64_t i0, uint64_t ni, uint64_t j0, uint64_t nj, uint64_t* out_bits) {
+    if (!r || (!out_bits && ni && nj)) return SK_EARG;
+    sk_ctx* c = r->ctx;
+    if (mode != 0 && mode != 1) SK_FAIL(c, SK_EARG, "commute_matrix_tile: mode must be 0 (general) or 1 (qubit-wise)");
+    if (i0 + ni > r->count || j0 + nj > r->count) SK_FAIL(c, SK_EDIM, "commute_matrix_tile: tile [%llu,+%llu) x [%llu,+%llu) outside the %llu rows", (unsigned long long)i0, (unsigned long long)ni, (unsigned long long)j0, (unsigned long long)nj, (unsigned long long)r->count);
+    if (ni == 0 || nj == 0) return SK_OK;
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    const size_t words = (nj + 63) / 64, total = ni * words;
+    rc = sk_ctx_reserve_tmp(c, total * 8 + 64);
+    if (rc) return rc;
+    u64* d_out = (u64*)c->d_tmp;
+    const size_t threads = total * 32;
+    k_commute_tile<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(r->m.rows, r->m.Wp, r->m.W, mode, int(i0), int(ni), int(j0), int(nj), int(words), d_out);
+    c->cnt.kernel_launches++;
+    c->cnt.pred_evals += ni * nj;
+    SK_CUDA(c, cudaGetLastError());
+    SK_CUDA(c, cudaMemcpyAsync(out_bits, d_out, total * 8, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
     return SK_OK;
 }
 extern "C" int32_t sk_rows_download(sk_rows* r, uint64_t* x, uint64_t* z, uint8_t* sign) {

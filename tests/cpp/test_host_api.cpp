@@ -108,6 +108,18 @@ static void gpu_checks() {
     std::vector<PauliString> rows = {PauliString::parse("ZZ"), PauliString::parse("ZI")};
     BitVec cv = commutation_vector(PauliString::parse("XX"), rows);
     CHECK(!cv.get(0) && cv.get(1));
+    // the same rows resident on the device: one upload, many vectors; append within the capacity (sk_rows_append)
+    { DeviceRows dr(2, rows, 3);
+      BitVec c1 = dr.commutation_vector(PauliString::parse("XX")), c2 = dr.commutation_vector(PauliString::parse("ZI"));
+      CHECK(!c1.get(0) && c1.get(1) && c2.count() == 0);
+      std::vector<PauliString> more = {PauliString::parse("XI")};
+      dr.append(more);
+      BitVec c3 = dr.commutation_vector(PauliString::parse("ZI"));
+      CHECK(dr.size() == 3 && c3.get(2) && c3.count() == 1);
+      CHECK(throws<DimensionError>([&] { dr.append(more); }));
+      CHECK(throws<DimensionError>([&] { dr.commutation_vector(PauliString::parse("XXX")); })); }
+    // EngineConfig.audit: the device checks the invariants of SPEC:111-116 after the run
+    { SimResult au = sim(surface_code_circuit(5, 2, true), EngineConfig{1, 3, true}); CHECK(!au.record.empty()); }
     // grouping
     std::vector<WeightedPauli> terms = {{1.0, PauliString::parse("ZZ")}, {0.9, PauliString::parse("XX")}, {0.5, PauliString::parse("ZI")}};
     GroupedHamiltonian gc = group_greedy(terms, GroupMode::GC), qwc = group_greedy(terms, GroupMode::QWC);

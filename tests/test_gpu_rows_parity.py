@@ -153,3 +153,108 @@ def test_transpile_default_matches_oracle_and_the_statevector(sk, ctx, orc):
     for n, G, pt in ((20, 2000, 0.2), (100, 4000, 0.1), (70, 3000, 0.4)):
         gates = rand_ct(np.random.default_rng(n + G + 1), n, G, pt)
         assert_same_pbc(sk.Pbc(ctx, sk.Circuit(n, gates)), orc.Pbc(n, gates, exact=True))
+
+
+# ---- BASELINE configs C4 / C5 at their stated size (SURVEY 8d generators: paper_2507_03092_b200/workloads.py) -----------------
+def test_c4_grouping_1e5_matches_oracle(sk, ctx, orc):
+    """Config C4 at N = 10^5 (the largest size the CPU oracle finishes in seconds): identical group ids, GC and QWC."""
+    from paper_2507_03092_b200 import workloads as wl
+    N = 100_000
+    x, z, _ = wl.c4_terms(N)
+    d = sk.Rows(ctx, 128, x, z); o = orc.Rows(128, x, z, np.zeros(N, np.uint8))
+    for mode in (0, 1):
+        g, ng = d.group_first_fit(mode)
+        og, ong, _ = o.group_first_fit(mode)
+        assert ng == ong and (g == og).all(), f"mode {mode}"
+        assert d.verify_grouping(mode, g) == 0
+    d.close()
+
+
+def test_c4_grouping_1e6_matches_golden(sk, ctx):
+    """Config C4 at its full size N = 10^6: the device's group ids against the checksum the CPU oracle produced once
+    (tools/make_c4_golden.py -> tests/golden/c4_groups_1000000.json; ~10-20 minutes of CPU per mode)."""
+    import hashlib, json, os
+    from paper_2507_03092_b200 import workloads as wl
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4_groups_1000000.json")
+    if not os.path.exists(path): pytest.skip("golden file not generated")
+    gold = json.load(open(path))
+    N = gold["N"]
+    x, z, _ = wl.c4_terms(N, gold["seed"])
+    d = sk.Rows(ctx, 128, x, z)
+    for mode, name in ((0, "GC"), (1, "QWC")):
+        g, ng = d.group_first_fit(mode)
+        g = np.ascontiguousarray(g, np.uint32)
+        assert ng == gold["modes"][name]["groups"], name
+        assert g[:16].tolist() == gold["modes"][name]["first16"] and g[-4:].tolist() == gold["modes"][name]["last4"], name
+        assert hashlib.sha256(g.tobytes()).hexdigest() == gold["modes"][name]["sha256"], name
+    d.close()
+
+
+def test_c5_transpile_1e5_matches_oracle(sk, ctx, orc):
+    """Config C5 at its full size: n = 1000, G = 10^5 gates, 10 % T: identical T layers, M_tab and statistics (exact form,
+    the default) and the published form of Algorithms 2-3."""
+    from paper_2507_03092_b200 import workloads as wl
+    gates = wl.c5_gates(1000, 100_000, gate_dtype=sk.GATE_DTYPE, kinds=(sk.H, sk.S, sk.CX, sk.T, sk.TDG))
+    circ = sk.Circuit(1000, gates)
+    assert abs(int(((gates["kind"] == sk.T) | (gates["kind"] == sk.TDG)).sum()) - 10_000) < 400
+    for exact in (True, False):
+        d = sk.Pbc(ctx, circ, exact=exact); o = orc.Pbc(1000, circ.gates, exact=exact)
+        assert_same_pbc(d, o)
+        d.close()
+
+
+def test_rows_append_and_commute_tile(sk, ctx, orc):
+    """sk_rows_append (T_tab grows row by row) and sk_commute_matrix_tile (pauli.cpp:117-140 over a tile of the pair
+    matrix) against the oracle's scalar predicates; appending beyond the capacity is SK_EDIM."""
+    rng = np.random.default_rng(8)
+    for n, m in ((5, 40), (130, 300), (128, 700)):
+        x, z, s = rand_rows(rng, n, m, 0.3)
+        d = sk.Rows(ctx, n, x[:m // 3], z[:m // 3], s[:m // 3], capacity=m)
+        d.append(x[m // 3:m - 7], z[m // 3:m - 7], s[m // 3:m - 7]); d.append(x[m - 7:], z[m - 7:], s[m - 7:])
+        assert d.count == m
+        dx, dz, ds = d.download()
+        assert (dx == x).all() and (dz == z).all() and (ds == s).all()
+        with pytest.raises(sk.DimensionError): d.append(x[:1], z[:1], s[:1])
+        W = x.shape[1]
+        for mode in (0, 1):
+            i0, ni, j0, nj = 3, min(37, m - 3), m // 4, m - m // 4
+            t = d.commute_tile(mode, i0, ni, j0, nj)
+            f = orc.lib().orc_commutes if mode == 0 else orc.lib().orc_qw_commutes
+            for a in (0, 5, ni - 1):
+                for b in (0, 1, 63, 64, 65, nj - 1):
+                    if b >= nj: continue
+                    ok = f(orc._p(x[i0 + a]), orc._p(z[i0 + a]), orc._p(x[j0 + b]), orc._p(z[j0 + b]), W)
+                    assert bool(t[a, b]) == (not ok), (n, mode, a, b)
+            # the whole tile through numpy: anticommutation parity / any overlap
+            v = (x[i0:i0 + ni, None, :] & z[None, j0:j0 + nj, :]) ^ (x[None, j0:j0 + nj, :] & z[i0:i0 + ni, None, :])
+            if mode == 0:
+                par = np.zeros((ni, nj), np.uint64)
+                for w in range(W):
+                    u = v[:, :, w].copy()
+                    for sh in (32, 16, 8, 4, 2, 1): u ^= u >> np.uint64(sh)
+                    par ^= u & np.uint64(1)
+                assert (t == (par == 1)).all()
+            else:
+                assert (t == (v != 0).any(axis=2)).all()
+        d.close()
+
+
+def test_tableau_audit_counts_violations(sk, ctx):
+    """sk_tableau_audit (EngineConfig.audit): 0 for tableaux the engine produced, the exact number of broken
+    row pairs after rows are tampered with."""
+    for circ in (sk.surface_code_circuit(7, 3, True), sk.random_layered_circuit(200, 4)):
+        t, _, _, _ = ctx.sim(circ, 5)
+        assert t.audit() == 0
+        x, z, r = t.download()
+        n = circ.n
+        x[0], z[0] = x[n].copy(), z[n].copy()            # stabilizer 0 := destabilizer 0: row 0 now commutes with its partner (1 pair broken),
+        t.upload(x, z, r)                                 # and anticommutes with whatever destabilizer 0 anticommuted with
+        bad = t.audit()
+        # expected count from the symplectic form on the host
+        def sym(a, b): return int(np.bitwise_xor.reduce([bin(int(v)).count("1") & 1 for v in ((x[a] & z[b]) ^ (x[b] & z[a]))]))
+        exp = 0
+        for b in range(1, 2 * n): exp += sym(0, b) != (1 if b == n else 0)
+        assert bad == exp and bad >= 1
+        t.close()
+    c = ctx.counters()
+    assert c["algorithmic_bytes"] > 0 and len(c["class_ms"]) == 3 and c["pred_evals"] >= 0

@@ -152,3 +152,24 @@ def test_algorithmic_bytes_formula_matches_the_oracles_copy(sk, orc):
     for n in (17, 1249, 10081):
         assert sk.algorithmic_bytes(n, cnt, fused_layers=5) == orc.algorithmic_bytes(n, cnt, fused_layers=5)
         assert sk.algorithmic_bytes(n, cnt) == orc.algorithmic_bytes(n, cnt)
+
+
+def test_workload_generators_follow_the_reference_stream():
+    """paper_2507_03092_b200/workloads.py restates SplitMix64 (proj/include/stabkit/rng.hpp:42-65) in vector form: pinned
+    against the oracle's sequential generator (itself pinned by the compiled reference, tests/test_oracle_golden.py) and
+    SURVEY 8c's known answers; C4 terms are sorted by |coeff| descending, C5 has ~10 % T gates."""
+    import importlib.util, os
+    import numpy as np
+    from oracle import oracle_py as orc
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("wl", os.path.join(root, "paper_2507_03092_b200", "workloads.py"))
+    wl = importlib.util.module_from_spec(spec); spec.loader.exec_module(wl)
+    raw = np.zeros(4096, np.uint64); orc.lib().orc_seq_fill(20250703, orc._p(raw), len(raw))
+    assert (wl.splitmix_stream(20250703, 4096) == raw).all()
+    assert [hex(int(v)) for v in wl.splitmix_stream(42, 4)] == ["0xbdd732262feb6e95", "0x28efe333b266f103", "0x47526757130f9f52", "0x581ce1ff0e4ae394"]
+    x, z, c = wl.c4_terms(2000)
+    assert x.shape == (2000, 2) and (np.abs(c[:-1]) >= np.abs(c[1:])).all() and (np.abs(c) < 1).all()
+    dt = np.dtype([("kind", "u1"), ("pad", "u1", 3), ("q0", "<u4"), ("q1", "<u4")])
+    g = wl.c5_gates(50, 4000, gate_dtype=dt, kinds=(0, 1, 6, 10, 11))
+    nt = int(((g["kind"] == 10) | (g["kind"] == 11)).sum())
+    assert 300 < nt < 500 and (g["q0"] < 50).all() and ((g["kind"] != 6) | (g["q0"] != g["q1"])).all()
