@@ -248,6 +248,21 @@ int32_t sk_pbc_layer_download(sk_pbc* p, uint64_t layer, uint64_t* x, uint64_t* 
 /* final M_tab, 2n rows row-major (measurement_rows are rows 0..n-1) */
 int32_t sk_pbc_mtab_download(sk_pbc* p, uint64_t* x, uint64_t* z, uint8_t* sign);
 
+/* ---- commutation grouping with the pair matrix sharded by row blocks ------
+ * Replaces nothing in the reference (single-process): it is the multi-GPU form of sk_group_first_fit.  Every
+ * shard holds the replicated rows and group assignment; per block of 1024 terms shard s of S evaluates the predicates
+ * (proj/src/pauli.cpp:117-140) against the groups of the bitmap words w with w % S == s, the driver ORs the shards' bitmaps
+ * (allreduce-SUM over disjoint words: ncclAllReduce / torch.distributed, or in process) and every shard resolves the block.
+ * Rows of at most 128 qubits (config C4).  d_bitmap: device buffer of sk_group_shard_bitmap_words() u32. */
+typedef struct sk_group_shard sk_group_shard;
+int32_t sk_group_shard_create(sk_rows* r, int mode, uint32_t shard, uint32_t nshards, sk_group_shard** out);
+void sk_group_shard_destroy(sk_group_shard* g);
+uint64_t sk_group_shard_blocks(const sk_group_shard* g);
+uint64_t sk_group_shard_bitmap_words(const sk_group_shard* g);
+int32_t sk_group_shard_conflicts(sk_group_shard* g, uint64_t block, uint32_t* d_bitmap);
+int32_t sk_group_shard_resolve(sk_group_shard* g, uint64_t block, uint32_t* d_bitmap);
+int32_t sk_group_shard_result(sk_group_shard* g, uint32_t* group_of, uint64_t* ngroups);
+
 /* ---- row sharding of one tableau across GPUs ------ */
 /* A shard owns the slots [slot_lo, slot_hi): stabilizer i AND destabilizer i for every i in the
  * range (the deterministic branch of SPEC:183 then needs no remote row).  One shard per GPU /

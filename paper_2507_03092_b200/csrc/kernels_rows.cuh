@@ -234,18 +234,20 @@ __device__ __forceinline__ bool conflict4(u64 ax0, u64 ax1, u64 az0, u64 az1, u6
 __global__ void __launch_bounds__(256)
 k_conflict_groups(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int Bt, const u32* __restrict__ ngroups,
                   const u32* __restrict__ off, const u64* __restrict__ gterms, int mode_, u32* __restrict__ bitmap, int GW32,
-                  unsigned long long* __restrict__ npred) {
+                  unsigned long long* __restrict__ npred, int shard = 0, int nshards = 1) {
     extern __shared__ u64 s_blk[];          // [Bt][4]: x0 x1 z0 z1 of each staged block term
     const int mode = mode_ & 0xff;
     const u32 ng = *ngroups;
-    if (blockIdx.x * blockDim.x >= ng) return;                 // the grid is sized for the worst case (one group per term)
+    // Sharding by row blocks of the pair matrix: shard s of S owns the bitmap WORDS w with w % S == s, i.e. the groups
+    // 32w .. 32w+31; its warps are dense over those words.  S == 1 is the plain kernel.
+    if ((size_t)blockIdx.x * blockDim.x * nshards >= ng) return;                 // the grid is sized for the worst case (one group per term)
     const int tb = t0 + blockIdx.y * Bt;
     for (int i = threadIdx.x; i < Bt * 4; i += blockDim.x) {
         const int k = i >> 2, w = i & 3, t = tb + k;
         s_blk[i] = (t < t0 + B && (w & 1) < W) ? rows[(size_t)(2 * t + (w >> 1)) * Wp + (w & 1)] : 0ull;
     }
     __syncthreads();
-    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 g = 32u * (((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * u32(nshards) + u32(shard)) + (threadIdx.x & 31u);
     const bool live = g < ng;
     const u32 start = live ? off[g] : 0u, cnt = live ? off[g + 1] - start : 0u;
     // first four members in registers; an all-zero (absent) member conflicts with nothing

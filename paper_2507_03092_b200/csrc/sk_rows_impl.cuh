@@ -403,6 +403,104 @@ extern "C" int32_t sk_group_first_fit(sk_rows* r, int mode, uint32_t* group_of, 
     return rc;
 }
 
+// ---- first fit with the pair matrix sharded by row blocks (north_star "Commutation grouping shards the pair matrix
+// by row blocks").  Every shard holds the replicated input and the replicated group assignment; the conflict bitmap of a block
+// of 1024 terms against the placed groups -- where the predicate evaluations are -- is split: shard s of S evaluates the groups
+// of the bitmap words w with w % S == s.  The driver (paper_2507_03092_b200/group_sharded.py: torch.distributed / NCCL, or several
+// shards in one process) ORs the shards' bitmaps -- an allreduce-SUM, the words are disjoint -- and every shard then resolves the
+// block itself (the resolver is sequential in the term index and deterministic: identical assignments everywhere).
+struct sk_group_shard {
+    sk_ctx* ctx = nullptr; sk_rows* rows = nullptr;
+    int mode = 0, shard = 0, nshards = 1, count = 0, B = 0, GW32 = 0;
+    u32 *d_group = nullptr, *d_ng = nullptr, *d_ff = nullptr, *d_cnt = nullptr, *d_off = nullptr, *d_fillc = nullptr, *d_gmin = nullptr;
+    u64* d_gterms = nullptr;
+    uint64_t next_block = 0;
+};
+extern "C" void sk_group_shard_destroy(sk_group_shard* g) {
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    for (void* p : {(void*)g->d_group, (void*)g->d_ng, (void*)g->d_cnt, (void*)g->d_off, (void*)g->d_fillc, (void*)g->d_gterms}) if (p) cudaFree(p);
+    delete g;
+}
+extern "C" int32_t sk_group_shard_create(sk_rows* r, int mode, uint32_t shard, uint32_t nshards, sk_group_shard** out) {
+    if (!r || !out || (mode != 0 && mode != 1)) return SK_EARG;
+    *out = nullptr;
+    sk_ctx* c = r->ctx;
+    if (nshards == 0 || shard >= nshards) SK_FAIL(c, SK_EARG, "group shard %u of %u", shard, nshards);
+    if (r->count == 0) SK_FAIL(c, SK_EARG, "group_greedy: empty input (SPEC:448)");
+    if (r->m.W > 2) SK_FAIL(c, SK_EUNSUPPORTED, "sharded grouping uses the group-major conflict kernel: rows of at most 128 qubits (BASELINE config 4), got %llu", (unsigned long long)r->n);
+    int32_t rc = rows_need_r(r);
+    if (rc) return rc;
+    sk_group_shard* g = new sk_group_shard();
+    g->ctx = c; g->rows = r; g->mode = mode; g->shard = int(shard); g->nshards = int(nshards);
+    g->count = int(r->count); g->B = std::min(g->count, 1024); g->GW32 = g->count / 32 + 2;
+    const size_t n = size_t(g->count);
+    cudaError_t e = cudaMalloc(&g->d_group, n * 4);
+    if (!e) e = cudaMalloc(&g->d_ng, 4 + (size_t)g->B * 4);
+    if (!e) e = cudaMalloc(&g->d_cnt, (n + 4) * 4);
+    if (!e) e = cudaMalloc(&g->d_off, (n + 2) * 4);
+    if (!e) e = cudaMalloc(&g->d_fillc, (n + 2) * 4);
+    if (!e) e = cudaMalloc(&g->d_gterms, n * 32);
+    if (e) { sk_group_shard_destroy(g); SK_FAIL(c, SK_ECUDA, "cudaMalloc failed for a grouping shard: %s", cudaGetErrorString(e)); }
+    g->d_ff = g->d_ng + 1; g->d_gmin = g->d_cnt + n + 3;
+    cudaMemsetAsync(g->d_ng, 0, 4, c->stream); cudaMemsetAsync(g->d_cnt, 0, (n + 4) * 4, c->stream);
+    *out = g;
+    return SK_OK;
+}
+extern "C" uint64_t sk_group_shard_blocks(const sk_group_shard* g) { return g ? uint64_t((g->count + g->B - 1) / g->B) : 0; }
+/* u32 words of one block's conflict bitmap: rows of GW32 words, one row per block term */
+extern "C" uint64_t sk_group_shard_bitmap_words(const sk_group_shard* g) { return g ? uint64_t(g->B) * uint64_t(g->GW32) : 0; }
+/* Conflicts of block k's terms with the groups this shard owns, into d_bitmap (device, bitmap_words u32, zeroed here). */
+extern "C" int32_t sk_group_shard_conflicts(sk_group_shard* g, uint64_t block, uint32_t* d_bitmap) {
+    if (!g || !d_bitmap) return SK_EARG;
+    sk_ctx* c = g->ctx;
+    if (block != g->next_block) SK_FAIL(c, SK_EARG, "grouping shard: block %llu out of order (next is %llu)", (unsigned long long)block, (unsigned long long)g->next_block);
+    const int t0 = int(block) * g->B;
+    if (t0 >= g->count) SK_FAIL(c, SK_EARG, "grouping shard: block %llu beyond the input", (unsigned long long)block);
+    const int b = std::min(g->B, g->count - t0);
+    const DMat& m = g->rows->m;
+    SK_CUDA(c, cudaMemsetAsync(d_bitmap, 0, (size_t)g->B * g->GW32 * 4, c->stream));
+    if (t0 > 0) {
+        const int Btg = std::min(g->B, 128);
+        SK_CUDA(c, cudaMemsetAsync(g->d_gmin, 0xff, 4, c->stream));
+        k_csr_count<<<(g->B + 255) / 256, 256, 0, c->stream>>>(g->d_group, t0 - g->B, t0, g->d_cnt, g->d_gmin);
+        k_csr_scan<<<1, 1024, 0, c->stream>>>(g->d_cnt, g->d_ng, g->d_off, g->d_gmin);
+        SK_CUDA(c, cudaMemsetAsync(g->d_fillc, 0, ((size_t)t0 + 1) * 4, c->stream));
+        k_csr_fill<<<(t0 + 255) / 256, 256, 0, c->stream>>>(m.rows, m.Wp, m.W, g->d_group, t0, g->d_off, g->d_fillc, g->d_gterms);
+        dim3 grid(((t0 + g->nshards - 1) / g->nshards + 255) / 256 + 1, (b + Btg - 1) / Btg);
+        k_conflict_groups<<<grid, 256, (size_t)Btg * 32, c->stream>>>(m.rows, m.Wp, m.W, t0, b, Btg, g->d_ng, g->d_off, g->d_gterms, g->mode, d_bitmap, g->GW32,
+                                                                     reinterpret_cast<unsigned long long*>(c->d_err) + 1, g->shard, g->nshards);
+        c->cnt.kernel_launches += 4;
+    }
+    SK_CUDA(c, cudaGetLastError());
+    return SK_OK;
+}
+/* First fit of block k given the COMBINED bitmap (all shards' words OR-ed together); every shard runs it and gets the same groups. */
+extern "C" int32_t sk_group_shard_resolve(sk_group_shard* g, uint64_t block, uint32_t* d_bitmap) {
+    if (!g || !d_bitmap) return SK_EARG;
+    sk_ctx* c = g->ctx;
+    if (block != g->next_block) SK_FAIL(c, SK_EARG, "grouping shard: block %llu out of order (next is %llu)", (unsigned long long)block, (unsigned long long)g->next_block);
+    const int t0 = int(block) * g->B, b = std::min(g->B, g->count - t0);
+    const DMat& m = g->rows->m;
+    k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, g->GW32, g->d_ng, g->d_ff);
+    k_first_fit_threads<<<1, 1024, 0, c->stream>>>(m.rows, m.Wp, m.W, t0, b, g->mode, d_bitmap, g->GW32, g->d_group, g->d_ng, g->d_ff);
+    c->cnt.kernel_launches += 2;
+    SK_CUDA(c, cudaGetLastError());
+    g->next_block++;
+    return SK_OK;
+}
+extern "C" int32_t sk_group_shard_result(sk_group_shard* g, uint32_t* group_of, uint64_t* ngroups) {
+    if (!g || !group_of || !ngroups) return SK_EARG;
+    sk_ctx* c = g->ctx;
+    if (g->next_block != sk_group_shard_blocks(g)) SK_FAIL(c, SK_EARG, "grouping shard: %llu of %llu blocks resolved", (unsigned long long)g->next_block, (unsigned long long)sk_group_shard_blocks(g));
+    u32 ng = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&ng, g->d_ng, 4, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(group_of, g->d_group, (size_t)g->count * 4, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    *ngroups = ng;
+    return SK_OK;
+}
+
 extern "C" int32_t sk_verify_grouping(sk_rows* r, int mode, const uint32_t* group_of, uint64_t* nviolations) {
     if (!r || !group_of || !nviolations || (mode != 0 && mode != 1)) return SK_EARG;
     sk_ctx* c = r->ctx;

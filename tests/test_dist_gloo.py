@@ -111,3 +111,35 @@ def test_world_size_2_gloo_row_sharded_protocol():
         print("rank", rank, "ok")
     """ % ROOT)
     _run_two_ranks(script)
+
+
+def test_world_size_2_gloo_grouping_sharded_by_row_blocks():
+    """SURVEY 8e, second row: the grouping driver (paper_2507_03092_b200/group_sharded.py) over a real 2-rank process group --
+    2 ranks x 2 local shards = 4 global shards, each evaluating the predicates of its own bitmap words; the block bitmaps are
+    OR-combined by an allreduce-SUM; every shard resolves the block itself.  Per-shard arithmetic is tests/group_shard_stub.py
+    here (no GPU in this container; the CUDA shards run the same driver in tests/test_gpu_sharded.py).  Groups == oracle."""
+    script = textwrap.dedent("""
+        import os, sys
+        sys.path.insert(0, %r)
+        import numpy as np
+        from paper_2507_03092_b200 import dist
+        from paper_2507_03092_b200.group_sharded import GroupExchange, group_first_fit_sharded
+        from tests.group_shard_stub import StubGroupShard
+        from oracle import oracle_py as orc
+        rank, local_rank, world = dist.init("gloo")
+        rng = np.random.default_rng(3)                   # same input on every rank (the term list is replicated)
+        for n, m, mode in ((128, 2600, 0), (128, 2100, 1), (20, 1500, 0)):
+            W = (n + 63) // 64
+            x = rng.integers(0, 1 << 62, (m, W), dtype=np.uint64); z = rng.integers(0, 1 << 62, (m, W), dtype=np.uint64)
+            if n < 64: x &= np.uint64((1 << n) - 1); z &= np.uint64((1 << n) - 1)
+            ex = GroupExchange(2)
+            assert ex.nshards == 4
+            shards = [StubGroupShard(x, z, mode, ex.rank * 2 + l, ex.nshards) for l in range(2)]
+            g, ng = group_first_fit_sharded(shards, ex)
+            og, ong, _ = orc.Rows(n, x, z, np.zeros(m, np.uint8)).group_first_fit(mode)
+            assert ng == ong and (g == og).all(), (n, m, mode, ng, ong)
+            assert ex.calls == shards[0].blocks
+        dist.finalize()
+        print("rank", rank, "ok")
+    """ % ROOT)
+    _run_two_ranks(script)

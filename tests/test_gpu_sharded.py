@@ -127,3 +127,28 @@ def test_two_processes_one_shard_each_over_a_process_group(sk, orc):
     outs = [p.communicate(timeout=280)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
     assert "rank 0 ok" in outs[0] and "rank 1 ok" in outs[1], outs
+
+
+@pytest.mark.parametrize("local", [1, 2, 3, 4])
+def test_grouping_sharded_by_row_blocks(sk, ctx, orc, local):
+    """SURVEY 8e, second row: first fit with the pair matrix sharded by row blocks (sk_group_shard_*; shard s evaluates the
+    groups of the bitmap words w % S == s); S local shards on one device, bitmaps OR-ed in process.  Groups identical to the
+    oracle and to the unsharded sk_group_first_fit, GC and QWC."""
+    from paper_2507_03092_b200.group_sharded import group_first_fit_cuda
+    rng = np.random.default_rng(17 + local)
+    for n, m, dens in ((128, 6000, 0.5), (128, 3000, 0.03), (40, 2500, 0.3)):
+        W = (n + 63) // 64
+        bits = rng.random((2, m, n)) < dens
+        x = np.zeros((m, W), np.uint64); z = np.zeros((m, W), np.uint64)
+        for q in range(n):
+            x[:, q >> 6] |= bits[0, :, q].astype(np.uint64) << np.uint64(q & 63); z[:, q >> 6] |= bits[1, :, q].astype(np.uint64) << np.uint64(q & 63)
+        rows = sk.Rows(ctx, n, x, z); o = orc.Rows(n, x, z, np.zeros(m, np.uint8))
+        for mode in (0, 1):
+            (g, ng), ex = group_first_fit_cuda(rows, mode, local_shards=local, device_index=0)
+            og, ong, _ = o.group_first_fit(mode)
+            assert ng == ong and (g == og).all(), (n, m, mode)
+            g1, ng1 = rows.group_first_fit(mode)
+            assert ng1 == ng and (g1 == g).all()
+        rows.close()
+    wide = sk.Rows(ctx, 200, np.ones((4, 4), np.uint64), np.zeros((4, 4), np.uint64))
+    with pytest.raises(sk.UnsupportedError): group_first_fit_cuda(wide, 0, local_shards=2, device_index=0)
