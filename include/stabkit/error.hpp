@@ -28,12 +28,13 @@ class DimensionError : public Error { public: using Error::Error; };     // size
 class UnsupportedError : public Error { public: using Error::Error; };   // valid construct, wrong code path
 class InvariantError : public Error { public: using Error::Error; };     // internal consistency failure
 
-// sk_status -> exception (1 EDIM, 2 EUNSUPPORTED, 3 EINVARIANT, 6 EPARSE, anything else Error)
+// sk_status -> exception (1 EDIM, 2 EUNSUPPORTED, 3 EINVARIANT, 5 ENCCL -> Error, 6 EPARSE, anything else Error)
 [[noreturn]] inline void throw_status(int code, const std::string& message) {
     switch (code) {
         case 1: throw DimensionError(message);
         case 2: throw UnsupportedError(message);
         case 3: throw InvariantError(message);
+        case 5: throw Error("NCCL: " + message);            // SK_ENCCL (stabkit/nccl_exchange.hpp)
         case 6: throw ParseError(0, message);
         default: throw Error(message);
     }

@@ -78,6 +78,28 @@ def build_host(force: bool = False) -> str | None:
     return tbin
 
 
+def build_nccl_test(force: bool = False) -> str | None:
+    """tests/cpp/test_nccl_exchange: the row-sharded tableau over stabkit::NcclExchange (links the system NCCL + cudart).
+    Returns None when nccl.h is not installed."""
+    tsrc = os.path.join(ROOT, "tests", "cpp", "test_nccl_exchange.cpp")
+    tbin = os.path.join(ROOT, "tests", "cpp", "test_nccl_exchange")
+    cuda_inc = "/usr/local/cuda/include"
+    if not os.path.exists(tsrc) or not any(os.path.exists(os.path.join(p, "nccl.h")) for p in ("/usr/include", cuda_inc)):
+        return None
+    inc = os.path.join(ROOT, "include", "stabkit")
+    deps = [tsrc, LIB, os.path.join(ROOT, "include", "stabkit_b200.h")] + [os.path.join(inc, f) for f in os.listdir(inc)]
+    if force or _stale(tbin, deps):
+        cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", cuda_inc, "-o", tbin, tsrc,
+               "-L", PKG, "-lstabkit_b200", "-L", "/usr/local/cuda/lib64", "-lcudart", "-lnccl",
+               f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_2507_03092_b200", "-Wl,-rpath,/usr/local/cuda/lib64"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("g++ failed building tests/cpp/test_nccl_exchange")
+    return tbin
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
     print(build_host(force="--force" in sys.argv))
+    print(build_nccl_test(force="--force" in sys.argv))

@@ -42,3 +42,18 @@ def test_cpp_host_api_cpu(binary):
 def test_cpp_host_api_gpu(binary):
     r = subprocess.run([binary, "gpu"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_row_sharded_tableau_over_nccl(sk):
+    """stabkit::NcclExchange (include/stabkit/nccl_exchange.hpp): the C++ ShardedTableau driver with its three exchanges as
+    ncclAllReduce(min) / ncclBroadcast / ncclAllGather on the library stream.  This box has one GPU, so the communicator has
+    one rank (NCCL refuses two ranks on a device) x 3 local shards; tests/cpp/test_nccl_exchange.cpp documents the
+    one-process-per-GPU launch.  Record and rows must equal the unsharded engine; an NCCL error must surface as stabkit::Error."""
+    from paper_2507_03092_b200 import _build
+    path = _build.build_nccl_test()
+    if path is None:
+        pytest.skip("nccl.h not installed")
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", NCCL_DEBUG="WARN")
+    r = subprocess.run([path, "7", "3", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0 and "rank 0 ok" in r.stdout and "record ok rows ok" in r.stdout, r.stdout + r.stderr
