@@ -33,6 +33,12 @@ __device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulon
 // (Measured, round 2: batching the first loads of up to four independent gates per thread -- 2 dependent round trips per batch
 // instead of 2 per gate -- is SLOWER, 17-23 us against 10-12 us per d=71 layer: 114 registers cut the resident warps 4x and the
 // kernel is L2-bandwidth bound (about 44 MB of sector traffic per CX layer), not latency bound.  Kept as is.)
+// (Measured, round 2 as well: a NONZERO MAP of the gate form -- one bit per 128-row vector of a column, kept exact by every store,
+// consulted by this kernel, by the C -> R transpose and rebuilt by the in-kernel R -> C -- cuts the DRAM reads of a d=71 layer from
+// 8.7 MB to 0.8 MB and those of the stabilizer-half transpose from 22.7 MB to 5 MB, and makes both SLOWER: layers 13-20 us against
+// 10-12 us (map words prefetched one gate ahead, warp-owned words without atomics, grid sized to one resident wave: all tried),
+// the transpose 28 us against 20 us.  Neither kernel is DRAM bound: each is bound by its chain of dependent accesses, and the
+// map lookup lengthens that chain.  Reverted; bit-exact while it existed.)
 // gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb), or [block_off[b], block_off[b+1]) when the host
 // supplies chunk boundaries; thread v owns 128-bit row-vector v of every column it visits.
 // Merged layers: a launch may hold several consecutive layers provided every set of gates that share qubits (a
