@@ -43,6 +43,13 @@ __device__ __forceinline__ u32 ld_acquire(const u32* p) {
     u32 v; asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
 }
 
+// ---- programmatic dependent launch (sm_90+): a kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may be
+// scheduled while its predecessor in the stream still runs; pdl_wait() blocks until the predecessor has completed and its writes
+// are visible (a no-op for a normal launch), pdl_trigger() lets the successor start being scheduled.  Hides the launch latency
+// between the small dependent kernels of a Clifford run.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- rng (ref: proj/include/stabkit/rng.hpp:23-39) ---------------------------
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;

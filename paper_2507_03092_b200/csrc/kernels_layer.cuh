@@ -47,6 +47,8 @@ __device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulon
 __global__ void __launch_bounds__(256)
 k_layer(u64* __restrict__ cols, u64* __restrict__ sgn, const sk_gate* __restrict__ gates,
         int ngates, int RW, int gpb, const u32* __restrict__ block_off) {
+    pdl_trigger();
+    pdl_wait();
     const int g0 = block_off ? int(block_off[blockIdx.x]) : blockIdx.x * gpb;
     const int g1 = block_off ? int(block_off[blockIdx.x + 1]) : min(ngates, g0 + gpb);
     const int RW2 = RW >> 1;

@@ -77,10 +77,10 @@ struct MeasWs {
     u32 progress;       // panel mode: factorisation steps published so far in this launch (monotone)
     u32 r0[4];          // per-wave ~index of the first random measurement (0 = none), max-reduced; 3 slots rotate
     u32 exitcnt;        // CTAs that have left the kernel: the last one re-zeroes this block for the next launch
-    u32 pad0;
+    u32 wdone;          // k_wave: CTAs that have finished (its last CTA does the accounting and re-zeroes this word and r0[3])
     // ---- persistent
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
-    u32 pad1;
+    u32 wpos;           // k_wave -> k_measure_block: measurements [0, wpos) of the block are done (deterministic prefix)
     u64 n_rand, n_det, k_rand, k_det, waves;
     u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
     u64 panels;
@@ -129,6 +129,7 @@ struct MeasArgs {
     int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
     int lv_enable;      // replicated level-form panel path (kernels_panel.cuh); SK_PANEL_REPL=0 disables
+    int from_wave;      // k_wave ran first: start at ws->wpos
     int seq_rows;       // SK_PANEL_SEQ=1: step-by-step row-form factorisation instead of the level form (A/B and testing aid)
 };
 
@@ -1108,12 +1109,17 @@ __device__ __forceinline__ int warp_mul_wide(const u64* __restrict__ base, int W
 // is empty -- K4, the product of the partner stabilizers (destabilizer half of the same column -> rows of the R form).
 // Results per slot go to recj/recn (measurement index or -1, partner count | odd-phase flag << 30); products with more than
 // kWarpList partners are left to the whole CTA (slot pushed to heavy[]).
+// grec != nullptr (k_wave): the records go to grec[j] (0x80000000 = not a finished deterministic measurement), the index of the first
+// random -- or too long -- measurement to *r0slot, and nothing is left to the CTA.
+// (a template so that each calling kernel gets a copy compiled for its own register budget)
+template <int KERNEL>
 __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u32 wave, int gw, int GW, u32* wlist, int* nheavy, int* heavy,
-                                        int* recj, int* recn, u64* acc_x, u64* acc_z) {
+                                        int* recj, int* recn, u64* acc_x, u64* acc_z, u32* grec = nullptr, u32* r0slot = nullptr) {
     const int lane = threadIdx.x & 31;
     const int W = a.m.W, Wp = a.m.Wp, RW = a.m.RW;
     const int nwl = (W + 31) / 32;
-    if (lane < kSlotsPerWarp) recj[lane] = -1;
+    if (!grec && lane < kSlotsPerWarp) recj[lane] = -1;
+    if (!r0slot) r0slot = &a.ws->r0[wave % 3];
     __syncwarp();
     int rec = 0;
     const bool trc = a.prof && lane == 0 && (gw == 0 || gw == GW / 2) && pos == 0;
@@ -1152,8 +1158,8 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
         piv = warp_min(piv);
         __syncwarp();
         WV_TRACE(1);
-        if (piv != 0xffffffffu) {       // random: the first one of the window ends the deterministic prefix
-            if (lane == 0) atomicMax(&a.ws->r0[wave % 3], ~(u32)j);      // stored inverted: zero-initialised, max = smallest index
+        if (piv != 0xffffffffu || (grec && (npart > kWarpList || nwl > 6))) {       // random: the first one of the window ends the deterministic prefix
+            if (lane == 0) { atomicMax(r0slot, ~(u32)j); if (grec) grec[j] = 0x80000000u; }      // stored inverted: zero-initialised, max = smallest index
             continue;
         }
         if (npart > kWarpList) {                  // tree-reduced by the whole CTA
@@ -1175,9 +1181,48 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
         WV_TRACE(3);
         if (lane == 0) {
             a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
-            if (rec < kSlotsPerWarp) { recj[rec] = j; recn[rec] = npart | ((e & 1) << 30); }
+            if (grec) grec[j] = u32(npart) | (u32(e & 1) << 30);
+            else if (rec < kSlotsPerWarp) { recj[rec] = j; recn[rec] = npart | ((e & 1) << 30); }
         }
         __syncwarp();
+    }
+}
+
+
+// Wave mode as a kernel of its own (launched in front of k_measure_block for long measurement blocks): an ordinary grid with
+// one warp per pending measurement instead of the one-CTA-per-SM cooperative grid whose warps walk three slots each, so the
+// deterministic rounds of a memory experiment are one short pass.  Speculative like the in-kernel wave: every slot is evaluated,
+// the last CTA to finish finds the first random (or too long) measurement r0, accounts for [0, r0) and leaves r0 in ws->wpos;
+// k_measure_block then starts there (and exits at once when the whole block was deterministic).
+constexpr int kWaveThreads = 256;
+__global__ void __launch_bounds__(kWaveThreads, 3)
+k_wave(const __grid_constant__ MeasArgs a, int wend) {
+    __shared__ u32 s_wlist[kWaveThreads / 32][kWarpList];
+    __shared__ int s_last, s_dummy[2];
+    __shared__ unsigned long long s_kd;
+    __shared__ u32 s_odd;
+    MeasWs* ws = a.ws;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    wave_slots<1>(a, 0, wend, 0, blockIdx.x * (kWaveThreads / 32) + warp, gridDim.x * (kWaveThreads / 32), s_wlist[warp], &s_dummy[0], &s_dummy[1],
+               nullptr, nullptr, nullptr, nullptr, a.wpiv, &ws->r0[3]);
+    __syncthreads();
+    if (tid == 0) { __threadfence(); s_last = atomicAdd(&ws->wdone, 1u) == gridDim.x - 1 ? 1 : 0; s_kd = 0; s_odd = 0; }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const u32 r0 = ~__ldcg(&ws->r0[3]);
+    const int dend = (r0 == 0xffffffffu) ? wend : int(r0);
+    unsigned long long kd = 0; u32 odd = 0;
+    for (int j = tid; j < dend; j += kWaveThreads) { const u32 r = __ldcg(a.wpiv + j); kd += r & 0x3fffffffu; odd |= (r >> 30) & 1u; }
+    kd = (unsigned long long)__reduce_add_sync(0xffffffffu, (u32)kd);
+    odd = __reduce_or_sync(0xffffffffu, odd);
+    if ((tid & 31) == 0) { atomicAdd(&s_kd, kd); if (odd) atomicOr(&s_odd, 1u); }
+    __syncthreads();
+    if (tid == 0) {
+        if (dend > 0) { atomicAdd(&ws->n_det, (u64)dend); atomicAdd(&ws->k_det, (u64)s_kd); }
+        atomicAdd(&ws->waves, 1ull);
+        if (s_odd) atomicOr(&ws->err, 1u);
+        ws->wpos = u32(dend); ws->r0[3] = 0u; ws->wdone = 0u;
     }
 }
 
@@ -1217,7 +1262,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
     u64* acc_z = acc_x + Wp;
 
-    int pos = 0;
+    int pos = a.from_wave ? int(__ldcg(&ws->wpos)) : 0;        // k_wave already finished the deterministic prefix of the block
     u32 wave = 1;
     bool panel_mode = false;
     u64 t_prof = a.prof ? gtime() : 0;
@@ -1230,7 +1275,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0u;
         if (tid == 0) s_nheavy = 0;
         __syncthreads();
-        wave_slots(a, pos, wend, wave, gw, GW, s_wlist[warp], &s_nheavy, s_heavy, s_recj[warp], s_recn[warp], acc_x, acc_z);
+        wave_slots<0>(a, pos, wend, wave, gw, GW, s_wlist[warp], &s_nheavy, s_heavy, s_recj[warp], s_recn[warp], acc_x, acc_z);
         __syncthreads();
         const int nheavy = s_nheavy;
         for (int h = 0; h < nheavy; ++h) {

@@ -25,6 +25,8 @@ k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, i
                  size_t src_zoff, size_t dst_zoff, const u32* __restrict__ flag) {
     __shared__ u32 tin[256][9];    // [src row in tile][word], +1 pad: conflict-free column reads
     __shared__ u32 tout[256][9];   // [dst row in tile][word]
+    pdl_trigger();
+    pdl_wait();
     if (flag && __ldcg(flag) == 0u) return;
     src += (size_t)blockIdx.z * src_zoff; dst += (size_t)blockIdx.z * dst_zoff;
     const int c0 = blockIdx.x * 256;          // first src row of the tile  (= dst bit offset)

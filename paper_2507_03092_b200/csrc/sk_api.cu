@@ -43,6 +43,8 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (const char* e = getenv("SK_ROW_CAP")) c->row_cap = atoi(e);
     if (const char* e = getenv("SK_PANEL_COLUMNS")) c->force_columns = atoi(e);
     if (const char* e = getenv("SK_PANEL_SEQ")) c->seq_rows = atoi(e);
+    if (const char* e = getenv("SK_PDL")) c->pdl = atoi(e);
+    if (const char* e = getenv("SK_WAVE_KERNEL")) c->no_wave_kernel = atoi(e) == 0;
     if (const char* e = getenv("SK_PANEL_REPL")) c->no_repl = atoi(e) == 0;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
@@ -127,6 +129,12 @@ static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int s
                                 u32* dst, size_t dstride, int drows, int dwords,
                                 size_t src_zoff, size_t dst_zoff, const u32* flag) {
     dim3 grid((srows + 255) / 256, (swords + 7) / 8, 2);
+    if (c->pdl) {
+        cudaLaunchConfig_t cfg = {}; cfg.gridDim = grid; cfg.blockDim = dim3(256); cfg.stream = c->stream;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization; at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        SK_CUDA(c, cudaLaunchKernelEx(&cfg, k_transpose_bits, src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag));
+    } else
     k_transpose_bits<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
@@ -349,13 +357,19 @@ static int layer_target_ctas(const sk_ctx* c, int threads) { return c->num_sms *
 static void launch_layer(sk_tableau* t, const sk_gate* d_gates, int ngates, const u32* d_boff = nullptr, int nblocks = 0, int nlayers = 1) {
     sk_ctx* c = t->ctx;
     const int threads = layer_threads(t);
-    if (d_boff) k_layer<<<nblocks, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, 0, d_boff);
-    else {
+    int grid = nblocks, gpb = 0;
+    if (!d_boff) {
         const int target_ctas = layer_target_ctas(c, threads);
-        const int gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
-        const int grid = (ngates + gpb - 1) / gpb;
-        k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb, nullptr);
+        gpb = std::max(1, (ngates + target_ctas - 1) / target_ctas);
+        grid = (ngates + gpb - 1) / gpb;
     }
+    if (c->pdl) {       // the launch may be scheduled while the previous layer still runs (griddepcontrol.wait inside the kernel)
+        cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(grid); cfg.blockDim = dim3(threads); cfg.stream = c->stream;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization; at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_layer, t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb, d_boff) != cudaSuccess) { c->err = "k_layer launch failed"; }
+    } else
+    k_layer<<<grid, threads, 0, c->stream>>>(t->m.cols, t->m.sgn, d_gates, ngates, t->RW, gpb, d_boff);
     c->cnt.kernel_launches++; c->cnt.layers += (uint64_t)nlayers;
     c->last_n = t->n;
     t->r_valid = false;
@@ -447,6 +461,19 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
     a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.tbits = t->d_tbits; a.tcap = t->tcap; a.fold = c->no_fold ? 0 : 1; a.row_cap = c->row_cap > 0 ? std::min(c->row_cap, kRowCap) : kRowCap; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
     a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.lv_enable = (t->lv_ok && !c->no_repl && !c->force_columns && !c->seq_rows) ? 1 : 0; a.destab_stale = t->r_destab_stale ? 1 : 0;
+    a.from_wave = 0;
+    const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
+    if (!c->no_wave_kernel && count >= 2048) {
+        // long blocks: the deterministic prefix (all of it in rounds 2..d of a memory experiment) by an ordinary one-warp-per-
+        // measurement grid first; the cooperative kernel continues at ws->wpos
+        const int wend = int(std::min<size_t>((size_t)count, 2 * window));      // (d_wpiv holds the slot records)
+        static int wave_per_sm = 0;
+        if (wave_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wave_per_sm, k_wave, kWaveThreads, 0) != cudaSuccess || wave_per_sm < 1)) wave_per_sm = 2;
+        const int grid = std::max(1, std::min((wend + kWaveThreads / 32 - 1) / (kWaveThreads / 32), c->num_sms * wave_per_sm));
+        k_wave<<<grid, kWaveThreads, 0, c->stream>>>(a, wend);
+        c->cnt.kernel_launches++;
+        a.from_wave = 1;
+    }
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;

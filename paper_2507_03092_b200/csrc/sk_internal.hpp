@@ -21,6 +21,8 @@ struct sk_ctx {
     int no_fold = 0;                        // SK_NO_FOLD=1: the measurement kernel gathers every panel in a phase of its own
     int row_cap = 0;                        // SK_ROW_CAP=<k>: row-form factorisation only up to k active rows (tests: exercises the regather path)
     uint64_t tableau_uid = 0;
+    int pdl = 1;                            // programmatic dependent launch of the layer and transpose kernels (SK_PDL=0 disables)
+    int no_wave_kernel = 0;                 // SK_WAVE_KERNEL=0: wave mode only inside the cooperative measurement kernel
     int no_repl = 0;                        // SK_PANEL_REPL=0: panel mode without the replicated level-form path (general path only)
     int seq_rows = 0;                       // SK_PANEL_SEQ=1: step-by-step row-form panel factorisation instead of the level form
     int force_columns = 0;                  // SK_PANEL_COLUMNS=1: column-form panel factorisation only (testing aid)
