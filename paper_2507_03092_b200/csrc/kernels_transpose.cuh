@@ -14,11 +14,79 @@ __device__ __forceinline__ void bfly(u32& v, int j, u32 m, int lane) {
     const u32 p = __shfl_xor_sync(0xffffffffu, v, j);
     v = (lane & j) ? (((p >> j) & m) | (v & ~m)) : ((v & m) | ((p & m) << j));
 }
+// 32x32-bit transpose across a warp (lane = row).  The two coarse stages exchange whole bytes: one byte permute each instead
+// of shift/mask/merge (the kernel is instruction bound: ncu, 58 % SM throughput at 86 % active warps).
+__device__ __forceinline__ u32 transpose32(u32 v, int lane) {
+    u32 p = __shfl_xor_sync(0xffffffffu, v, 16);
+    v = __byte_perm(v, p, (lane & 16) ? 0x3276u : 0x5410u);      // halves:  low lanes keep v.lo | p.lo << 16, high lanes p.hi >> 16 | v.hi
+    p = __shfl_xor_sync(0xffffffffu, v, 8);
+    v = __byte_perm(v, p, (lane & 8) ? 0x3715u : 0x6240u);       // bytes of each half
+    bfly(v, 4, 0x0f0f0f0fu, lane); bfly(v, 2, 0x33333333u, lane); bfly(v, 1, 0x55555555u, lane);
+    return v;
+}
 
 // All sizes in 32-bit words.  Loads outside [src_rows) x [src_words) read 0;
 // stores outside [dst_rows) x [dst_words) are dropped.  blockIdx.z selects one of gridDim.z
 // independent matrices (src + z*src_zoff -> dst + z*dst_zoff: the x and z halves of a store).
 // If `flag` is given the kernel is a no-op unless *flag != 0 (device-side "C form is stale").
+// VEC: every row start and width is a multiple of four 32-bit words (true for tableaux): 16-byte loads and stores, two per
+// thread instead of eight 4-byte ones (the kernel is instruction bound, see transpose32).
+template <bool VEC>
+__device__ __forceinline__ void transpose_bits_body(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                                                    u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                                                    u32 (*tin)[9], u32 (*tout)[9]) {
+    const int c0 = blockIdx.x * 256;          // first src row of the tile  (= dst bit offset)
+    const int w0 = blockIdx.y * 8;            // first src word of the tile (= dst row offset / 32)
+    const int t = threadIdx.x;
+    if (VEC) {
+        // two threads read the 32 contiguous bytes a src row has in the tile
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int rr = k * 128 + (t >> 1), ww = (t & 1) * 4;
+            const int gr = c0 + rr, gw = w0 + ww;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (gr < src_rows && gw < src_words) v = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)gr * src_stride + gw));
+            tin[rr][ww] = v.x; tin[rr][ww + 1] = v.y; tin[rr][ww + 2] = v.z; tin[rr][ww + 3] = v.w;
+        }
+    } else {
+        // load: 8 consecutive threads read 32 contiguous bytes of one src row
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int rr = k * 32 + (t >> 3), ww = t & 7;
+            int gr = c0 + rr, gw = w0 + ww;
+            u32 v = 0;
+            if (gr < src_rows && gw < src_words) v = __ldcg(src + (size_t)gr * src_stride + gw);
+            tin[rr][ww] = v;
+        }
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    // 8 x 8 blocks of 32x32 bits; warp handles block-row `warp` (src rows 32*warp ..)
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) {
+        // src row (c0 + 32*warp + lane), bits 32*(w0+bj) .. : 32x32 bit transpose across the warp
+        const u32 mine = transpose32(tin[warp * 32 + lane][bj], lane);
+        // lane b holds dst row (32*(w0+bj) + b), word (c0/32 + warp)
+        tout[bj * 32 + lane][warp] = mine;
+    }
+    __syncthreads();
+    if (VEC) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int rr = k * 128 + (t >> 1), ww = (t & 1) * 4;
+            const int gr = w0 * 32 + rr, gw = (c0 >> 5) + ww;
+            if (gr < dst_rows && gw < dst_words)
+                __stcg(reinterpret_cast<uint4*>(dst + (size_t)gr * dst_stride + gw), make_uint4(tout[rr][ww], tout[rr][ww + 1], tout[rr][ww + 2], tout[rr][ww + 3]));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int rr = k * 32 + (t >> 3), ww = t & 7;
+            int gr = w0 * 32 + rr, gw = (c0 >> 5) + ww;
+            if (gr < dst_rows && gw < dst_words) __stcg(dst + (size_t)gr * dst_stride + gw, tout[rr][ww]);
+        }
+    }
+}
 __global__ void __launch_bounds__(256)
 k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
                  u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
@@ -29,38 +97,10 @@ k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, i
     pdl_wait();
     if (flag && __ldcg(flag) == 0u) return;
     src += (size_t)blockIdx.z * src_zoff; dst += (size_t)blockIdx.z * dst_zoff;
-    const int c0 = blockIdx.x * 256;          // first src row of the tile  (= dst bit offset)
-    const int w0 = blockIdx.y * 8;            // first src word of the tile (= dst row offset / 32)
-    const int t = threadIdx.x;
-    // load: 8 consecutive threads read 32 contiguous bytes of one src row
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        int rr = k * 32 + (t >> 3), ww = t & 7;
-        int gr = c0 + rr, gw = w0 + ww;
-        u32 v = 0;
-        if (gr < src_rows && gw < src_words) v = __ldcg(src + (size_t)gr * src_stride + gw);
-        tin[rr][ww] = v;
-    }
-    __syncthreads();
-    const int warp = t >> 5, lane = t & 31;
-    // 8 x 8 blocks of 32x32 bits; warp handles block-row `warp` (src rows 32*warp ..)
-#pragma unroll
-    for (int bj = 0; bj < 8; ++bj) {
-        u32 v = tin[warp * 32 + lane][bj];    // src row (c0 + 32*warp + lane), bits 32*(w0+bj) ..
-        // 32x32 bit transpose across the warp: 5 butterfly stages (swap off-diagonal j x j blocks)
-        bfly(v, 16, 0x0000ffffu, lane); bfly(v, 8, 0x00ff00ffu, lane); bfly(v, 4, 0x0f0f0f0fu, lane);
-        bfly(v, 2, 0x33333333u, lane); bfly(v, 1, 0x55555555u, lane);
-        const u32 mine = v;
-        // lane b holds dst row (32*(w0+bj) + b), word (c0/32 + warp)
-        tout[bj * 32 + lane][warp] = mine;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        int rr = k * 32 + (t >> 3), ww = t & 7;
-        int gr = w0 * 32 + rr, gw = (c0 >> 5) + ww;
-        if (gr < dst_rows && gw < dst_words) __stcg(dst + (size_t)gr * dst_stride + gw, tout[rr][ww]);
-    }
+    const bool vec = ((src_stride | dst_stride | src_zoff | dst_zoff | (size_t)src_words | (size_t)dst_words) & 3) == 0 &&
+                     ((reinterpret_cast<size_t>(src) | reinterpret_cast<size_t>(dst)) & 15) == 0;
+    if (vec) transpose_bits_body<true>(src, src_stride, src_rows, src_words, dst, dst_stride, dst_rows, dst_words, tin, tout);
+    else transpose_bits_body<false>(src, src_stride, src_rows, src_words, dst, dst_stride, dst_rows, dst_words, tin, tout);
 }
 
 // The same tile move as a device function for use inside a persistent kernel: `nthr` = 256 threads of one half-CTA
@@ -80,10 +120,7 @@ __device__ __forceinline__ void transpose_tile_256(const u32* __restrict__ src, 
     const int warp = t >> 5, lane = t & 31;
 #pragma unroll
     for (int bj = 0; bj < 8; ++bj) {
-        u32 v = tin[warp * 32 + lane][bj];
-        bfly(v, 16, 0x0000ffffu, lane); bfly(v, 8, 0x00ff00ffu, lane); bfly(v, 4, 0x0f0f0f0fu, lane);
-        bfly(v, 2, 0x33333333u, lane); bfly(v, 1, 0x55555555u, lane);
-        tout[bj * 32 + lane][warp] = v;
+        tout[bj * 32 + lane][warp] = transpose32(tin[warp * 32 + lane][bj], lane);
     }
     asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
 #pragma unroll
