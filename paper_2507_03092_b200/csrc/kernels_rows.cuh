@@ -497,6 +497,128 @@ k_first_fit_threads(const u64* __restrict__ rows, int Wp, int W, int t0, int B, 
     if (tid == 0) *ngroups_io = s_ng;
 }
 
+// ---- first fit by free lists (rows of at most 128 qubits; the default resolver of config C4) --------------------------------
+// A term of a GC instance fits very few of the groups that exist when its block starts (two on average at N = 10^6: a group of k
+// random members accepts a term with probability 2^-k), so instead of walking bitmap rows the resolver works on
+//   * the term's FREE LIST: its first kFreeList free pre-block groups in ascending order (k_free_lists, all rows in parallel), and
+//   * a per-term bit mask over the groups created inside the block (at most one per term: 1024 bits, in shared memory).
+// The sequential part is then one barrier per placed term: the term whose turn it is takes the first live entry of its list, else the
+// first in-block group without a conflicting member, else a new group; every later term that conflicts with it strikes that group
+// from its own list / mask.  Identical groups to the scanning resolvers (same first-fit rule).
+constexpr int kFreeList = 12;
+// free pre-block groups of every block term, ascending; fcnt = how many there are (kFreeList + 1 stands for "more than the list holds").
+// Coalesced sweep in chunks of 256 words: a chunk without a free bit costs one barrier (GC rows are almost all ones), one with
+// free bits is compacted in word order (warp scan + one shared-memory hop), and the sweep stops once the list is full.
+__global__ void __launch_bounds__(256)
+k_free_lists(const u32* __restrict__ bitmap, int GW32, const u32* __restrict__ ngroups, u32* __restrict__ fl, u32* __restrict__ fcnt) {
+    __shared__ u32 s_w[8];
+    const u32* bm = bitmap + (size_t)blockIdx.x * GW32;
+    const u32 ng = *ngroups;
+    const int words = int((ng + 31) >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 found = 0;                                    // entries written so far (CTA-uniform)
+    for (int w0 = 0; w0 < words && found <= (u32)kFreeList; w0 += 256) {
+        const int w = w0 + int(threadIdx.x);
+        u32 freeb = (w < words) ? ~__ldcg(bm + w) : 0u;
+        if (w == words - 1 && (ng & 31u)) freeb &= (1u << (ng & 31u)) - 1u;      // groups >= ng do not exist yet
+        if (!__syncthreads_or(freeb != 0u)) continue;
+        const u32 cnt = __popc(freeb);
+        u32 incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const u32 v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        u32 at = found + incl - cnt, tot = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) { if (t < warp) at += s_w[t]; tot += s_w[t]; }
+        while (freeb && at < (u32)kFreeList) { const int b = __ffs(int(freeb)) - 1; freeb &= freeb - 1; fl[(size_t)blockIdx.x * kFreeList + at] = u32(w * 32 + b); ++at; }
+        found += tot;
+        __syncthreads();                               // s_w is reused by the next chunk
+    }
+    if (threadIdx.x == 0) fcnt[blockIdx.x] = min(found, (u32)kFreeList + 1u);
+}
+
+// dynamic shared memory: terms [B][4] u64, in-block masks [32][1024] u32
+__global__ void __launch_bounds__(1024)
+k_first_fit_lists(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode,
+                  u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io,
+                  const u32* __restrict__ fl, const u32* __restrict__ fcnt) {
+    extern __shared__ u64 s_dyn[];
+    u64* s_term = s_dyn;                                            // [1024][4]: x0 x1 z0 z1
+    u32* s_nb = reinterpret_cast<u32*>(s_dyn + 4 * 1024);           // [32][1024]: in-block groups struck for thread tid, bit (g - ng0)
+    __shared__ u32 s_g[2], s_ng;
+    const int tid = threadIdx.x;
+    const bool mine = tid < B;
+    const u32 ng0 = *ngroups_io;                                    // groups that exist when the block starts
+    u64 m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    if (mine) {
+        const u64* mx = rows + (size_t)(2 * (t0 + tid)) * Wp;
+        m0 = mx[0]; m1 = W > 1 ? mx[1] : 0ull; m2 = mx[Wp]; m3 = W > 1 ? mx[Wp + 1] : 0ull;
+    }
+    s_term[4 * tid] = m0; s_term[4 * tid + 1] = m1; s_term[4 * tid + 2] = m2; s_term[4 * tid + 3] = m3;
+#pragma unroll
+    for (int w = 0; w < 32; ++w) s_nb[w * 1024 + tid] = 0u;
+    u32 lst[kFreeList];
+    const u32 total = mine ? fcnt[tid] : 0u;
+    const int have = int(min(total, (u32)kFreeList));
+#pragma unroll
+    for (int i = 0; i < kFreeList; ++i) lst[i] = (mine && i < have) ? fl[(size_t)tid * kFreeList + i] : 0xffffffffu;
+    const u32 last_listed = have ? fl[(size_t)tid * kFreeList + have - 1] : 0u;
+    u32 nbfull = 0;
+    const bool ovf = total > (u32)kFreeList;                        // more free pre-block groups than the list holds: strikes also go to the bitmap row
+    u32* myrow = bitmap + (size_t)(mine ? tid : 0) * GW32;
+    if (tid == 0) s_ng = ng0;
+    __syncthreads();
+    for (int k = 0; k < B; ++k) {
+        if (tid == k) {
+            // my turn: first live list entry, else (list truncated) the rest of my bitmap row, else the first in-block group, else a new one
+            const u32 ng = s_ng;
+            u32 g = 0xffffffffu;
+#pragma unroll
+            for (int i = 0; i < kFreeList; ++i) if (g == 0xffffffffu && lst[i] != 0xffffffffu) g = lst[i];
+            if (g == 0xffffffffu && ovf) {
+                for (u32 c = last_listed + 1; c < ng0;) {                      // behind the last listed group
+                    const u32 w = c >> 5;
+                    u32 freeb = ~__ldcg(myrow + w);
+                    if (c & 31u) freeb &= ~((1u << (c & 31u)) - 1u);
+                    if (freeb) { const u32 f = w * 32 + u32(__ffs(int(freeb)) - 1); if (f < ng0) g = f; break; }
+                    c = (w + 1) * 32;
+                }
+            }
+            if (g == 0xffffffffu) {
+                const u32 nnew = ng - ng0;
+                for (u32 w = nbfull; w * 32 < nnew; ++w) {
+                    u32 freeb = ~s_nb[w * 1024 + tid];
+                    if ((w + 1) * 32 > nnew) freeb &= (1u << (nnew & 31u)) - 1u;
+                    if (freeb) { g = ng0 + w * 32 + u32(__ffs(int(freeb)) - 1); break; }
+                }
+            }
+            if (g == 0xffffffffu) g = ng;
+            group_of[t0 + k] = g; s_g[k & 1] = g;
+            if (g == ng) s_ng = ng + 1;
+        }
+        __syncthreads();
+        if (tid > k && mine) {
+            const u64 tx0 = s_term[4 * k], tx1 = s_term[4 * k + 1], tz0 = s_term[4 * k + 2], tz1 = s_term[4 * k + 3];
+            if (conflict4(m0, m1, m2, m3, tx0, tx1, tz0, tz1, mode)) {
+                const u32 g = s_g[k & 1];
+                if (g >= ng0) {
+                    const u32 w = (g - ng0) >> 5;
+                    const u32 v = s_nb[w * 1024 + tid] | (1u << ((g - ng0) & 31u));
+                    s_nb[w * 1024 + tid] = v;
+                    if (v == 0xffffffffu && w == nbfull) ++nbfull;       // leading words that are full (a lower bound is enough: the search starts there)
+                } else if (g <= last_listed || ovf) {
+#pragma unroll
+                    for (int i = 0; i < kFreeList; ++i) if (lst[i] == g) lst[i] = 0xffffffffu;
+                    if (ovf) atomicOr(myrow + (g >> 5), 1u << (g & 31));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *ngroups_io = s_ng;
+}
+
 // verify_grouping: number of intra-group pairs violating the predicate.
 // Thread per row j sweeps all i < j (broadcast loads of group ids).
 __global__ void __launch_bounds__(256)

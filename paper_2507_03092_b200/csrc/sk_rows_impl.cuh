@@ -75,6 +75,18 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
         SK_CUDA(c, cudaMemsetAsync(d_cnt, 0, ((size_t)count + 4) * 4, c->stream));
         d_gmin = d_cnt + count + 3;
     }
+    // free-list resolver (k_first_fit_lists): rows of <= 128 qubits, plain first fit; SK_GROUP_RESOLVER=1 selects the candidate-tracking one
+    static const bool lists_off = getenv("SK_GROUP_RESOLVER") != nullptr;
+    constexpr size_t kListSmem = (size_t)4 * 1024 * 8 + (size_t)32 * 1024 * 4;
+    const bool use_lists = W <= 2 && !(mode & kOrderedFit) && !lists_off && B == 1024;
+    u32* d_fl = nullptr; u32* d_fcnt = nullptr;
+    scope.own(&d_fl);
+    if (use_lists) {
+        SK_CUDA(c, cudaMalloc(&d_fl, (size_t)B * (kFreeList + 1) * 4));
+        d_fcnt = d_fl + (size_t)B * kFreeList;
+        static bool attr_set = false;
+        if (!attr_set) { SK_CUDA(c, cudaFuncSetAttribute(k_first_fit_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kListSmem))); attr_set = true; }
+    }
     const int Btg = std::min(B, 128);                                           // block terms per CTA: 8 CTAs per 256 groups keep the SMs busy while groups are few (GC)
     for (int t0 = 0; t0 < count; t0 += B) {
         const int b = std::min(B, count - t0);
@@ -94,9 +106,14 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
             k_conflict_bitmap<<<grid, 256, smem, c->stream>>>(d_rows, Wp, W, t0, b, Bt, d_group, mode, d_bitmap, GW32);
             c->cnt.kernel_launches++;
         }
-        k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_ff);
-        if ((mode & kOrderedFit) || legacy_resolver) k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
-        else k_first_fit_threads<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+        if (use_lists) {
+            k_free_lists<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_fl, d_fcnt);
+            k_first_fit_lists<<<1, 1024, kListSmem, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_fl, d_fcnt);
+        } else {
+            k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_ff);
+            if ((mode & kOrderedFit) || legacy_resolver) k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+            else k_first_fit_threads<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
+        }
         c->cnt.kernel_launches += 2;
     }
     SK_CUDA(c, cudaGetLastError());
