@@ -46,8 +46,15 @@ class ShardedTableau {
         pw_ = size_t(sk_shard_partial_words(shards_[0]));
         d.check(sk_dev_alloc(d.ctx(), pw_ * 8, reinterpret_cast<void**>(&d_row_)));
     }
+    // Random measurement blocks on the tableau assembled from all shards (one allgather of the rows per block; the elimination is
+    // replicated on every rank) -- the default; false = an exchange per measurement throughout (tableaux beyond one GPU's memory).
+    bool replicate_random_blocks = true;
+    size_t replicated_blocks = 0;
+
     ~ShardedTableau() {
         Device& d = Device::instance();
+        if (full_) sk_tableau_destroy(full_);
+        sk_dev_free(d.ctx(), d_blk_); sk_dev_free(d.ctx(), d_blks_);
         for (sk_shard* s : shards_) sk_shard_destroy(s);
         sk_dev_free(d.ctx(), d_row_); sk_dev_free(d.ctx(), d_cand_); sk_dev_free(d.ctx(), d_part_); sk_dev_free(d.ctx(), d_all_);
     }
@@ -93,6 +100,14 @@ class ShardedTableau {
                 std::vector<uint8_t> o(r0);
                 d.check(sk_shard_det_combine(shards_[0], d_all_, uint32_t(G), r0, o.data()));
                 for (size_t j = 0; j < r0; ++j) out[pos + j] = {o[j] != 0, true};
+            }
+            if (r0 < w && replicate_random_blocks) {            // the rest of the block on the assembled tableau
+                const size_t rest = m - (pos + r0);
+                std::vector<uint8_t> o(rest + 1), dt(rest + 1);
+                replicated_block(qubits.data() + pos + r0, rest, seed, ordinal0 + pos + r0, o.data(), dt.data());
+                for (size_t j = 0; j < rest; ++j) out[pos + r0 + j] = {o[j] != 0, dt[j] != 0};
+                win_ = 64;
+                return out;
             }
             if (r0 < w) {                                        // the first random measurement of the window
                 const uint64_t p = uint64_t(cand[r0]);
@@ -153,6 +168,31 @@ class ShardedTableau {
     }
 
   private:
+    // every shard's rows as one block -> allgather -> full sk_tableau -> sk_measure_batch (identical on every rank) -> rows back
+    void replicated_block(const uint32_t* qubits, size_t m, uint64_t seed, uint64_t ordinal0, uint8_t* outcomes, uint8_t* dets) {
+        Device& d = Device::instance();
+        sk_ctx* ctx = d.ctx();
+        const size_t G = ranges_.size();
+        const size_t Wp = (words_for_bits(n_) + 1) & ~size_t(1);
+        if (!blk_words_) {
+            for (const auto& [lo, hi] : ranges_) { const size_t k = size_t(hi - lo); blk_words_ = std::max(blk_words_, 4 * k * Wp + 2 * ((k + 63) / 64)); }
+            blk_words_ = std::max<size_t>(blk_words_, 2);
+            d.check(sk_dev_alloc(ctx, size_t(local_) * blk_words_ * 8, reinterpret_cast<void**>(&d_blk_)));
+            d.check(sk_dev_alloc(ctx, G * blk_words_ * 8, reinterpret_cast<void**>(&d_blks_)));
+            d.check(sk_tableau_create(ctx, n_, &full_));
+        }
+        for (int l = 0; l < local_; ++l) d.check(sk_shard_export_rows(shards_[size_t(l)], d_blk_ + size_t(l) * blk_words_));
+        ex_->allgather(ctx, d_blk_, d_blks_, size_t(local_) * blk_words_);
+        for (size_t g = 0; g < G; ++g) d.check(sk_tableau_import_block(full_, ranges_[g].first, ranges_[g].second, d_blks_ + g * blk_words_));
+        d.check(sk_tableau_commit_blocks(full_));
+        d.check(sk_measure_batch(full_, qubits, m, seed, ordinal0, outcomes, dets));
+        for (int l = 0; l < local_; ++l) {
+            const auto [lo, hi] = ranges_[size_t(ex_->rank() * local_ + l)];
+            d.check(sk_tableau_export_block(full_, lo, hi, d_blk_ + size_t(l) * blk_words_));
+            d.check(sk_shard_import_rows(shards_[size_t(l)], d_blk_ + size_t(l) * blk_words_));
+        }
+        ++replicated_blocks;
+    }
     void reserve(size_t w, size_t G) {
         if (w <= cap_) return;
         Device& d = Device::instance();
@@ -167,6 +207,7 @@ class ShardedTableau {
     std::vector<std::pair<uint64_t, uint64_t>> ranges_;
     std::vector<sk_shard*> shards_;
     size_t pw_ = 0, cap_ = 0, win_ = 64;
+    sk_tableau* full_ = nullptr; uint64_t* d_blk_ = nullptr; uint64_t* d_blks_ = nullptr; size_t blk_words_ = 0;
     int32_t* d_cand_ = nullptr; uint64_t* d_part_ = nullptr; uint64_t* d_all_ = nullptr; uint64_t* d_row_ = nullptr;
 };
 

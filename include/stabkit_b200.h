@@ -295,6 +295,16 @@ int32_t sk_shard_pivot_row(sk_shard* s, uint64_t p, uint64_t* d_row);
 int32_t sk_shard_random_update(sk_shard* s, uint32_t q, uint64_t p, const uint64_t* d_row, uint8_t outcome);
 /* This shard's rows, row-major: stabilizers slot_lo..slot_hi-1, then their destabilizers. Synchronises. */
 int32_t sk_shard_download(sk_shard* s, uint64_t* x, uint64_t* z, uint8_t* sign);
+/* Replicated elimination of a random measurement block: a shard's rows as one contiguous device block (stabilizer rows, destabilizer
+ * rows, sign words of the two halves; sk_shard_export_words() 64-bit words), the blocks of all shards placed into a full
+ * sk_tableau (import_block per shard, then commit), sk_measure_batch on it -- identical on every rank -- and the rows back
+ * (export_block -> sk_shard_import_rows).  One allgather of the tableau per random block instead of an exchange per measurement. */
+uint64_t sk_shard_export_words(const sk_shard* s);
+int32_t sk_shard_export_rows(sk_shard* s, uint64_t* d_buf);
+int32_t sk_shard_import_rows(sk_shard* s, const uint64_t* d_buf);
+int32_t sk_tableau_import_block(sk_tableau* t, uint64_t slot_lo, uint64_t slot_hi, const uint64_t* d_buf);
+int32_t sk_tableau_commit_blocks(sk_tableau* t);
+int32_t sk_tableau_export_block(sk_tableau* t, uint64_t slot_lo, uint64_t slot_hi, uint64_t* d_buf);
 /* rowsums performed: out2[0] random branch, out2[1] deterministic branch. Synchronises. */
 int32_t sk_shard_counters(sk_shard* s, uint64_t out2[2]);
 /* Plain device buffers for the exchange, so that a host binding needs no CUDA headers of its own.

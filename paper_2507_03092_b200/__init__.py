@@ -104,6 +104,12 @@ def lib() -> C.CDLL:
             "sk_rows_append": (i32, [vp, vp, vp, vp, u64]),
             "sk_commute_matrix_tile": (i32, [vp, C.c_int, u64, u64, u64, u64, vp]),
             "sk_tableau_audit": (i32, [vp, P(u64)]),
+            "sk_shard_export_words": (u64, [vp]),
+            "sk_shard_export_rows": (i32, [vp, vp]),
+            "sk_shard_import_rows": (i32, [vp, vp]),
+            "sk_tableau_import_block": (i32, [vp, u64, u64, vp]),
+            "sk_tableau_commit_blocks": (i32, [vp]),
+            "sk_tableau_export_block": (i32, [vp, u64, u64, vp]),
             "sk_group_shard_create": (i32, [vp, C.c_int, u32, u32, P(vp)]),
             "sk_group_shard_destroy": (None, [vp]),
             "sk_group_shard_blocks": (u64, [vp]),
@@ -156,7 +162,8 @@ EXPORTS = [
     "sk_program_measurements", "sk_program_run", "sk_program_run_profiled", "sk_program_read_record", "sk_program_run_shots", "sk_sim", "sk_free",
     "sk_circuit_surface_code", "sk_circuit_random_layered", "sk_circuit_parse_native", "sk_circuit_parse_qasm2",
     "sk_circuit_validate_chunks", "sk_circuit_validate_chunks_ex", "sk_rows_create", "sk_rows_destroy", "sk_rows_count", "sk_rows_upload",
-    "sk_rows_download", "sk_rows_append", "sk_commute_matrix_tile", "sk_tableau_audit",
+    "sk_rows_download", "sk_rows_append", "sk_commute_matrix_tile", "sk_tableau_audit", "sk_shard_export_words", "sk_shard_export_rows", "sk_shard_import_rows",
+    "sk_tableau_import_block", "sk_tableau_commit_blocks", "sk_tableau_export_block",
     "sk_group_shard_create", "sk_group_shard_destroy", "sk_group_shard_blocks", "sk_group_shard_bitmap_words", "sk_group_shard_conflicts",
     "sk_group_shard_resolve", "sk_group_shard_result", "sk_rows_conj_layer", "sk_commutation_vector",
     "sk_rowsum_plus_i_where_anticommuting", "sk_find_first_duplicate", "sk_weight_sum",

@@ -13,7 +13,19 @@ struct sk_shard {
     u64* d_mask = nullptr; u64* d_cnt = nullptr;          // d_cnt: [0] rowsums in the random branch, [1] in the deterministic branch
     u32* d_q = nullptr; size_t q_cap = 0; uint8_t* d_out = nullptr;
     std::vector<uint32_t> scratch;
+    // Clifford runs already layered and resident on the device, keyed by a hash of the gate bytes: the rounds of a memory experiment
+    // repeat the same run, so validation, layering, the upload and its synchronisation are paid once
+    struct Run { uint64_t hash = 0; size_t ngates = 0; sk_gate* d_gates = nullptr; std::vector<uint32_t> sizes; uint64_t used = 0; };
+    std::vector<Run> runs; uint64_t run_clock = 0;
 };
+static uint64_t gate_bytes_hash(const sk_gate* g, size_t n) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(g);
+    const size_t bytes = n * sizeof(sk_gate), words = bytes / 8;
+    uint64_t h = 0x9e3779b97f4a7c15ull ^ bytes;
+    for (size_t i = 0; i < words; ++i) { uint64_t w; memcpy(&w, p + 8 * i, 8); h = (h ^ w) * 0xff51afd7ed558ccdull; h ^= h >> 32; }
+    for (size_t i = words * 8; i < bytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+    return h;
+}
 
 static int32_t shard_identity(sk_shard* s) {
     sk_ctx* c = s->ctx;
@@ -35,6 +47,7 @@ extern "C" void sk_shard_destroy(sk_shard* s) {
     sk_ctx* c = s->ctx;
     cudaSetDevice(c->device);
     for (void* p : {(void*)s->m.cols, (void*)s->m.rows, (void*)s->m.sgn, (void*)s->d_mask, (void*)s->d_cnt, (void*)s->d_q, (void*)s->d_out}) dfree(c, p);
+    for (auto& r : s->runs) dfree(c, r.d_gates);
     delete s;
 }
 
@@ -69,28 +82,42 @@ extern "C" int32_t sk_shard_apply_gates(sk_shard* s, const sk_gate* gates, size_
     if (!s || (!gates && ngates)) return SK_EARG;
     sk_ctx* c = s->ctx;
     if (ngates == 0) return SK_OK;
-    for (size_t i = 0; i < ngates; ++i) {
-        int32_t rc = validate_gate(c, gates[i], s->n, i);
-        if (rc) return rc;
-        if (gates[i].kind >= SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: M/T/TDG in a Clifford sequence (SPEC:191)", i);
+    const uint64_t hsh = gate_bytes_hash(gates, ngates);
+    sk_shard::Run* run = nullptr;
+    for (auto& r : s->runs) if (r.hash == hsh && r.ngates == ngates) { run = &r; break; }
+    if (!run) {
+        for (size_t i = 0; i < ngates; ++i) {
+            int32_t rc = validate_gate(c, gates[i], s->n, i);
+            if (rc) return rc;
+            if (gates[i].kind >= SK_M) SK_FAIL(c, SK_EUNSUPPORTED, "gate %zu: M/T/TDG in a Clifford sequence (SPEC:191)", i);
+        }
+        std::vector<sk_gate> ordered; std::vector<uint32_t> sizes;
+        sk_layer_run(gates, ngates, s->n, s->scratch, ordered, sizes);
+        if (s->runs.size() >= 8) {             // evict the least recently used run
+            size_t victim = 0;
+            for (size_t i = 1; i < s->runs.size(); ++i) if (s->runs[i].used < s->runs[victim].used) victim = i;
+            dfree(c, s->runs[victim].d_gates);
+            s->runs.erase(s->runs.begin() + victim);
+        }
+        sk_shard::Run nr; nr.hash = hsh; nr.ngates = ngates; nr.sizes = sizes;
+        SK_CUDA(c, dmalloc(c, &nr.d_gates, ngates * sizeof(sk_gate)));
+        SK_CUDA(c, cudaMemcpyAsync(nr.d_gates, ordered.data(), ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));     // `ordered` dies at the end of this block
+        s->runs.push_back(std::move(nr));
+        run = &s->runs.back();
     }
-    std::vector<sk_gate> ordered; std::vector<uint32_t> sizes;
-    sk_layer_run(gates, ngates, s->n, s->scratch, ordered, sizes);
-    int32_t rc = sk_ctx_reserve_gates(c, ngates * sizeof(sk_gate));
-    if (rc) return rc;
-    SK_CUDA(c, cudaMemcpyAsync(c->d_gates, ordered.data(), ngates * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream));
+    run->used = ++s->run_clock;
     const int threads = std::min(256, std::max(32, (s->RW / 2 + 31) & ~31));
     const int target_ctas = layer_target_ctas(c, threads);
     size_t off = 0;
-    for (uint32_t sz : sizes) {
+    for (uint32_t sz : run->sizes) {
         const int ng = int(sz), gpb = std::max(1, (ng + target_ctas - 1) / target_ctas);
-        k_layer<<<(ng + gpb - 1) / gpb, threads, 0, c->stream>>>(s->m.cols, s->m.sgn, (const sk_gate*)c->d_gates + off, ng, s->RW, gpb, nullptr);
+        k_layer<<<(ng + gpb - 1) / gpb, threads, 0, c->stream>>>(s->m.cols, s->m.sgn, (const sk_gate*)run->d_gates + off, ng, s->RW, gpb, nullptr);
         c->cnt.kernel_launches++; c->cnt.layers++;
         off += sz;
     }
     s->r_valid = false;
     SK_CUDA(c, cudaGetLastError());
-    SK_CUDA(c, cudaStreamSynchronize(c->stream));     // the staging buffer is reused by the next call
     return SK_OK;
 }
 
@@ -204,6 +231,81 @@ extern "C" int32_t sk_shard_download(sk_shard* s, uint64_t* x, uint64_t* z, uint
     SK_CUDA(c, cudaMemcpyAsync(z, dz, words * 8, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaMemcpyAsync(sign, ds, nrows, cudaMemcpyDeviceToHost, c->stream));
     return check_ws(c);
+}
+
+// ---- replicated elimination of a random measurement block ------------------------------------------
+// A shard's rows travel as one contiguous block: stabilizer rows (nloc x 2*Wp words), destabilizer rows (same), then the sign words of
+// the two halves (ceil(nloc/64) each; slot ranges are whole 64-row words, so they are word aligned in the full tableau as well).
+// Every rank gathers all blocks into a full sk_tableau, runs the single-GPU measurement kernel on it -- the result is the same on
+// every rank -- and takes its own rows back.  Communication: one allgather of the tableau per random block instead of an exchange per
+// measurement; the elimination itself is replicated, not sharded (tableaux beyond one GPU's memory keep the per-measurement protocol).
+static size_t shard_block_words(int nloc, int Wp) { return (size_t)2 * nloc * 2 * Wp + 2 * (size_t)((nloc + 63) / 64); }
+extern "C" uint64_t sk_shard_export_words(const sk_shard* s) { return s ? uint64_t(shard_block_words(s->nloc, s->Wp)) : 0; }
+extern "C" int32_t sk_shard_export_rows(sk_shard* s, uint64_t* d_buf) {
+    if (!s || !d_buf) return SK_EARG;
+    sk_ctx* c = s->ctx;
+    if (s->nloc == 0) return SK_OK;
+    int32_t rc = shard_rows(s);
+    if (rc) return rc;
+    const size_t half = (size_t)s->nloc * 2 * s->Wp, sw = (size_t)(s->nloc + 63) / 64;
+    SK_CUDA(c, cudaMemcpyAsync(d_buf, s->m.rows, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + half, s->m.rows + (size_t)s->NS * 2 * s->Wp, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + 2 * half, s->m.sgn, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + 2 * half + sw, s->m.sgn + s->NS / 64, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return SK_OK;
+}
+extern "C" int32_t sk_shard_import_rows(sk_shard* s, const uint64_t* d_buf) {
+    if (!s || !d_buf) return SK_EARG;
+    sk_ctx* c = s->ctx;
+    if (s->nloc == 0) return SK_OK;
+    const size_t half = (size_t)s->nloc * 2 * s->Wp, sw = (size_t)(s->nloc + 63) / 64;
+    SK_CUDA(c, cudaMemcpyAsync(s->m.rows, d_buf, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(s->m.rows + (size_t)s->NS * 2 * s->Wp, d_buf + half, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(s->m.sgn, d_buf + 2 * half, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(s->m.sgn + s->NS / 64, d_buf + 2 * half + sw, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    s->r_valid = true;
+    // the gate form follows from the rows (R -> C, both halves)
+    int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(s->m.rows), (size_t)4 * s->Wp, 64 * s->RW, 2 * s->Wp,
+                                  reinterpret_cast<u32*>(s->m.cols), (size_t)4 * s->RW, int(s->n), 2 * s->RW,
+                                  (size_t)2 * s->Wp, (size_t)2 * s->RW, nullptr);
+    if (rc) return rc;
+    c->cnt.transposes++;
+    return SK_OK;
+}
+// the block of the slots [lo, hi) into / out of a full tableau (same block layout); commit derives the gate form after all imports
+extern "C" int32_t sk_tableau_import_block(sk_tableau* t, uint64_t lo, uint64_t hi, const uint64_t* d_buf) {
+    if (!t || !d_buf) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (lo == hi) return SK_OK;                         // a shard without slots
+    if (lo > hi || hi > t->n || (lo & 63)) SK_FAIL(c, SK_EDIM, "import_block: slots [%llu, %llu) of %llu qubits (lo must be a multiple of 64)", (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)t->n);
+    const int nloc = int(hi - lo);
+    if (nloc == 0) return SK_OK;
+    const size_t half = (size_t)nloc * 2 * t->Wp, sw = (size_t)(nloc + 63) / 64;
+    SK_CUDA(c, cudaMemcpyAsync(t->m.rows + (size_t)lo * 2 * t->Wp, d_buf, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(t->m.rows + ((size_t)t->NS + lo) * 2 * t->Wp, d_buf + half, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(t->m.sgn + lo / 64, d_buf + 2 * half, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(t->m.sgn + ((size_t)t->NS + lo) / 64, d_buf + 2 * half + sw, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return SK_OK;
+}
+extern "C" int32_t sk_tableau_commit_blocks(sk_tableau* t) {
+    if (!t) return SK_EARG;
+    t->r_valid = true; t->r_destab_stale = false;
+    return cols_from_rows(t);
+}
+extern "C" int32_t sk_tableau_export_block(sk_tableau* t, uint64_t lo, uint64_t hi, uint64_t* d_buf) {
+    if (!t || !d_buf) return SK_EARG;
+    sk_ctx* c = t->ctx;
+    if (lo == hi) return SK_OK;
+    if (lo > hi || hi > t->n || (lo & 63)) SK_FAIL(c, SK_EDIM, "export_block: slots [%llu, %llu) of %llu qubits (lo must be a multiple of 64)", (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)t->n);
+    const int nloc = int(hi - lo);
+    if (nloc == 0) return SK_OK;
+    { int32_t rc = rows_full(t); if (rc) return rc; }
+    const size_t half = (size_t)nloc * 2 * t->Wp, sw = (size_t)(nloc + 63) / 64;
+    SK_CUDA(c, cudaMemcpyAsync(d_buf, t->m.rows + (size_t)lo * 2 * t->Wp, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + half, t->m.rows + ((size_t)t->NS + lo) * 2 * t->Wp, half * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + 2 * half, t->m.sgn + lo / 64, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    SK_CUDA(c, cudaMemcpyAsync(d_buf + 2 * half + sw, t->m.sgn + ((size_t)t->NS + lo) / 64, sw * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return SK_OK;
 }
 
 // rowsums performed by this shard: out2[0] random branch, out2[1] deterministic branch.  Synchronises.

@@ -99,6 +99,25 @@ class CudaShard:
     def random_update(self, q: int, p: int, row, outcome: int):
         self.ctx.check(self._lib.sk_shard_random_update(self._h, q, p, C.c_void_p(row.data_ptr()), outcome))
 
+    # -- replicated elimination of a random block: rows as one contiguous device block -----------------------
+    def block_words(self, nloc: int | None = None) -> int:
+        nloc = (self.hi - self.lo) if nloc is None else nloc
+        Wp = (self.W + 1) & ~1
+        return 4 * nloc * Wp + 2 * ((nloc + 63) // 64)
+
+    def new_block(self, words: int):
+        return self._torch.zeros(max(words, 1), dtype=self._torch.int64, device=self.device)
+
+    def export_rows(self, buf):
+        self.ctx.check(self._lib.sk_shard_export_rows(self._h, C.c_void_p(buf.data_ptr())))
+
+    def import_rows(self, buf):
+        self.ctx.check(self._lib.sk_shard_import_rows(self._h, C.c_void_p(buf.data_ptr())))
+
+    def make_full(self):
+        """The full tableau the blocks of all shards are assembled in (single-GPU engine, same context / stream)."""
+        return _CudaFull(self.ctx, self.n)
+
     def download(self):
         nloc = self.hi - self.lo
         x = np.zeros((2 * nloc, self.W), np.uint64); z = np.zeros_like(x); r = np.zeros(2 * nloc, np.uint8)
@@ -109,6 +128,29 @@ class CudaShard:
         out = (C.c_uint64 * 2)()
         self.ctx.check(self._lib.sk_shard_counters(self._h, out))
         return int(out[0]), int(out[1])
+
+
+class _CudaFull:
+    """A full sk_tableau fed with shard blocks (sk_tableau_import_block / commit / export_block)."""
+
+    def __init__(self, ctx, n):
+        from . import Tableau, lib
+        self._lib, self.ctx, self.t = lib(), ctx, Tableau(ctx, n)
+
+    def import_block(self, lo, hi, buf):
+        self.ctx.check(self._lib.sk_tableau_import_block(self.t._h, lo, hi, C.c_void_p(buf.data_ptr())))
+
+    def commit(self):
+        self.ctx.check(self._lib.sk_tableau_commit_blocks(self.t._h))
+
+    def measure_batch(self, qubits, seed, ordinal0):
+        return self.t.measure_batch(qubits, seed, ordinal0)
+
+    def export_block(self, lo, hi, buf):
+        self.ctx.check(self._lib.sk_tableau_export_block(self.t._h, lo, hi, C.c_void_p(buf.data_ptr())))
+
+    def close(self):
+        self.t.close()
 
 
 class Exchange:
@@ -178,7 +220,13 @@ class ShardedTableau:
         for l, s in enumerate(self.shards):
             assert (s.lo, s.hi) == self.ranges[self.first + l], "shard does not hold the slots of its global index"
         self._win = 64
-        self.stats = {"n_rand": 0, "n_det": 0, "searches": 0}
+        self.stats = {"n_rand": 0, "n_det": 0, "searches": 0, "replicated_blocks": 0}
+        # A measurement block is handled by the exchange-per-measurement protocol only up to its first random measurement; from
+        # there every rank assembles the full tableau (ONE allgather of the shards' rows), runs the single-GPU measurement kernel on
+        # it -- the same result everywhere -- and takes its rows back.  False: the per-measurement protocol throughout (the only
+        # option when the full tableau does not fit one GPU).
+        self.replicate_random_blocks = True
+        self._full = None
 
     # -- construction on CUDA ------------------------------------------------------------------
     @classmethod
@@ -199,6 +247,8 @@ class ShardedTableau:
         return t
 
     def close(self):
+        if self._full is not None:
+            self._full.close(); self._full = None
         for s in self.shards:
             s.close()
         self.shards = []
@@ -243,6 +293,12 @@ class ShardedTableau:
                     out[pos:pos + r0] = self.shards[0].det_combine(parts)
                     det[pos:pos + r0] = 1
                     self.stats["n_det"] += r0
+                if r0 < w and self.replicate_random_blocks:         # the rest of the block on the assembled tableau
+                    o, d = self._replicated_block(qubits[pos + r0:], seed, ordinal0 + pos + r0)
+                    out[pos + r0:] = o; det[pos + r0:] = d
+                    self.stats["n_rand"] += int((d == 0).sum()); self.stats["n_det"] += int((d != 0).sum())
+                    self._win = 64
+                    return out, det
                 if r0 < w:                                          # first random measurement of the window
                     p, q = int(cand[r0]), int(qs[r0])
                     owner = self.owner_of(p)
@@ -260,6 +316,28 @@ class ShardedTableau:
                     pos += w
                     self._win = min(8192, self._win * 4)
         return out, det
+
+    def _replicated_block(self, qubits, seed: int, ordinal0: int):
+        """Measurements `qubits` (ordinals ordinal0..) on the full tableau assembled from all shards; rows back afterwards."""
+        sh0 = self.shards[0]
+        words = max(sh0.block_words(hi - lo) for lo, hi in self.ranges)
+        loc = [s.new_block(words) for s in self.shards]
+        for s, b in zip(self.shards, loc):
+            s.export_rows(b)
+        allb = self.ex.allgather([b.view(1, words) for b in loc])       # [G, 1, words], shard order
+        if self._full is None:
+            self._full = sh0.make_full()
+        for g, (lo, hi) in enumerate(self.ranges):
+            if hi > lo:
+                self._full.import_block(lo, hi, allb[g, 0])
+        self._full.commit()
+        o, d = self._full.measure_batch(np.ascontiguousarray(qubits, np.uint32), seed, ordinal0)
+        for s, b in zip(self.shards, loc):
+            if s.hi > s.lo:
+                self._full.export_block(s.lo, s.hi, b)
+                s.import_rows(b)
+        self.stats["replicated_blocks"] += 1
+        return o, d
 
     def sim(self, circ, seed: int):
         """Clifford runs -> apply_gates, measurement runs -> measure_batch.  -> (outcomes, deterministic)"""

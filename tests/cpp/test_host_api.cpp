@@ -95,6 +95,12 @@ static void gpu_checks() {
       SimResult ref = sim(c5, EngineConfig{1, 20250703, false});
       ShardedTableau st(c5.n, 3);
       MeasurementRecord rec = st.sim(c5, 20250703);
+      CHECK(st.replicated_blocks >= 1);                 // random blocks ran on the assembled tableau (the default)
+      { ShardedTableau per(c5.n, 3); per.replicate_random_blocks = false;      // ... and with an exchange per measurement: same record
+        MeasurementRecord r2 = per.sim(c5, 20250703);
+        bool eq = r2.size() == rec.size() && per.replicated_blocks == 0;
+        for (size_t i = 0; eq && i < rec.size(); ++i) eq = r2[i].outcome == rec[i].outcome && r2[i].deterministic == rec[i].deterministic;
+        CHECK(eq); }
       bool same = rec.size() == ref.record.size();
       for (size_t i = 0; same && i < rec.size(); ++i)
           same = rec[i].gate_index == ref.record[i].gate_index && rec[i].outcome == ref.record[i].outcome && rec[i].deterministic == ref.record[i].deterministic;

@@ -42,19 +42,29 @@ int main(int argc, char** argv) {
         NcclExchange ex(id, rank, world);
         Circuit c = surface_code_circuit(d, rounds, true);
         SimResult ref = sim(c, EngineConfig{1, 20250703, false});
-        ShardedTableau st(c.n, local, &ex);
-        const auto t0 = std::chrono::steady_clock::now();
-        MeasurementRecord rec = st.sim(c, 20250703);
-        Device::instance().sync();
-        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        bool same = rec.size() == ref.record.size();
-        for (size_t i = 0; same && i < rec.size(); ++i) same = rec[i].outcome == ref.record[i].outcome && rec[i].deterministic == ref.record[i].deterministic;
-        auto all = ref.tableau.rows(); auto mine = st.local_rows();
-        bool rows_same = !mine.empty() || world * local > int((c.n + 63) / 64);
-        for (const auto& [idx, row] : mine) rows_same = rows_same && row == all[idx];
-        std::printf("rank %d/%d: d=%u rounds=%u local_shards=%d record %s rows %s | ncclAllReduce(min) %zu ncclAllGather %zu ncclBroadcast %zu, %zu payload bytes, %.1f ms\n",
-                    rank, world, d, rounds, local, same ? "ok" : "DIFFERS", rows_same ? "ok" : "DIFFER", ex.calls()[0], ex.calls()[1], ex.calls()[2], ex.bytes(), ms);
-        if (!same || !rows_same || ex.calls()[0] == 0 || ex.calls()[2] == 0) return 1;
+        auto all = ref.tableau.rows();
+        for (int per_measurement = 0; per_measurement < 2; ++per_measurement) {
+            // 0: random blocks on the tableau assembled by ONE ncclAllGather of the rows (the default); 1: an exchange per measurement
+            ShardedTableau st(c.n, local, &ex);
+            st.replicate_random_blocks = per_measurement == 0;
+            const size_t c0[3] = {ex.calls()[0], ex.calls()[1], ex.calls()[2]};
+            const size_t b0 = ex.bytes();
+            const auto t0 = std::chrono::steady_clock::now();
+            MeasurementRecord rec = st.sim(c, 20250703);
+            Device::instance().sync();
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            bool same = rec.size() == ref.record.size();
+            for (size_t i = 0; same && i < rec.size(); ++i) same = rec[i].outcome == ref.record[i].outcome && rec[i].deterministic == ref.record[i].deterministic;
+            auto mine = st.local_rows();
+            bool rows_same = !mine.empty() || world * local > int((c.n + 63) / 64);
+            for (const auto& [idx, row] : mine) rows_same = rows_same && row == all[idx];
+            const size_t nar = ex.calls()[0] - c0[0], nag = ex.calls()[1] - c0[1], nbc = ex.calls()[2] - c0[2];
+            std::printf("rank %d/%d: d=%u rounds=%u local_shards=%d %s: record %s rows %s | ncclAllReduce(min) %zu ncclAllGather %zu ncclBroadcast %zu, %zu payload bytes, %.1f ms\n",
+                        rank, world, d, rounds, local, per_measurement ? "exchange per measurement" : "replicated random blocks", same ? "ok" : "DIFFERS", rows_same ? "ok" : "DIFFER",
+                        nar, nag, nbc, ex.bytes() - b0, ms);
+            if (!same || !rows_same || nar == 0 || nag == 0) return 1;
+            if (per_measurement ? nbc == 0 : (nbc != 0 || st.replicated_blocks == 0)) return 1;
+        }
         // an NCCL failure surfaces as stabkit::Error with the SK_ENCCL text
         bool threw = false;
         try { std::vector<uint64_t> dummy; ex.broadcast(nullptr, nullptr, 8, world + 7); } catch (const Error& e) { threw = std::strstr(e.what(), "ncclBroadcast") != nullptr; }

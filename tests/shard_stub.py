@@ -130,6 +130,40 @@ class StubShard:
             self.destab[pl] = [px, pz, pr]
             self.stab[pl] = [0, 1 << q, outcome]
 
+    # -- replicated elimination of a random block (same block layout as sk_shard_export_rows) ---------------
+    def block_words(self, nloc=None):
+        nloc = (self.hi - self.lo) if nloc is None else nloc
+        return 4 * nloc * self.Wp + 2 * ((nloc + 63) // 64)
+
+    def new_block(self, words):
+        return torch.zeros(max(words, 1), dtype=torch.int64)
+
+    def export_rows(self, buf):
+        k = self.hi - self.lo
+        w = np.zeros(buf.numel(), np.uint64)
+        sw = (k + 63) // 64
+        for half, rows in enumerate((self.stab, self.destab)):
+            for i, r in enumerate(rows):
+                base = (half * k + i) * 2 * self.Wp
+                w[base:base + self.W] = np.frombuffer(r[0].to_bytes(8 * self.W, "little"), np.uint64)
+                w[base + self.Wp:base + self.Wp + self.W] = np.frombuffer(r[1].to_bytes(8 * self.W, "little"), np.uint64)
+                if r[2]: w[4 * k * self.Wp + half * sw + (i >> 6)] |= np.uint64(1) << np.uint64(i & 63)
+        buf.copy_(torch.from_numpy(w.view(np.int64)))
+
+    def import_rows(self, buf):
+        k = self.hi - self.lo
+        w = np.ascontiguousarray(buf.numpy()).view(np.uint64)
+        sw = (k + 63) // 64
+        for half, rows in enumerate((self.stab, self.destab)):
+            for i in range(k):
+                base = (half * k + i) * 2 * self.Wp
+                x = int.from_bytes(w[base:base + self.W].tobytes(), "little"); z = int.from_bytes(w[base + self.Wp:base + self.Wp + self.W].tobytes(), "little")
+                sg = int((int(w[4 * k * self.Wp + half * sw + (i >> 6)]) >> (i & 63)) & 1)
+                rows[i] = [x, z, sg]
+
+    def make_full(self):
+        return StubFull(self.n)
+
     def download(self):
         k = self.hi - self.lo
         x = np.zeros((2 * k, self.W), np.uint64); z = np.zeros_like(x); r = np.zeros(2 * k, np.uint8)
@@ -138,3 +172,50 @@ class StubShard:
             z[i] = np.frombuffer(row[1].to_bytes(8 * self.W, "little"), np.uint64)
             r[i] = row[2]
         return x, z, r
+
+
+class StubFull:
+    """Full tableau for the replicated block on CPU: the oracle's tableau (test infrastructure) fed with shard blocks."""
+
+    def __init__(self, n):
+        from oracle import oracle_py as orc
+        self.orc, self.n, self.W = orc, n, (n + 63) // 64
+        self.Wp = (self.W + 1) & ~1
+        self.x = np.zeros((2 * n, self.W), np.uint64); self.z = np.zeros_like(self.x); self.r = np.zeros(2 * n, np.uint8)
+        self.t = orc.Tableau(n)
+
+    def import_block(self, lo, hi, buf):
+        k = hi - lo
+        w = np.ascontiguousarray(buf.numpy()).view(np.uint64)
+        sw = (k + 63) // 64
+        for half in range(2):
+            for i in range(k):
+                base = (half * k + i) * 2 * self.Wp
+                row = half * self.n + lo + i
+                self.x[row] = w[base:base + self.W]; self.z[row] = w[base + self.Wp:base + self.Wp + self.W]
+                self.r[row] = (int(w[4 * k * self.Wp + half * sw + (i >> 6)]) >> (i & 63)) & 1
+
+    def commit(self):
+        self.t.set(self.x, self.z, self.r)
+
+    def measure_batch(self, qubits, seed, ordinal0):
+        gates = [(M, int(q), 0) for q in qubits]
+        o, d, rc = self.t.sim(gates, seed, 1, ordinal0)
+        assert rc == 0
+        self.x, self.z, self.r = self.t.get()
+        return o, d
+
+    def export_block(self, lo, hi, buf):
+        k = hi - lo
+        w = np.zeros(buf.numel(), np.uint64)
+        sw = (k + 63) // 64
+        for half in range(2):
+            for i in range(k):
+                base = (half * k + i) * 2 * self.Wp
+                row = half * self.n + lo + i
+                w[base:base + self.W] = self.x[row]; w[base + self.Wp:base + self.Wp + self.W] = self.z[row]
+                if self.r[row]: w[4 * k * self.Wp + half * sw + (i >> 6)] |= np.uint64(1) << np.uint64(i & 63)
+        buf.copy_(torch.from_numpy(w.view(np.int64)))
+
+    def close(self):
+        pass

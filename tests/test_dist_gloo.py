@@ -91,10 +91,12 @@ def test_world_size_2_gloo_row_sharded_protocol():
             if k >= 6: b = int(rng.integers(0, n - 1)); b += b >= a
             gates.append((k, a, b))
         for circ, seed in ((sk.surface_code_circuit(3, 3, True), 20250703), (sk.surface_code_circuit(5, 2, True), 1), (sk.Circuit(n, gates), 99)):
+          for replicate in (True, False):       # random blocks on the assembled tableau (default) / exchange per measurement
             ex = Exchange(2)
             assert ex.nshards == 4
             shards = [StubShard(circ.n, *dist.slot_range(circ.n, rank * 2 + l, 4)) for l in range(2)]
             t = ShardedTableau(circ.n, shards, ex)
+            t.replicate_random_blocks = replicate
             out, det = t.sim(circ, seed)
             x, z, r = t.gather_tableau()
             o = orc.Tableau(circ.n)
@@ -103,7 +105,10 @@ def test_world_size_2_gloo_row_sharded_protocol():
             assert rc == 0 and (out == oo).all() and (det == od).all(), "record differs from the oracle"
             assert (x == ox).all() and (z == oz).all() and (r == orr).all(), "tableau differs from the oracle"
             assert ex.calls["allreduce_min"] >= 1 and ex.calls["allgather"] >= 1
-            if (od == 0).any(): assert ex.calls["broadcast"] == int((od == 0).sum())
+            assert t.stats["n_rand"] == int((od == 0).sum()) and t.stats["n_det"] == int((od != 0).sum())
+            if (od == 0).any():
+                if replicate: assert ex.calls["broadcast"] == 0 and t.stats["replicated_blocks"] >= 1
+                else: assert ex.calls["broadcast"] == int((od == 0).sum()) and t.stats["replicated_blocks"] == 0
         # CounterRng bits (ref: rng.hpp:33-39; SURVEY 8c probe values)
         assert "".join(str(counter_bit(0, i)) for i in range(32)) == "01111010000000100000010000111101"
         assert "".join(str(counter_bit(7, i)) for i in range(32)) == "01010011011101100101001001101001"

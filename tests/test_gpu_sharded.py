@@ -12,8 +12,16 @@ SEED = 20250703
 
 
 def run_both(sk, orc, circ, seed, local_shards):
+    """Both ways a random measurement block can run: on the tableau assembled from all shards (the default: one allgather of
+    the rows per block) and with an exchange per measurement (replicate_random_blocks = False)."""
+    run_one(sk, orc, circ, seed, local_shards, False)
+    return run_one(sk, orc, circ, seed, local_shards, True)
+
+
+def run_one(sk, orc, circ, seed, local_shards, replicate):
     from paper_2507_03092_b200.sharded import ShardedTableau
     t = ShardedTableau.create_cuda(circ.n, local_shards=local_shards, device_index=0)
+    t.replicate_random_blocks = replicate
     try:
         out, det = t.sim(circ, seed)
         x, z, r = t.gather_tableau()
@@ -30,6 +38,7 @@ def run_both(sk, orc, circ, seed, local_shards):
     assert (x == ox).all() and (z == oz).all(), "tableau bits differ"
     assert (r == orr).all(), "signs differ"
     assert stats["n_rand"] == int((od == 0).sum()) and stats["n_det"] == int((od == 1).sum())
+    if (od == 0).any(): assert (stats["replicated_blocks"] >= 1) == replicate
     return stats, k
 
 
@@ -105,17 +114,21 @@ def test_two_processes_one_shard_each_over_a_process_group(sk, orc):
         from oracle import oracle_py as orc
         rank, local_rank, world = dist.init("gloo")
         for circ, seed in ((sk.surface_code_circuit(7, 7, True), 20250703), (sk.random_layered_circuit(128, 3), 5)):
+          for replicate in (True, False):
             t = ShardedTableau.create_cuda(circ.n, local_shards=1, device_index=0)
+            t.replicate_random_blocks = replicate
             out, det = t.sim(circ, seed)
             x, z, r = t.gather_tableau()
-            calls = dict(t.ex.calls)
+            calls = dict(t.ex.calls); nrep = t.stats["replicated_blocks"]
             t.close()
             o = orc.Tableau(circ.n)
             oo, od, rc = o.sim(circ.gates, seed)
             ox, oz, orr = o.get()
             assert rc == 0 and (out == oo).all() and (det == od).all(), "record differs from the oracle"
             assert (x == ox).all() and (z == oz).all() and (r == orr).all(), "tableau differs from the oracle"
-            assert calls["broadcast"] == int((od == 0).sum()) and calls["allgather"] >= 1 and calls["allreduce_min"] >= 1
+            assert calls["allgather"] >= 1 and calls["allreduce_min"] >= 1
+            if replicate: assert calls["broadcast"] == 0 and nrep >= 1
+            else: assert calls["broadcast"] == int((od == 0).sum())
         dist.finalize()
         print("rank", rank, "ok")
     """ % root)
