@@ -1078,12 +1078,23 @@ __device__ __noinline__ void panel_factorise(const MeasArgs& a, u64* sp, PanelSm
 // Product of the listed rows (R layout) with the running product in REGISTERS: every lane owns NWL lane-strided words and the
 // words of two rows are in flight together, so a short list costs one L2 round trip instead of one per word chunk.
 // Returns this lane's share of the i-exponent (row signs not included).
-template <int NWL>
+template <int NWL, int ROWS = 2>      // ROWS = partner rows in flight (2, or 1 where registers are scarce)
 __device__ __forceinline__ int warp_mul_wide(const u64* __restrict__ base, int W, int Wp, const u32* list, int cnt, int lane) {
     u64 ax[NWL], az[NWL];
 #pragma unroll
     for (int k = 0; k < NWL; ++k) { ax[k] = 0; az[k] = 0; }
     int e = 0;
+    if (ROWS == 1) {
+        for (int i0 = 0; i0 < cnt; ++i0) {
+            const u64* r0 = base + (size_t)(2 * list[i0]) * Wp;
+            u64 x0[NWL], z0[NWL];
+#pragma unroll
+            for (int k = 0; k < NWL; ++k) { const int w = lane + 32 * k; const bool ok = w < W; x0[k] = ok ? ldcg(r0 + w) : 0ull; z0[k] = ok ? ldcg(r0 + Wp + w) : 0ull; }
+#pragma unroll
+            for (int k = 0; k < NWL; ++k) { e += g_word(x0[k], z0[k], ax[k], az[k]); ax[k] ^= x0[k]; az[k] ^= z0[k]; }
+        }
+        return e;
+    }
     for (int i0 = 0; i0 < cnt; i0 += 2) {
         const bool two = i0 + 1 < cnt;
         const u64* r0 = base + (size_t)(2 * list[i0]) * Wp;
@@ -1167,10 +1178,11 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
             continue;
         }
         int e;
-        if (nwl <= 1) e = warp_mul_wide<1>(a.m.rows, W, Wp, wlist, npart, lane);
-        else if (nwl <= 2) e = warp_mul_wide<2>(a.m.rows, W, Wp, wlist, npart, lane);
-        else if (nwl <= 4) e = warp_mul_wide<4>(a.m.rows, W, Wp, wlist, npart, lane);
-        else if (nwl <= 6) e = warp_mul_wide<6>(a.m.rows, W, Wp, wlist, npart, lane);
+        constexpr int RIF = KERNEL == 1 ? 1 : 2;        // k_wave trades rows in flight for resident warps (one measurement per warp)
+        if (nwl <= 1) e = warp_mul_wide<1, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 2) e = warp_mul_wide<2, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 4) e = warp_mul_wide<4, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 6) e = warp_mul_wide<6, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
         else {
             for (int w = lane; w < Wp; w += 32) { acc_x[w] = 0; acc_z[w] = 0; }
             e = warp_mul_list(a.m.rows, W, Wp, wlist, npart, acc_x, acc_z, lane);
@@ -1195,7 +1207,7 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
 // the last CTA to finish finds the first random (or too long) measurement r0, accounts for [0, r0) and leaves r0 in ws->wpos;
 // k_measure_block then starts there (and exits at once when the whole block was deterministic).
 constexpr int kWaveThreads = 256;
-__global__ void __launch_bounds__(kWaveThreads, 3)
+__global__ void __launch_bounds__(kWaveThreads, 4)
 k_wave(const __grid_constant__ MeasArgs a, int wend) {
     __shared__ u32 s_wlist[kWaveThreads / 32][kWarpList];
     __shared__ int s_last, s_dummy[2];
