@@ -77,10 +77,10 @@ struct MeasWs {
     u32 progress;       // panel mode: factorisation steps published so far in this launch (monotone)
     u32 r0[4];          // per-wave ~index of the first random measurement (0 = none), max-reduced; 3 slots rotate
     u32 exitcnt;        // CTAs that have left the kernel: the last one re-zeroes this block for the next launch
-    u32 wdone;          // k_wave: CTAs that have finished (its last CTA does the accounting and re-zeroes this word and r0[3])
+    u32 wdone;          // k_wave_cols / k_wave_rows: CTAs that have finished (the last one publishes wpos / accounts, and re-zeroes this word and r0[3])
     // ---- persistent
     u32 err;            // bit0 odd phase (invariant), bit31 barrier timeout, bit30 TMA timeout
-    u32 wpos;           // k_wave -> k_measure_block: measurements [0, wpos) of the block are done (deterministic prefix)
+    u32 wpos;           // k_wave_cols -> k_wave_rows, k_measure_block: measurements [0, wpos) of the block are deterministic and left to k_wave_rows
     u64 n_rand, n_det, k_rand, k_det, waves;
     u64 prof[8];        // CTA-0 wall time (ns): P1, P2, gather, factorise, values+detA, apply+detB, barriers(wave), barriers(panel)
     u64 panels;
@@ -109,6 +109,8 @@ struct MeasArgs {
     uint8_t* dets;      // [count]
     MeasWs* ws;
     u32* wpiv;          // [2][window] pivot of a window slot (0xffffffff = deterministic), by wave parity
+    u32* wl;            // [2*window][kWarpList] k_wave_cols -> k_wave_rows: partner stabilizers of each measurement
+    u64* wsgn;          // [W] k_wave_cols -> k_wave_rows: the stabilizer signs at the time of the measurement block
     // panel mode scratch
     int B;              // panel width (<= kPanelMax)
     u64* pan;           // [B][RW] gathered panel ; after F: destabilizer halves of deterministic steps hold D_j
@@ -129,7 +131,7 @@ struct MeasArgs {
     int destab_stale;   // the R form holds only the stabilizer rows (host transposed that half): panel mode derives the rest itself
     int force_columns;  // SK_PANEL_COLUMNS=1: always use the column-form factorisation (testing aid)
     int lv_enable;      // replicated level-form panel path (kernels_panel.cuh); SK_PANEL_REPL=0 disables
-    int from_wave;      // k_wave ran first: start at ws->wpos
+    int from_wave;      // the wave kernels ran first: start at ws->wpos
     int seq_rows;       // SK_PANEL_SEQ=1: step-by-step row-form factorisation instead of the level form (A/B and testing aid)
 };
 
@@ -1120,17 +1122,13 @@ __device__ __forceinline__ int warp_mul_wide(const u64* __restrict__ base, int W
 // is empty -- K4, the product of the partner stabilizers (destabilizer half of the same column -> rows of the R form).
 // Results per slot go to recj/recn (measurement index or -1, partner count | odd-phase flag << 30); products with more than
 // kWarpList partners are left to the whole CTA (slot pushed to heavy[]).
-// grec != nullptr (k_wave): the records go to grec[j] (0x80000000 = not a finished deterministic measurement), the index of the first
-// random -- or too long -- measurement to *r0slot, and nothing is left to the CTA.
-// (a template so that each calling kernel gets a copy compiled for its own register budget)
-template <int KERNEL>
 __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u32 wave, int gw, int GW, u32* wlist, int* nheavy, int* heavy,
-                                        int* recj, int* recn, u64* acc_x, u64* acc_z, u32* grec = nullptr, u32* r0slot = nullptr) {
+                                        int* recj, int* recn, u64* acc_x, u64* acc_z) {
     const int lane = threadIdx.x & 31;
     const int W = a.m.W, Wp = a.m.Wp, RW = a.m.RW;
     const int nwl = (W + 31) / 32;
-    if (!grec && lane < kSlotsPerWarp) recj[lane] = -1;
-    if (!r0slot) r0slot = &a.ws->r0[wave % 3];
+    if (lane < kSlotsPerWarp) recj[lane] = -1;
+    u32* r0slot = &a.ws->r0[wave % 3];
     __syncwarp();
     int rec = 0;
     const bool trc = a.prof && lane == 0 && (gw == 0 || gw == GW / 2) && pos == 0;
@@ -1169,8 +1167,8 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
         piv = warp_min(piv);
         __syncwarp();
         WV_TRACE(1);
-        if (piv != 0xffffffffu || (grec && (npart > kWarpList || nwl > 6))) {       // random: the first one of the window ends the deterministic prefix
-            if (lane == 0) { atomicMax(r0slot, ~(u32)j); if (grec) grec[j] = 0x80000000u; }      // stored inverted: zero-initialised, max = smallest index
+        if (piv != 0xffffffffu) {       // random: the first one of the window ends the deterministic prefix
+            if (lane == 0) atomicMax(r0slot, ~(u32)j);      // stored inverted: zero-initialised, max = smallest index
             continue;
         }
         if (npart > kWarpList) {                  // tree-reduced by the whole CTA
@@ -1178,7 +1176,7 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
             continue;
         }
         int e;
-        constexpr int RIF = KERNEL == 1 ? 1 : 2;        // k_wave trades rows in flight for resident warps (one measurement per warp)
+        constexpr int RIF = 2;
         if (nwl <= 1) e = warp_mul_wide<1, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
         else if (nwl <= 2) e = warp_mul_wide<2, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
         else if (nwl <= 4) e = warp_mul_wide<4, RIF>(a.m.rows, W, Wp, wlist, npart, lane);
@@ -1193,49 +1191,139 @@ __device__ __noinline__ void wave_slots(const MeasArgs& a, int pos, int wend, u3
         WV_TRACE(3);
         if (lane == 0) {
             a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1;
-            if (grec) grec[j] = u32(npart) | (u32(e & 1) << 30);
-            else if (rec < kSlotsPerWarp) { recj[rec] = j; recn[rec] = npart | ((e & 1) << 30); }
+            if (rec < kSlotsPerWarp) { recj[rec] = j; recn[rec] = npart | ((e & 1) << 30); }
         }
         __syncwarp();
     }
 }
 
 
-// Wave mode as a kernel of its own (launched in front of k_measure_block for long measurement blocks): an ordinary grid with
+// Wave mode as two kernels of their own (launched in front of k_measure_block for long measurement blocks): ordinary grids with
 // one warp per pending measurement instead of the one-CTA-per-SM cooperative grid whose warps walk three slots each, so the
-// deterministic rounds of a memory experiment are one short pass.  Speculative like the in-kernel wave: every slot is evaluated,
-// the last CTA to finish finds the first random (or too long) measurement r0, accounts for [0, r0) and leaves r0 in ws->wpos;
-// k_measure_block then starts there (and exits at once when the whole block was deterministic).
+// deterministic rounds of a memory experiment are two short passes -- and, being split by the FORM they read, they leave the
+// critical path:
+//   k_wave_cols  reads only the gate (C) form: pivot search on the stabilizer half of each measured x column, partner list from
+//                the destabilizer half (written to a.wl), the stabilizer signs copied to a.wsgn.  Shares a launch with the
+//                C -> R transposition, which reads the same columns (k_transpose_wave).
+//   k_wave_rows  reads only the row (R) form, the lists and the sign copy: the partner products and the outcomes.  Nothing the
+//                next run of gate layers writes (C form, live signs), so it runs on the side stream UNDER those layers.
+// Speculative like the in-kernel wave: k_wave_cols evaluates every slot and its last CTA leaves in ws->wpos where k_measure_block
+// has to start: at the end of the block when no measurement was random or too long for a warp (k_measure_block then exits at once
+// and k_wave_rows owns the block); otherwise at 0 when the two overlap (`pipe`: k_wave_rows then does nothing, the cooperative
+// kernel is about to change rows) or at the first such measurement when they run in order (k_wave_rows does the prefix).
 constexpr int kWaveThreads = 256;
+// CTA `cta` of `nctas` (any grid shape)
+__device__ __forceinline__ void wave_cols_body(const MeasArgs& a, int wend, int pipe, int cta, int nctas) {
+    __shared__ int s_last;
+    MeasWs* ws = a.ws;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int W = a.m.W, RW = a.m.RW;
+    const int nwl = (W + 31) / 32;
+    const int GW = nctas * (kWaveThreads / 32);
+    if (cta == 0) for (int w = tid; w < W; w += kWaveThreads) a.wsgn[w] = ldcg(a.m.sgn + w);
+    for (int j = cta * (kWaveThreads / 32) + (tid >> 5); j < wend; j += GW) {
+        const u64* xcol = a.m.cols + (size_t)(2 * a.qubits[j]) * RW;
+        u32* wl = a.wl + (size_t)j * kWarpList;
+        u32 piv = 0xffffffffu;
+        int npart = 0;
+        for (int w0 = 0; w0 < W; w0 += 32 * kColChunk) {        // both halves of the column in one round trip per chunk
+            u64 sv[kColChunk], dv[kColChunk];
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) { const int w = w0 + 32 * t + lane; sv[t] = (w < W) ? ldcg(xcol + w) : 0ull; dv[t] = (w < W) ? ldcg(xcol + W + w) : 0ull; }
+            int mine = 0;
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                if (sv[t]) piv = min(piv, u32(w * 64 + __ffsll((long long)sv[t]) - 1));
+                mine += __popcll(dv[t]);
+            }
+            int incl = mine;                                    // partner list: exclusive prefix of the lanes' counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+            int ti = npart + incl - mine;
+            npart += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+            for (int t = 0; t < kColChunk; ++t) {
+                const int w = w0 + 32 * t + lane;
+                u64 v = dv[t];
+                while (v) { const int b = __ffsll((long long)v) - 1; v &= v - 1; if (ti < kWarpList) wl[ti] = u32(w * 64 + b); ++ti; }
+            }
+        }
+        piv = warp_min(piv);
+        if (lane == 0) {
+            const bool hard = piv != 0xffffffffu || npart > kWarpList || nwl > 6;
+            if (hard) atomicMax(&ws->r0[3], ~(u32)j);           // stored inverted: zero-initialised, max = smallest index
+            a.wpiv[j] = hard ? 0x80000000u : u32(npart);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) { __threadfence(); s_last = atomicAdd(&ws->wdone, 1u) == u32(nctas) - 1 ? 1 : 0; }
+    __syncthreads();
+    if (!s_last || tid) return;
+    __threadfence();
+    const u32 r0 = ~__ldcg(&ws->r0[3]);
+    ws->wpos = (r0 == 0xffffffffu) ? u32(wend) : (pipe ? 0u : r0);
+    ws->r0[3] = 0u; ws->wdone = 0u;
+}
+
 __global__ void __launch_bounds__(kWaveThreads, 4)
-k_wave(const __grid_constant__ MeasArgs a, int wend) {
+k_wave_cols(const __grid_constant__ MeasArgs a, int wend, int pipe) { wave_cols_body(a, wend, pipe, blockIdx.x, gridDim.x); }
+
+// The C -> R transposition (x and z halves: planes 1 and 2 of the grid) and k_wave_cols (plane 0, scheduled first: its chains of
+// dependent loads are the longer ones) as ONE launch: both only read the gate form, so they share the machine instead of a place
+// each on the critical path of a round.
+__global__ void __launch_bounds__(256, 4)
+k_transpose_wave(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                 u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                 size_t src_zoff, size_t dst_zoff, const __grid_constant__ MeasArgs a, int wend, int pipe) {
+    __shared__ __align__(16) u32 tin[kTrSmemWords];
+    pdl_trigger();
+    pdl_wait();
+    if (blockIdx.z == 0) { wave_cols_body(a, wend, pipe, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y); return; }
+    const int z = blockIdx.z - 1;
+    transpose_tile_regs(src + (size_t)z * src_zoff, src_stride, src_rows, src_words, dst + (size_t)z * dst_zoff, dst_stride, dst_rows, dst_words,
+                        blockIdx.x, blockIdx.y, tin);
+}
+
+__global__ void __launch_bounds__(kWaveThreads, 4)
+k_wave_rows(const __grid_constant__ MeasArgs a, int wend) {
     __shared__ u32 s_wlist[kWaveThreads / 32][kWarpList];
-    __shared__ int s_last, s_dummy[2];
+    __shared__ int s_last;
     __shared__ unsigned long long s_kd;
     __shared__ u32 s_odd;
     MeasWs* ws = a.ws;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    wave_slots<1>(a, 0, wend, 0, blockIdx.x * (kWaveThreads / 32) + warp, gridDim.x * (kWaveThreads / 32), s_wlist[warp], &s_dummy[0], &s_dummy[1],
-               nullptr, nullptr, nullptr, nullptr, a.wpiv, &ws->r0[3]);
-    __syncthreads();
-    if (tid == 0) { __threadfence(); s_last = atomicAdd(&ws->wdone, 1u) == gridDim.x - 1 ? 1 : 0; s_kd = 0; s_odd = 0; }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const u32 r0 = ~__ldcg(&ws->r0[3]);
-    const int dend = (r0 == 0xffffffffu) ? wend : int(r0);
+    wend = int(__ldcg(&ws->wpos));                            // deterministic prefix; 0: the cooperative kernel owns this block
+    if (wend == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = a.m.W, Wp = a.m.Wp;
+    const int nwl = (W + 31) / 32;
+    const int GW = gridDim.x * (kWaveThreads / 32);
+    u32* wlist = s_wlist[warp];
     unsigned long long kd = 0; u32 odd = 0;
-    for (int j = tid; j < dend; j += kWaveThreads) { const u32 r = __ldcg(a.wpiv + j); kd += r & 0x3fffffffu; odd |= (r >> 30) & 1u; }
-    kd = (unsigned long long)__reduce_add_sync(0xffffffffu, (u32)kd);
-    odd = __reduce_or_sync(0xffffffffu, odd);
-    if ((tid & 31) == 0) { atomicAdd(&s_kd, kd); if (odd) atomicOr(&s_odd, 1u); }
-    __syncthreads();
-    if (tid == 0) {
-        if (dend > 0) { atomicAdd(&ws->n_det, (u64)dend); atomicAdd(&ws->k_det, (u64)s_kd); }
-        atomicAdd(&ws->waves, 1ull);
-        if (s_odd) atomicOr(&ws->err, 1u);
-        ws->wpos = u32(dend); ws->r0[3] = 0u; ws->wdone = 0u;
+    for (int j = blockIdx.x * (kWaveThreads / 32) + warp; j < wend; j += GW) {
+        const int npart = int(__ldcg(a.wpiv + j));
+        const u32* wl = a.wl + (size_t)j * kWarpList;
+        for (int i = lane; i < npart; i += 32) wlist[i] = __ldcg(wl + i);
+        __syncwarp();
+        int e;
+        if (nwl <= 1) e = warp_mul_wide<1, 1>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 2) e = warp_mul_wide<2, 1>(a.m.rows, W, Wp, wlist, npart, lane);
+        else if (nwl <= 4) e = warp_mul_wide<4, 1>(a.m.rows, W, Wp, wlist, npart, lane);
+        else e = warp_mul_wide<6, 1>(a.m.rows, W, Wp, wlist, npart, lane);
+        for (int i = lane; i < npart; i += 32) e += 2 * sign_bit(a.wsgn, int(wlist[i]));
+        e = warp_sum(e) & 3;
+        if (lane == 0) { a.outcomes[j] = uint8_t(e >> 1); a.dets[j] = 1; kd += (unsigned long long)npart; odd |= u32(e & 1); }
+        __syncwarp();
     }
+    if (tid == 0) { s_kd = 0; s_odd = 0; }
+    __syncthreads();
+    if (lane == 0) { if (kd) atomicAdd(&s_kd, kd); if (odd) atomicOr(&s_odd, 1u); }
+    __syncthreads();
+    if (tid) return;
+    if (s_kd) atomicAdd(&ws->k_det, (u64)s_kd);
+    if (s_odd) atomicOr(&ws->err, 1u);
+    __threadfence();
+    if (atomicAdd(&ws->wdone, 1u) == gridDim.x - 1) { atomicAdd(&ws->n_det, (u64)wend); atomicAdd(&ws->waves, 1ull); ws->wdone = 0u; }
 }
 
 }  // namespace skd
@@ -1274,7 +1362,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
     u64* acc_x = sm.acc + (size_t)warp * 2 * Wp;
     u64* acc_z = acc_x + Wp;
 
-    int pos = a.from_wave ? int(__ldcg(&ws->wpos)) : 0;        // k_wave already finished the deterministic prefix of the block
+    int pos = a.from_wave ? int(__ldcg(&ws->wpos)) : 0;        // the wave kernels own the deterministic prefix of the block
     u32 wave = 1;
     bool panel_mode = false;
     u64 t_prof = a.prof ? gtime() : 0;
@@ -1287,7 +1375,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         if (blockIdx.x == 0 && tid == 0) ws->r0[(wave + 1) % 3] = 0u;
         if (tid == 0) s_nheavy = 0;
         __syncthreads();
-        wave_slots<0>(a, pos, wend, wave, gw, GW, s_wlist[warp], &s_nheavy, s_heavy, s_recj[warp], s_recn[warp], acc_x, acc_z);
+        wave_slots(a, pos, wend, wave, gw, GW, s_wlist[warp], &s_nheavy, s_heavy, s_recj[warp], s_recn[warp], acc_x, acc_z);
         __syncthreads();
         const int nheavy = s_nheavy;
         for (int h = 0; h < nheavy; ++h) {

@@ -103,6 +103,70 @@ k_transpose_bits(const u32* __restrict__ src, size_t src_stride, int src_rows, i
     else transpose_bits_body<false>(src, src_stride, src_rows, src_words, dst, dst_stride, dst_rows, dst_words, tin, tout);
 }
 
+// ---- register-block variant -------------------------------------------------------------------------------------------
+// The shuffle version above is bound by the shared-memory / shuffle pipe (ncu round 2: short-scoreboard stalls 13 of 30 cycles per
+// issue, L1 pipe 77 % busy, 8.4 M warp instructions for the stabilizer half at d=71): seven such operations per 32x32 block.  Here
+// ONE THREAD owns a 32x32-bit block in 32 registers and transposes it with the five swap stages as plain ALU work (two byte
+// permutes per pair for the 16- and 8-bit stages), so a block costs one conflict-free shared load and one global store per word:
+// about a quarter of the instructions and a seventh of the shared-memory traffic.
+//   tile = 512 src rows x 16 src words (64 contiguous bytes per src row: two full sectors per load);
+//   thread (warp wv, lane l): row-block l & 15, src word 2*wv + (l >> 4)  ->  a half-warp stores 16 consecutive words (64 bytes)
+//   of each of its 32 dst rows straight from registers.
+// Requires every stride / width / offset to be a multiple of four 32-bit words (checked by the host).
+constexpr int kTrRows = 512, kTrWords = 16, kTrBlkStride = 32 * kTrWords + 2;     // +2 words: the 16 row-blocks x 2 words of a warp hit 32 distinct banks
+constexpr int kTrSmemWords = (kTrRows / 32) * kTrBlkStride;
+__device__ __forceinline__ void transpose_tile_regs(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                                                    u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                                                    int bx, int by, u32* tin) {
+    const int c0 = bx * kTrRows, w0 = by * kTrWords;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int idx = k * 256 + t, rr = idx >> 2, part = idx & 3;
+        const int gr = c0 + rr, gw = w0 + 4 * part;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (gr < src_rows && gw < src_words) v = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)gr * src_stride + gw));
+        u32* p = tin + (rr >> 5) * kTrBlkStride + (rr & 31) * kTrWords + 4 * part;      // 8-byte aligned (kTrBlkStride is even)
+        *reinterpret_cast<uint2*>(p) = make_uint2(v.x, v.y);
+        *reinterpret_cast<uint2*>(p + 2) = make_uint2(v.z, v.w);
+    }
+    __syncthreads();
+    const int lane = t & 31, blk = lane & 15, word = 2 * (t >> 5) + (lane >> 4);
+    u32 a[32];
+    const u32* q = tin + blk * kTrBlkStride + word;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = q[i * kTrWords];
+    // a[i] bit b  ->  a[b] bit i
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { const u32 lo = a[k], hi = a[k + 16]; a[k] = __byte_perm(lo, hi, 0x5410u); a[k + 16] = __byte_perm(lo, hi, 0x7632u); }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) if (!(k & 8)) { const u32 lo = a[k], hi = a[k + 8]; a[k] = __byte_perm(lo, hi, 0x6240u); a[k + 8] = __byte_perm(lo, hi, 0x7351u); }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) if (!(k & 4)) { const u32 x = ((a[k] >> 4) ^ a[k + 4]) & 0x0f0f0f0fu; a[k + 4] ^= x; a[k] ^= x << 4; }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) if (!(k & 2)) { const u32 x = ((a[k] >> 2) ^ a[k + 2]) & 0x33333333u; a[k + 2] ^= x; a[k] ^= x << 2; }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) if (!(k & 1)) { const u32 x = ((a[k] >> 1) ^ a[k + 1]) & 0x55555555u; a[k + 1] ^= x; a[k] ^= x << 1; }
+    const int gw = (c0 >> 5) + blk;
+    if (gw < dst_words) {
+        u32* d = dst + (size_t)(32 * (w0 + word)) * dst_stride + gw;
+        const int left = dst_rows - 32 * (w0 + word);
+#pragma unroll
+        for (int b = 0; b < 32; ++b) if (b < left) __stcg(d + (size_t)b * dst_stride, a[b]);
+    }
+}
+__global__ void __launch_bounds__(256, 4)
+k_transpose_regs(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,
+                 u32* __restrict__ dst, size_t dst_stride, int dst_rows, int dst_words,
+                 size_t src_zoff, size_t dst_zoff, const u32* __restrict__ flag) {
+    __shared__ __align__(16) u32 tin[kTrSmemWords];
+    pdl_trigger();
+    pdl_wait();
+    if (flag && __ldcg(flag) == 0u) return;
+    transpose_tile_regs(src + (size_t)blockIdx.z * src_zoff, src_stride, src_rows, src_words, dst + (size_t)blockIdx.z * dst_zoff, dst_stride, dst_rows, dst_words,
+                        blockIdx.x, blockIdx.y, tin);
+}
+
 // The same tile move as a device function for use inside a persistent kernel: `nthr` = 256 threads of one half-CTA
 // (thread index t in [0,256)), synchronised with the named barrier `bar_id`; tin/tout = 2 x 256 x 9 words of shared memory.
 __device__ __forceinline__ void transpose_tile_256(const u32* __restrict__ src, size_t src_stride, int src_rows, int src_words,

@@ -45,6 +45,8 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (const char* e = getenv("SK_PANEL_SEQ")) c->seq_rows = atoi(e);
     if (const char* e = getenv("SK_PDL")) c->pdl = atoi(e);
     if (const char* e = getenv("SK_WAVE_KERNEL")) c->no_wave_kernel = atoi(e) == 0;
+    if (const char* e = getenv("SK_PIPELINE")) c->no_pipe = atoi(e) == 0;
+    if (const char* e = getenv("SK_TRANSPOSE_REGS")) c->no_tr_regs = atoi(e) == 0;
     if (const char* e = getenv("SK_PANEL_REPL")) c->no_repl = atoi(e) == 0;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
     c->max_smem_optin = int(prop.sharedMemPerBlockOptin);
@@ -53,6 +55,10 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return SK_ECUDA; }
         c->own_stream = true;
     }
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) c->no_pipe = 1;
+    for (cudaEvent_t* e : {&c->ev_fork, &c->ev_cols, &c->ev_rows, &c->ev_side})
+        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) c->no_pipe = 1;
+    cudaGetLastError();
     {
         cudaMemPool_t pool = nullptr;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) { uint64_t keep = ~0ull; cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep); }
@@ -69,6 +75,8 @@ extern "C" void sk_ctx_destroy(sk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    for (cudaEvent_t e : {c->ev_fork, c->ev_cols, c->ev_rows, c->ev_side}) if (e) cudaEventDestroy(e);
     cudaFree(c->d_gates); cudaFree(c->d_tmp); cudaFree(c->d_err); cudaFree(c->d_ws);
     if (c->h_pin) cudaFreeHost(c->h_pin);
     if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -117,36 +125,48 @@ struct sk_tableau {
     size_t cols_bytes = 0, rows_bytes = 0, sgn_bytes = 0;
     u32* d_q = nullptr; uint8_t* d_out = nullptr; uint8_t* d_det = nullptr; size_t rec_cap = 0;
     int meas_grid = 0; size_t meas_smem = 0; bool lv_ok = false;
-    u32* d_wpiv = nullptr;
+    u32* d_wpiv = nullptr; u32* d_wl = nullptr; u64* d_wsgn = nullptr;
     // panel-mode scratch (kernels_measure.cuh)
     uint64_t uid = 0;               // distinguishes tableaux that reuse a host address (graph cache key)
     int B = 0; u64* d_pan = nullptr; u64* d_pivbuf = nullptr; u64* d_detacc = nullptr; PanelInfo* d_info = nullptr;
     u32* d_tlist = nullptr; u64* d_tM = nullptr; u64* d_rowM = nullptr; u64* d_tbits = nullptr; u32 tcap = 0; u32* d_alist_h = nullptr; u64* d_alist_b = nullptr; u32* d_dpart = nullptr;
 };
 
+// the main stream waits for what is still running on the side stream (k_wave_rows of the last measurement block): called
+// before anything that writes the row form or reuses the wave buffers, and before control goes back to the caller
+static void join_side(sk_ctx* c) {
+    if (!c->side_pending) return;
+    cudaStreamWaitEvent(c->stream, c->ev_side, 0);
+    c->side_pending = false;
+}
 // x and z halves in one launch (grid.z = 2); `flag` != nullptr makes the launch conditional on *flag
 static int32_t launch_transpose(sk_ctx* c, const u32* src, size_t sstride, int srows, int swords,
                                 u32* dst, size_t dstride, int drows, int dwords,
-                                size_t src_zoff, size_t dst_zoff, const u32* flag) {
-    dim3 grid((srows + 255) / 256, (swords + 7) / 8, 2);
-    if (c->pdl) {
+                                size_t src_zoff, size_t dst_zoff, const u32* flag, bool pdl = true) {
+    // register-block kernel when every row start and width is 16-byte aligned (true for tableaux with an even word count)
+    // and the matrix is large enough for its 512 x 512-bit tiles to fill the machine
+    const bool regs = !c->no_tr_regs && (size_t)((srows + kTrRows - 1) / kTrRows) * ((swords + kTrWords - 1) / kTrWords) * 2 >= (size_t)c->num_sms && ((sstride | dstride | src_zoff | dst_zoff | (size_t)swords | (size_t)dwords) & 3) == 0 &&
+                      ((reinterpret_cast<size_t>(src) | reinterpret_cast<size_t>(dst)) & 15) == 0;
+    dim3 grid = regs ? dim3((srows + kTrRows - 1) / kTrRows, (swords + kTrWords - 1) / kTrWords, 2) : dim3((srows + 255) / 256, (swords + 7) / 8, 2);
+    auto* kern = regs ? k_transpose_regs : k_transpose_bits;
+    if (c->pdl && pdl) {
         cudaLaunchConfig_t cfg = {}; cfg.gridDim = grid; cfg.blockDim = dim3(256); cfg.stream = c->stream;
         cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization; at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at; cfg.numAttrs = 1;
-        SK_CUDA(c, cudaLaunchKernelEx(&cfg, k_transpose_bits, src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag));
+        SK_CUDA(c, cudaLaunchKernelEx(&cfg, kern, src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag));
     } else
-    k_transpose_bits<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag);
+    kern<<<grid, 256, 0, c->stream>>>(src, sstride, srows, swords, dst, dstride, drows, dwords, src_zoff, dst_zoff, flag);
     c->cnt.kernel_launches++;
     SK_CUDA(c, cudaGetLastError());
     return SK_OK;
 }
 // C -> R ; stab_only: just the stabilizer rows (all an all-deterministic measurement block reads; the measurement kernel
 // derives the destabilizer rows itself if it has to enter panel mode)
-static int32_t rows_from_cols(sk_tableau* t, bool stab_only = false) {
+static int32_t rows_from_cols(sk_tableau* t, bool stab_only = false, bool pdl = true) {
     sk_ctx* c = t->ctx;
     int32_t rc = launch_transpose(c, reinterpret_cast<const u32*>(t->m.cols), (size_t)4 * t->RW, int(t->n), stab_only ? t->RW : 2 * t->RW,
                                   reinterpret_cast<u32*>(t->m.rows), (size_t)4 * t->Wp, stab_only ? t->NS : 64 * t->RW, 2 * t->Wp,
-                                  (size_t)2 * t->RW, (size_t)2 * t->Wp, nullptr);
+                                  (size_t)2 * t->RW, (size_t)2 * t->Wp, nullptr, pdl);
     if (rc) return rc;
     c->cnt.transposes++;
     t->r_valid = true; t->r_destab_stale = stab_only;
@@ -222,6 +242,8 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     cudaError_t e3 = dmalloc(c, &t->m.sgn, t->sgn_bytes);
     const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
     cudaError_t e4 = dmalloc(c, &t->d_wpiv, 2 * window * 4);
+    if (!e4) e4 = dmalloc(c, &t->d_wl, 2 * window * kWarpList * 4);
+    if (!e4) e4 = dmalloc(c, &t->d_wsgn, (size_t)t->W * 8);
     cudaError_t e5 = dmalloc(c, &t->d_pan, (size_t)t->B * t->RW * 8);
     cudaError_t e6 = dmalloc(c, &t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
     cudaError_t e7 = dmalloc(c, &t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
@@ -250,7 +272,7 @@ extern "C" void sk_tableau_destroy(sk_tableau* t) {
     if (!t) return;
     sk_ctx* c = t->ctx;
     cudaSetDevice(c->device);
-    for (void* p : {(void*)t->m.cols, (void*)t->m.rows, (void*)t->m.sgn, (void*)t->d_wpiv, (void*)t->d_pan, (void*)t->d_pivbuf, (void*)t->d_detacc,
+    for (void* p : {(void*)t->m.cols, (void*)t->m.rows, (void*)t->m.sgn, (void*)t->d_wpiv, (void*)t->d_wl, (void*)t->d_wsgn, (void*)t->d_pan, (void*)t->d_pivbuf, (void*)t->d_detacc,
                     (void*)t->d_info, (void*)t->d_tlist, (void*)t->d_tM, (void*)t->d_rowM, (void*)t->d_tbits, (void*)t->d_alist_h, (void*)t->d_alist_b, (void*)t->d_dpart,
                     (void*)t->d_q, (void*)t->d_out, (void*)t->d_det})
         dfree(c, p);          // stream-ordered: queued behind the work that still uses the buffers
@@ -452,31 +474,63 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     sk_ctx* c = t->ctx;
     if (count <= 0) return SK_OK;
     c->last_n = t->n;
-    if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; }
+    const bool joined = c->side_pending;
+    join_side(c);          // the previous block's k_wave_rows is done with the row form, the lists and the sign copy
     // the launch-scoped words (barrier counter, progress counter, wave slots) are zero: the previous launch's last CTA
     // re-zeroed them on its way out (check_ws does it after an error)
     MeasWs* ws = (MeasWs*)c->d_ws;
     MeasArgs a;
     a.m = t->m; a.n = int(t->n); a.NS = t->NS; a.qubits = d_qubits; a.count = count;
-    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv;
+    a.seed = seed; a.ordinal0 = ordinal0; a.outcomes = d_out; a.dets = d_det; a.ws = ws; a.wpiv = t->d_wpiv; a.wl = t->d_wl; a.wsgn = t->d_wsgn;
     a.B = t->B; a.pan = t->d_pan; a.pivbuf = t->d_pivbuf; a.detacc = t->d_detacc; a.info = t->d_info; a.tlist = t->d_tlist; a.tM = t->d_tM; a.rowM = t->d_rowM; a.tbits = t->d_tbits; a.tcap = t->tcap; a.fold = c->no_fold ? 0 : 1; a.row_cap = c->row_cap > 0 ? std::min(c->row_cap, kRowCap) : kRowCap; a.alist_h = t->d_alist_h; a.alist_b = t->d_alist_b; a.dpart = t->d_dpart;
-    a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.lv_enable = (t->lv_ok && !c->no_repl && !c->force_columns && !c->seq_rows) ? 1 : 0; a.destab_stale = t->r_destab_stale ? 1 : 0;
+    a.prof = c->prof; a.force_columns = c->force_columns; a.seq_rows = c->seq_rows; a.lv_enable = (t->lv_ok && !c->no_repl && !c->force_columns && !c->seq_rows) ? 1 : 0;
     a.from_wave = 0;
     const size_t window = (size_t)c->num_sms * kMeasWarps * kSlotsPerWarp;
-    if (!c->no_wave_kernel && count >= 2048) {
-        // long blocks: the deterministic prefix (all of it in rounds 2..d of a memory experiment) by an ordinary one-warp-per-
-        // measurement grid first; the cooperative kernel continues at ws->wpos
-        const int wend = int(std::min<size_t>((size_t)count, 2 * window));      // (d_wpiv holds the slot records)
-        static int wave_per_sm = 0;
-        if (wave_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wave_per_sm, k_wave, kWaveThreads, 0) != cudaSuccess || wave_per_sm < 1)) wave_per_sm = 2;
-        const int grid = std::max(1, std::min((wend + kWaveThreads / 32 - 1) / (kWaveThreads / 32), c->num_sms * wave_per_sm));
-        k_wave<<<grid, kWaveThreads, 0, c->stream>>>(a, wend);
-        c->cnt.kernel_launches++;
+    const bool wave = !c->no_wave_kernel && count >= 2048;
+    // long blocks: the deterministic measurements (all of them in rounds 2..d of a memory experiment) by two ordinary
+    // one-warp-per-measurement grids; the cooperative kernel starts at ws->wpos.  When the whole block fits the wave buffers the
+    // two run on the side stream: k_wave_cols next to the transposition (both only read the gate form), k_wave_rows after the
+    // cooperative kernel was enqueued -- it reads nothing the NEXT gate layers write, so those need not wait for it.
+    const int wend = int(std::min<size_t>((size_t)count, 2 * window));
+    const bool pipe = wave && !c->no_pipe && count <= wend;
+    static int wave_per_sm = 0;
+    if (wave && wave_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wave_per_sm, k_wave_rows, kWaveThreads, 0) != cudaSuccess || wave_per_sm < 1)) wave_per_sm = 2;
+    const int wgrid = std::max(1, std::min((wend + kWaveThreads / 32 - 1) / (kWaveThreads / 32), c->num_sms * std::max(1, wave_per_sm)));
+    if (wave && !t->r_valid && !c->no_tr_regs && (t->W & 1) == 0) {
+        // transposition of the stabilizer half (register-block tiles: 16-byte aligned rows) + k_wave_cols in one launch
+        dim3 grid((unsigned)((t->n + kTrRows - 1) / kTrRows), (unsigned)((t->RW + kTrWords - 1) / kTrWords), 3);
+        const u32* src = reinterpret_cast<const u32*>(t->m.cols); u32* dst = reinterpret_cast<u32*>(t->m.rows);
+        const size_t ss = (size_t)4 * t->RW, ds = (size_t)4 * t->Wp, sz = (size_t)2 * t->RW, dz = (size_t)2 * t->Wp;
+        const int srows = int(t->n), swords = t->RW, drows = t->NS, dwords = 2 * t->Wp, pp = pipe ? 1 : 0;
+        if (c->pdl && !joined) {         // (no programmatic launch behind a cross-stream wait)
+            cudaLaunchConfig_t cfg = {}; cfg.gridDim = grid; cfg.blockDim = dim3(256); cfg.stream = c->stream;
+            cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization; at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            SK_CUDA(c, cudaLaunchKernelEx(&cfg, k_transpose_wave, src, ss, srows, swords, dst, ds, drows, dwords, sz, dz, a, wend, pp));
+        } else
+        k_transpose_wave<<<grid, 256, 0, c->stream>>>(src, ss, srows, swords, dst, ds, drows, dwords, sz, dz, a, wend, pp);
+        c->cnt.kernel_launches++; c->cnt.transposes++;
+        t->r_valid = true; t->r_destab_stale = true;
+    } else {
+        if (wave) { k_wave_cols<<<wgrid, kWaveThreads, 0, c->stream>>>(a, wend, pipe ? 1 : 0); c->cnt.kernel_launches++; }
+        if (!t->r_valid) { int32_t rc = rows_from_cols(t, true, !joined); if (rc) return rc; }
+    }
+    a.destab_stale = t->r_destab_stale ? 1 : 0;
+    if (wave) {
         a.from_wave = 1;
+        if (pipe) SK_CUDA(c, cudaEventRecord(c->ev_rows, c->stream));
+        else { k_wave_rows<<<wgrid, kWaveThreads, 0, c->stream>>>(a, wend); c->cnt.kernel_launches++; }
     }
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
+    if (pipe) {
+        SK_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_rows, 0));
+        k_wave_rows<<<wgrid, kWaveThreads, 0, c->side>>>(a, wend);
+        c->cnt.kernel_launches++;
+        SK_CUDA(c, cudaEventRecord(c->ev_side, c->side));
+        c->side_pending = true;
+    }
     return SK_OK;          // (a block that entered panel mode re-derives the C form itself before it exits)
 }
 
@@ -504,6 +558,7 @@ extern "C" int32_t sk_measure_batch(sk_tableau* t, const uint32_t* qubits, size_
     if (rc) return rc;
     SK_CUDA(c, cudaMemcpyAsync(t->d_q, qubits, m * 4, cudaMemcpyHostToDevice, c->stream));
     rc = launch_measure(t, t->d_q, int(m), seed, ordinal0, t->d_out, t->d_det);
+    join_side(c);
     if (rc) return rc;
     c->cnt.gate_hist[SK_M] += m;
     SK_CUDA(c, cudaMemcpyAsync(outcomes, t->d_out, m, cudaMemcpyDeviceToHost, c->stream));
@@ -919,14 +974,18 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
                 launch_layer(t, p->d_gates + op.off, int(op.count), op.nblocks ? p->d_boff + op.boff : nullptr, int(op.nblocks), int(op.nlayers));
                 mark(0);
             } else {
-                if (!t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; mark(1); }
+                if (class_ms && !t->r_valid) { int32_t rc = rows_from_cols(t, true); if (rc) return rc; mark(1); }    // (otherwise launch_measure transposes, next to k_wave_cols)
                 int32_t rc = launch_measure(t, p->d_mq + op.off, int(op.count), seed, op.off, p->d_out + op.off, p->d_det + op.off);
                 if (rc) return rc;
                 mark(2);
             }
         }
+        join_side(c);
         return SK_OK;
     };
+    const int no_pipe_in = c->no_pipe;
+    if (class_ms) c->no_pipe = 1;            // class times: every kernel on the one stream, in order
+    struct Restore { sk_ctx* c; int v; ~Restore() { c->no_pipe = v; } } restore{c, no_pipe_in};
     const bool want_graph = !class_ms && !p->g_disabled && !c->no_graph && p->ops.size() >= 8;
     if (want_graph && p->gexec && p->g_tab_uid == t->uid && p->g_seed == seed && p->g_r_in == t->r_valid && p->g_d_in == t->r_destab_stale) {
         SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));                     // replay
@@ -938,6 +997,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
         const sk_counters before = c->cnt;
         cudaGraph_t graph = nullptr;
         int32_t rc = SK_OK;
+        join_side(c);
         if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
             rc = enqueue_all();
             cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
@@ -945,7 +1005,7 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
                 p->g_tab_uid = t->uid; p->g_seed = seed; p->g_r_in = r_in; p->g_r_out = t->r_valid; p->g_d_in = d_in; p->g_d_out = t->r_destab_stale;
                 p->g_launches = c->cnt.kernel_launches - before.kernel_launches; p->g_layers = c->cnt.layers - before.layers;
                 p->g_transposes = c->cnt.transposes - before.transposes;
-            } else { p->gexec = nullptr; p->g_disabled = true; }
+            } else { p->gexec = nullptr; p->g_disabled = true; c->side_pending = false; }
             if (graph) cudaGraphDestroy(graph);
             cudaGetLastError();
         } else { p->g_disabled = true; cudaGetLastError(); }
@@ -1129,10 +1189,12 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
         const bool r_in = t->r_valid, d_in = t->r_destab_stale;
         const sk_counters before = c->cnt;
         cudaGraph_t graph = nullptr;
+        join_side(c);                         // (a wait for an event recorded outside the capture is not allowed inside it)
         bool ok = !rc && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
         if (ok) {
             int32_t rcc = SK_OK;
             for (size_t si = graph_from; si < segs.size() && !rcc; ++si) rcc = launch_seg(si);
+            join_side(c);
             ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && !rcc && graph;
             if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
             if (graph) cudaGraphDestroy(graph);
@@ -1150,11 +1212,12 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             if (ok) ok = cudaGraphLaunch(gexec, c->stream) == cudaSuccess;
         }
         if (!rc && !ok) {                    // capture is not possible here: plain stream launches
-            cudaGetLastError();
+            cudaGetLastError(); c->side_pending = false;
             t->r_valid = r_in; t->r_destab_stale = d_in; c->cnt = before;
             for (size_t si = graph_from; si < segs.size() && !rc; ++si) rc = launch_seg(si);
         }
     }
+    join_side(c);
     ts_enq = since();
     next = segs.size();
     for (auto& w : workers) w.join();

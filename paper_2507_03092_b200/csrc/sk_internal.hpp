@@ -14,6 +14,12 @@ struct sk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // measurement pipeline: k_wave_cols runs on `side` next to the C -> R transposition, k_wave_rows under the next gate layers
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_cols = nullptr, ev_rows = nullptr, ev_side = nullptr;
+    bool side_pending = false;              // work on `side` that `stream` has not waited for yet
+    int no_tr_regs = 0;                     // SK_TRANSPOSE_REGS=0: shuffle transposition kernel only (A/B aid)
+    int no_pipe = 0;                        // SK_PIPELINE=0: the two wave kernels on the main stream, in order
     int num_sms = 0;
     int max_smem_optin = 0;
     int prof = 0;                           // SK_DEBUG_PROF: device-side phase timers (slows the kernel)
