@@ -11,6 +11,7 @@
 //   CX   r ^= xc&zt&~(xt^zc) ; xt ^= xc ; zc ^= zt
 //   CZ   r ^= xa&xb&(za^zb)  ; za ^= xb ; zb ^= xa
 //   SWAP exchange columns
+//   XCX  r ^= zc&zt&(xc^xt)     ; xc ^= zt ; xt ^= zc        (= H_c CX_{c->t} H_c, the three rules above composed)
 // Here one "bit" is a 64-bit word = 64 rows, processed as 128-bit vectors.
 //
 // Roofline: HBM/L2 streaming.  Algorithmic bytes per gate (fused form):
@@ -22,6 +23,8 @@ namespace skd {
 
 // internal op kinds of the Clifford+T pass (never cross the C ABI): append a T / T-dagger row
 constexpr uint8_t SK_APPEND_T = 12, SK_APPEND_TDG = 13;
+// internal kind made by the host's H-window pass (compile_segment): H_c ; CX c->t ; H_c as one gate, "X-controlled X"
+constexpr uint8_t SK_XCX = 14;
 
 __device__ __forceinline__ ulonglong2 ld2(const ulonglong2* p) { return __ldcg(p); }
 __device__ __forceinline__ void st2(ulonglong2* p, ulonglong2 v) { __stcg(p, v); }
@@ -85,6 +88,18 @@ k_layer(u64* __restrict__ cols, u64* __restrict__ sgn, const sk_gate* __restrict
                         s = s ^ (xc & ztv & ~(xtv ^ zc));
                         if (hx) st2(xt, xtv ^ xc);
                         if (hz) st2(za, zc ^ ztv);
+                    }
+                } break;
+                case SK_XCX: {
+                    ulonglong2* xt = reinterpret_cast<ulonglong2*>(cols + (size_t)(2 * G.q1) * RW) + v;
+                    ulonglong2* zt = xt + RW2;
+                    ulonglong2 zc = ld2(za), ztv = ld2(zt);
+                    bool hc = nz2(zc), ht = nz2(ztv);
+                    if (hc | ht) {
+                        ulonglong2 xc = ld2(xa), xtv = ld2(xt);
+                        s = s ^ (zc & ztv & (xc ^ xtv));
+                        if (ht) st2(xa, xc ^ ztv);
+                        if (hc) st2(xt, xtv ^ zc);
                     }
                 } break;
                 case SK_CZ: {

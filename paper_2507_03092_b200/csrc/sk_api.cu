@@ -46,6 +46,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
     if (const char* e = getenv("SK_PDL")) c->pdl = atoi(e);
     if (const char* e = getenv("SK_WAVE_KERNEL")) c->no_wave_kernel = atoi(e) == 0;
     if (const char* e = getenv("SK_PIPELINE")) c->no_pipe = atoi(e) == 0;
+    if (const char* e = getenv("SK_FUSE_H")) c->no_fuse_h = atoi(e) == 0;
     if (const char* e = getenv("SK_TRANSPOSE_REGS")) c->no_tr_regs = atoi(e) == 0;
     if (const char* e = getenv("SK_PANEL_REPL")) c->no_repl = atoi(e) == 0;
     if (const char* e = getenv("SK_MEAS_GRID")) c->meas_grid_override = atoi(e);
@@ -496,7 +497,8 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     static int wave_per_sm = 0;
     if (wave && wave_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wave_per_sm, k_wave_rows, kWaveThreads, 0) != cudaSuccess || wave_per_sm < 1)) wave_per_sm = 2;
     const int wgrid = std::max(1, std::min((wend + kWaveThreads / 32 - 1) / (kWaveThreads / 32), c->num_sms * std::max(1, wave_per_sm)));
-    if (wave && !t->r_valid && !c->no_tr_regs && (t->W & 1) == 0) {
+    static const bool no_fuse = getenv("SK_FUSE_COLS") && atoi(getenv("SK_FUSE_COLS")) == 0;      // A/B aid
+    if (wave && !t->r_valid && !c->no_tr_regs && (t->W & 1) == 0 && !no_fuse) {
         // transposition of the stabilizer half (register-block tiles: 16-byte aligned rows) + k_wave_cols in one launch
         dim3 grid((unsigned)((t->n + kTrRows - 1) / kTrRows), (unsigned)((t->RW + kTrWords - 1) / kTrWords), 3);
         const u32* src = reinterpret_cast<const u32*>(t->m.cols); u32* dst = reinterpret_cast<u32*>(t->m.rows);
@@ -748,27 +750,57 @@ static std::vector<Seg> scan_segments(const sk_gate* gates, size_t ngates, size_
     }
     return segs;
 }
-struct SegScratch { std::vector<uint32_t> level, lay, start, parent, csize, cid, corder, cstart; std::vector<sk_gate> tmp; };
+struct SegScratch { std::vector<uint32_t> level, lay, start, parent, csize, cid, corder, cstart, hopen, whead, wnext; std::vector<sk_gate> tmp, fused; };
+static inline bool two_q(uint8_t k) { return sk_is_two_qubit(k) || k == SK_XCX; }
 constexpr uint32_t kMaxCluster = 4;      // gates that share qubits across merged layers (e.g. H a ; CX a d) -- kept small so chunks stay balanced
 // Layering of one Clifford run + merging of consecutive layers into launch groups.  Layers l and l+1 may share a launch
 // when the gates that share qubits form small clusters: each cluster is then placed whole, in program order, inside one
 // chunk of the launch (k_layer applies a chunk's gates in order per row-vector).  Surface-code rounds: H | CX | CX | CX | CX | H
 // becomes {H,CX} {CX} {CX} {CX,H} -- 4 launches instead of 6.
-static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* ordered, uint32_t* mq, SegScratch& sc, int target_ctas) {
-    const sk_gate* g = gates + sg.lo; const size_t cnt = sg.hi - sg.lo;
+// H-window pass over one Clifford run:  H a ; ... ; H a  with nothing but CX a->d on qubit a in between is the same Clifford as
+// the window without its two H and every CX a->d replaced by XCX a,d = H_a CX H_a (H_a H_a = 1 between consecutive ones; gates
+// on other qubits commute with H_a).  The X-type checks of a surface-code round lose both of their H layers this way: same
+// tableau, bit for bit, two sub-layers less to stream.  Returns the (possibly shorter) run in sc.fused.
+static size_t fuse_h_windows(const sk_gate* g, size_t cnt, uint64_t n, SegScratch& sc) {
+    constexpr uint32_t NONE = 0xffffffffu; constexpr uint8_t DEL = 0xff;
+    if (sc.hopen.size() < n) { sc.hopen.assign(n, 0); sc.whead.assign(n, NONE); }
+    sc.fused.assign(g, g + cnt); sc.wnext.resize(cnt);
+    std::vector<sk_gate>& f = sc.fused;
+    size_t removed = 0;
+    for (size_t i = 0; i < cnt; ++i) {
+        const sk_gate G = f[i];
+        if (G.kind == SK_H) {
+            const uint32_t q = G.q0;
+            if (sc.hopen[q]) {
+                f[sc.hopen[q] - 1].kind = DEL; f[i].kind = DEL; removed += 2;
+                for (uint32_t j = sc.whead[q]; j != NONE; j = sc.wnext[j]) f[j].kind = SK_XCX;
+                sc.hopen[q] = 0;
+            } else { sc.hopen[q] = uint32_t(i) + 1; sc.whead[q] = NONE; }
+        } else if (G.kind == SK_CX) {
+            sc.hopen[G.q1] = 0;                                   // a window does not survive being a target
+            if (sc.hopen[G.q0]) { sc.wnext[i] = sc.whead[G.q0]; sc.whead[G.q0] = uint32_t(i); }
+        } else { sc.hopen[G.q0] = 0; if (sk_is_two_qubit(G.kind)) sc.hopen[G.q1] = 0; }
+    }
+    for (size_t i = 0; i < cnt; ++i) { sc.hopen[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) sc.hopen[g[i].q1] = 0; }
+    if (removed) { size_t o = 0; for (size_t i = 0; i < cnt; ++i) if (f[i].kind != DEL) f[o++] = f[i]; f.resize(o); }
+    return f.size();
+}
+static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* ordered, uint32_t* mq, SegScratch& sc, int target_ctas, bool fuse_h) {
+    const sk_gate* g = gates + sg.lo; size_t cnt = sg.hi - sg.lo;
     if (sg.meas) { for (size_t i = 0; i < cnt; ++i) mq[sg.out + i] = g[i].q0; }
     else {
+        if (fuse_h) { cnt = fuse_h_windows(g, cnt, n, sc); g = sc.fused.data(); }      // (the launch sizes below then add up to less than the run's length)
         if (sc.level.size() < n) { sc.level.assign(n, 0); sc.parent.assign(n, 0xffffffffu); sc.csize.assign(n, 0); }
         sc.lay.resize(cnt);
         uint32_t depth = 0;
         for (size_t i = 0; i < cnt; ++i) {
             uint32_t l = sc.level[g[i].q0];
-            const bool two = sk_is_two_qubit(g[i].kind);
+            const bool two = two_q(g[i].kind);
             if (two) l = std::max(l, sc.level[g[i].q1]);
             sc.lay[i] = l; sc.level[g[i].q0] = l + 1; if (two) sc.level[g[i].q1] = l + 1;
             depth = std::max(depth, l + 1);
         }
-        for (size_t i = 0; i < cnt; ++i) { sc.level[g[i].q0] = 0; if (sk_is_two_qubit(g[i].kind)) sc.level[g[i].q1] = 0; }
+        for (size_t i = 0; i < cnt; ++i) { sc.level[g[i].q0] = 0; if (two_q(g[i].kind)) sc.level[g[i].q1] = 0; }
         sc.start.assign(depth + 1, 0);
         for (size_t i = 0; i < cnt; ++i) sc.start[sc.lay[i] + 1]++;
         std::vector<uint32_t> lsize(depth);
@@ -778,11 +810,11 @@ static void compile_segment(const sk_gate* gates, uint64_t n, Seg& sg, sk_gate* 
         // ---- merge consecutive levels into launch groups
         auto find = [&](uint32_t q) { while (sc.parent[q] != q) { sc.parent[q] = sc.parent[sc.parent[q]]; q = sc.parent[q]; } return q; };
         auto touch = [&](uint32_t q) { if (sc.parent[q] == 0xffffffffu) { sc.parent[q] = q; sc.csize[q] = 0; } };
-        auto reset = [&](size_t lo, size_t hi) { for (size_t i = lo; i < hi; ++i) { sc.parent[og[i].q0] = 0xffffffffu; if (sk_is_two_qubit(og[i].kind)) sc.parent[og[i].q1] = 0xffffffffu; } };
+        auto reset = [&](size_t lo, size_t hi) { for (size_t i = lo; i < hi; ++i) { sc.parent[og[i].q0] = 0xffffffffu; if (two_q(og[i].kind)) sc.parent[og[i].q1] = 0xffffffffu; } };
         auto add_gate = [&](const sk_gate& G) -> uint32_t {       // returns the gate count of the cluster the gate joins
             touch(G.q0);
             uint32_t r = find(G.q0);
-            if (sk_is_two_qubit(G.kind)) {
+            if (two_q(G.kind)) {
                 touch(G.q1);
                 uint32_t r1 = find(G.q1);
                 if (r1 != r) { sc.parent[r1] = r; sc.csize[r] += sc.csize[r1]; }
@@ -897,7 +929,7 @@ extern "C" int32_t sk_program_create(sk_ctx* c, uint64_t n, const sk_gate* gates
         const int tctas = target_ctas_for(c, n);
         parallel_for(nthreads, nthreads, [&](size_t, size_t, unsigned) {
             SegScratch sc;
-            for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], ordered.data(), mq.data(), sc, tctas);
+            for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], ordered.data(), mq.data(), sc, tctas, !c->no_fuse_h);
         });
         for (const Seg& sg : segs) {
             if (sg.meas) { p->ops.push_back({1, uint32_t(sg.out), uint32_t(sg.hi - sg.lo)}); continue; }
@@ -1124,13 +1156,13 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
     ts_alloc = since();
     std::atomic<size_t> next{0};
     std::vector<std::thread> workers;
-    auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc, tctas); };
+    auto work = [&] { SegScratch sc; for (size_t si = next++; si < segs.size(); si = next++) compile_segment(gates, n, segs[si], h_gates, h_mq, sc, tctas, !c->no_fuse_h); };
     for (unsigned k = 1; k < nthreads; ++k) workers.emplace_back(work);
     SegScratch mine;
     size_t uploaded = 0, nbatches = 0;          // segments [0, uploaded) are on the device
     auto wait_done = [&](size_t si) {           // helps compiling while it waits
         while (!segs[si].done.load(std::memory_order_acquire)) {
-            if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine, tctas); }
+            if (nthreads == 1 || next.load() <= si) { size_t k = next++; if (k < segs.size()) compile_segment(gates, n, segs[k], h_gates, h_mq, mine, tctas, !c->no_fuse_h); }
             else std::this_thread::yield();
         }
     };

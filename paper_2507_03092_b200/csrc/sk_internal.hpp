@@ -19,6 +19,7 @@ struct sk_ctx {
     cudaEvent_t ev_fork = nullptr, ev_cols = nullptr, ev_rows = nullptr, ev_side = nullptr;
     bool side_pending = false;              // work on `side` that `stream` has not waited for yet
     int no_tr_regs = 0;                     // SK_TRANSPOSE_REGS=0: shuffle transposition kernel only (A/B aid)
+    int no_fuse_h = 0;                      // SK_FUSE_H=0: programs keep their H ; CX.. ; H windows as written (no XCX rewriting)
     int no_pipe = 0;                        // SK_PIPELINE=0: the two wave kernels on the main stream, in order
     int num_sms = 0;
     int max_smem_optin = 0;

@@ -271,6 +271,43 @@ def test_surface_code_d71_full_length_bit_parity(sk, ctx, orc):           # BASE
     prog.close(); tab.close()
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_h_window_rewriting(sk, orc, fuse):
+    """The program compiler drops  H a ; CX a->d ... ; H a  windows in favour of the internal XCX gate (sk_api.cu
+    fuse_h_windows; SK_FUSE_H=0 keeps the program as written).  Programs made of such windows -- closed, interrupted by other
+    gates on the window qubit, by the qubit becoming a target, nested on both qubits of a CX, cut by a measurement -- leave the
+    tableau and the record of the oracle."""
+    os.environ["SK_FUSE_H"] = fuse
+    try:
+        ctx = sk.Context(0)
+    finally:
+        del os.environ["SK_FUSE_H"]
+    rng = np.random.default_rng(41)
+    fixed = [
+        (3, [(H, 0, 0), (CX, 0, 1), (CX, 0, 2), (H, 0, 0)]),
+        (3, [(X, 0, 0), (H, 0, 0), (H, 1, 0), (CX, 0, 1), (H, 0, 0), (H, 1, 0)]),              # windows on both qubits of one CX
+        (3, [(S, 0, 0), (H, 0, 0), (CX, 0, 1), (S, 0, 0), (CX, 0, 2), (H, 0, 0)]),             # interrupted by S
+        (3, [(H, 1, 0), (H, 0, 0), (CX, 0, 1), (CX, 2, 0), (H, 0, 0), (CX, 0, 2), (H, 0, 0)]),   # became a target, reopened
+        (2, [(H, 0, 0), (H, 0, 0), (S, 1, 0), (H, 1, 0), (CX, 1, 0), (M, 1, 0), (H, 1, 0), (M, 0, 0), (M, 1, 0)]),
+        (4, [(H, 0, 0), (S, 1, 0), (H, 1, 0), (CX, 0, 2), (Y, 2, 0), (CZ, 2, 3), (CX, 0, 3), (H, 0, 0), (CX, 1, 3), (H, 1, 0), (M, 0, 0), (M, 3, 0), (M, 1, 0)]),
+    ]
+    cases = [(n, g) for n, g in fixed]
+    for n in (2, 3, 6, 20, 70):
+        for pm in (0.0, 0.05):
+            cases.append((n, [(S, q, 0) for q in range(0, n, 2)] + rand_gates(rng, n, 60 * n, kinds=(H, H, H, CX, CX, CX, CX, S, X, CZ), pm=pm)))
+    for n, gates in cases:
+        circ = sk.Circuit(n, gates)
+        t, out, det, _ = ctx.sim(circ, SEED)
+        o = orc.Tableau(n)
+        oo, od, rc = o.sim(gates, SEED)
+        assert rc == 0 and (out == oo).all() and (det == od).all(), (n, gates[:12])
+        assert_same_tableau(t, o)
+        prog = sk.Program(ctx, circ); t2 = sk.Tableau(ctx, n)
+        prog.run(t2, SEED); ctx.sync()
+        assert_same_tableau(t2, o)
+        t.close(); t2.close()
+
+
 @pytest.mark.parametrize("seq", [0, 1])
 @pytest.mark.parametrize("columns,width,rowcap,fold", [(1, 64, 0, 1), (1, 5, 0, 1), (1, 1, 0, 1), (0, 7, 0, 1), (0, 1, 0, 1),
                                                        (0, 64, 12, 1), (0, 9, 30, 1), (0, 64, 0, 0), (0, 16, 25, 0)])
