@@ -120,15 +120,24 @@ __device__ __forceinline__ void transpose_tile_regs(const u32* __restrict__ src,
                                                     int bx, int by, u32* tin) {
     const int c0 = bx * kTrRows, w0 = by * kTrWords;
     const int t = threadIdx.x;
+    {
+        // thread t loads 16 bytes of src rows (t >> 2) + 64 k: one pointer, advanced by 64 rows (the kernel is issue bound --
+        // ncu round 2: 56 % issue active at 50 % occupancy -- so the address arithmetic is kept out of the unrolled bodies)
+        const int part = t & 3, r0 = t >> 2;
+        const int gw = w0 + 4 * part;
+        const uint4* sp = reinterpret_cast<const uint4*>(src + (size_t)(c0 + r0) * src_stride + gw);
+        const size_t sstep = (size_t)16 * src_stride;           // 64 rows, in uint4
+        u32* p = tin + (r0 >> 5) * kTrBlkStride + (r0 & 31) * kTrWords + 4 * part;      // 8-byte aligned (kTrBlkStride is even)
+        const bool wok = gw < src_words;
+        const int rleft = src_rows - c0 - r0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int idx = k * 256 + t, rr = idx >> 2, part = idx & 3;
-        const int gr = c0 + rr, gw = w0 + 4 * part;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (gr < src_rows && gw < src_words) v = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)gr * src_stride + gw));
-        u32* p = tin + (rr >> 5) * kTrBlkStride + (rr & 31) * kTrWords + 4 * part;      // 8-byte aligned (kTrBlkStride is even)
-        *reinterpret_cast<uint2*>(p) = make_uint2(v.x, v.y);
-        *reinterpret_cast<uint2*>(p + 2) = make_uint2(v.z, v.w);
+        for (int k = 0; k < 8; ++k) {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (wok && 64 * k < rleft) v = __ldcg(sp);
+            sp += sstep;
+            *reinterpret_cast<uint2*>(p + 2 * k * kTrBlkStride) = make_uint2(v.x, v.y);
+            *reinterpret_cast<uint2*>(p + 2 * k * kTrBlkStride + 2) = make_uint2(v.z, v.w);
+        }
     }
     __syncthreads();
     const int lane = t & 31, blk = lane & 15, word = 2 * (t >> 5) + (lane >> 4);
@@ -151,8 +160,13 @@ __device__ __forceinline__ void transpose_tile_regs(const u32* __restrict__ src,
     if (gw < dst_words) {
         u32* d = dst + (size_t)(32 * (w0 + word)) * dst_stride + gw;
         const int left = dst_rows - 32 * (w0 + word);
+        if (left >= 32) {
 #pragma unroll
-        for (int b = 0; b < 32; ++b) if (b < left) __stcg(d + (size_t)b * dst_stride, a[b]);
+            for (int b = 0; b < 32; ++b) { __stcg(d, a[b]); d += dst_stride; }
+        } else {
+#pragma unroll
+            for (int b = 0; b < 32; ++b) { if (b < left) __stcg(d, a[b]); d += dst_stride; }
+        }
     }
 }
 __global__ void __launch_bounds__(256, 4)

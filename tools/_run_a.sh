@@ -1,4 +1,5 @@
-echo "== parity"; timeout 1200 python -m pytest tests/test_gpu_tableau_parity.py -m gpu -q -x --timeout 600 2>&1 | tail -6
-echo "== d=71"; timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -4
-echo "== d=71 no H fusion"; SK_FUSE_H=0 timeout 300 python tools/quick_time.py 71 71 3 2>&1 | grep -v phases | tail -3
-echo "== d=25"; timeout 300 python tools/quick_time.py 25 25 3 2>&1 | grep -v phases | tail -3
+echo "== parity"; timeout 1200 python -m pytest tests/test_gpu_tableau_parity.py -m gpu -q -x --timeout 600 2>&1 | tail -3
+echo "== d=71 NV=2"; timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
+echo "== d=71 NV=1"; SK_LAYER_NV=1 timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
+echo "== d=25 NV=2"; timeout 300 python tools/quick_time.py 25 25 4 2>&1 | grep -v phases | tail -3
+echo "== d=25 NV=1"; SK_LAYER_NV=1 timeout 300 python tools/quick_time.py 25 25 4 2>&1 | grep -v phases | tail -3
