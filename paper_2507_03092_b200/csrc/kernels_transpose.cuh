@@ -145,17 +145,23 @@ __device__ __forceinline__ void transpose_tile_regs(const u32* __restrict__ src,
     const u32* q = tin + blk * kTrBlkStride + word;
 #pragma unroll
     for (int i = 0; i < 32; ++i) a[i] = q[i * kTrWords];
-    // a[i] bit b  ->  a[b] bit i
+    // a[i] bit b  ->  a[b] bit i ; skipped by a warp whose 32 blocks are all zero (tableaux of local codes are mostly zero blocks
+    // away from a band around the diagonal, and the kernel is issue bound)
+    u32 any = 0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) { const u32 lo = a[k], hi = a[k + 16]; a[k] = __byte_perm(lo, hi, 0x5410u); a[k + 16] = __byte_perm(lo, hi, 0x7632u); }
+    for (int i = 0; i < 32; ++i) any |= a[i];
+    if (__any_sync(0xffffffffu, any != 0)) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) if (!(k & 8)) { const u32 lo = a[k], hi = a[k + 8]; a[k] = __byte_perm(lo, hi, 0x6240u); a[k + 8] = __byte_perm(lo, hi, 0x7351u); }
+        for (int k = 0; k < 16; ++k) { const u32 lo = a[k], hi = a[k + 16]; a[k] = __byte_perm(lo, hi, 0x5410u); a[k + 16] = __byte_perm(lo, hi, 0x7632u); }
 #pragma unroll
-    for (int k = 0; k < 32; ++k) if (!(k & 4)) { const u32 x = ((a[k] >> 4) ^ a[k + 4]) & 0x0f0f0f0fu; a[k + 4] ^= x; a[k] ^= x << 4; }
+        for (int k = 0; k < 32; ++k) if (!(k & 8)) { const u32 lo = a[k], hi = a[k + 8]; a[k] = __byte_perm(lo, hi, 0x6240u); a[k + 8] = __byte_perm(lo, hi, 0x7351u); }
 #pragma unroll
-    for (int k = 0; k < 32; ++k) if (!(k & 2)) { const u32 x = ((a[k] >> 2) ^ a[k + 2]) & 0x33333333u; a[k + 2] ^= x; a[k] ^= x << 2; }
+        for (int k = 0; k < 32; ++k) if (!(k & 4)) { const u32 x = ((a[k] >> 4) ^ a[k + 4]) & 0x0f0f0f0fu; a[k + 4] ^= x; a[k] ^= x << 4; }
 #pragma unroll
-    for (int k = 0; k < 32; ++k) if (!(k & 1)) { const u32 x = ((a[k] >> 1) ^ a[k + 1]) & 0x55555555u; a[k + 1] ^= x; a[k] ^= x << 1; }
+        for (int k = 0; k < 32; ++k) if (!(k & 2)) { const u32 x = ((a[k] >> 2) ^ a[k + 2]) & 0x33333333u; a[k + 2] ^= x; a[k] ^= x << 2; }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) if (!(k & 1)) { const u32 x = ((a[k] >> 1) ^ a[k + 1]) & 0x55555555u; a[k + 1] ^= x; a[k] ^= x << 1; }
+    }
     const int gw = (c0 >> 5) + blk;
     if (gw < dst_words) {
         u32* d = dst + (size_t)(32 * (w0 + word)) * dst_stride + gw;

@@ -1,5 +1,2 @@
-echo "== parity"; timeout 1200 python -m pytest tests/test_gpu_tableau_parity.py -m gpu -q -x --timeout 600 2>&1 | tail -3
-echo "== d=71 NV=2"; timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
-echo "== d=71 NV=1"; SK_LAYER_NV=1 timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
-echo "== d=25 NV=2"; timeout 300 python tools/quick_time.py 25 25 4 2>&1 | grep -v phases | tail -3
-echo "== d=25 NV=1"; SK_LAYER_NV=1 timeout 300 python tools/quick_time.py 25 25 4 2>&1 | grep -v phases | tail -3
+echo "== d=71 fused"; timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
+echo "== d=71 unfused"; SK_FUSE_COLS=0 timeout 300 python tools/quick_time.py 71 71 4 2>&1 | grep -v phases | tail -3
