@@ -523,6 +523,10 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
         if (pipe) SK_CUDA(c, cudaEventRecord(c->ev_rows, c->stream));
         else { k_wave_rows<<<wgrid, kWaveThreads, 0, c->stream>>>(a, wend); c->cnt.kernel_launches++; }
     }
+    // (Measured, round 2: inside a captured graph the cooperative kernel as the body of an IF node whose condition k_wave_cols
+    // sets -- so that the deterministic blocks skip the empty 148-CTA launch, 6 us each -- works, bit-exact, and is SLOWER: d=71
+    // 8.88 ms against 8.41 ms, graph launch 0.19 ms against 0.02 ms and sk_sim end to end 28 ms against 19 ms for the
+    // instantiation.  A conditional node costs more than the launch it saves.  Removed.)
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
