@@ -1206,52 +1206,16 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
         }
         return SK_OK;
     };
-    // Everything behind the first measurement block is launched as ONE CUDA graph: while the device works on that block
-    // (panel mode: milliseconds at d=71) the host finishes compiling, uploads the rest in one batch, captures and
-    // instantiates the remaining launches -- graph replay has none of the gaps of ~420 separate stream launches.
-    size_t first_meas = segs.size();
-    for (size_t si = 0; si < segs.size(); ++si) if (segs[si].meas) { first_meas = si; break; }
-    const size_t graph_from = (!c->no_graph && first_meas + 33 <= segs.size()) ? first_meas + 1 : segs.size();   // short programs: plain launches (instantiation would cost more than the gaps)
-    cudaGraphExec_t gexec = nullptr; cudaStream_t side_stream = nullptr;
-    for (size_t si = 0; si < graph_from && !rc; ++si) {
+    // Plain stream launches, segment by segment as the worker threads finish compiling them.  (Round 1 launched everything behind
+    // the first measurement block as one captured CUDA graph; measured again in round 2 with the shorter kernels: capture +
+    // instantiation of the ~500 nodes is 3.8 ms of host time -- 7.7 ms with the two-stream measurement pipeline in the graph --
+    // during which the device idles once the first block is done, against 1.8 ms of launch gaps this way: d=71 end to end 11.7 ms
+    // here, 12.0 ms with the graph and no pipeline, 15.7 ms with both.  Graph replay stays where it pays: sk_program_run.)
+    for (size_t si = 0; si < segs.size() && !rc; ++si) {
         wait_done(si);
         if (si == 0) ts_first = since();
         if (si >= uploaded) rc = upload_from(si);
         if (!rc) rc = launch_seg(si);
-    }
-    if (!rc && graph_from < segs.size()) {
-        for (size_t si = graph_from; si < segs.size(); ++si) wait_done(si);
-        while (uploaded < segs.size() && !rc) rc = upload_from(std::max(uploaded, graph_from));   // all done: one batch up to the end
-        const bool r_in = t->r_valid, d_in = t->r_destab_stale;
-        const sk_counters before = c->cnt;
-        cudaGraph_t graph = nullptr;
-        join_side(c);                         // (a wait for an event recorded outside the capture is not allowed inside it)
-        bool ok = !rc && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-        if (ok) {
-            int32_t rcc = SK_OK;
-            for (size_t si = graph_from; si < segs.size() && !rcc; ++si) rcc = launch_seg(si);
-            join_side(c);
-            ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && !rcc && graph;
-            if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
-            if (graph) cudaGraphDestroy(graph);
-            if (ok) {
-                // the executable graph is moved to the device on a side stream while the first block is still running, so
-                // that the launch below does not pay for it
-                cudaStream_t side = nullptr; cudaEvent_t up = nullptr;
-                if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess && cudaEventCreateWithFlags(&up, cudaEventDisableTiming) == cudaSuccess
-                    && cudaGraphUpload(gexec, side) == cudaSuccess && cudaEventRecord(up, side) == cudaSuccess)
-                    cudaStreamWaitEvent(c->stream, up, 0);
-                else cudaGetLastError();
-                if (up) cudaEventDestroy(up);
-                if (side) { side_stream = side; }
-            }
-            if (ok) ok = cudaGraphLaunch(gexec, c->stream) == cudaSuccess;
-        }
-        if (!rc && !ok) {                    // capture is not possible here: plain stream launches
-            cudaGetLastError(); c->side_pending = false;
-            t->r_valid = r_in; t->r_destab_stale = d_in; c->cnt = before;
-            for (size_t si = graph_from; si < segs.size() && !rc; ++si) rc = launch_seg(si);
-        }
     }
     join_side(c);
     ts_enq = since();
@@ -1268,8 +1232,6 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
         if (dbg) fprintf(stderr, "sk_sim host ms: validate %.2f scan %.2f alloc+tableau %.2f first segment ready %.2f all enqueued %.2f workers joined %.2f histogram %.2f record read (device done) %.2f | %u threads, %zu segments in %zu uploads\n",
                          ts_val, ts_scan, ts_alloc, ts_first, ts_enq, ts_join, ts_hist, since(), nthreads, segs.size(), nbatches);
     } else cudaStreamSynchronize(c->stream);
-    if (gexec) cudaGraphExecDestroy(gexec);          // the stream is idle here (record read / synchronised)
-    if (side_stream) cudaStreamDestroy(side_stream);
     sk_program_destroy(p);
     if (rc) { sk_tableau_destroy(t); return rc; }
     *out_t = t;
