@@ -77,7 +77,8 @@ typedef struct sk_counters {
     uint64_t pred_evals;           /* commutation predicates evaluated by the grouping conflict kernels (config C4 roofline)      */
     double   algorithmic_bytes;    /* SURVEY 8d byte count of the gates and measurements run since the last reset, for the qubit
                                       count of the tableau used last (exact when one tableau size was in use)                      */
-    double   class_ms[3];          /* device time of the last sk_program_run_profiled by kernel class: layers, measurement, transposes */
+    double   class_ms[4];          /* device time of the last sk_program_run_profiled by kernel class: fused layers, transposes,
+                                      k_measure_block, wave kernels (k_wave_cols + k_wave_rows) */
 } sk_counters;
 
 /* ---- context ---------------------------------------------------------- */
@@ -139,9 +140,10 @@ uint64_t sk_program_measurements(const sk_program* p);
 /* Runs the whole program on t from its current state (asynchronous; the
  * measurement record stays on the device until read). */
 int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed);
-/* Same, with CUDA events around every launch: class_ms = device ms spent in {fused layers,
- * transposes, measurement blocks}.  Synchronises; for roofline reporting, not for timing runs. */
-int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[3]);
+/* Same, with CUDA events around every launch and every kernel on the one stream, in order: class_ms = device ms spent in
+ * {fused layers, transposes, k_measure_block, wave kernels (k_wave_cols + k_wave_rows)}.  Synchronises; for roofline
+ * reporting, not for timing runs: an ordinary run overlaps the wave kernels with the transposition and the next layers. */
+int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[4]);
 /* SPEC:330-338 run_shots: `shots` runs from the identity tableau with seeds seed ^ shot_index.
  * ones[i] = number of shots in which measurement site i gave 1 (accumulated on the device);
  * records (optional, may be NULL) receives every shot's outcome bytes, [shots][measurements].

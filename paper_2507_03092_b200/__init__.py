@@ -44,7 +44,7 @@ class Counters(C.Structure):
     _fields_ = [("n_rand", C.c_uint64), ("n_det", C.c_uint64), ("k_rand", C.c_uint64), ("k_det", C.c_uint64),
                 ("gate_hist", C.c_uint64 * 12), ("layers", C.c_uint64), ("waves", C.c_uint64),
                 ("transposes", C.c_uint64), ("kernel_launches", C.c_uint64), ("meas_phase_ns", C.c_uint64 * 8),
-                ("pred_evals", C.c_uint64), ("algorithmic_bytes", C.c_double), ("class_ms", C.c_double * 3)]
+                ("pred_evals", C.c_uint64), ("algorithmic_bytes", C.c_double), ("class_ms", C.c_double * 4)]
 
 
 _lib = None
@@ -443,9 +443,9 @@ class Program:
         self.ctx.check(lib().sk_program_run(self._h, t._h, seed))
 
     def run_profiled(self, t: Tableau, seed: int) -> dict:
-        ms = (C.c_float * 3)()
+        ms = (C.c_float * 4)()
         self.ctx.check(lib().sk_program_run_profiled(self._h, t._h, seed, ms))
-        return {"layer_ms": float(ms[0]), "transpose_ms": float(ms[1]), "measure_ms": float(ms[2])}
+        return {"layer_ms": float(ms[0]), "transpose_ms": float(ms[1]), "measure_ms": float(ms[2]), "wave_ms": float(ms[3])}
 
     def run_shots(self, t: Tableau, shots: int, seed: int, records: bool = False):
         """SPEC:330-338.  -> (ones[nm] u32, records[shots, nm] u8 or None); shot s uses seed ^ s."""

@@ -6,6 +6,7 @@
 #include <thread>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <new>
 
 #include "kernels_layer.cuh"
@@ -527,6 +528,7 @@ static int32_t launch_measure(sk_tableau* t, const u32* d_qubits, int count, uin
     // sets -- so that the deterministic blocks skip the empty 148-CTA launch, 6 us each -- works, bit-exact, and is SLOWER: d=71
     // 8.88 ms against 8.41 ms, graph launch 0.19 ms against 0.02 ms and sk_sim end to end 28 ms against 19 ms for the
     // instantiation.  A conditional node costs more than the launch it saves.  Removed.)
+    if (c->prof_mark && wave) (*c->prof_mark)(3);          // profiled run: the wave kernels are a class of their own
     void* args[] = {&a};
     SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_measure_block, dim3(t->meas_grid), dim3(kMeasThreads), args, t->meas_smem, c->stream));
     c->cnt.kernel_launches++;
@@ -619,7 +621,7 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
         b += double(h.n_rand) * (col + 48.0 * W) + double(h.k_rand) * 32.0 * W + double(h.n_det) * col + double(h.k_det) * 16.0 * W;
         out->algorithmic_bytes = b;
     }
-    for (int k = 0; k < 3; ++k) out->class_ms[k] = c->class_ms[k];
+    for (int k = 0; k < 4; ++k) out->class_ms[k] = c->class_ms[k];
     for (int k = 0; k < 8; ++k) out->meas_phase_ns[k] = h.prof[k];
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "measure kernel CTA0 us: P1 %.0f P2 %.0f | gather %.0f factorise %.0f values+detA %.0f apply+detB %.0f | barriers wave %.0f panel %.0f | panels %llu\n",
                                          h.prof[0] / 1e3, h.prof[1] / 1e3, h.prof[2] / 1e3, h.prof[3] / 1e3, h.prof[4] / 1e3, h.prof[5] / 1e3, h.prof[6] / 1e3, h.prof[7] / 1e3, (unsigned long long)h.panels);
@@ -1021,7 +1023,9 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
     };
     const int no_pipe_in = c->no_pipe;
     if (class_ms) c->no_pipe = 1;            // class times: every kernel on the one stream, in order
-    struct Restore { sk_ctx* c; int v; ~Restore() { c->no_pipe = v; } } restore{c, no_pipe_in};
+    std::function<void(int)> mark_fn = mark;
+    c->prof_mark = class_ms ? &mark_fn : nullptr;
+    struct Restore { sk_ctx* c; int v; ~Restore() { c->no_pipe = v; c->prof_mark = nullptr; } } restore{c, no_pipe_in};
     const bool want_graph = !class_ms && !p->g_disabled && !c->no_graph && p->ops.size() >= 8;
     if (want_graph && p->gexec && p->g_tab_uid == t->uid && p->g_seed == seed && p->g_r_in == t->r_valid && p->g_d_in == t->r_destab_stale) {
         SK_CUDA(c, cudaGraphLaunch(p->gexec, c->stream));                     // replay
@@ -1061,15 +1065,15 @@ static int32_t program_run_impl(sk_program* p, sk_tableau* t, uint64_t seed, flo
     p->last_t = t;
     if (class_ms) {
         SK_CUDA(c, cudaStreamSynchronize(c->stream));
-        class_ms[0] = class_ms[1] = class_ms[2] = 0.f;
+        class_ms[0] = class_ms[1] = class_ms[2] = class_ms[3] = 0.f;
         for (size_t i = 1; i < ev.size(); ++i) { float ms = 0; cudaEventElapsedTime(&ms, ev[i - 1], ev[i]); class_ms[cls[i]] += ms; }
-        for (int k = 0; k < 3; ++k) c->class_ms[k] = class_ms[k];
+        for (int k = 0; k < 4; ++k) c->class_ms[k] = class_ms[k];
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
     return SK_OK;
 }
 extern "C" int32_t sk_program_run(sk_program* p, sk_tableau* t, uint64_t seed) { return program_run_impl(p, t, seed, nullptr); }
-extern "C" int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[3]) {
+extern "C" int32_t sk_program_run_profiled(sk_program* p, sk_tableau* t, uint64_t seed, float class_ms[4]) {
     if (!class_ms) return SK_EARG;
     return program_run_impl(p, t, seed, class_ms);
 }

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <string>
 #include <vector>
+#include <functional>
 
 #include "common.cuh"
 #include "stabkit_b200.h"
@@ -44,7 +45,8 @@ struct sk_ctx {
     // host-side counters (device-side ones live in MeasWs)
     sk_counters cnt{};
     uint64_t last_n = 0;                    // qubit count of the tableau used last (for sk_counters.algorithmic_bytes)
-    double class_ms[3] = {0, 0, 0};         // last sk_program_run_profiled: layers, measurement, transposes
+    double class_ms[4] = {0, 0, 0, 0};      // last sk_program_run_profiled: layers, transposes, k_measure_block, wave kernels
+    std::function<void(int)>* prof_mark = nullptr;      // set while a profiled run enqueues: event + class of the launches before it
     std::vector<uint32_t> q_epoch; uint32_t epoch = 0;   // qubit-collision scratch
 };
 

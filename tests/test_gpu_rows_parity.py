@@ -257,4 +257,4 @@ def test_tableau_audit_counts_violations(sk, ctx):
         assert bad == exp and bad >= 1
         t.close()
     c = ctx.counters()
-    assert c["algorithmic_bytes"] > 0 and len(c["class_ms"]) == 3 and c["pred_evals"] >= 0
+    assert c["algorithmic_bytes"] > 0 and len(c["class_ms"]) == 4 and c["pred_evals"] >= 0
