@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
     deps += [os.path.join(ROOT, "include", "stabkit_b200.h")]
     if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs]
+        extra = ["-DSK_PANEL_TRACE"] if os.environ.get("SK_BUILD_PANEL_TRACE") else []      # per-panel debug timeline (tools/panel_trace.sh)
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs]
         if verbose:
             cmd.insert(1, "-Xptxas"); cmd.insert(2, "-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

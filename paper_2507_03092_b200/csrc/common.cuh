@@ -90,14 +90,15 @@ __device__ __forceinline__ bool grid_barrier(u32* bar, u32& epoch, u32* err) {
     epoch += gridDim.x;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
+        // arrive: one release reduction (orders this CTA's writes -- bar.sync above made them cumulative -- before the count);
+        // wait: acquire loads (the bar.sync below hands the acquired view to the other threads).  Measured against
+        // fence + atomicAdd ... fence: 0.09 ms of 8.6 ms at d=71 (316 barriers).
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         u32 ok = 1;
         unsigned long long spins = 0;
         while (int(ld_acquire(bar) - epoch) < 0) {
             if (++spins > (1ull << 24)) { ok = 0; atomicExch(err, 0x80000000u); break; }
         }
-        __threadfence();
         s_ok = ok;
     }
     __syncthreads();

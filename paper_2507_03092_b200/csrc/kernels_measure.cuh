@@ -87,6 +87,7 @@ struct MeasWs {
     u64 cprof[16];      // debug: SM cycles per step section, thread 0 [0..7] and thread 96 [8..15]: random {search+bar, gather+bar, update}, det {search+bar, gather+bar, rest}
     u64 ctaphase[160 * 4];   // debug: per-CTA own time (ns) in panel phases G, F, V+D1, A+D2 (excluding barrier waits)
     u64 fprof[8];       // factorise (CTA 0) ns: load, random steps, deterministic steps, tail ; [4] random steps, [5] deterministic steps
+    u64 ptl[160 * 6];   // debug (SK_DEBUG_PROF): per panel of the last launch: start, last arrival at barrier 1, barrier 1 left, last arrival at barrier 2, barrier 2 left (ns)
     u64 trace[8 * 3 * 8];   // debug timeline (globaltimer ns): panels 20..27 of a launch x CTA {0, 1, last} x 8 events
 };
 
@@ -1411,6 +1412,12 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         if (r0 != 0xffffffffu) { panel_mode = true; break; }
     }
     if (!panel_mode) { SK_MEAS_EXIT(); return; }
+#ifdef SK_PANEL_TRACE
+#define SK_STAGE(k) do { if (a.prof && blockIdx.x == 0 && tid == 0) ws->cprof[8 + (k)] = gtime(); } while (0)
+#else
+#define SK_STAGE(k) do { } while (0)
+#endif
+    SK_STAGE(0);
 
     // =============================================================== panel mode =====
     // (the P2 reads above touch nothing that is written before the next grid barrier)
@@ -1430,7 +1437,9 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         }
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return;
     }
+    SK_STAGE(1);
     if (a.lv_enable) { pos = panel_levels_loop(a, pos, epoch); if (pos < 0) return; }
+    SK_STAGE(2);
     const int B = a.B;
     PanelInfo* info = a.info;
     const int gwi = warp * G + blockIdx.x;           // item index interleaved over the CTAs
@@ -1968,6 +1977,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
         pbase += u32(Bn);
         pos += Bn;
     }
+    SK_STAGE(3);
     {   // the last panel's entries (buffers of parity kpar ^ 1 after the final toggle)
         const u32* ptl = a.tlist + (size_t)(kpar ^ 1) * a.tcap;
         u64* prm = a.rowM + (size_t)(kpar ^ 1) * rowcap;
@@ -1991,6 +2001,7 @@ k_measure_block(const __grid_constant__ MeasArgs a) {
                                bx * 256, by * 8, t, 2 + half, tin, tout);
         }
     }
+    SK_STAGE(4);
     SK_MEAS_EXIT();
 }
 

@@ -459,6 +459,9 @@ __device__ __noinline__ void lv_apply(const MeasArgs& a, int pos, int Bn, int Bn
             const int b = born[s];
             const u64 ms = Ms[s], md = Md[s];
             if (!(pv || ms || md || b)) continue;
+#ifdef SK_PANEL_TRACE
+            const u64 t_pair = a.prof ? gtime() : 0;
+#endif
             const u32 pid = id[s];
             u64 rbs = 0, rbd = 0;
 #pragma unroll
@@ -530,6 +533,10 @@ __device__ __noinline__ void lv_apply(const MeasArgs& a, int pos, int Bn, int Bn
                 }
                 group_sync(gid, TW);        // gx and gpe are reused by the next row
             }
+#ifdef SK_PANEL_TRACE
+            if (a.prof && gt == 0)      // debug: the longest pair of the launch: ns << 24 | steps of the stabilizer << 16 | of the destabilizer << 8 | born, pivot flags
+                atomicMax((unsigned long long*)&ws->cprof[15], ((gtime() - t_pair) << 24) | ((u64)__popcll(ms) << 16) | ((u64)__popcll(md) << 8) | (u64)((b ? 2 : 0) | (pv ? 1 : 0)));
+#endif
             if (gt == 0 && (rbs | rbd)) {
                 const u32 at = atomicAdd(&info->lvcount[kpar ^ 1], 1u);
                 __stcg(lh2 + at, pid); __stcg(lb2 + 2 * (size_t)at, rbs); __stcg(lb2 + 2 * (size_t)at + 1, rbd);
@@ -549,6 +556,22 @@ __device__ __noinline__ int panel_levels_loop(const MeasArgs& a, int pos, u32& e
 #define LV_CSTART() do { if (a.prof && tid == 0) t_cta = gtime(); } while (0)
 #define LV_CPROF(k) do { if (a.prof && tid == 0 && bid < 160) { const u64 _n = gtime(); ws->ctaphase[bid * 4 + (k)] += _n - t_cta; t_cta = _n; } } while (0)
 #define LV_PROF(k) do { if (a.prof && bid == 0 && tid == 0) { const u64 _n = gtime(); ws->prof[k] += _n - t_prof; t_prof = _n; } } while (0)
+    // debug timeline of panels 20..27 of the launch (SK_DEBUG_PROF): CTAs {0, G/2, G-1}: start, F done, V+D1 done, barrier 1 left, A done
+    // (thread 0), barrier 2 left; row of CTA 0, slots 6 / 7: the last CTA's arrival at barrier 2 / 1; row of CTA G/2, slot 6: who that was
+    // (compiled in with -DSK_PANEL_TRACE only: the extra code costs the production kernel registers -- 0.25 ms at d=71)
+#ifdef SK_PANEL_TRACE
+    const int tsel = bid == 0 ? 0 : (bid == G / 2 ? 1 : (bid == G - 1 ? 2 : -1));
+    int pidx = 0;
+#define LV_TRACE(ev) do { if (a.prof && tid == 0 && tsel >= 0 && pidx >= 20 && pidx < 28) ws->trace[((pidx - 20) * 3 + tsel) * 8 + (ev)] = gtime(); } while (0)
+#define LV_PLOG(k) do { if (a.prof && tid == 0 && pidx < 160) { if ((k) & 1) atomicMax((unsigned long long*)&ws->ptl[pidx * 6 + (k)], (unsigned long long)gtime()); else if (bid == 0) ws->ptl[pidx * 6 + (k)] = gtime(); } } while (0)
+#define LV_ARRIVE(slot) do { if (a.prof) { __syncthreads(); if (tid == 0 && pidx >= 20 && pidx < 28) { \
+        atomicMax((unsigned long long*)&ws->trace[((pidx - 20) * 3) * 8 + (slot)], (unsigned long long)gtime()); \
+        if ((slot) == 6) atomicMax((unsigned long long*)&ws->trace[((pidx - 20) * 3 + 1) * 8 + 6], ((unsigned long long)(gtime() & 0xffffffffffull) << 8) | (unsigned long long)bid); } } } while (0)
+#else
+#define LV_TRACE(ev) do { } while (0)
+#define LV_PLOG(k) do { } while (0)
+#define LV_ARRIVE(slot) do { } while (0)
+#endif
     while (pos < a.count) {
         const int Bn = min(B, a.count - pos), Bn2 = min(B, a.count - pos - Bn);
         u32* lh = a.alist_h + (size_t)kpar * lcap; u64* lb = a.alist_b + (size_t)kpar * 2 * lcap;
@@ -566,7 +589,7 @@ __device__ __noinline__ int panel_levels_loop(const MeasArgs& a, int pos, u32& e
             LV_PROF(7);
         }
         // ================================================================ F (every CTA, identical result) =====
-        LV_CSTART();
+        LV_CSTART(); LV_TRACE(0); LV_PLOG(0);
         const u32 A = __ldcg(&info->lvcount[kpar]);
         if (A > (u32)Pc || A > (u32)a.row_cap) {
             // too many active pairs for the slots: hand the panel to the general path (which gathers for itself)
@@ -575,24 +598,33 @@ __device__ __noinline__ int panel_levels_loop(const MeasArgs& a, int pos, u32& e
             return pos;
         }
         const int P = int(A);
+#ifdef SK_PANEL_TRACE
+        if (a.prof && bid == 0 && tid == 0 && pidx < 160) ws->ptl[pidx * 6 + 5] = (u64)P;
+#endif
         lv_factorise(a, pos, Bn, kpar, P);
-        LV_PROF(3); LV_CPROF(1);
+        LV_PROF(3); LV_CPROF(1); LV_TRACE(1);
         lv_values(a, pos, Bn, kpar, P);
-        LV_PROF(4); LV_CPROF(2);
+        LV_PROF(4); LV_CPROF(2); LV_TRACE(2); LV_ARRIVE(7); LV_PLOG(1);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return -1;
-        LV_PROF(7); LV_CSTART();
+        LV_PROF(7); LV_CSTART(); LV_TRACE(3); LV_PLOG(2);
         lv_apply(a, pos, Bn, Bn2, kpar, P);
         LV_CPROF(3);
         // the untouched pairs' bits in the next panel's columns, straight from the R form (from the far end of the warp index space)
         if (Bn2 > 0) lv_gather_pairs(a, ps.q2, Bn2, tb, lh2, lb2, &info->lvcount[kpar ^ 1], GW - 1 - gwi, GW);
-        LV_PROF(5); LV_CPROF(0);
+        LV_PROF(5); LV_CPROF(0); LV_TRACE(4); LV_ARRIVE(6); LV_PLOG(3);
         if (!grid_barrier(&ws->bar, epoch, &ws->err)) return -1;
-        LV_PROF(7);
+        LV_PROF(7); LV_TRACE(5); LV_PLOG(4);
         have_list = Bn2 > 0;
         kpar ^= 1;
         pos += Bn;
+#ifdef SK_PANEL_TRACE
+        ++pidx;
+#endif
     }
 #undef LV_PROF
+#undef LV_TRACE
+#undef LV_PLOG
+#undef LV_ARRIVE
 #undef LV_CPROF
 #undef LV_CSTART
     return pos;

@@ -642,14 +642,23 @@ extern "C" int32_t sk_get_counters(sk_ctx* c, sk_counters* out) {
         }
     } else
     if (getenv("SK_DEBUG_PROF") && h.trace[0]) {
-        fprintf(stderr, "timeline (us from panel 20 start on CTA 0): events start, F/published seen, V, V+D1, bar1 exit, items, fold, bar2 exit\n");
+        fprintf(stderr, "timeline (us from panel 20 start on CTA 0; replicated path: start, F, V+D1, barrier 1 left, A (thread 0), barrier 2 left, last arrival at barrier 2, at barrier 1; CTAs 0, G/2, G-1)\n");
         const u64 t0 = h.trace[0];
         for (int pnl = 0; pnl < 8; ++pnl) for (int cs = 0; cs < 3; ++cs) {
             fprintf(stderr, "  panel %d cta %s:", 20 + pnl, cs == 0 ? "0   " : cs == 1 ? "1   " : "last");
-            for (int ev = 0; ev < 8; ++ev) { const u64 v = h.trace[(pnl * 3 + cs) * 8 + ev]; if (v) fprintf(stderr, " %7.2f", (double)(long long)(v - t0) / 1e3); else fprintf(stderr, "       -"); }
+            for (int ev = 0; ev < 8; ++ev) { const u64 v = h.trace[(pnl * 3 + cs) * 8 + ev]; if (cs == 1 && ev == 6 && v) fprintf(stderr, " (last at barrier 2: CTA %llu)", (unsigned long long)(v & 0xff)); else if (v) fprintf(stderr, " %7.2f", (double)(long long)(v - t0) / 1e3); else fprintf(stderr, "       -"); }
             fprintf(stderr, "\n");
         }
     }
+    if (getenv("SK_DEBUG_PROF") && h.cprof[8]) fprintf(stderr, "last panel-mode launch, CTA 0 us: destabilizer C->R %.1f, level-form panel loop %.1f, general panel loop %.1f, tail + R->C %.1f\n",
+        (double)(long long)(h.cprof[9] - h.cprof[8]) / 1e3, (double)(long long)(h.cprof[10] - h.cprof[9]) / 1e3, (double)(long long)(h.cprof[11] - h.cprof[10]) / 1e3, (double)(long long)(h.cprof[12] - h.cprof[11]) / 1e3);
+    if (getenv("SK_DEBUG_PANELS")) {
+        fprintf(stderr, "per panel us: phase 1 (to the last arrival), barrier 1, phase 2, barrier 2\n");
+        for (int pnl = 0; pnl < 160 && h.ptl[pnl * 6]; ++pnl)
+            fprintf(stderr, "  panel %3d: %6.2f %5.2f %6.2f %5.2f  pairs %llu\n", pnl, (double)(long long)(h.ptl[pnl * 6 + 1] - h.ptl[pnl * 6]) / 1e3, (double)(long long)(h.ptl[pnl * 6 + 2] - h.ptl[pnl * 6 + 1]) / 1e3,
+                    (double)(long long)(h.ptl[pnl * 6 + 3] - h.ptl[pnl * 6 + 2]) / 1e3, (double)(long long)(h.ptl[pnl * 6 + 4] - h.ptl[pnl * 6 + 3]) / 1e3, (unsigned long long)h.ptl[pnl * 6 + 5]);
+    }
+    if (getenv("SK_DEBUG_PROF") && h.cprof[15]) fprintf(stderr, "longest pair of the apply phase: %.2f us, %llu + %llu steps (stabilizer + destabilizer), flags %llu\n", (double)(h.cprof[15] >> 24) / 1e3, (unsigned long long)((h.cprof[15] >> 16) & 0xff), (unsigned long long)((h.cprof[15] >> 8) & 0xff), (unsigned long long)(h.cprof[15] & 0xff));
     if (getenv("SK_DEBUG_PROF")) { fprintf(stderr, "cprof cycles:"); for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", (unsigned long long)h.cprof[k]); fprintf(stderr, "\n"); }
     if (getenv("SK_DEBUG_PROF")) fprintf(stderr, "factorise us: load %.0f random steps %.0f (n=%llu) deterministic steps %.0f (n=%llu) tail %.0f\n",
                                          h.fprof[0] / 1e3, h.fprof[1] / 1e3, (unsigned long long)h.fprof[4], h.fprof[2] / 1e3, (unsigned long long)h.fprof[5], h.fprof[3] / 1e3);
