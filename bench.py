@@ -519,9 +519,9 @@ def main():
                                "see measure_ms_per_step / wave_ms_per_step; bound by chains of dependent accesses and two grid barriers per 64 "
                                "measurements, not by bandwidth: the fraction of the HBM peak is reported, not claimed as a roof",
             "k_layer": "NOT at a bandwidth roof although the algorithmic figure exceeds the HBM peak: SURVEY 8d charges every column of every gate, the "
-                       "kernel skips the dependent loads and all stores of all-zero source words (ncu, one CX sub-layer: 28.5 MB of DRAM reads and 0 "
-                       "written against 76.3 MB algorithmic) and the 51 MB gate form is partly L2 resident; ncu shows 49 % warps active, 16 % SM "
-                       "throughput, long-scoreboard stalls: the launch is as long as its chain of dependent loads (4-6 gates x 2 per thread)"}
+                       "kernel skips the dependent loads and all stores of all-zero source words (ncu, one XCX/CX sub-layer, cold: 28.5 MB of DRAM reads and 0 "
+                       "written against 76 MB algorithmic; warm: 6-7 MB read, 4-5 MB written) and the 51 MB gate form is partly L2 resident; ncu shows 49 % warps active, 16 % SM "
+                       "throughput, long-scoreboard stalls: the launch is as long as its chain of dependent loads (8 gates x 2 per thread).  H a ; CX a->d.. ; H a windows are rewritten to XCX gates by the program compiler (4 sub-layers per surface-code round instead of 6); the algorithmic bytes keep counting the circuit's own gates"}
         roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom][0] / (kern[dom][1] * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "traffic": traffic, "peak_source": peak_src, "note": notes[dom],
                 "whole_step": {"algorithmic_bytes": total_bytes, "achieved": total_bytes / (ms_per_step * 1e-3) / 1e9,

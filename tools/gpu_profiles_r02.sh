@@ -25,13 +25,15 @@ with open('gpurun_out/launches_bench_${R}_summary.txt', 'w') as f:
 print(open('gpurun_out/launches_bench_${R}_summary.txt').read())
 PY
 bash tools/gpu_ncu_warm.sh > gpurun_out/launches_warm_${R}_summary.txt 2>&1
-# full captures: k_layer (CX layer), the transpose, measurement block #0 (round 1: panel mode), k_wave of round 2
+# full captures: k_layer (XCX/CX layer), the fused transposition + k_wave_cols, measurement block #0 (round 1: panel mode), k_wave_rows of round 2
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_layer -s 10 -c 1 -f -o gpurun_out/k_layer_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_transpose -s 0 -c 1 -f -o gpurun_out/k_transpose_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_measure_block -s 0 -c 1 -f -o gpurun_out/k_measure_panel_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wave -s 1 -c 1 -f -o gpurun_out/k_wave_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wave_rows -s 1 -c 1 -f -o gpurun_out/k_wave_${R} python tools/quick_time.py 71 3 1 > /dev/null 2>&1
 for k in k_layer k_transpose k_measure_panel k_wave; do
   ncu -i gpurun_out/${k}_${R}.ncu-rep --page raw --csv > gpurun_out/${k}_${R}_raw.csv 2>/dev/null
 done
+python tools/make_traffic_json.py ${R} gpurun_out > /dev/null
 SK_DEBUG_PROF=1 timeout 300 python tools/quick_time.py 71 71 2 > gpurun_out/phases_${R}.log 2>&1
+bash tools/panel_trace.sh > gpurun_out/panel_trace_${R}.txt 2>&1
 ls -la gpurun_out/ | tail -30
