@@ -502,9 +502,9 @@ k_first_fit_threads(const u64* __restrict__ rows, int Wp, int W, int t0, int B, 
 // random members accepts a term with probability 2^-k), so instead of walking bitmap rows the resolver works on
 //   * the term's FREE LIST: its first kFreeList free pre-block groups in ascending order (k_free_lists, all rows in parallel), and
 //   * a per-term bit mask over the groups created inside the block (at most one per term: 1024 bits, in shared memory).
-// The sequential part is then one barrier per placed term: the term whose turn it is takes the first live entry of its list, else the
-// first in-block group without a conflicting member, else a new group; every later term that conflicts with it strikes that group
-// from its own list / mask.  Identical groups to the scanning resolvers (same first-fit rule).
+// The sequential part: the term whose turn it is takes the first live entry of its list, else the first in-block group without a
+// conflicting member, else a new group; every later term that conflicts with it strikes that group from its own list / mask --
+// inside a warp of 32 consecutive terms by shuffles, across warps once per 32 terms (one block barrier).  Identical groups to the scanning resolvers (same first-fit rule).
 constexpr int kFreeList = 12;
 // free pre-block groups of every block term, ascending; fcnt = how many there are (kFreeList + 1 stands for "more than the list holds").
 // Coalesced sweep in chunks of 256 words: a chunk without a free bit costs one barrier (GC rows are almost all ones), one with
@@ -538,81 +538,136 @@ k_free_lists(const u32* __restrict__ bitmap, int GW32, const u32* __restrict__ n
     if (threadIdx.x == 0) fcnt[blockIdx.x] = min(found, (u32)kFreeList + 1u);
 }
 
-// dynamic shared memory: terms [B][4] u64, in-block masks [32][1024] u32
+__device__ __forceinline__ void load_term4(const u64* __restrict__ rows, int Wp, int W, int m, u64* o) {
+    const u64* x = rows + (size_t)(2 * m) * Wp; const u64* z = x + Wp;
+    o[0] = x[0]; o[1] = W > 1 ? x[1] : 0ull; o[2] = z[0]; o[3] = W > 1 ? z[1] : 0ull;
+}
+// In-block conflict matrix for the free-list resolver: cb[i][w] bit k = term t0+i conflicts with term t0+32w+k (i, 32w+k < B).
+// A thread per (term, word): the 1024 x 1024 pair checks of a block on the whole machine instead of on the resolver's one SM.
+__global__ void __launch_bounds__(256)
+k_conflict_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode, u32* __restrict__ cb) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = idx >> 5, w = idx & 31;
+    if (i >= B) return;
+    u32 bits = 0;
+    if (32 * w < i) {                                   // only earlier terms matter to term i
+        u64 a[4]; load_term4(rows, Wp, W, t0 + i, a);
+        const int kend = min(32, i - 32 * w);
+        for (int k = 0; k < kend; ++k) {
+            u64 b[4]; load_term4(rows, Wp, W, t0 + 32 * w + k, b);
+            if (conflict4(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3], mode)) bits |= 1u << k;
+        }
+    }
+    cb[(size_t)i * 32 + w] = bits;
+}
+__device__ __forceinline__ u32 lst_last(const u32* fl, int tid, int have) { return fl[(size_t)tid * kFreeList + have - 1]; }
+// dynamic shared memory: in-block masks [32][1024] u32
 __global__ void __launch_bounds__(1024)
-k_first_fit_lists(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int mode,
-                  u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io,
-                  const u32* __restrict__ fl, const u32* __restrict__ fcnt) {
+k_first_fit_lists(int t0, int B, u32* __restrict__ bitmap, int GW32, u32* __restrict__ group_of, u32* __restrict__ ngroups_io,
+                  const u32* __restrict__ fl, const u32* __restrict__ fcnt, const u32* __restrict__ cb) {
     extern __shared__ u64 s_dyn[];
-    u64* s_term = s_dyn;                                            // [1024][4]: x0 x1 z0 z1
-    u32* s_nb = reinterpret_cast<u32*>(s_dyn + 4 * 1024);           // [32][1024]: in-block groups struck for thread tid, bit (g - ng0)
-    __shared__ u32 s_g[2], s_ng;
+    u32* s_nb = reinterpret_cast<u32*>(s_dyn);                      // [32][1024]: in-block groups struck for thread tid, bit (g - ng0)
+    __shared__ u32 s_gl[1024], s_ng;                                // groups of the block's terms placed so far ; groups that exist now
     const int tid = threadIdx.x;
     const bool mine = tid < B;
     const u32 ng0 = *ngroups_io;                                    // groups that exist when the block starts
-    u64 m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    if (mine) {
-        const u64* mx = rows + (size_t)(2 * (t0 + tid)) * Wp;
-        m0 = mx[0]; m1 = W > 1 ? mx[1] : 0ull; m2 = mx[Wp]; m3 = W > 1 ? mx[Wp + 1] : 0ull;
-    }
-    s_term[4 * tid] = m0; s_term[4 * tid + 1] = m1; s_term[4 * tid + 2] = m2; s_term[4 * tid + 3] = m3;
 #pragma unroll
     for (int w = 0; w < 32; ++w) s_nb[w * 1024 + tid] = 0u;
-    u32 lst[kFreeList];
+    u32 lst[16];                                                    // my free pre-block groups, ascending (constant; `live` says which are still free)
     const u32 total = mine ? fcnt[tid] : 0u;
     const int have = int(min(total, (u32)kFreeList));
+    unsigned long long hmask = 0;                                   // bit (g & 63) of every listed group: most strikes miss the list and stop here
 #pragma unroll
-    for (int i = 0; i < kFreeList; ++i) lst[i] = (mine && i < have) ? fl[(size_t)tid * kFreeList + i] : 0xffffffffu;
-    const u32 last_listed = have ? fl[(size_t)tid * kFreeList + have - 1] : 0u;
-    u32 nbfull = 0;
+    for (int i = 0; i < 16; ++i) { lst[i] = (mine && i < have) ? fl[(size_t)tid * kFreeList + i] : 0xffffffffu; if (lst[i] != 0xffffffffu) hmask |= 1ull << (lst[i] & 63u); }
+    u32 live = (1u << have) - 1u;
+    const u32 last_listed = have ? lst_last(fl, tid, have) : 0u;
+    u32 nbfull = 0, nb0 = 0, nb1 = 0;                               // in-block groups struck for me: words 0 and 1 here, the rest in s_nb
     const bool ovf = total > (u32)kFreeList;                        // more free pre-block groups than the list holds: strikes also go to the bitmap row
     u32* myrow = bitmap + (size_t)(mine ? tid : 0) * GW32;
+    const u32* mycb = cb + (size_t)(mine ? tid : 0) * 32;           // my conflicts with the earlier terms of the block, a word per sub-batch
     if (tid == 0) s_ng = ng0;
     __syncthreads();
-    for (int k = 0; k < B; ++k) {
-        if (tid == k) {
-            // my turn: first live list entry, else (list truncated) the rest of my bitmap row, else the first in-block group, else a new one
-            const u32 ng = s_ng;
-            u32 g = 0xffffffffu;
+    // a conflicting earlier term placed in group g: g leaves my list / my in-block mask
+    auto strike = [&](u32 g) {
+        if (g >= ng0) {
+            const u32 w = (g - ng0) >> 5, bit = 1u << ((g - ng0) & 31u);
+            u32 v;
+            if (w == 0) v = (nb0 |= bit);                        // the first 64 in-block groups live in registers: no shared-memory
+            else if (w == 1) v = (nb1 |= bit);                   // round trip on the chain from one term's decision to the next
+            else { v = s_nb[w * 1024 + tid] | bit; s_nb[w * 1024 + tid] = v; }
+            if (v == 0xffffffffu && w == nbfull) ++nbfull;       // leading words that are full (a lower bound is enough: the search starts there)
+        } else {
+            if ((hmask >> (g & 63u)) & 1ull) {
+                u32 hit = 0;                                        // independent compares: nothing here lengthens the chain from one term's decision to the next
 #pragma unroll
-            for (int i = 0; i < kFreeList; ++i) if (g == 0xffffffffu && lst[i] != 0xffffffffu) g = lst[i];
-            if (g == 0xffffffffu && ovf) {
-                for (u32 c = last_listed + 1; c < ng0;) {                      // behind the last listed group
-                    const u32 w = c >> 5;
-                    u32 freeb = ~__ldcg(myrow + w);
-                    if (c & 31u) freeb &= ~((1u << (c & 31u)) - 1u);
-                    if (freeb) { const u32 f = w * 32 + u32(__ffs(int(freeb)) - 1); if (f < ng0) g = f; break; }
-                    c = (w + 1) * 32;
+                for (int i = 0; i < kFreeList; ++i) hit |= (lst[i] == g) ? (1u << i) : 0u;
+                live &= ~hit;
+            }
+            if (ovf) atomicOr(myrow + (g >> 5), 1u << (g & 31));
+        }
+    };
+    // The terms are placed in order, 32 at a time: the warp that owns sub-batch j places its terms one after the other with warp
+    // shuffles only, publishes the 32 groups, and after ONE block barrier every later warp strikes them from its own terms' lists
+    // (conflicts come precomputed from k_conflict_block: the loop visits the set bits of one word).  32 barriers per block of 1024
+    // terms instead of 1024.  Same order of decisions, same information at each decision: identical groups.
+    const int lane = tid & 31, warp = tid >> 5;
+    const int nsub = (B + 31) >> 5;
+    for (int j = 0; j < nsub; ++j) {
+        const int base = 32 * j, cntk = min(32, B - base);
+        u32 cw = (mine && warp >= j) ? __ldg(mycb + j) : 0u;       // (for my own sub-batch: the lanes before me)
+        if (warp == j) {
+            u32 ng = s_ng, myg = 0;
+            const u32 cmask = cw;
+            // Every lane keeps its CANDIDATE -- the group it would take if its turn were now: first live list entry, else (list
+            // truncated) the rest of its bitmap row, else the first in-block group without a conflicting member, else the next new
+            // group, written as the number that group would get.  A turn is then one shuffle; only the lanes that conflict with
+            // the placed term AND had exactly its group as candidate look for the next one.  (A lane whose candidate was "new" and
+            // does not conflict with the lane that just opened that group keeps the same number: it now means "join it".)
+            auto candidate = [&](u32 ngc) -> u32 {
+                u32 g = 0xffffffffu;
+                if (live) {
+                    const int idx = __ffs(int(live)) - 1;          // four select levels instead of a chain of twelve
+                    const u32 a0 = (idx & 1) ? lst[1] : lst[0], a1 = (idx & 1) ? lst[3] : lst[2], a2 = (idx & 1) ? lst[5] : lst[4], a3 = (idx & 1) ? lst[7] : lst[6];
+                    const u32 a4 = (idx & 1) ? lst[9] : lst[8], a5 = (idx & 1) ? lst[11] : lst[10], a6 = (idx & 1) ? lst[13] : lst[12], a7 = (idx & 1) ? lst[15] : lst[14];
+                    const u32 b0 = (idx & 2) ? a1 : a0, b1 = (idx & 2) ? a3 : a2, b2 = (idx & 2) ? a5 : a4, b3 = (idx & 2) ? a7 : a6;
+                    const u32 c0 = (idx & 4) ? b1 : b0, c1 = (idx & 4) ? b3 : b2;
+                    g = (idx & 8) ? c1 : c0;
+                }
+                if (g == 0xffffffffu && ovf) {
+                    for (u32 c = last_listed + 1; c < ng0;) {                      // behind the last listed group
+                        const u32 w = c >> 5;
+                        u32 freeb = ~__ldcg(myrow + w);
+                        if (c & 31u) freeb &= ~((1u << (c & 31u)) - 1u);
+                        if (freeb) { const u32 f = w * 32 + u32(__ffs(int(freeb)) - 1); if (f < ng0) g = f; break; }
+                        c = (w + 1) * 32;
+                    }
+                }
+                if (g == 0xffffffffu) {
+                    const u32 nnew = ngc - ng0;
+                    for (u32 w = nbfull; w * 32 < nnew; ++w) {
+                        u32 freeb = ~(w == 0 ? nb0 : (w == 1 ? nb1 : s_nb[w * 1024 + tid]));
+                        if ((w + 1) * 32 > nnew) freeb &= (1u << (nnew & 31u)) - 1u;
+                        if (freeb) { g = ng0 + w * 32 + u32(__ffs(int(freeb)) - 1); break; }
+                    }
+                }
+                return g == 0xffffffffu ? ngc : g;
+            };
+            u32 cand = mine ? candidate(ng) : 0xffffffffu;
+            for (int k = 0; k < cntk; ++k) {
+                const u32 g = __shfl_sync(0xffffffffu, cand, k);
+                if (lane == k) { group_of[t0 + base + k] = g; myg = g; }
+                if (g == ng) ++ng;
+                if ((cmask >> k) & 1u) {
+                    strike(g);
+                    if (cand == g) cand = candidate(ng);
                 }
             }
-            if (g == 0xffffffffu) {
-                const u32 nnew = ng - ng0;
-                for (u32 w = nbfull; w * 32 < nnew; ++w) {
-                    u32 freeb = ~s_nb[w * 1024 + tid];
-                    if ((w + 1) * 32 > nnew) freeb &= (1u << (nnew & 31u)) - 1u;
-                    if (freeb) { g = ng0 + w * 32 + u32(__ffs(int(freeb)) - 1); break; }
-                }
-            }
-            if (g == 0xffffffffu) g = ng;
-            group_of[t0 + k] = g; s_g[k & 1] = g;
-            if (g == ng) s_ng = ng + 1;
+            s_gl[tid] = myg;
+            if (lane == 0) s_ng = ng;
         }
         __syncthreads();
-        if (tid > k && mine) {
-            const u64 tx0 = s_term[4 * k], tx1 = s_term[4 * k + 1], tz0 = s_term[4 * k + 2], tz1 = s_term[4 * k + 3];
-            if (conflict4(m0, m1, m2, m3, tx0, tx1, tz0, tz1, mode)) {
-                const u32 g = s_g[k & 1];
-                if (g >= ng0) {
-                    const u32 w = (g - ng0) >> 5;
-                    const u32 v = s_nb[w * 1024 + tid] | (1u << ((g - ng0) & 31u));
-                    s_nb[w * 1024 + tid] = v;
-                    if (v == 0xffffffffu && w == nbfull) ++nbfull;       // leading words that are full (a lower bound is enough: the search starts there)
-                } else if (g <= last_listed || ovf) {
-#pragma unroll
-                    for (int i = 0; i < kFreeList; ++i) if (lst[i] == g) lst[i] = 0xffffffffu;
-                    if (ovf) atomicOr(myrow + (g >> 5), 1u << (g & 31));
-                }
-            }
+        if (warp > j) {
+            while (cw) { const int k = __ffs(int(cw)) - 1; cw &= cw - 1; strike(s_gl[base + k]); }
         }
     }
     __syncthreads();

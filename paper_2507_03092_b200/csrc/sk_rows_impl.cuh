@@ -77,12 +77,13 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     }
     // free-list resolver (k_first_fit_lists): rows of <= 128 qubits, plain first fit; SK_GROUP_RESOLVER=1 selects the candidate-tracking one
     static const bool lists_off = getenv("SK_GROUP_RESOLVER") != nullptr;
-    constexpr size_t kListSmem = (size_t)4 * 1024 * 8 + (size_t)32 * 1024 * 4;
+    constexpr size_t kListSmem = (size_t)32 * 1024 * 4;
     const bool use_lists = W <= 2 && !(mode & kOrderedFit) && !lists_off && B == 1024;
-    u32* d_fl = nullptr; u32* d_fcnt = nullptr;
-    scope.own(&d_fl);
+    u32* d_fl = nullptr; u32* d_fcnt = nullptr; u32* d_cb = nullptr;
+    scope.own(&d_fl); scope.own(&d_cb);
     if (use_lists) {
         SK_CUDA(c, cudaMalloc(&d_fl, (size_t)B * (kFreeList + 1) * 4));
+        SK_CUDA(c, cudaMalloc(&d_cb, (size_t)B * 32 * 4));                      // in-block conflict matrix, a 1024-bit row per term
         d_fcnt = d_fl + (size_t)B * kFreeList;
         static bool attr_set = false;
         if (!attr_set) { SK_CUDA(c, cudaFuncSetAttribute(k_first_fit_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kListSmem))); attr_set = true; }
@@ -108,7 +109,9 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
         }
         if (use_lists) {
             k_free_lists<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_fl, d_fcnt);
-            k_first_fit_lists<<<1, 1024, kListSmem, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_fl, d_fcnt);
+            k_conflict_block<<<(b * 32 + 255) / 256, 256, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode & 0xff, d_cb);
+            k_first_fit_lists<<<1, 1024, kListSmem, c->stream>>>(t0, b, d_bitmap, GW32, d_group, d_ng, d_fl, d_fcnt, d_cb);
+            c->cnt.kernel_launches++;
         } else {
             k_first_free<<<b, 256, 0, c->stream>>>(d_bitmap, GW32, d_ng, d_ff);
             if ((mode & kOrderedFit) || legacy_resolver) k_first_fit_block<<<1, 1024, 0, c->stream>>>(d_rows, Wp, W, t0, b, mode, d_bitmap, GW32, d_group, d_ng, d_ff);
