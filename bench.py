@@ -51,14 +51,16 @@ class ClockSampler:
     start) at 20 ms; stop(t0, t1) keeps the samples whose timestamps fall inside the timed region [t0, t1] (wall clock),
     or, if the region was shorter than the sampling period, the samples closest to it."""
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, index: int, period_ms: int = 20):
+        # (launch-heavy, second-long regions -- configs C4 / C5 -- are sampled at 250 ms: every nvidia-smi query takes the
+        #  driver lock and the 20 ms cadence cost the grouping run up to 40 % of its time)
+        self.index, self.rows, self.proc, self.period_ms = index, [], None, period_ms
 
     def start(self):
         q = "timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20"],
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -243,7 +245,7 @@ def bench_c4(args):
     xp = torch.from_numpy(x).pin_memory().numpy(); zp = torch.from_numpy(z).pin_memory().numpy(); sp = torch.zeros(N, dtype=torch.uint8).pin_memory().numpy()
     rows = sk.Rows(ctx, 128, xp, zp, sp)
     steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
-    sampler = ClockSampler(0); sampler.start()
+    sampler = ClockSampler(0, 250); sampler.start()
     for _ in range(warm):
         g, ng = rows.group_first_fit(mode)
     ctx.sync(); ctx.reset_counters()
@@ -336,7 +338,7 @@ def bench_c5(args):
     gp = torch.empty(G * 12, dtype=torch.uint8).pin_memory().numpy().view(sk.GATE_DTYPE); gp[:] = gates
     circ = sk.Circuit(n, gp)
     steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
-    sampler = ClockSampler(0); sampler.start()
+    sampler = ClockSampler(0, 250); sampler.start()
     for _ in range(warm):
         sk.Pbc(ctx, circ).close()
     ctx.sync(); ctx.reset_counters()
