@@ -560,6 +560,31 @@ k_conflict_block(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int
     }
     cb[(size_t)i * 32 + w] = bits;
 }
+// Pipelined grouping: the group-major conflict kernel of block n runs on a side stream, beside the resolver of block n-1, over
+// the groups as they were after block n-2.  This kernel adds what it could not know: the conflicts of block n's terms with the
+// terms block n-1 has placed meanwhile (into old groups or new ones).  A thread per (term, 32 previous terms); GC bitmap rows
+// are almost all ones already, so the bit is read first and few atomics are issued.
+__global__ void __launch_bounds__(256)
+k_conflict_prev(const u64* __restrict__ rows, int Wp, int W, int t0, int B, int tp0, int Bp, int mode, const u32* __restrict__ group_of,
+                u32* __restrict__ bitmap, int GW32, unsigned long long* __restrict__ npred) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = idx >> 5, w = idx & 31;
+    u32 evals = 0;
+    if (i < B && 32 * w < Bp) {
+        u64 a[4]; load_term4(rows, Wp, W, t0 + i, a);
+        u32* row = bitmap + (size_t)i * GW32;
+        const int kend = min(32, Bp - 32 * w);
+        for (int k = 0; k < kend; ++k) {
+            u64 b[4]; load_term4(rows, Wp, W, tp0 + 32 * w + k, b);
+            if (conflict4(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3], mode)) {
+                const u32 g = group_of[tp0 + 32 * w + k], bit = 1u << (g & 31u);
+                if (!(__ldcg(row + (g >> 5)) & bit)) atomicOr(row + (g >> 5), bit);
+            }
+        }
+        evals = (u32)kend;
+    }
+    if (npred) { evals = __reduce_add_sync(0xffffffffu, evals); if ((threadIdx.x & 31) == 0 && evals) atomicAdd(npred, (unsigned long long)evals); }
+}
 __device__ __forceinline__ u32 lst_last(const u32* fl, int tid, int have) { return fl[(size_t)tid * kFreeList + have - 1]; }
 // dynamic shared memory: in-block masks [32][1024] u32
 __global__ void __launch_bounds__(1024)
@@ -612,9 +637,11 @@ k_first_fit_lists(int t0, int B, u32* __restrict__ bitmap, int GW32, u32* __rest
     // terms instead of 1024.  Same order of decisions, same information at each decision: identical groups.
     const int lane = tid & 31, warp = tid >> 5;
     const int nsub = (B + 31) >> 5;
+    u32 cw_next = (mine && warp >= 0) ? __ldg(mycb) : 0u;
     for (int j = 0; j < nsub; ++j) {
         const int base = 32 * j, cntk = min(32, B - base);
-        u32 cw = (mine && warp >= j) ? __ldg(mycb + j) : 0u;       // (for my own sub-batch: the lanes before me)
+        u32 cw = cw_next;                                           // my conflicts with sub-batch j (for my own sub-batch: with the lanes before me),
+        cw_next = (mine && warp >= j + 1 && j + 1 < nsub) ? __ldg(mycb + j + 1) : 0u;      // fetched one sub-batch ahead: the load is never on the chain
         if (warp == j) {
             u32 ng = s_ng, myg = 0;
             const u32 cmask = cw;

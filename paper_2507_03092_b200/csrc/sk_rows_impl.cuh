@@ -77,7 +77,9 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
     }
     // free-list resolver (k_first_fit_lists): rows of <= 128 qubits, plain first fit; SK_GROUP_RESOLVER=1 selects the candidate-tracking one
     static const bool lists_off = getenv("SK_GROUP_RESOLVER") != nullptr;
-    constexpr size_t kListSmem = (size_t)32 * 1024 * 4;
+    // (the resolver asks for ALL the shared memory of its SM although it uses 128 KB: no CTA of the conflict kernel that runs beside it on
+    //  the side stream may become co-resident and take issue slots from the one warp that is the critical path of the whole grouping)
+    const size_t kListSmem = std::max<size_t>((size_t)32 * 1024 * 4, (size_t)c->max_smem_optin - 6 * 1024);
     const bool use_lists = W <= 2 && !(mode & kOrderedFit) && !lists_off && B == 1024;
     u32* d_fl = nullptr; u32* d_fcnt = nullptr; u32* d_cb = nullptr;
     scope.own(&d_fl); scope.own(&d_cb);
@@ -89,6 +91,74 @@ static int32_t device_first_fit(sk_ctx* c, const u64* d_rows, int Wp, int W, int
         if (!attr_set) { SK_CUDA(c, cudaFuncSetAttribute(k_first_fit_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kListSmem))); attr_set = true; }
     }
     const int Btg = std::min(B, 128);                                           // block terms per CTA: 8 CTAs per 256 groups keep the SMs busy while groups are few (GC)
+    unsigned long long* npred = reinterpret_cast<unsigned long long*>(c->d_err) + 1;
+    static const bool pipe_off = getenv("SK_GROUP_PIPELINE") && atoi(getenv("SK_GROUP_PIPELINE")) == 0;      // A/B switch
+    const int nblocks = (count + B - 1) / B;
+    if (use_lists && csr && !pipe_off && nblocks >= 3) {
+        // Two streams.  The resolver occupies ONE SM for about 0.35 ms per block; the group-major conflict kernel of the NEXT block
+        // (0.15 ms on the whole machine) does not have to wait for it if it works on the groups as they were one block earlier:
+        //   side:  [resolver n-2 done] -> CSR of the terms of blocks <= n-2 -> conflicts of block n with those groups -> in-block matrix of block n
+        //   main:  [side done] -> k_conflict_prev: block n against the terms block n-1 placed -> free lists -> resolver n
+        // Same bitmap as the one-stream order by the time the free lists are made: identical groups.
+        u32* d_bm2 = nullptr; u32* d_cb2 = nullptr; u32* d_ngh = nullptr;
+        scope.own(&d_bm2); scope.own(&d_cb2); scope.own(&d_ngh);
+        SK_CUDA(c, cudaMalloc(&d_bm2, (size_t)B * GW32 * 4));
+        SK_CUDA(c, cudaMalloc(&d_cb2, (size_t)B * 32 * 4));
+        SK_CUDA(c, cudaMalloc(&d_ngh, (size_t)nblocks * 4));
+        // Stream priorities: the resolver's chain runs on a stream of the HIGHEST priority, the side stream on the lowest (the
+        // default, which is also what the context's stream has): when the chain has a kernel to run (k_conflict_prev,
+        // k_free_lists) its CTAs go first instead of queueing behind the ~30 000 CTAs of the next block's conflict kernel
+        // (in situ those two kernels take 130 + 70 us against 37 + 10 alone -- they share the memory system with the conflict
+        // kernel -- and 147 + 75 without the priorities; the resolver itself, alone on its SM, is not slowed).
+        cudaStream_t S = nullptr, M = nullptr;
+        { int lo = 0, hi = 0; cudaDeviceGetStreamPriorityRange(&lo, &hi);
+          if (cudaStreamCreateWithPriority(&S, cudaStreamNonBlocking, lo) != cudaSuccess) { cudaGetLastError(); S = nullptr; }
+          if (cudaStreamCreateWithPriority(&M, cudaStreamNonBlocking, hi) != cudaSuccess) { cudaGetLastError(); M = nullptr; } }
+        struct StScope { cudaStream_t* s; ~StScope() { if (*s) { cudaStreamSynchronize(*s); cudaStreamDestroy(*s); } } } stscope{&S}, mtscope{&M};
+        if (!S || !M) SK_FAIL(c, SK_ECUDA, "could not create the streams of the grouping pipeline");
+        cudaEvent_t e_conf[2] = {nullptr, nullptr}, e_res[2] = {nullptr, nullptr};
+        struct EvScope { cudaEvent_t* a; cudaEvent_t* b; ~EvScope() { for (int k = 0; k < 2; ++k) { if (a[k]) cudaEventDestroy(a[k]); if (b[k]) cudaEventDestroy(b[k]); } } } evscope{e_conf, e_res};
+        for (int k = 0; k < 2; ++k) { SK_CUDA(c, cudaEventCreateWithFlags(&e_conf[k], cudaEventDisableTiming)); SK_CUDA(c, cudaEventCreateWithFlags(&e_res[k], cudaEventDisableTiming)); }
+        SK_CUDA(c, cudaEventRecord(e_res[0], c->stream)); SK_CUDA(c, cudaStreamWaitEvent(S, e_res[0], 0)); SK_CUDA(c, cudaStreamWaitEvent(M, e_res[0], 0));     // both start behind the set-up above
+        for (int n = 0; n < nblocks; ++n) {
+            const int t0 = n * B, b = std::min(B, count - t0), par = n & 1;
+            u32* bm = par ? d_bm2 : d_bitmap; u32* cbn = par ? d_cb2 : d_cb;
+            // ---- side stream
+            if (n >= 2) SK_CUDA(c, cudaStreamWaitEvent(S, e_res[par], 0));          // resolver n-2: its groups are final, its bitmap buffer is free
+            SK_CUDA(c, cudaMemsetAsync(bm, 0, (size_t)b * GW32 * 4, S));
+            if (n >= 2) {
+                const int tl = t0 - B;                                               // terms [0, tl) are in the lagging CSR
+                SK_CUDA(c, cudaMemsetAsync(d_gmin, 0xff, 4, S));
+                k_csr_count<<<(B + 255) / 256, 256, 0, S>>>(d_group, tl - B, tl, d_cnt, d_gmin);
+                k_csr_scan<<<1, 1024, 0, S>>>(d_cnt, d_ngh + (n - 2), d_off, d_gmin);
+                SK_CUDA(c, cudaMemsetAsync(d_fillc, 0, ((size_t)tl + 1) * 4, S));
+                k_csr_fill<<<(tl + 255) / 256, 256, 0, S>>>(d_rows, Wp, W, d_group, tl, d_off, d_fillc, d_gterms);
+                dim3 grid((tl + 255) / 256, (b + Btg - 1) / Btg);
+                // (28 KB of shared memory requested, 4 KB used: at most seven of these long-running CTAs per SM, so that a 256-thread
+                //  slot stays free on every SM for the short kernels of the resolver's chain)
+                k_conflict_groups<<<grid, 256, std::max<size_t>((size_t)Btg * 32, 28 * 1024), S>>>(d_rows, Wp, W, t0, b, Btg, d_ngh + (n - 2), d_off, d_gterms, mode, bm, GW32, npred);
+                c->cnt.kernel_launches += 4;
+            }
+            k_conflict_block<<<(b * 32 + 255) / 256, 256, 0, S>>>(d_rows, Wp, W, t0, b, mode & 0xff, cbn);
+            SK_CUDA(c, cudaEventRecord(e_conf[par], S));
+            // ---- main stream
+            SK_CUDA(c, cudaStreamWaitEvent(M, e_conf[par], 0));
+            if (n >= 1) { k_conflict_prev<<<(b * 32 + 255) / 256, 256, 0, M>>>(d_rows, Wp, W, t0, b, t0 - B, B, mode & 0xff, d_group, bm, GW32, npred); c->cnt.kernel_launches++; }
+            k_free_lists<<<b, 256, 0, M>>>(bm, GW32, d_ng, d_fl, d_fcnt);
+            k_first_fit_lists<<<1, 1024, kListSmem, M>>>(t0, b, bm, GW32, d_group, d_ng, d_fl, d_fcnt, cbn);
+            SK_CUDA(c, cudaMemcpyAsync(d_ngh + n, d_ng, 4, cudaMemcpyDeviceToDevice, M));
+            SK_CUDA(c, cudaEventRecord(e_res[par], M));
+            c->cnt.kernel_launches += 3;
+        }
+        SK_CUDA(c, cudaGetLastError());
+        u32 ngp = 0;
+        SK_CUDA(c, cudaMemcpyAsync(&ngp, d_ng, 4, cudaMemcpyDeviceToHost, M));
+        SK_CUDA(c, cudaStreamSynchronize(M));
+        SK_CUDA(c, cudaStreamSynchronize(S));
+        SK_CUDA(c, cudaStreamSynchronize(c->stream));
+        *ngroups = ngp;
+        return SK_OK;
+    }
     for (int t0 = 0; t0 < count; t0 += B) {
         const int b = std::min(B, count - t0);
         SK_CUDA(c, cudaMemsetAsync(d_bitmap, 0, (size_t)b * GW32 * 4, c->stream));
