@@ -69,6 +69,8 @@ struct PanelInfo {      // global scratch describing the current panel (written 
     u32 dcnt[kPanelMax];   // dmode 1: partners per deterministic step
     uint8_t outc[kPanelMax];   // outcome of the random steps (counter RNG)
     u32 lvcount[2];        // replicated path (kernels_panel.cuh): pairs in the two pair-list buffers
+    // replicated path, D1 split over several CTAs: what parts 1..3 of a deterministic step found (part 0 stays in its CTA's shared memory)
+    int dp_e[3][kPanelMax]; u64 dp_N[3][kPanelMax], dp_Z[3][kPanelMax];
 };
 
 struct MeasWs {

@@ -28,7 +28,7 @@ struct LvShared {
     int gpe[kMeasThreads / 32];
     u64 wN[kMeasThreads / 32], wZ[kMeasThreads / 32];
     // this CTA's deterministic steps of the current panel (D1 -> D2 across the grid barrier)
-    int dj[kPanelMax], de[kPanelMax]; u64 dN[kPanelMax], dZ[kPanelMax]; int nd;
+    int dj[kPanelMax], de[kPanelMax]; u64 dN[kPanelMax], dZ[kPanelMax]; int nd, dparts;
 };
 
 // geometry of the thread-per-word groups of the apply phase
@@ -328,23 +328,34 @@ __device__ __noinline__ void lv_values(const MeasArgs& a, int pos, int Bn, int k
         }
     }
     // ================================================================ D1: panel-start partner products =====
-    // the idx-th deterministic step belongs to CTA G-1 - idx % G (from the far end: the first CTAs own the most V words)
+    // A deterministic step's product is cut into NP parts by the pair index (NP = 4 while there are CTAs for it): part p of the
+    // idx-th step belongs to CTA G-1 - (p*ndet + idx) % G (from the far end: the first CTAs own the most V words and apply work).  The owner of
+    // part 0 keeps its partial product in detacc[j] and its record in shared memory -- it also does D2 -- the others leave theirs
+    // in detacc[p][j] and info->dp_*: all factors are stabilizer rows (commuting), D2 folds the parts in any order.
     {
-        u64 bits = detmask; int idx = 0;
-        while (bits) {
-            const int j = __ffsll((long long)bits) - 1; bits &= bits - 1;
-            const int my = idx++;
-            if (G - 1 - my % G != bid) continue;
+        const int ndet = __popcll(detmask);
+        const int NP = ndet ? max(1, min(4, G / ndet)) : 1;
+        const int Pq = (P + NP - 1) / NP;
+        const size_t part_stride = (size_t)B * 2 * Wp;
+        if (tid == 0) ps.dparts = NP;
+        // this CTA's items: G-1-bid, G-1-bid + G, .. (at most two: NP * ndet <= 256) -- no loop over everybody's items
+        for (int it = G - 1 - bid; it < NP * ndet; it += G) {
+            const int part = it / ndet, my = it - part * ndet;        // part-major: the owners of part 0 (who also do D2) are the last CTAs, which have the least apply work
+            u64 bits = detmask;
+            for (int i = 0; i < my; ++i) bits &= bits - 1;             // the my-th deterministic step
+            const int j = __ffsll((long long)bits) - 1;
+            {
+            const int s_lo = part * Pq, s_hi = min(P, s_lo + Pq);
             // partner list: original destabilizers (their stabilizer's index), N = XOR of those stabilizers' step masks, Z = earlier
             // steps of this panel whose +-Z row is a partner
             __syncthreads();
             if (tid == 0) ps.nlist = 0;
             __syncthreads();
             u64 N = 0, Z = 0;
-            for (int s0 = 0; s0 < P; s0 += T) {
+            for (int s0 = s_lo; s0 < s_hi; s0 += T) {
                 const int s = s0 + tid;
                 bool orig = false;
-                if (s < P && ((Dm[s] >> j) & 1ull)) {
+                if (s < s_hi && ((Dm[s] >> j) & 1ull)) {
                     const int b = born[s];
                     if (b == 0 || j < b - 1) { orig = true; N ^= Ms[s]; } else Z |= 1ull << (b - 1);
                 }
@@ -385,15 +396,18 @@ __device__ __noinline__ void lv_values(const MeasArgs& a, int pos, int Bn, int k
                         e += g_word(bx, bz, ax, az); ax ^= bx; az ^= bz;
                     }
             }
-            if (gid == 0 && gt < W) { __stcg(a.detacc + (size_t)(2 * j) * Wp + gt, ax); __stcg(a.detacc + (size_t)(2 * j + 1) * Wp + gt, az); }
+            u64* acc = a.detacc + (size_t)part * part_stride;
+            if (gid == 0 && gt < W) { __stcg(acc + (size_t)(2 * j) * Wp + gt, ax); __stcg(acc + (size_t)(2 * j + 1) * Wp + gt, az); }
             e = warp_sum(e);
             if (lane == 0) ps.gpe[warp] = e;
             __syncthreads();
             if (tid == 0) {
                 int et = 0; u64 Nt = 0, Zt = 0;
                 for (int t = 0; t < T / 32; ++t) { et += ps.gpe[t]; Nt ^= ps.wN[t]; Zt |= ps.wZ[t]; }
-                const int k = ps.nd++;
-                ps.dj[k] = j; ps.de[k] = et & 3; ps.dN[k] = Nt & randmask & bits_below(j); ps.dZ[k] = Zt;
+                Nt &= randmask & bits_below(j);
+                if (part == 0) { const int k = ps.nd++; ps.dj[k] = j; ps.de[k] = et & 3; ps.dN[k] = Nt; ps.dZ[k] = Zt; }
+                else { info->dp_e[part - 1][j] = et & 3; info->dp_N[part - 1][j] = Nt; info->dp_Z[part - 1][j] = Zt; }
+            }
             }
         }
     }
@@ -418,12 +432,23 @@ __device__ __noinline__ void lv_apply(const MeasArgs& a, int pos, int Bn, int Bn
     __syncthreads();
     const u64 psign = ps.psign;
     // ================================================================ D2: outcomes of this CTA's deterministic steps =====
+    const int NP = ps.dparts;
     for (int k = 0; k < ps.nd; ++k) {
         const int j = ps.dj[k];
-        const u64 N = ps.dN[k], Z = ps.dZ[k];
+        u64 N = ps.dN[k], Z = ps.dZ[k];
+        int ep = 0;
+        for (int p = 1; p < NP; ++p) { N ^= __ldcg(&info->dp_N[p - 1][j]); Z |= __ldcg(&info->dp_Z[p - 1][j]); ep += __ldcg(&info->dp_e[p - 1][j]); }
         u64 ax = 0, az = 0; int e = 0;
         if (gid == 0 && gt < W) {
             ax = ldcg(a.detacc + (size_t)(2 * j) * Wp + gt); az = ldcg(a.detacc + (size_t)(2 * j + 1) * Wp + gt);
+            if (NP > 1) {          // the other CTAs' parts of the partner product (all loads in flight at once)
+                u64 px[3], pz[3];
+#pragma unroll
+                for (int p = 1; p < 4; ++p) if (p < NP) { const u64* acc = a.detacc + (size_t)p * B * 2 * Wp; px[p - 1] = ldcg(acc + (size_t)(2 * j) * Wp + gt); pz[p - 1] = ldcg(acc + (size_t)(2 * j + 1) * Wp + gt); }
+#pragma unroll
+                for (int p = 1; p < 4; ++p) if (p < NP) { e += g_word(px[p - 1], pz[p - 1], ax, az); ax ^= px[p - 1]; az ^= pz[p - 1]; }
+            }
+            if (gt == 0) e += ep;
             u64 b = N;
             while (b) {
                 const int l = __ffsll((long long)b) - 1; b &= b - 1;

@@ -248,7 +248,7 @@ extern "C" int32_t sk_tableau_create(sk_ctx* c, uint64_t n, sk_tableau** out) {
     if (!e4) e4 = dmalloc(c, &t->d_wsgn, (size_t)t->W * 8);
     cudaError_t e5 = dmalloc(c, &t->d_pan, (size_t)t->B * t->RW * 8);
     cudaError_t e6 = dmalloc(c, &t->d_pivbuf, (size_t)t->B * 2 * t->Wp * 8);
-    cudaError_t e7 = dmalloc(c, &t->d_detacc, (size_t)t->B * 2 * t->Wp * 8);
+    cudaError_t e7 = dmalloc(c, &t->d_detacc, (size_t)4 * t->B * 2 * t->Wp * 8);       // x4: a deterministic step's partner product may come in four parts (kernels_panel.cuh D1)
     cudaError_t e8 = dmalloc(c, &t->d_info, sizeof(PanelInfo));
     t->tcap = u32(64 * t->RW + 2 * kPanelMax);
     cudaError_t e9 = dmalloc(c, &t->d_tlist, (size_t)2 * t->tcap * 4);
