@@ -371,6 +371,8 @@ __device__ __noinline__ void lv_values(const MeasArgs& a, int pos, int Bn, int k
             if (lane == 0) { ps.wN[warp] = N; ps.wZ[warp] = Z; }
             __syncthreads();
             const int cnt = int(ps.nlist);
+            // the partners' sign words are requested before the rows, used after them: one round trip instead of two in a row
+            const u64 sgw = tid < cnt ? ldcg(a.m.sgn + (dl[tid] >> 6)) : 0ull;
             // product of the listed stabilizer rows: the groups split the list, a thread owns one word, 8 rows in flight
             u64 ax = 0, az = 0; int e = 0;
             if (gid < ngroups && gt < W) {
@@ -386,7 +388,8 @@ __device__ __noinline__ void lv_values(const MeasArgs& a, int pos, int Bn, int k
                     for (int t = 0; t < 8; ++t) { e += g_word(sx[t], sz[t], ax, az); ax ^= sx[t]; az ^= sz[t]; }
                 }
             }
-            for (int i = tid; i < cnt; i += T) e += 2 * sign_bit(a.m.sgn, int(dl[i]));
+            if (tid < cnt) e += 2 * int((sgw >> (dl[tid] & 63u)) & 1ull);
+            for (int i = tid + T; i < cnt; i += T) e += 2 * sign_bit(a.m.sgn, int(dl[i]));
             if (ngroups > 1) {       // fold the groups' partial products (commuting factors: any grouping)
                 if (gid > 0 && gid < ngroups && gt < W) { gw[(size_t)gid * 2 * Wp + gt] = ax; gw[(size_t)gid * 2 * Wp + Wp + gt] = az; }
                 __syncthreads();
