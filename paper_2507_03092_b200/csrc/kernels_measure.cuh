@@ -1336,6 +1336,9 @@ namespace skd {
 // dynamic smem (u64): max( acc[kMeasWarps][2*Wp] + values scratch, panel [B][RW] + pivmask [W] )
 __global__ void __launch_bounds__(kMeasThreads, 1)
 k_measure_block(const __grid_constant__ MeasArgs a) {
+    // the wave kernels own the whole block (every deterministic round of a memory experiment): nothing of this launch's state was
+    // touched, so there is nothing to re-zero on the way out either
+    if (a.from_wave && int(__ldcg(&a.ws->wpos)) >= a.count) return;
     extern __shared__ __align__(16) u64 smem[];
     __shared__ int s_nheavy, s_heavy[kMeasWarps * kSlotsPerWarp], s_pe[kMeasWarps], s_pk[kMeasWarps];
     __shared__ int s_wcnt[kMeasWarps];
