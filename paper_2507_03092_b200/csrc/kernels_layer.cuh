@@ -45,7 +45,7 @@ __device__ __forceinline__ ulonglong2 operator~(ulonglong2 a) { return make_ulon
 // (Measured, round 2, third attempt at the chain: TWO row-vectors per thread, the loads of a gate issued for both before either
 // is used, CTAs of half the threads and chunks of half the gates -- 64 registers with the two-qubit kinds folded into one body;
 // d=71 whole program 8.66 ms against 8.42 ms, and the folded body alone with one vector per thread 8.82 ms.  The per-kind bodies
-// below at 40 registers stay.)
+// below at 40 registers stay.  A cap of 32 registers -- 12 CTAs per SM instead of 9, chunks of 6 gates -- spills 40 bytes: 8.61 ms.)
 // gates: ngates entries; CTA b handles gates [b*gpb, (b+1)*gpb), or [block_off[b], block_off[b+1]) when the host
 // supplies chunk boundaries; thread v owns 128-bit row-vector v of every column it visits.
 // Merged layers: a launch may hold several consecutive layers provided every set of gates that share qubits (a
