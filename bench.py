@@ -247,7 +247,7 @@ def bench_c4(args):
     x, z, _ = wl.c4_terms(N)
     xp = torch.from_numpy(x).pin_memory().numpy(); zp = torch.from_numpy(z).pin_memory().numpy(); sp = torch.zeros(N, dtype=torch.uint8).pin_memory().numpy()
     rows = sk.Rows(ctx, 128, xp, zp, sp)
-    steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
+    steps, warm = max(1, min(args.steps, 5)), max(3, min(args.warmup, 5))
     sampler = ClockSampler(0, 250); sampler.start()
     for _ in range(warm):
         g, ng = rows.group_first_fit(mode)
@@ -340,7 +340,7 @@ def bench_c5(args):
     ctx = sk.Context(0)
     gp = torch.empty(G * 12, dtype=torch.uint8).pin_memory().numpy().view(sk.GATE_DTYPE); gp[:] = gates
     circ = sk.Circuit(n, gp)
-    steps, warm = max(1, min(args.steps, 5)), max(1, min(args.warmup, 2))
+    steps, warm = max(1, min(args.steps, 5)), max(3, min(args.warmup, 5))
     sampler = ClockSampler(0, 250); sampler.start()
     for _ in range(warm):
         sk.Pbc(ctx, circ).close()
