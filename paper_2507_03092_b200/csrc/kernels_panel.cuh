@@ -526,9 +526,15 @@ __device__ __noinline__ void lv_apply(const MeasArgs& a, int pos, int Bn, int Bn
                             for (int t = 0; t < 8; ++t) { ls[t] = 0; if (bits) { ls[t] = __ffsll((long long)bits) - 1; bits &= bits - 1; nl = t + 1; } }
                             u64 bx[8], bz[8];
 #pragma unroll
-                            for (int t = 0; t < 8; ++t) if (t < nl) { bx[t] = ldcg(a.pivbuf + (size_t)(2 * ls[t]) * Wp + gt); bz[t] = ldcg(a.pivbuf + (size_t)(2 * ls[t] + 1) * Wp + gt); }
+                            for (int t = 0; t < 8; ++t) { bx[t] = 0; bz[t] = 0; if (t < nl) { bx[t] = ldcg(a.pivbuf + (size_t)(2 * ls[t]) * Wp + gt); bz[t] = ldcg(a.pivbuf + (size_t)(2 * ls[t] + 1) * Wp + gt); } }
+                            // the eight factors as a tree (pairs, quads, then onto the row): same product and, by associativity, the same
+                            // phase exponent as one after the other -- with a dependency depth of four instead of eight
 #pragma unroll
-                            for (int t = 0; t < 8; ++t) if (t < nl) { e += g_word(bx[t], bz[t], ax, az); ax ^= bx[t]; az ^= bz[t]; }
+                            for (int t = 0; t < 8; t += 2) { e += g_word(bx[t + 1], bz[t + 1], bx[t], bz[t]); bx[t] ^= bx[t + 1]; bz[t] ^= bz[t + 1]; }
+#pragma unroll
+                            for (int t = 0; t < 8; t += 4) { e += g_word(bx[t + 2], bz[t + 2], bx[t], bz[t]); bx[t] ^= bx[t + 2]; bz[t] ^= bz[t + 2]; }
+                            e += g_word(bx[0], bz[0], ax, az); ax ^= bx[0]; az ^= bz[0];
+                            e += g_word(bx[4], bz[4], ax, az); ax ^= bx[4]; az ^= bz[4];
                         }
                         __stcg(tx + gt, ax); __stcg(tx + Wp + gt, az);
                         gx[gt] = ax;
