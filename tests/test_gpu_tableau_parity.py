@@ -271,6 +271,42 @@ def test_surface_code_d71_full_length_bit_parity(sk, ctx, orc):           # BASE
     prog.close(); tab.close()
 
 
+@pytest.mark.parametrize("n", [4480, 4416])
+def test_long_measurement_blocks_off_the_surface_code(sk, ctx, orc, n):
+    """The kernels that only run at size -- k_wave_cols / k_wave_rows for blocks of >= 2 048 measurements, k_transpose_wave and the
+    register-block transposition when the word count is even (n = 4 480), the shuffle transposition + a separate k_wave_cols when it
+    is odd (4 416) -- on circuits that are not surface codes: blocks that are mixed, all deterministic (the wave kernels own them)
+    and random again, Clifford layers in between; through sk_sim and through the replayed program."""
+    rng = np.random.default_rng(n)
+    g = []
+    def layer(kinds, frac):
+        qs = rng.permutation(n); k = 0
+        while k + 1 < int(frac * n):
+            kind = int(rng.choice(kinds))
+            if kind in (CX, CZ, SWAP): g.append((kind, int(qs[k]), int(qs[k + 1]))); k += 2
+            else: g.append((kind, int(qs[k]), 0)); k += 1
+    for _ in range(2): layer((H, S, X), 0.5); layer((CX, CZ), 0.8); layer((H, SDG, Y), 0.3); layer((CX, SWAP), 0.6)
+    g += [(M, q, 0) for q in range(n)]
+    g += [(M, int(q), 0) for q in rng.permutation(n)[:3000]]
+    layer((H, H, S), 0.4); layer((CX, CZ), 0.9)
+    g += [(M, int(q), 0) for q in rng.permutation(n)[:2500]]
+    layer((CX,), 0.7)
+    g += [(M, q, 0) for q in range(n - 1, -1, -1)]
+    circ = sk.Circuit(n, g)
+    t, out, det, _ = ctx.sim(circ, SEED)
+    o = orc.Tableau(n); oo, od, rc = o.sim(circ.gates, SEED, workers=8)
+    assert rc == 0 and (out == oo).all() and (det == od).all()
+    assert (od == 0).sum() > 1000 and (od == 1).sum() > 5000
+    assert_same_tableau(t, o)
+    prog = sk.Program(ctx, circ); t2 = sk.Tableau(ctx, n)
+    for _ in range(2):                                   # second run: graph replay
+        t2.reset(); prog.run(t2, SEED); ctx.sync()
+        o2, d2 = prog.read_record()
+        assert (o2 == oo).all() and (d2 == od).all()
+        assert_same_tableau(t2, o)
+    t.close(); t2.close()
+
+
 @pytest.mark.parametrize("fuse", ["1", "0"])
 def test_h_window_rewriting(sk, orc, fuse):
     """The program compiler drops  H a ; CX a->d ... ; H a  windows in favour of the internal XCX gate (sk_api.cu
