@@ -71,16 +71,9 @@ __device__ __forceinline__ int g_word(u64 ax, u64 az, u64 bx, u64 bz) {
     return __popcll(plus) - __popcll(anti & ~plus);
 }
 
-__device__ __forceinline__ int warp_sum(int v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-__device__ __forceinline__ u32 warp_min(u32 v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
+// (one REDUX instruction each instead of five shuffle + op steps)
+__device__ __forceinline__ int warp_sum(int v) { return __reduce_add_sync(0xffffffffu, v); }
+__device__ __forceinline__ u32 warp_min(u32 v) { return __reduce_min_sync(0xffffffffu, v); }
 
 // ---- grid-wide barrier for cooperative (co-resident) launches ---------------
 // Monotone counter; `epoch` is the per-thread running target.  Bounded spin:

@@ -156,10 +156,9 @@ __device__ __forceinline__ bool wait_geq(const u32* p, u32 target) {
     }
     return false;
 }
-__device__ __forceinline__ u64 warp_xor64(u64 v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+__device__ __forceinline__ u64 warp_xor64(u64 v) {        // two REDUX instead of ten shuffles
+    const u32 lo = __reduce_xor_sync(0xffffffffu, (u32)v), hi = __reduce_xor_sync(0xffffffffu, (u32)(v >> 32));
+    return ((u64)hi << 32) | lo;
 }
 
 // Multiplies the rows listed in `list` (row indices into `base`, R layout: x words then z words,
@@ -582,7 +581,8 @@ __device__ __forceinline__ void smem_or64(u64* p, u64 v) {
     if ((u32)(v >> 32)) atomicOr(q + 1, (u32)(v >> 32));
 }
 __device__ __forceinline__ u64 warp_or64(u64 v) {
-    return (u64)__reduce_or_sync(0xffffffffu, (u32)v) | ((u64)__reduce_or_sync(0xffffffffu, (u32)(v >> 32)) << 32);
+    const u32 lo = __reduce_or_sync(0xffffffffu, (u32)v), hi = __reduce_or_sync(0xffffffffu, (u32)(v >> 32));
+    return ((u64)hi << 32) | lo;
 }
 
 struct LevelSmem {
