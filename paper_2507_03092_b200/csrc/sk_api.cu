@@ -1183,6 +1183,14 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             else std::this_thread::yield();
         }
     };
+    // uploads go through a stream of their own, ordered behind the allocations above and in front of the launches that use them
+    cudaStream_t copy_stream = nullptr; std::vector<cudaEvent_t> copy_events;
+    struct CopyScope { cudaStream_t& s; std::vector<cudaEvent_t>& ev; ~CopyScope() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } for (cudaEvent_t x : ev) cudaEventDestroy(x); } } copy_scope{copy_stream, copy_events};
+    if (!getenv("SK_NO_COPY_STREAM") && cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking) == cudaSuccess) {
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) { copy_events.push_back(ev); cudaEventRecord(ev, c->stream); cudaStreamWaitEvent(copy_stream, ev, 0); }
+        else { cudaStreamDestroy(copy_stream); copy_stream = nullptr; }
+    } else { cudaGetLastError(); copy_stream = nullptr; }
     // one copy per array for every segment the workers have finished by now (they run ahead while the device is busy
     // with a measurement block): the ordered gates and the measured qubits are contiguous across segments
     auto upload_from = [&](size_t si) -> int32_t {
@@ -1200,9 +1208,17 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
                 }
             }
         }
-        if (!e && m_hi > m_lo) e = cudaMemcpyAsync(p->d_mq + m_lo, h_mq + m_lo, (m_hi - m_lo) * 4, cudaMemcpyHostToDevice, c->stream);
-        if (!e && g_hi > g_lo) e = cudaMemcpyAsync(p->d_gates + g_lo, h_gates + g_lo, (g_hi - g_lo) * sizeof(sk_gate), cudaMemcpyHostToDevice, c->stream);
-        if (!e && b_hi > b_lo) e = cudaMemcpyAsync(p->d_boff + b_lo, h_boff + b_lo, (b_hi - b_lo) * 4, cudaMemcpyHostToDevice, c->stream);
+        // on the copy stream: the kernels of earlier segments keep running on the main stream while the next batch comes up
+        cudaStream_t cs = copy_stream ? copy_stream : c->stream;
+        if (!e && m_hi > m_lo) e = cudaMemcpyAsync(p->d_mq + m_lo, h_mq + m_lo, (m_hi - m_lo) * 4, cudaMemcpyHostToDevice, cs);
+        if (!e && g_hi > g_lo) e = cudaMemcpyAsync(p->d_gates + g_lo, h_gates + g_lo, (g_hi - g_lo) * sizeof(sk_gate), cudaMemcpyHostToDevice, cs);
+        if (!e && b_hi > b_lo) e = cudaMemcpyAsync(p->d_boff + b_lo, h_boff + b_lo, (b_hi - b_lo) * 4, cudaMemcpyHostToDevice, cs);
+        if (!e && copy_stream) {
+            cudaEvent_t ev = nullptr;
+            e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (!e) { copy_events.push_back(ev); e = cudaEventRecord(ev, copy_stream); }
+            if (!e) e = cudaStreamWaitEvent(c->stream, ev, 0);
+        }
         if (e) { c->err = cudaGetErrorString(e); return SK_ECUDA; }
         uploaded = e_seg; ++nbatches;
         return SK_OK;
