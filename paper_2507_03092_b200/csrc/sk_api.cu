@@ -58,6 +58,7 @@ extern "C" int32_t sk_ctx_create(int device, void* stream, sk_ctx** out) {
         c->own_stream = true;
     }
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) c->no_pipe = 1;
+    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) c->copy = nullptr;
     for (cudaEvent_t* e : {&c->ev_fork, &c->ev_cols, &c->ev_rows, &c->ev_side})
         if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) c->no_pipe = 1;
     cudaGetLastError();
@@ -78,6 +79,7 @@ extern "C" void sk_ctx_destroy(sk_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
     for (cudaEvent_t e : {c->ev_fork, c->ev_cols, c->ev_rows, c->ev_side}) if (e) cudaEventDestroy(e);
     cudaFree(c->d_gates); cudaFree(c->d_tmp); cudaFree(c->d_err); cudaFree(c->d_ws);
     if (c->h_pin) cudaFreeHost(c->h_pin);
@@ -1183,14 +1185,15 @@ static int32_t sim_pipelined(sk_ctx* c, uint64_t n, const sk_gate* gates, size_t
             else std::this_thread::yield();
         }
     };
-    // uploads go through a stream of their own, ordered behind the allocations above and in front of the launches that use them
+    // uploads of large programs go through a stream of their own, ordered behind the allocations above and in front of the
+    // launches that use them (small ones stay on the main stream: the events would cost more than the overlap gives)
     cudaStream_t copy_stream = nullptr; std::vector<cudaEvent_t> copy_events;
-    struct CopyScope { cudaStream_t& s; std::vector<cudaEvent_t>& ev; ~CopyScope() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } for (cudaEvent_t x : ev) cudaEventDestroy(x); } } copy_scope{copy_stream, copy_events};
-    if (!getenv("SK_NO_COPY_STREAM") && cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking) == cudaSuccess) {
+    struct CopyScope { cudaStream_t& s; std::vector<cudaEvent_t>& ev; ~CopyScope() { if (s) cudaStreamSynchronize(s); for (cudaEvent_t x : ev) cudaEventDestroy(x); } } copy_scope{copy_stream, copy_events};
+    if (c->copy && !getenv("SK_NO_COPY_STREAM") && ng * sizeof(sk_gate) + nm * 4 >= (size_t)1 << 20) {
         cudaEvent_t ev = nullptr;
-        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) { copy_events.push_back(ev); cudaEventRecord(ev, c->stream); cudaStreamWaitEvent(copy_stream, ev, 0); }
-        else { cudaStreamDestroy(copy_stream); copy_stream = nullptr; }
-    } else { cudaGetLastError(); copy_stream = nullptr; }
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) { copy_events.push_back(ev); cudaEventRecord(ev, c->stream); cudaStreamWaitEvent(c->copy, ev, 0); copy_stream = c->copy; }
+        else cudaGetLastError();
+    }
     // one copy per array for every segment the workers have finished by now (they run ahead while the device is busy
     // with a measurement block): the ordered gates and the measured qubits are contiguous across segments
     auto upload_from = [&](size_t si) -> int32_t {

@@ -17,6 +17,7 @@ struct sk_ctx {
     bool own_stream = false;
     // measurement pipeline: k_wave_cols runs on `side` next to the C -> R transposition, k_wave_rows under the next gate layers
     cudaStream_t side = nullptr;
+    cudaStream_t copy = nullptr;            // sk_sim: host -> device uploads of large programs, beside the kernels of earlier segments
     cudaEvent_t ev_fork = nullptr, ev_cols = nullptr, ev_rows = nullptr, ev_side = nullptr;
     bool side_pending = false;              // work on `side` that `stream` has not waited for yet
     int no_tr_regs = 0;                     // SK_TRANSPOSE_REGS=0: shuffle transposition kernel only (A/B aid)
